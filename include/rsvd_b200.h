@@ -1,0 +1,179 @@
+/*
+ * rsvd_b200.h — C ABI of the B200-native randomized-SVD engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (reference proj/include/rsvd/ sketch, rangefinder, factor, singlepass,
+ * core .hpp).  The reference has no FFI of its own: its "operator API" is the
+ * header-only C++ namespace rsvd.  The headers in include/rsvd/ re-expose it
+ * (same names, argument meaning and exceptions) on top of the entry points
+ * below; INTEGRATION.md shows how a maintainer binds them.
+ *
+ * Conventions
+ *  - Every matrix is column-major double precision (reference core.hpp:1-4),
+ *    given as (pointer, rows, cols, leading dimension).
+ *  - Functions named *_dev take DEVICE pointers on the handle's GPU and run on
+ *    the handle's stream; A is never modified.  Functions named *_host take
+ *    HOST pointers (pageable or pinned) and include the host<->device copies.
+ *  - Multi-GPU (row-sharded A): a handle created with rsvd_create_dist holds
+ *    rows [row_offset, row_offset + m_local) of A on each rank; per-rank
+ *    outputs are the local rows of U / Q, while V, sigma, lambda are
+ *    replicated.  Only l x n / n x l / l x l partials cross NVLink (NCCL).
+ *  - Errors are returned as rsvd_status; the C++ layer rethrows them as the
+ *    reference's DimensionError / ParameterError / NumericError
+ *    (core.hpp:23-39).  rsvd_last_error() returns the message (thread-local).
+ *  - The RNG is the reference's stream: std::mt19937_64 feeding
+ *    std::normal_distribution<double> (sketch.hpp:19-45).  Its full state
+ *    (312-word MT vector, position, cached second polar variate) is passed in
+ *    and returned advanced by exactly the draws consumed, so a host
+ *    rsvd::Rng continues bit-identically after a device call.
+ */
+#ifndef RSVD_B200_H_
+#define RSVD_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum rsvd_status {
+  RSVD_OK = 0,
+  RSVD_ERR_DIMENSION = 1, /* reference DimensionError (std::invalid_argument) */
+  RSVD_ERR_PARAMETER = 2, /* reference ParameterError (std::invalid_argument) */
+  RSVD_ERR_NUMERIC = 3,   /* reference NumericError (std::runtime_error)      */
+  RSVD_ERR_CUDA = 4,
+  RSVD_ERR_NCCL = 5,
+  RSVD_ERR_INTERNAL = 9
+} rsvd_status;
+
+/* RangeMode, reference rangefinder.hpp:13-17. */
+typedef enum rsvd_range_mode {
+  RSVD_MODE_BASIC = 0,
+  RSVD_MODE_POWER = 1,
+  RSVD_MODE_POWER_ORTHO = 2
+} rsvd_range_mode;
+
+/* Full state of the reference Rng (sketch.hpp:41-44): mt19937_64's 312-word
+ * vector and index (libstdc++ _M_x / _M_p), plus normal_distribution's cached
+ * second polar variate (_M_saved_available / _M_saved). */
+typedef struct rsvd_rng_state {
+  uint64_t mt[312];
+  uint64_t pos;
+  int32_t has_cached;
+  int32_t pad_;
+  double cached;
+} rsvd_rng_state;
+
+/* Block-application counters: the reference CountingOperator contract
+ * (singlepass.hpp:15-40) plus the number of physical streaming passes over A
+ * (a fused Alg-6 pass counts one apply, one adjoint and ONE physical pass). */
+typedef struct rsvd_counters {
+  int64_t apply;
+  int64_t adjoint;
+  int64_t physical_passes;
+  int64_t kernel_launches;
+} rsvd_counters;
+
+typedef struct rsvd_handle rsvd_handle;
+
+/* ---------------------------------------------------------------- handle */
+rsvd_status rsvd_create(rsvd_handle** h, int device);
+/* Multi-GPU: one handle per rank/GPU.  nccl_id is the 128-byte ncclUniqueId
+ * produced by rsvd_nccl_unique_id on rank 0 and broadcast by the caller. */
+rsvd_status rsvd_nccl_unique_id(void* nccl_id_out128);
+rsvd_status rsvd_create_dist(rsvd_handle** h, int device, int rank, int nranks,
+                             const void* nccl_id128);
+void rsvd_destroy(rsvd_handle* h);
+const char* rsvd_last_error(void);
+const char* rsvd_version(void);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores
+ * the handle's own stream. */
+rsvd_status rsvd_set_stream(rsvd_handle* h, void* cuda_stream);
+rsvd_status rsvd_synchronize(rsvd_handle* h);
+rsvd_status rsvd_get_counters(rsvd_handle* h, rsvd_counters* out);
+rsvd_status rsvd_reset_counters(rsvd_handle* h);
+/* Row-sharding info (1 / 0 for a single-GPU handle). */
+rsvd_status rsvd_dist_info(rsvd_handle* h, int* rank, int* nranks);
+
+/* ---------------------------------------------------- sketch.hpp (L1') */
+/* gaussian(n, l, rng): n x l i.i.d. N(0,1), column-major fill
+ * (reference sketch.hpp:48-59).  ParameterError if n < 1 or l < 1. */
+rsvd_status rsvd_gaussian_dev(rsvd_handle* h, int64_t n, int64_t l, rsvd_rng_state* rng,
+                              double* out, int64_t ld_out);
+
+/* ------------------------------------------------------ core.hpp (L1) */
+/* orthonormalize(M): m x n -> m x n orthonormal Q with range(Q) >= range(M),
+ * padded to full width when rank deficient (reference core.hpp:93-105).
+ * DimensionError if n > m, NumericError on non-finite input. In == out allowed. */
+rsvd_status rsvd_orthonormalize_dev(rsvd_handle* h, int64_t m, int64_t n, const double* in,
+                                    int64_t ld_in, double* q, int64_t ld_q);
+/* svd_small(M): thin SVD, r = min(m,n) triples, sigma descending, sign rule
+ * of reference core.hpp:111-124.  U m x r, s r, V n x r (device). */
+rsvd_status rsvd_svd_small_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                               int64_t lda, double* u, int64_t ldu, double* s, double* v,
+                               int64_t ldv);
+/* evd_symmetric(C): reference core.hpp:130-162 (asymmetry check, |lambda|
+ * descending stable order).  U n x n, lambda n (device). */
+rsvd_status rsvd_evd_symmetric_dev(rsvd_handle* h, int64_t n, const double* c, int64_t ldc,
+                                   double* u, int64_t ldu, double* lambda);
+/* solve_ls(G, H): min-norm least squares, cutoff 1e-12 * sigma_max
+ * (reference core.hpp:166-177).  G m x n, H m x r, X n x r (device). */
+rsvd_status rsvd_solve_ls_dev(rsvd_handle* h, int64_t m, int64_t n, const double* g,
+                              int64_t ldg, int64_t r, const double* hm, int64_t ldh, double* x,
+                              int64_t ldx);
+/* detail::solve_joint_core(g1, h1, g2, h2) (reference singlepass.hpp:84-101),
+ * computed by the exactly equivalent Kronecker-diagonalised route. All l x l. */
+rsvd_status rsvd_solve_joint_core_dev(rsvd_handle* h, int64_t l, const double* g1,
+                                      const double* h1, const double* g2, const double* h2,
+                                      double* c);
+
+/* -------------------------------------------- streaming passes over A */
+/* Y = A X   (A m x n, X n x l, Y m x l): the sketch / power product. */
+rsvd_status rsvd_apply_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a, int64_t lda,
+                           int64_t l, const double* x, int64_t ldx, double* y, int64_t ldy);
+/* Z = A^T Y (A m x n, Y m x l, Z n x l): the adjoint / projection product
+ * (B = Q^T A is returned transposed as Z = A^T Q).  Multi-GPU: allreduced. */
+rsvd_status rsvd_apply_adjoint_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                   int64_t lda, int64_t l, const double* y, int64_t ldy,
+                                   double* z, int64_t ldz);
+
+/* ------------------------------------------- rangefinder.hpp (L2) */
+/* range_basis(A, cfg, rng) (reference rangefinder.hpp:97-105): Q m x (k+p). */
+rsvd_status rsvd_range_basis_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                 int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                 rsvd_rng_state* rng, double* q_out, int64_t ldq);
+
+/* --------------------------------------------- factor.hpp (L3) */
+/* rsvd(A, cfg, rng) (reference factor.hpp:12-18): full width l = k+p.
+ * U m x l, sigma l, V n x l (device pointers). */
+rsvd_status rsvd_rsvd_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a, int64_t lda,
+                          int64_t k, int64_t p, int q, int mode, rsvd_rng_state* rng, double* u,
+                          int64_t ldu, double* sigma, double* v, int64_t ldv);
+rsvd_status rsvd_rsvd_host(rsvd_handle* h, int64_t m, int64_t n, const double* a, int64_t lda,
+                           int64_t k, int64_t p, int q, int mode, rsvd_rng_state* rng, double* u,
+                           int64_t ldu, double* sigma, double* v, int64_t ldv);
+
+/* ----------------------------------------- singlepass.hpp (L3) */
+/* spevd_hermitian(A, k, p, rng) (reference singlepass.hpp:45-78): one
+ * counted pass over A.  U n x k, lambda k (device).  check_symmetry != 0 runs
+ * the reference's uncounted asymmetry precondition (singlepass.hpp:49-53). */
+rsvd_status rsvd_spevd_dev(rsvd_handle* h, int64_t n, const double* a, int64_t lda, int64_t k,
+                           int64_t p, rsvd_rng_state* rng, int check_symmetry, double* u,
+                           int64_t ldu, double* lambda);
+rsvd_status rsvd_spevd_host(rsvd_handle* h, int64_t n, const double* a, int64_t lda, int64_t k,
+                            int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
+                            double* lambda);
+/* spsvd_general(A, k, p, rng) (reference singlepass.hpp:109-137): Y_c = A
+ * Omega_c and W = A^T Psi in ONE fused pass.  U m x k, sigma k, V n x k. */
+rsvd_status rsvd_spsvd_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a, int64_t lda,
+                           int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
+                           double* sigma, double* v, int64_t ldv);
+rsvd_status rsvd_spsvd_host(rsvd_handle* h, int64_t m, int64_t n, const double* a, int64_t lda,
+                            int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
+                            double* sigma, double* v, int64_t ldv);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSVD_B200_H_ */

@@ -1,0 +1,640 @@
+"""rsvd-b200: B200-native randomized SVD (Algorithms 2-6 of arXiv:2402.17794).
+
+Python mirror of the reference's C++ API (namespace ``rsvd``,
+/root/reference/proj/include/rsvd/{sketch,rangefinder,factor,singlepass,core}.hpp)
+over the C ABI of ``lib/librsvd_b200.so`` (include/rsvd_b200.h).  Same names,
+argument meaning and exception types as the reference:
+
+    Rng(seed), gaussian(n, l, rng)                        sketch.hpp:19-59
+    orthonormalize, svd_small, evd_symmetric, solve_ls    core.hpp:96-177
+    fixed_rank_range, power_range, subspace_iter_range,
+    range_basis, SketchConfig, RangeMode                  rangefinder.hpp:13-105
+    rsvd, truncate, SvdApprox                             factor.hpp:12-34
+    CountingOperator, spevd_hermitian, spsvd_general      singlepass.hpp:15-137
+
+Matrices are column-major float64: either host numpy arrays or torch CUDA
+tensors (device-resident, zero-copy; a column-major tensor is a transposed
+contiguous tensor or any tensor with stride (1, ld)).  Results come back in the
+same kind as the input.  There is no CPU fallback: if the CUDA library is
+missing or no GPU is visible, calls raise ``EngineUnavailable``.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "DimensionError", "ParameterError", "NumericError", "EngineError", "EngineUnavailable",
+    "Rng", "RngState", "gaussian", "orthonormalize", "svd_small", "evd_symmetric", "solve_ls",
+    "solve_joint_core", "RangeMode", "SketchConfig", "fixed_rank_range", "power_range",
+    "subspace_iter_range", "range_basis", "SvdApprox", "EvdApprox", "rsvd", "truncate",
+    "CountingOperator", "spevd_hermitian", "spsvd_general", "apply", "apply_adjoint", "Engine",
+    "default_engine", "lib_path", "build",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "lib", "librsvd_b200.so")
+
+
+def lib_path() -> str:
+    return _LIB
+
+
+def build(quiet: bool = True) -> str:
+    """Compile csrc/ for sm_100a into lib/librsvd_b200.so (nvcc, in-tree)."""
+    import subprocess
+    cmd = ["make", "-j8", "-C", os.path.join(_HERE, "csrc")]
+    subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL if quiet else None)
+    return _LIB
+
+
+# ---------------------------------------------------------------- errors
+class DimensionError(ValueError):
+    """Bad shape (reference core.hpp:23-26, std::invalid_argument)."""
+
+
+class ParameterError(ValueError):
+    """Invalid parameter value (reference core.hpp:29-32, std::invalid_argument)."""
+
+
+class NumericError(RuntimeError):
+    """Numerical failure (reference core.hpp:35-39, std::runtime_error)."""
+
+
+class EngineError(RuntimeError):
+    """CUDA / NCCL / internal failure of the engine."""
+
+
+class EngineUnavailable(RuntimeError):
+    """The CUDA library or a GPU is missing (no CPU fallback exists)."""
+
+
+_STATUS = {1: DimensionError, 2: ParameterError, 3: NumericError, 4: EngineError, 5: EngineError,
+           9: EngineError}
+
+
+class RngState(ctypes.Structure):
+    """rsvd_rng_state: mt19937_64 vector + index + cached polar variate."""
+    _fields_ = [("mt", ctypes.c_uint64 * 312), ("pos", ctypes.c_uint64),
+                ("has_cached", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("cached", ctypes.c_double)]
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [("apply", ctypes.c_int64), ("adjoint", ctypes.c_int64),
+                ("physical_passes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB):
+            raise EngineUnavailable(f"{_LIB} not built (run __graft_entry__.build())")
+        L = ctypes.CDLL(_LIB)
+        P, I64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        PS = ctypes.POINTER(RngState)
+        sigs = {
+            "rsvd_create": [ctypes.POINTER(P), I],
+            "rsvd_nccl_unique_id": [P],
+            "rsvd_create_dist": [ctypes.POINTER(P), I, I, I, P],
+            "rsvd_set_stream": [P, P],
+            "rsvd_synchronize": [P],
+            "rsvd_get_counters": [P, ctypes.POINTER(Counters)],
+            "rsvd_reset_counters": [P],
+            "rsvd_dist_info": [P, ctypes.POINTER(I), ctypes.POINTER(I)],
+            "rsvd_gaussian_dev": [P, I64, I64, PS, P, I64],
+            "rsvd_orthonormalize_dev": [P, I64, I64, P, I64, P, I64],
+            "rsvd_svd_small_dev": [P, I64, I64, P, I64, P, I64, P, P, I64],
+            "rsvd_evd_symmetric_dev": [P, I64, P, I64, P, I64, P],
+            "rsvd_solve_ls_dev": [P, I64, I64, P, I64, I64, P, I64, P, I64],
+            "rsvd_solve_joint_core_dev": [P, I64, P, P, P, P, P],
+            "rsvd_apply_dev": [P, I64, I64, P, I64, I64, P, I64, P, I64],
+            "rsvd_apply_adjoint_dev": [P, I64, I64, P, I64, I64, P, I64, P, I64],
+            "rsvd_range_basis_dev": [P, I64, I64, P, I64, I64, I64, I, I, PS, P, I64],
+            "rsvd_rsvd_dev": [P, I64, I64, P, I64, I64, I64, I, I, PS, P, I64, P, P, I64],
+            "rsvd_rsvd_host": [P, I64, I64, P, I64, I64, I64, I, I, PS, P, I64, P, P, I64],
+            "rsvd_spevd_dev": [P, I64, P, I64, I64, I64, PS, I, P, I64, P],
+            "rsvd_spevd_host": [P, I64, P, I64, I64, I64, PS, P, I64, P],
+            "rsvd_spsvd_dev": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
+            "rsvd_spsvd_host": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
+        }
+        for name, argt in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = argt
+            f.restype = ctypes.c_int
+        L.rsvd_destroy.argtypes = [P]
+        L.rsvd_destroy.restype = None
+        L.rsvd_last_error.restype = ctypes.c_char_p
+        L.rsvd_version.restype = ctypes.c_char_p
+        L.rsvd_debug_log_cr.argtypes = [D]
+        L.rsvd_debug_log_cr.restype = D
+        _lib = L
+        return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _load().rsvd_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, EngineError)(msg)
+
+
+# ---------------------------------------------------------------- engine
+class Engine:
+    """Owns one rsvd_handle (one GPU; a row shard when created distributed)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        L = _load()
+        self._h = ctypes.c_void_p()
+        self.device = device
+        if nranks > 1:
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            _check(L.rsvd_create_dist(ctypes.byref(self._h), device, rank, nranks, buf))
+        else:
+            _check(L.rsvd_create(ctypes.byref(self._h), device))
+        self.rank, self.nranks = rank, nranks
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(_load().rsvd_nccl_unique_id(buf))
+        return buf.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _load().rsvd_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int) -> None:
+        _check(_load().rsvd_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
+
+    def counters(self) -> dict:
+        c = Counters()
+        _check(_load().rsvd_get_counters(self._h, ctypes.byref(c)))
+        return {"apply": c.apply, "adjoint": c.adjoint, "physical_passes": c.physical_passes,
+                "kernel_launches": c.kernel_launches}
+
+    def reset_counters(self) -> None:
+        _check(_load().rsvd_reset_counters(self._h))
+
+    def synchronize(self) -> None:
+        _check(_load().rsvd_synchronize(self._h))
+
+
+_engines: dict = {}
+_eng_lock = threading.Lock()
+
+
+def default_engine(device: Optional[int] = None) -> Engine:
+    import torch
+    if not torch.cuda.is_available():
+        raise EngineUnavailable("no CUDA device visible; the rsvd engine has no CPU fallback")
+    if device is None:
+        device = torch.cuda.current_device()
+    with _eng_lock:
+        e = _engines.get(device)
+        if e is None:
+            e = Engine(device)
+            _engines[device] = e
+        return e
+
+
+# ------------------------------------------------------------------- RNG
+_MT_F = 6364136223846793005
+_M64 = (1 << 64) - 1
+
+
+class Rng:
+    """The reference's rsvd::Rng (sketch.hpp:19-45): std::mt19937_64(seed)
+    feeding std::normal_distribution<double>, as an explicit state that the
+    device generator advances exactly like the host library would."""
+
+    def __init__(self, seed: int):
+        st = RngState()
+        x = seed & _M64
+        st.mt[0] = x
+        for i in range(1, 312):
+            x = (_MT_F * (x ^ (x >> 62)) + i) & _M64
+            st.mt[i] = x
+        st.pos = 312
+        st.has_cached = 0
+        st.cached = 0.0
+        self.state = st
+
+    @staticmethod
+    def identity() -> str:
+        return "mt19937_64/std-normal/v1"
+
+    @staticmethod
+    def for_trial(seed_base: int, trial: int) -> "Rng":
+        return Rng((seed_base + trial) & _M64)
+
+    def normal(self) -> float:
+        return float(gaussian(1, 1, self)[0, 0])
+
+    def copy(self) -> "Rng":
+        r = Rng.__new__(Rng)
+        r.state = RngState.from_buffer_copy(self.state)
+        return r
+
+
+# ---------------------------------------------------------- array plumbing
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+class _Dev:
+    """A device view (ptr, rows, cols, ld) of a numpy or torch input."""
+
+    def __init__(self, x, name="matrix"):
+        import torch
+        self.host = not _is_torch(x)
+        if self.host:
+            a = np.asarray(x, dtype=np.float64)
+            if a.ndim == 1:
+                a = a.reshape(-1, 1)
+            if a.ndim != 2:
+                raise DimensionError(f"{name}: expected a matrix")
+            self.rows, self.cols = a.shape
+            t = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()  # (cols, rows) row-major == col-major
+            self.t = t
+            self.ld = max(self.rows, 1)
+        else:
+            t = x
+            if t.dtype != torch.float64:
+                raise ParameterError(f"{name}: expected float64")
+            if t.ndim == 1:
+                t = t.reshape(-1, 1)
+            if not t.is_cuda:
+                return self.__init__(t.cpu().numpy(), name)
+            self.rows, self.cols = t.shape
+            if self.rows * self.cols > 0 and (t.stride(0) != 1 or t.stride(1) < max(self.rows, 1)):
+                t = t.t().contiguous().t()  # make column-major
+            self.t = t
+            self.ld = t.stride(1) if self.cols > 1 else max(self.rows, 1)
+            if self.cols == 1:
+                self.ld = max(self.rows, 1)
+        self.ptr = self.t.data_ptr()
+
+
+def _empty(rows, cols, like_host, device=None):
+    import torch
+    t = torch.empty((max(cols, 0), max(rows, 0)), dtype=torch.float64,
+                    device=device if device is not None else "cuda").t()
+    return t
+
+
+def _out(t, host: bool):
+    if host:
+        return np.asfortranarray(t.cpu().numpy())
+    return t
+
+
+def _vec_out(t, host: bool):
+    return t.cpu().numpy() if host else t
+
+
+def _eng(x=None) -> Engine:
+    import torch
+    dev = None
+    if x is not None and _is_torch(x) and x.is_cuda:
+        dev = x.device.index
+    e = default_engine(dev)
+    if dev is not None:
+        torch.cuda.set_device(dev)
+    e.set_stream(torch.cuda.current_stream().cuda_stream)
+    return e
+
+
+def _sync_torch():
+    import torch
+    torch.cuda.current_stream().synchronize()
+
+
+# ------------------------------------------------------------ sketch.hpp
+def gaussian(n: int, l: int, rng: Rng, *, device_out: bool = False):
+    """n x l i.i.d. N(0,1), column-major fill (reference sketch.hpp:48-59)."""
+    if n < 1 or l < 1:
+        raise ParameterError("gaussian: dimensions must be positive")
+    e = _eng()
+    out = _empty(n, l, True)
+    _check(_load().rsvd_gaussian_dev(e.handle, n, l, ctypes.byref(rng.state), out.data_ptr(),
+                                     max(n, 1)))
+    return out if device_out else np.asfortranarray(out.cpu().numpy())
+
+
+# -------------------------------------------------------------- core.hpp
+def orthonormalize(m):
+    """Householder-quality orthonormal basis, padded to full width
+    (reference core.hpp:96-105)."""
+    d = _Dev(m, "orthonormalize")
+    if d.cols > d.rows:
+        raise DimensionError(f"orthonormalize: more columns than rows ({d.cols} > {d.rows})")
+    e = _eng(None if d.host else m)
+    q = _empty(d.rows, d.cols, d.host)
+    if d.rows * d.cols:
+        _check(_load().rsvd_orthonormalize_dev(e.handle, d.rows, d.cols, d.ptr, d.ld,
+                                               q.data_ptr(), max(d.rows, 1)))
+    return _out(q, d.host)
+
+
+@dataclass
+class SvdApprox:
+    """U * diag(sigma) * V^T (reference core.hpp:43-53)."""
+    U: object
+    sigma: object
+    V: object
+
+    def factor_count(self) -> int:
+        return int(self.sigma.shape[0])
+
+    def reconstruct(self):
+        if _is_torch(self.U):
+            return (self.U * self.sigma) @ self.V.T
+        return (self.U * self.sigma) @ self.V.T
+
+
+@dataclass
+class EvdApprox:
+    """U * diag(lambda) * U^T (reference core.hpp:57-66)."""
+    U: object
+    lam: object
+
+    @property
+    def lambda_(self):
+        return self.lam
+
+    def factor_count(self) -> int:
+        return int(self.lam.shape[0])
+
+    def reconstruct(self):
+        return (self.U * self.lam) @ self.U.T
+
+
+def svd_small(m) -> SvdApprox:
+    """Thin SVD with the reference sign rule (core.hpp:111-124)."""
+    d = _Dev(m, "svd_small")
+    e = _eng(None if d.host else m)
+    r = min(d.rows, d.cols)
+    import torch
+    u, v = _empty(d.rows, r, d.host), _empty(d.cols, r, d.host)
+    s = torch.empty(max(r, 1), dtype=torch.float64, device="cuda")
+    if r:
+        _check(_load().rsvd_svd_small_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, u.data_ptr(),
+                                          max(d.rows, 1), s.data_ptr(), v.data_ptr(),
+                                          max(d.cols, 1)))
+    return SvdApprox(_out(u, d.host), _vec_out(s[:r], d.host), _out(v, d.host))
+
+
+def evd_symmetric(c) -> EvdApprox:
+    """Symmetric EVD ordered by |lambda| desc (core.hpp:130-162)."""
+    d = _Dev(c, "evd_symmetric")
+    if d.rows != d.cols:
+        raise DimensionError("evd_symmetric: matrix is not square")
+    e = _eng(None if d.host else c)
+    import torch
+    u = _empty(d.rows, d.rows, d.host)
+    lam = torch.empty(max(d.rows, 1), dtype=torch.float64, device="cuda")
+    if d.rows:
+        _check(_load().rsvd_evd_symmetric_dev(e.handle, d.rows, d.ptr, d.ld, u.data_ptr(),
+                                              max(d.rows, 1), lam.data_ptr()))
+    return EvdApprox(_out(u, d.host), _vec_out(lam[:d.rows], d.host))
+
+
+def solve_ls(g, h):
+    """Min-norm least squares, cutoff 1e-12 * sigma_max (core.hpp:166-177)."""
+    dg, dh = _Dev(g, "solve_ls"), _Dev(h, "solve_ls")
+    if dg.rows != dh.rows:
+        raise DimensionError(f"solve_ls: row counts differ ({dg.rows} vs {dh.rows})")
+    e = _eng(None if dg.host else g)
+    x = _empty(dg.cols, dh.cols, dg.host)
+    if dg.cols and dh.cols:
+        _check(_load().rsvd_solve_ls_dev(e.handle, dg.rows, dg.cols, dg.ptr, dg.ld, dh.cols,
+                                         dh.ptr, dh.ld, x.data_ptr(), max(dg.cols, 1)))
+    return _out(x, dg.host)
+
+
+def solve_joint_core(g1, h1, g2, h2):
+    """detail::solve_joint_core (singlepass.hpp:84-101), Kronecker route."""
+    ds = [_Dev(x, "solve_joint_core") for x in (g1, h1, g2, h2)]
+    l = ds[0].rows
+    for d in ds:
+        if d.rows != l or d.cols != l:
+            raise DimensionError("solve_joint_core: blocks must be l x l")
+    # the C ABI takes packed l x l blocks
+    import torch
+    packed = [d.t if d.ld == l else d.t.t().contiguous().t() for d in ds]
+    e = _eng(None if ds[0].host else g1)
+    c = _empty(l, l, ds[0].host)
+    _check(_load().rsvd_solve_joint_core_dev(e.handle, l, *[p.data_ptr() for p in packed],
+                                             c.data_ptr()))
+    return _out(c, ds[0].host)
+
+
+# ------------------------------------------------------- rangefinder.hpp
+class RangeMode(enum.IntEnum):
+    basic = 0
+    power = 1
+    power_ortho = 2
+
+
+def to_string(mode: RangeMode) -> str:
+    return {RangeMode.basic: "basic", RangeMode.power: "power", RangeMode.power_ortho: "ortho"}[mode]
+
+
+@dataclass
+class SketchConfig:
+    """Every Stage-1 tunable (rangefinder.hpp:30-42)."""
+    k: int = 1
+    p: int = 0
+    q: int = 0
+    mode: RangeMode = RangeMode.basic
+    seed: int = 0
+
+    def normalized(self) -> "SketchConfig":
+        c = SketchConfig(self.k, self.p, self.q, self.mode, self.seed)
+        if c.mode == RangeMode.basic:
+            c.q = 0
+        return c
+
+
+def range_basis(a, cfg: SketchConfig, rng: Rng):
+    """Dispatch on the Stage-1 variant (rangefinder.hpp:97-105)."""
+    c = cfg.normalized()
+    d = _Dev(a, "range_basis")
+    e = _eng(None if d.host else a)
+    l = c.k + c.p
+    q = _empty(d.rows, max(l, 0), d.host)
+    _check(_load().rsvd_range_basis_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, c.k, c.p, c.q,
+                                        int(c.mode), ctypes.byref(rng.state), q.data_ptr(),
+                                        max(d.rows, 1)))
+    return _out(q, d.host)
+
+
+def fixed_rank_range(a, k: int, p: int, rng: Rng):
+    """Alg 2 Stage 1 (rangefinder.hpp:60-65)."""
+    return range_basis(a, SketchConfig(k, p, 0, RangeMode.basic), rng)
+
+
+def power_range(a, k: int, p: int, q: int, rng: Rng):
+    """Alg 3 Stage 1 (rangefinder.hpp:70-79)."""
+    return range_basis(a, SketchConfig(k, p, q, RangeMode.power), rng)
+
+
+def subspace_iter_range(a, k: int, p: int, q: int, rng: Rng):
+    """Alg 4 Stage 1 (rangefinder.hpp:83-94)."""
+    return range_basis(a, SketchConfig(k, p, q, RangeMode.power_ortho), rng)
+
+
+# ------------------------------------------------------------ factor.hpp
+def rsvd(a, cfg: SketchConfig, rng: Optional[Rng] = None) -> SvdApprox:
+    """Two-stage randomized SVD, full width k+p (factor.hpp:12-24)."""
+    if rng is None:
+        rng = Rng(cfg.seed)
+    d = _Dev(a, "rsvd")
+    e = _eng(None if d.host else a)
+    import torch
+    l = max(cfg.k + cfg.p, 0)
+    u, v = _empty(d.rows, l, d.host), _empty(d.cols, l, d.host)
+    s = torch.empty(max(l, 1), dtype=torch.float64, device="cuda")
+    _check(_load().rsvd_rsvd_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, cfg.k, cfg.p, cfg.q,
+                                 int(cfg.mode), ctypes.byref(rng.state), u.data_ptr(),
+                                 max(d.rows, 1), s.data_ptr(), v.data_ptr(), max(d.cols, 1)))
+    return SvdApprox(_out(u, d.host), _vec_out(s[:l], d.host), _out(v, d.host))
+
+
+def truncate(f: SvdApprox, k: int) -> SvdApprox:
+    """Keep the first k factor triples (factor.hpp:27-34)."""
+    if k < 0 or k > f.factor_count():
+        raise DimensionError(f"truncate: k = {k} exceeds factor count {f.factor_count()}")
+    return SvdApprox(f.U[:, :k], f.sigma[:k], f.V[:, :k])
+
+
+# -------------------------------------------------------- singlepass.hpp
+class CountingOperator:
+    """Operator view counting block applications (singlepass.hpp:15-40).  The
+    engine counts the passes it makes over A; this wrapper exposes them."""
+
+    def __init__(self, a):
+        self._a = a
+        self.apply_count_ = 0
+        self.adjoint_count_ = 0
+
+    def matrix(self):
+        return self._a
+
+    def rows(self) -> int:
+        return int(self._a.shape[0])
+
+    def cols(self) -> int:
+        return int(self._a.shape[1])
+
+    def apply_count(self) -> int:
+        return self.apply_count_
+
+    def adjoint_count(self) -> int:
+        return self.adjoint_count_
+
+    def apply(self, x):
+        self.apply_count_ += 1
+        return apply(self._a, x)
+
+    def apply_adjoint(self, x):
+        self.adjoint_count_ += 1
+        return apply_adjoint(self._a, x)
+
+
+def _counted(a, fn):
+    op = a if isinstance(a, CountingOperator) else None
+    mat = op.matrix() if op else a
+    d = _Dev(mat, "operator")
+    e = _eng(None if d.host else mat)
+    before = e.counters()
+    res = fn(d, e)
+    after = e.counters()
+    if op is not None:
+        op.apply_count_ += after["apply"] - before["apply"]
+        op.adjoint_count_ += after["adjoint"] - before["adjoint"]
+    return res
+
+
+def spevd_hermitian(a, k: int, p: int, rng: Rng) -> EvdApprox:
+    """Single-pass symmetric EVD, Alg 5 (singlepass.hpp:45-78)."""
+    def run(d, e):
+        import torch
+        if d.rows != d.cols:
+            raise DimensionError("spevd_hermitian: matrix is not square")
+        u = _empty(d.rows, max(k, 0), d.host)
+        lam = torch.empty(max(k, 1), dtype=torch.float64, device="cuda")
+        _check(_load().rsvd_spevd_dev(e.handle, d.rows, d.ptr, d.ld, k, p, ctypes.byref(rng.state),
+                                      1, u.data_ptr(), max(d.rows, 1), lam.data_ptr()))
+        return EvdApprox(_out(u, d.host), _vec_out(lam[:max(k, 0)], d.host))
+    return _counted(a, run)
+
+
+def spsvd_general(a, k: int, p: int, rng: Rng) -> SvdApprox:
+    """Single-pass general SVD, Alg 6 (singlepass.hpp:109-137)."""
+    def run(d, e):
+        import torch
+        kk = max(k, 0)
+        u, v = _empty(d.rows, kk, d.host), _empty(d.cols, kk, d.host)
+        s = torch.empty(max(kk, 1), dtype=torch.float64, device="cuda")
+        _check(_load().rsvd_spsvd_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, k, p,
+                                      ctypes.byref(rng.state), u.data_ptr(), max(d.rows, 1),
+                                      s.data_ptr(), v.data_ptr(), max(d.cols, 1)))
+        return SvdApprox(_out(u, d.host), _vec_out(s[:kk], d.host), _out(v, d.host))
+    return _counted(a, run)
+
+
+# ------------------------------------------------------ streaming passes
+def apply(a, x):
+    """Y = A X on the DMMA pass engine."""
+    da, dx = _Dev(a, "apply"), _Dev(x, "apply")
+    if da.cols != dx.rows:
+        raise DimensionError("apply: inner dimensions differ")
+    e = _eng(None if da.host else a)
+    y = _empty(da.rows, dx.cols, da.host)
+    _check(_load().rsvd_apply_dev(e.handle, da.rows, da.cols, da.ptr, da.ld, dx.cols, dx.ptr,
+                                  dx.ld, y.data_ptr(), max(da.rows, 1)))
+    return _out(y, da.host)
+
+
+def apply_adjoint(a, y):
+    """Z = A^T Y on the DMMA pass engine."""
+    da, dy = _Dev(a, "apply_adjoint"), _Dev(y, "apply_adjoint")
+    if da.rows != dy.rows:
+        raise DimensionError("apply_adjoint: inner dimensions differ")
+    e = _eng(None if da.host else a)
+    z = _empty(da.cols, dy.cols, da.host)
+    _check(_load().rsvd_apply_adjoint_dev(e.handle, da.rows, da.cols, da.ptr, da.ld, dy.cols,
+                                          dy.ptr, dy.ld, z.data_ptr(), max(da.cols, 1)))
+    return _out(z, da.host)
+
+
+def debug_log_cr(x: float) -> float:
+    """Host evaluation of the device polar-sampler log (ddlog.cuh), for tests."""
+    return _load().rsvd_debug_log_cr(float(x))

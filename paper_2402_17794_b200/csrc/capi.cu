@@ -1,0 +1,358 @@
+// extern "C" boundary (include/rsvd_b200.h).  Every entry point: select the
+// handle's device, reset the per-call workspace, run the device pipeline on the
+// handle's stream, synchronize once, map internal errors to rsvd_status.
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "dist.cuh"
+#include "engine.cuh"
+#include "pass.cuh"
+#include "rng.cuh"
+#include "small.cuh"
+
+struct rsvd_handle {
+  rsvdb::Handle h;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
+  try {
+    if (!hd) throw rsvdb::Error(RSVD_ERR_PARAMETER, "null handle");
+    rsvdb::Handle& h = hd->h;
+    RSVD_CUDA(cudaSetDevice(h.device));
+    h.ws.reset();
+    h.rng_user_out = nullptr;
+    f(h);
+    rsvdb::finish_call(h, what);
+    return RSVD_OK;
+  } catch (const rsvdb::Error& e) {
+    g_err = e.what();
+    cudaGetLastError();  // clear a non-sticky runtime error so the next call starts clean
+    if (hd) {
+      hd->h.rng_user_out = nullptr;
+      cudaStreamSynchronize(hd->h.stream);
+      cudaMemsetAsync(hd->h.d_flags, 0, sizeof(int), hd->h.stream);
+    }
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RSVD_ERR_INTERNAL;
+  }
+}
+
+rsvdb::DMat dm(const double* p, int64_t r, int64_t c, int64_t ld) {
+  if (r < 0 || c < 0) throw rsvdb::Error(RSVD_ERR_DIMENSION, "negative dimension");
+  if (r > 0 && c > 0 && ld < r) throw rsvdb::Error(RSVD_ERR_DIMENSION, "leading dimension < rows");
+  return rsvdb::DMat(const_cast<double*>(p), r, c, ld);
+}
+
+rsvd_status create_impl(rsvd_handle** out, int device, int rank, int nranks, const void* id) {
+  try {
+    if (!out) throw rsvdb::Error(RSVD_ERR_PARAMETER, "null output handle");
+    auto* hd = new rsvd_handle;
+    rsvdb::Handle& h = hd->h;
+    h.device = device;
+    RSVD_CUDA(cudaSetDevice(device));
+    RSVD_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamNonBlocking));
+    h.stream = h.own_stream;
+    RSVD_CUDA(cudaMalloc(&h.d_flags, 64));
+    RSVD_CUDA(cudaMemset(h.d_flags, 0, 64));
+    RSVD_CUDA(cudaMallocHost(&h.h_flags, 64));
+    RSVD_CUDA(cudaMallocHost(&h.h_rng, sizeof(rsvd_rng_state)));
+    RSVD_CUDA(cudaDeviceGetAttribute(&h.sm_count, cudaDevAttrMultiProcessorCount, device));
+    rsvdb::rng_init_device(h);
+    rsvdb::comm_create(h, rank, nranks, id);
+    *out = hd;
+    return RSVD_OK;
+  } catch (const rsvdb::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RSVD_ERR_INTERNAL;
+  }
+}
+
+// Host-buffer wrapper: upload A, run, download outputs (the e2e path).
+struct HostIO {
+  rsvdb::Handle& h;
+  rsvdb::DMat up(const double* a, int64_t r, int64_t c, int64_t ld) {
+    rsvdb::DMat d = h.ws.mat(r, c);
+    if (r * c > 0)
+      RSVD_CUDA(cudaMemcpy2DAsync(d.p, d.ld * 8, a, ld * 8, r * 8, c, cudaMemcpyHostToDevice,
+                                  h.stream));
+    return d;
+  }
+  void down(const rsvdb::DMat& d, double* a, int64_t ld) {
+    if (d.rows * d.cols > 0)
+      RSVD_CUDA(cudaMemcpy2DAsync(a, ld * 8, d.p, d.ld * 8, d.rows * 8, d.cols,
+                                  cudaMemcpyDeviceToHost, h.stream));
+  }
+  void down_vec(const double* d, double* a, int64_t n) {
+    if (n > 0) RSVD_CUDA(cudaMemcpyAsync(a, d, size_t(n) * 8, cudaMemcpyDeviceToHost, h.stream));
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* rsvd_last_error(void) { return g_err.c_str(); }
+const char* rsvd_version(void) { return "rsvd-b200 0.1.0 (reference rsvd 0.1.0 API)"; }
+
+rsvd_status rsvd_create(rsvd_handle** h, int device) {
+  return create_impl(h, device, 0, 1, nullptr);
+}
+
+rsvd_status rsvd_nccl_unique_id(void* out128) {
+  try {
+    rsvdb::nccl_unique_id(out128);
+    return RSVD_OK;
+  } catch (const rsvdb::Error& e) {
+    g_err = e.what();
+    return e.code;
+  }
+}
+
+rsvd_status rsvd_create_dist(rsvd_handle** h, int device, int rank, int nranks,
+                             const void* nccl_id128) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) {
+    g_err = "rsvd_create_dist: bad rank/nranks";
+    return RSVD_ERR_PARAMETER;
+  }
+  if (nranks > 1 && !nccl_id128) {
+    g_err = "rsvd_create_dist: null NCCL id";
+    return RSVD_ERR_PARAMETER;
+  }
+  return create_impl(h, device, rank, nranks, nccl_id128);
+}
+
+void rsvd_destroy(rsvd_handle* hd) {
+  if (!hd) return;
+  rsvdb::Handle& h = hd->h;
+  cudaSetDevice(h.device);
+  cudaStreamSynchronize(h.stream);
+  rsvdb::comm_destroy(h);
+  if (h.d_counters) cudaFree(h.d_counters);
+  if (h.d_flags) cudaFree(h.d_flags);
+  if (h.h_flags) cudaFreeHost(h.h_flags);
+  if (h.h_rng) cudaFreeHost(h.h_rng);
+  if (h.own_stream) cudaStreamDestroy(h.own_stream);
+  delete hd;
+}
+
+rsvd_status rsvd_set_stream(rsvd_handle* hd, void* s) {
+  if (!hd) return RSVD_ERR_PARAMETER;
+  hd->h.stream = s ? static_cast<cudaStream_t>(s) : hd->h.own_stream;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_synchronize(rsvd_handle* hd) {
+  if (!hd) return RSVD_ERR_PARAMETER;
+  return cudaStreamSynchronize(hd->h.stream) == cudaSuccess ? RSVD_OK : RSVD_ERR_CUDA;
+}
+
+rsvd_status rsvd_get_counters(rsvd_handle* hd, rsvd_counters* out) {
+  if (!hd || !out) return RSVD_ERR_PARAMETER;
+  *out = hd->h.counters;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_reset_counters(rsvd_handle* hd) {
+  if (!hd) return RSVD_ERR_PARAMETER;
+  hd->h.counters = rsvd_counters{};
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_dist_info(rsvd_handle* hd, int* rank, int* nranks) {
+  if (!hd) return RSVD_ERR_PARAMETER;
+  if (rank) *rank = hd->h.rank;
+  if (nranks) *nranks = hd->h.nranks;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_gaussian_dev(rsvd_handle* hd, int64_t n, int64_t l, rsvd_rng_state* rng,
+                              double* out, int64_t ld) {
+  return guard(hd, "gaussian", [&](rsvdb::Handle& h) {
+    if (n < 1 || l < 1) rsvdb::throw_param("gaussian: dimensions must be positive");
+    if (!rng) rsvdb::throw_param("gaussian: null rng");
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::gaussian_dev(h, n, l, r, dm(out, n, l, ld));
+    rsvdb::rng_download(h, r, rng);
+  });
+}
+
+rsvd_status rsvd_orthonormalize_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* in,
+                                    int64_t ld_in, double* q, int64_t ld_q) {
+  return guard(hd, "orthonormalize", [&](rsvdb::Handle& h) {
+    rsvdb::orthonormalize(h, dm(in, m, n, ld_in), dm(q, m, n, ld_q));
+  });
+}
+
+rsvd_status rsvd_svd_small_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                               int64_t lda, double* u, int64_t ldu, double* s, double* v,
+                               int64_t ldv) {
+  return guard(hd, "svd_small", [&](rsvdb::Handle& h) {
+    const int64_t r = std::min(m, n);
+    if (r == 0) return;
+    rsvdb::svd_small_impl(h, dm(a, m, n, lda), dm(u, m, r, ldu), s, dm(v, n, r, ldv));
+  });
+}
+
+rsvd_status rsvd_evd_symmetric_dev(rsvd_handle* hd, int64_t n, const double* c, int64_t ldc,
+                                   double* u, int64_t ldu, double* lambda) {
+  return guard(hd, "evd_symmetric", [&](rsvdb::Handle& h) {
+    if (n == 0) return;
+    rsvdb::evd_symmetric_impl(h, dm(c, n, n, ldc), dm(u, n, n, ldu), lambda);
+  });
+}
+
+rsvd_status rsvd_solve_ls_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* g,
+                              int64_t ldg, int64_t r, const double* hm, int64_t ldh, double* x,
+                              int64_t ldx) {
+  return guard(hd, "solve_ls", [&](rsvdb::Handle& h) {
+    if (n == 0 || r == 0) return;
+    rsvdb::solve_ls_impl(h, dm(g, m, n, ldg), dm(hm, m, r, ldh), dm(x, n, r, ldx));
+  });
+}
+
+rsvd_status rsvd_solve_joint_core_dev(rsvd_handle* hd, int64_t l, const double* g1,
+                                      const double* h1, const double* g2, const double* h2,
+                                      double* c) {
+  return guard(hd, "solve_joint_core", [&](rsvdb::Handle& h) {
+    if (l < 1) rsvdb::throw_dim("solve_joint_core: l must be >= 1");
+    rsvdb::solve_joint_core_impl(h, dm(g1, l, l, l), dm(h1, l, l, l), dm(g2, l, l, l),
+                                 dm(h2, l, l, l), dm(c, l, l, l));
+  });
+}
+
+rsvd_status rsvd_apply_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
+                           int64_t l, const double* x, int64_t ldx, double* y, int64_t ldy) {
+  return guard(hd, "apply", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P;
+    P.A = dm(a, m, n, lda);
+    rsvdb::op_apply(h, P, dm(x, n, l, ldx), dm(y, m, l, ldy));
+  });
+}
+
+rsvd_status rsvd_apply_adjoint_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                   int64_t lda, int64_t l, const double* y, int64_t ldy,
+                                   double* z, int64_t ldz) {
+  return guard(hd, "apply_adjoint", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P;
+    P.A = dm(a, m, n, lda);
+    P.dist = h.nranks > 1;
+    rsvdb::op_adjoint(h, P, dm(y, m, l, ldy), dm(z, n, l, ldz));
+  });
+}
+
+rsvd_status rsvd_range_basis_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                 int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                 rsvd_rng_state* rng, double* q_out, int64_t ldq) {
+  return guard(hd, "range_basis", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::range_basis_impl(h, P, k, p, q, mode, r, dm(q_out, m, std::max<int64_t>(k + p, 0), ldq));
+    rsvdb::rng_download(h, r, rng);
+  });
+}
+
+rsvd_status rsvd_rsvd_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
+                          int64_t k, int64_t p, int q, int mode, rsvd_rng_state* rng, double* u,
+                          int64_t ldu, double* sigma, double* v, int64_t ldv) {
+  return guard(hd, "rsvd", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
+    const int64_t l = std::max<int64_t>(k + p, 0);
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::rsvd_impl(h, P, k, p, q, mode, r, dm(u, m, l, ldu), sigma, dm(v, n, l, ldv));
+    rsvdb::rng_download(h, r, rng);
+  });
+}
+
+rsvd_status rsvd_rsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
+                           int64_t k, int64_t p, int q, int mode, rsvd_rng_state* rng, double* u,
+                           int64_t ldu, double* sigma, double* v, int64_t ldv) {
+  return guard(hd, "rsvd", [&](rsvdb::Handle& h) {
+    HostIO io{h};
+    rsvdb::DMat A = io.up(a, m, n, lda);
+    rsvdb::Problem P = rsvdb::make_problem(h, A.p, m, n, A.ld);
+    const int64_t l = std::max<int64_t>(k + p, 0);
+    rsvdb::DMat U = h.ws.mat(m, l), V = h.ws.mat(n, l);
+    double* s = h.ws.alloc(std::max<int64_t>(l, 1));
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::rsvd_impl(h, P, k, p, q, mode, r, U, s, V);
+    rsvdb::rng_download(h, r, rng);
+    io.down(U, u, ldu);
+    io.down_vec(s, sigma, l);
+    io.down(V, v, ldv);
+  });
+}
+
+rsvd_status rsvd_spevd_dev(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
+                           int64_t p, rsvd_rng_state* rng, int check_symmetry, double* u,
+                           int64_t ldu, double* lambda) {
+  return guard(hd, "spevd_hermitian", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P = rsvdb::make_problem(h, a, n, n, lda);
+    // local rows: for a single GPU m_local == n
+    P.A = dm(a, P.A.rows, n, lda);
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::spevd_impl(h, P, k, p, r, check_symmetry != 0,
+                      dm(u, P.A.rows, std::max<int64_t>(k, 0), ldu), lambda);
+    rsvdb::rng_download(h, r, rng);
+  });
+}
+
+rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
+                            int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
+                            double* lambda) {
+  return guard(hd, "spevd_hermitian", [&](rsvdb::Handle& h) {
+    HostIO io{h};
+    rsvdb::DMat A = io.up(a, n, n, lda);
+    rsvdb::Problem P = rsvdb::make_problem(h, A.p, n, n, A.ld);
+    const int64_t kk = std::max<int64_t>(k, 0);
+    rsvdb::DMat U = h.ws.mat(n, kk);
+    double* lam = h.ws.alloc(std::max<int64_t>(kk, 1));
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::spevd_impl(h, P, k, p, r, true, U, lam);
+    rsvdb::rng_download(h, r, rng);
+    io.down(U, u, ldu);
+    io.down_vec(lam, lambda, kk);
+  });
+}
+
+rsvd_status rsvd_spsvd_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
+                           int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
+                           double* sigma, double* v, int64_t ldv) {
+  return guard(hd, "spsvd_general", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
+    const int64_t kk = std::max<int64_t>(k, 0);
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::spsvd_impl(h, P, k, p, r, dm(u, m, kk, ldu), sigma, dm(v, n, kk, ldv));
+    rsvdb::rng_download(h, r, rng);
+  });
+}
+
+rsvd_status rsvd_spsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
+                            int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
+                            double* sigma, double* v, int64_t ldv) {
+  return guard(hd, "spsvd_general", [&](rsvdb::Handle& h) {
+    HostIO io{h};
+    rsvdb::DMat A = io.up(a, m, n, lda);
+    rsvdb::Problem P = rsvdb::make_problem(h, A.p, m, n, A.ld);
+    const int64_t kk = std::max<int64_t>(k, 0);
+    rsvdb::DMat U = h.ws.mat(m, kk), V = h.ws.mat(n, kk);
+    double* s = h.ws.alloc(std::max<int64_t>(kk, 1));
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::spsvd_impl(h, P, k, p, r, U, s, V);
+    rsvdb::rng_download(h, r, rng);
+    io.down(U, u, ldu);
+    io.down_vec(s, sigma, kk);
+    io.down(V, v, ldv);
+  });
+}
+
+}  // extern "C"

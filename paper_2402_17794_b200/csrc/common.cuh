@@ -1,0 +1,110 @@
+// Shared plumbing of the B200 rsvd engine: error model, handle, workspace.
+//
+// Error model mirrors the reference (core.hpp:23-39): internal C++ exceptions
+// of three kinds are mapped to rsvd_status at the C-ABI boundary (capi.cu)
+// and rethrown as rsvd::DimensionError / ParameterError / NumericError by
+// include/rsvd/*.hpp.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rsvd_b200.h"
+
+namespace rsvdb {
+
+struct Error : std::runtime_error {
+  rsvd_status code;
+  Error(rsvd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void throw_dim(const std::string& m) { throw Error(RSVD_ERR_DIMENSION, m); }
+[[noreturn]] inline void throw_param(const std::string& m) { throw Error(RSVD_ERR_PARAMETER, m); }
+[[noreturn]] inline void throw_numeric(const std::string& m) { throw Error(RSVD_ERR_NUMERIC, m); }
+
+#define RSVD_CUDA(x)                                                                       \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::rsvdb::Error(RSVD_ERR_CUDA, std::string(#x " failed: ") + cudaGetErrorString(e_) + \
+                                              " at " __FILE__ ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+#define RSVD_LAUNCH_CHECK() RSVD_CUDA(cudaGetLastError())
+// Every kernel launch of the engine goes through this: error check + count
+// (rsvd_counters.kernel_launches, reported by bench.py as gpu_launches).
+#define RSVD_LAUNCHED(hh)    \
+  do {                       \
+    RSVD_LAUNCH_CHECK();     \
+    (hh).counters.kernel_launches++; \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Device matrix view (column-major).
+struct DMat {
+  double* p = nullptr;
+  int64_t rows = 0, cols = 0, ld = 0;
+  DMat() = default;
+  DMat(double* ptr, int64_t r, int64_t c, int64_t l) : p(ptr), rows(r), cols(c), ld(l) {}
+  double* col(int64_t j) const { return p + j * ld; }
+};
+
+// Chunked device arena with a bump allocator.  reset() runs at the start of
+// every top-level C-ABI call; every call ends with a stream synchronization, so
+// no kernel of the previous call can still be using the memory.  A call that
+// outgrows the current chunk gets a new chunk; at the next reset the chunks
+// are merged into one allocation of the high-water size.
+class Arena {
+ public:
+  ~Arena();
+  void reset();
+  void* alloc_bytes(size_t bytes);
+  double* alloc(int64_t n) { return static_cast<double*>(alloc_bytes(sizeof(double) * size_t(n))); }
+  DMat mat(int64_t r, int64_t c) {
+    const int64_t ld = round_up(r < 2 ? 2 : r, 2);  // even ld keeps TMA strides 16B aligned
+    return DMat(alloc(ld * c), r, c, ld);
+  }
+  size_t high_water() const { return high_; }
+
+ private:
+  struct Chunk {
+    char* p;
+    size_t cap, off;
+  };
+  std::vector<Chunk> chunks_;
+  size_t used_total_ = 0, high_ = 0;
+};
+
+struct Comm;  // NCCL communicator wrapper (dist.cu)
+
+struct Handle {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  Arena ws;
+  int* d_counters = nullptr;   // split-K tile semaphores (kept zeroed)
+  int64_t n_counters = 0;
+  int* d_flags = nullptr;      // device status flags (non-finite, breakdown)
+  int* h_flags = nullptr;      // pinned mirror
+  int sm_count = 148;
+  rsvd_counters counters{};
+  Comm* comm = nullptr;        // null => single GPU
+  int rank = 0, nranks = 1;
+  // pinned staging for the RNG state copy-back (rng.cu)
+  void* h_rng = nullptr;
+  rsvd_rng_state* rng_user_out = nullptr;
+};
+
+// End of a top-level call: synchronize, raise NumericError on device flags,
+// copy back a pending RNG state.
+void finish_call(Handle& h, const char* what);
+
+// Split-K semaphores, at least n of them.
+int* tile_counters(Handle& h, int64_t n);
+
+}  // namespace rsvdb

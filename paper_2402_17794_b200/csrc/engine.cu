@@ -1,0 +1,415 @@
+// Pipelines of the rsvd hot path on B200, restating the reference's
+// algorithms statement by statement on device-resident data:
+//   range finders  rangefinder.hpp:60-105   (Alg 2 / 3 / 4, Stage 1)
+//   rsvd           factor.hpp:12-24         (Stage 2)
+//   svd_small      core.hpp:111-124, solve_ls core.hpp:166-177,
+//   evd_symmetric  core.hpp:130-162
+//   spevd_hermitian singlepass.hpp:45-78    (Alg 5, one pass over A)
+//   spsvd_general   singlepass.hpp:109-137  (Alg 6, solve_joint_core :84-101)
+// A is row-sharded when the handle spans several GPUs: products with A are
+// local, and only the n x l / l x l partials are NCCL-allreduced (dist.cu).
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "dist.cuh"
+#include "engine.cuh"
+#include "pass.cuh"
+#include "rng.cuh"
+#include "small.cuh"
+
+namespace rsvdb {
+
+// ------------------------------------------------------------------ arena
+Arena::~Arena() {
+  for (auto& c : chunks_) cudaFree(c.p);
+}
+
+void Arena::reset() {
+  size_t cap = 0;
+  for (auto& c : chunks_) cap += c.cap;
+  if (chunks_.size() > 1 || (chunks_.size() == 1 && chunks_[0].cap < high_)) {
+    for (auto& c : chunks_) cudaFree(c.p);
+    chunks_.clear();
+    Chunk c{nullptr, size_t(round_up(int64_t(high_), int64_t(1) << 20)), 0};
+    RSVD_CUDA(cudaMalloc(&c.p, c.cap));
+    chunks_.push_back(c);
+  }
+  for (auto& c : chunks_) c.off = 0;
+  used_total_ = 0;
+  (void)cap;
+}
+
+void* Arena::alloc_bytes(size_t bytes) {
+  bytes = size_t(round_up(int64_t(std::max<size_t>(bytes, 1)), 256));
+  if (chunks_.empty() || chunks_.back().off + bytes > chunks_.back().cap) {
+    size_t want = std::max<size_t>(bytes, size_t(64) << 20);
+    if (!chunks_.empty()) want = std::max(want, 2 * chunks_.back().cap);
+    Chunk c{nullptr, want, 0};
+    cudaError_t e = cudaMalloc(&c.p, c.cap);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c.cap = bytes;
+      RSVD_CUDA(cudaMalloc(&c.p, c.cap));
+    }
+    chunks_.push_back(c);
+  }
+  Chunk& c = chunks_.back();
+  void* p = c.p + c.off;
+  c.off += bytes;
+  used_total_ += bytes;
+  high_ = std::max(high_, used_total_);
+  return p;
+}
+
+int* tile_counters(Handle& h, int64_t n) {
+  if (n > h.n_counters) {
+    if (h.d_counters) {
+      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      RSVD_CUDA(cudaFree(h.d_counters));
+    }
+    const int64_t cap = std::max<int64_t>(n, 4096);
+    RSVD_CUDA(cudaMalloc(&h.d_counters, size_t(cap) * sizeof(int)));
+    RSVD_CUDA(cudaMemsetAsync(h.d_counters, 0, size_t(cap) * sizeof(int), h.stream));
+    h.n_counters = cap;
+  }
+  return h.d_counters;
+}
+
+void finish_call(Handle& h, const char* what) {
+  rsvd_rng_state* user = h.rng_user_out;
+  h.rng_user_out = nullptr;
+  check_flags(h, what);  // synchronizes
+  if (user) std::memcpy(user, h.h_rng, sizeof(rsvd_rng_state));
+}
+
+namespace {
+
+// ------------------------------------------------------- small kernels
+// Rows i of T scaled by 1/s_i, or zeroed when s_i < max(1e-12 s_max, DBL_MIN)
+// (Eigen SVDBase::rank threshold as used by solve_ls, core.hpp:164-176).
+__global__ void pinv_rows_kernel(double* T, int64_t rows, int64_t cols, int64_t ld,
+                                 const double* s) {
+  const double thr = fmax(s[0] * 1e-12, DBL_MIN);
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    const double si = s[i];
+    T[j * ld + i] = (si >= thr) ? T[j * ld + i] / si : 0.0;
+  }
+}
+
+// Kronecker-diagonalised joint core: X_ij = (s1_i a_ij + s2_j b_ij) / (s1_i^2 + s2_j^2),
+// zero where sqrt(s1_i^2 + s2_j^2) < 1e-12 * sqrt(s1_0^2 + s2_0^2).
+__global__ void kron_core_kernel(const double* a, const double* b, int64_t l, int64_t lda,
+                                 const double* s1, const double* s2, double* X, int64_t ldx) {
+  const double smax = sqrt(s1[0] * s1[0] + s2[0] * s2[0]);
+  const double thr = fmax(smax * 1e-12, DBL_MIN);
+  const int64_t n = l * l;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % l, j = e / l;
+    const double x1 = s1[i], x2 = s2[j];
+    const double den = x1 * x1 + x2 * x2;
+    X[j * ldx + i] =
+        (sqrt(den) < thr) ? 0.0 : (x1 * a[j * lda + i] + x2 * b[j * lda + i]) / den;
+  }
+}
+
+// max|A| and max|A - A^T| over an n x n matrix, one read of A (tile pairs).
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), __double_as_longlong(v));
+}
+__global__ void asym_kernel(const double* __restrict__ A, int64_t n, int64_t lda, double* out) {
+  // blockIdx.x enumerates tile pairs (bi <= bj) of the upper triangle
+  const int64_t nt = (n + 31) / 32;
+  int64_t t = blockIdx.x, bi = 0;
+  while (t >= nt - bi) {
+    t -= nt - bi;
+    ++bi;
+  }
+  const int64_t bj = bi + t;
+  __shared__ double T1[32][33], T2[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += blockDim.y) {
+    const int64_t r1 = bi * 32 + tx, c1 = bj * 32 + k;  // tile (bi, bj)
+    T1[k][tx] = (r1 < n && c1 < n) ? A[c1 * lda + r1] : 0.0;
+    const int64_t r2 = bj * 32 + tx, c2 = bi * 32 + k;  // tile (bj, bi)
+    T2[k][tx] = (r2 < n && c2 < n) ? A[c2 * lda + r2] : 0.0;
+  }
+  __syncthreads();
+  double mabs = 0.0, masym = 0.0;
+  for (int k = ty; k < 32; k += blockDim.y) {
+    // element (i = bi*32+tx, j = bj*32+k) vs (j, i) = T2[tx][k]
+    const double a = T1[k][tx], b = T2[tx][k];
+    mabs = fmax(mabs, fmax(fabs(a), fabs(b)));
+    masym = fmax(masym, fabs(a - b));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+    masym = fmax(masym, __shfl_xor_sync(0xffffffffu, masym, o));
+  }
+  if (tx == 0) {
+    atomic_max_nonneg(&out[0], mabs);
+    atomic_max_nonneg(&out[1], masym);
+  }
+}
+__global__ void asym_flag_kernel(const double* mm, int* flags, int bit) {
+  if (!(mm[1] <= 1e-8 * (1.0 + mm[0]))) atomicOr(flags, bit);
+}
+
+int grid_for(int64_t n, const Handle& h) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 4 * h.sm_count)));
+}
+
+}  // namespace
+
+// Asymmetry precondition (core.hpp:135-140 / singlepass.hpp:49-53).
+void check_symmetric(Handle& h, const DMat& C, bool dist_unused) {
+  (void)dist_unused;
+  const int64_t n = C.rows;
+  if (n == 0) return;
+  double* mm = h.ws.alloc(2);
+  RSVD_CUDA(cudaMemsetAsync(mm, 0, 16, h.stream));
+  const int64_t nt = ceil_div(n, 32);
+  asym_kernel<<<unsigned(nt * (nt + 1) / 2), dim3(32, 8), 0, h.stream>>>(C.p, n, C.ld, mm);
+  RSVD_LAUNCHED(h);
+  asym_flag_kernel<<<1, 1, 0, h.stream>>>(mm, h.d_flags, kFlagAsymmetric);
+  RSVD_LAUNCHED(h);
+}
+
+// ------------------------------------------------------------ operators
+void op_apply(Handle& h, const Problem& P, const DMat& X, DMat Y) {
+  gemm_nn(h, P.A, X, Y);
+  h.counters.apply++;
+  h.counters.physical_passes++;
+}
+
+void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z) {
+  gemm_tn(h, P.A, Y, Z);
+  if (P.dist) allreduce_mat(h, Z);
+  h.counters.adjoint++;
+  h.counters.physical_passes++;
+}
+
+Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda) {
+  Problem P;
+  P.A = DMat(const_cast<double*>(a), m, n, lda);
+  P.dist = h.nranks > 1;
+  shard_rows(h, m, &P.m_global, &P.row_off);
+  return P;
+}
+
+// ------------------------------------------------- svd_small / solve_ls
+// Square l x l:  M J = W S  =>  M = W S J^T  (U = W, V = J).
+// Tall m > n:    M = Q R, R J = W S  =>  U = Q W, V = J.
+// Wide m < n:    M^T = Q R, R J = W S =>  U = J, V = Q W.
+void svd_core(Handle& h, const DMat& M, DMat U, double* s, DMat V) {
+  const int64_t m = M.rows, n = M.cols;
+  if (m == n) {
+    jacobi_svd_square(h, M, V, U, s);
+  } else if (m > n) {
+    DMat Qm = h.ws.mat(m, n), R = h.ws.mat(n, n), W = h.ws.mat(n, n);
+    orthonormalize(h, M, Qm, &R);
+    jacobi_svd_square(h, R, V, W, s);
+    gemm_nn(h, Qm, W, U);
+  } else {
+    DMat Mt = h.ws.mat(n, m), Qm = h.ws.mat(n, m), R = h.ws.mat(m, m), W = h.ws.mat(m, m);
+    transpose(h, M, Mt);
+    orthonormalize(h, Mt, Qm, &R);
+    jacobi_svd_square(h, R, U, W, s);
+    gemm_nn(h, Qm, W, V);
+  }
+}
+
+void svd_small_impl(Handle& h, const DMat& M, DMat U, double* s, DMat V) {
+  check_finite(h, M, kFlagNonFinite);
+  svd_core(h, M, U, s, V);
+  sign_rule(h, U, &V);
+}
+
+void solve_ls_impl(Handle& h, const DMat& G, const DMat& Hm, DMat X) {
+  const int64_t m = G.rows, n = G.cols, r = Hm.cols;
+  check_finite(h, G, kFlagNonFinite);
+  check_finite(h, Hm, kFlagNonFinite);
+  const int64_t k = std::min(m, n);
+  DMat U = h.ws.mat(m, k), V = h.ws.mat(n, k);
+  double* s = h.ws.alloc(k);
+  svd_core(h, G, U, s, V);
+  DMat T = h.ws.mat(k, r);
+  gemm_tn(h, U, Hm, T);  // U^T H
+  pinv_rows_kernel<<<grid_for(k * r, h), 256, 0, h.stream>>>(T.p, k, r, T.ld, s);
+  RSVD_LAUNCHED(h);
+  gemm_nn(h, V, T, X);
+}
+
+void evd_symmetric_impl(Handle& h, const DMat& C, DMat U, double* lambda) {
+  check_finite(h, C, kFlagNonFinite);
+  check_symmetric(h, C, false);
+  DMat S = h.ws.mat(C.rows, C.rows);
+  sym_part(h, C, S);
+  jacobi_evd_sym(h, S, U, lambda);
+}
+
+void solve_joint_core_impl(Handle& h, const DMat& G1, const DMat& H1, const DMat& G2,
+                           const DMat& H2, DMat C) {
+  const int64_t l = G1.rows;
+  for (const DMat* x : {&G1, &H1, &G2, &H2}) check_finite(h, *x, kFlagNonFinite);
+  DMat U1 = h.ws.mat(l, l), V1 = h.ws.mat(l, l), U2 = h.ws.mat(l, l), V2 = h.ws.mat(l, l);
+  double* s1 = h.ws.alloc(l);
+  double* s2 = h.ws.alloc(l);
+  jacobi_svd_square(h, G1, V1, U1, s1);  // G1 V1 = U1 S1
+  jacobi_svd_square(h, G2, V2, U2, s2);
+  DMat T = h.ws.mat(l, l), a = h.ws.mat(l, l), b = h.ws.mat(l, l), X = h.ws.mat(l, l);
+  gemm_tn(h, U1, H1, T);  // U1^T H1
+  gemm_nn(h, T, U2, a);   // (U1^T H1) U2
+  gemm_tn(h, V1, H2, T);  // V1^T H2
+  gemm_nn(h, T, V2, b);   // (V1^T H2) V2
+  kron_core_kernel<<<grid_for(l * l, h), 256, 0, h.stream>>>(a.p, b.p, l, a.ld, s1, s2, X.p, X.ld);
+  RSVD_LAUNCHED(h);
+  DMat U2t = h.ws.mat(l, l);
+  transpose(h, U2, U2t);
+  gemm_nn(h, V1, X, T);   // V1 X
+  gemm_nn(h, T, U2t, C);  // V1 X U2^T
+}
+
+// -------------------------------------------------------- range finders
+static void check_sketch_shape(const Problem& P, int64_t k, int64_t p, int q) {
+  if (k < 1) throw_param("target rank k must be >= 1");
+  if (p < 0) throw_param("oversampling p must be >= 0");
+  if (q < 0) throw_param("power steps q must be >= 0");
+  const int64_t mn = std::min(P.m_global, P.A.cols);
+  if (k + p > mn)
+    throw_dim("k+p = " + std::to_string(k + p) + " exceeds min(m,n) = " + std::to_string(mn));
+}
+
+void range_basis_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, int mode,
+                      DevRng& rng, DMat Q) {
+  if (mode == RSVD_MODE_BASIC) q = 0;  // SketchConfig::normalized (rangefinder.hpp:37-41)
+  if (mode < 0 || mode > 2) throw_param("unknown range mode");
+  check_sketch_shape(P, k, p, q);
+  const int64_t n = P.A.cols, ml = P.A.rows, l = k + p;
+  DMat Omega = h.ws.mat(n, l);
+  gaussian_dev(h, n, l, rng, Omega);
+  DMat Y = h.ws.mat(ml, l);
+  op_apply(h, P, Omega, Y);  // Y = A Omega
+  if (mode == RSVD_MODE_POWER) {
+    DMat Z = h.ws.mat(n, l);
+    for (int j = 0; j < q; ++j) {  // rangefinder.hpp:74-77
+      op_adjoint(h, P, Y, Z);
+      op_apply(h, P, Z, Y);
+    }
+    orthonormalize(h, Y, Q, nullptr, P.dist);
+  } else if (mode == RSVD_MODE_POWER_ORTHO) {
+    orthonormalize(h, Y, Q, nullptr, P.dist);
+    DMat Z = h.ws.mat(n, l), W = h.ws.mat(n, l);
+    for (int j = 0; j < q; ++j) {  // rangefinder.hpp:89-92
+      op_adjoint(h, P, Q, Z);
+      orthonormalize(h, Z, W, nullptr, false);  // replicated n x l
+      op_apply(h, P, W, Y);
+      orthonormalize(h, Y, Q, nullptr, P.dist);
+    }
+  } else {
+    orthonormalize(h, Y, Q, nullptr, P.dist);
+  }
+}
+
+void rsvd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, int mode, DevRng& rng,
+               DMat U, double* sigma, DMat V) {
+  const int64_t n = P.A.cols, ml = P.A.rows, l = k + p;
+  check_sketch_shape(P, k, p, mode == RSVD_MODE_BASIC ? 0 : q);
+  DMat Q = h.ws.mat(ml, l);
+  range_basis_impl(h, P, k, p, q, mode, rng, Q);
+  // Stage 2 (factor.hpp:14-16): B = Q^T A is formed transposed, Z = A^T Q.
+  DMat Z = h.ws.mat(n, l);
+  op_adjoint(h, P, Q, Z);
+  // svd_small(B), B = Z^T (l x n, n >= l): Z = Qb Rb, Rb J = W S
+  //   => B = J S (Qb W)^T, U_B = J, V = Qb W.
+  DMat Qb = h.ws.mat(n, l), Rb = h.ws.mat(l, l), J = h.ws.mat(l, l), W = h.ws.mat(l, l);
+  orthonormalize(h, Z, Qb, &Rb, false);
+  jacobi_svd_square(h, Rb, J, W, sigma);
+  gemm_nn(h, Qb, W, V);
+  sign_rule(h, J, &V);  // core.hpp:115-122 on U_B, flip propagated to V
+  gemm_nn(h, Q, J, U);  // U = Q U_B
+}
+
+// --------------------------------------------------------- single pass
+void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, bool check_sym,
+                DMat U, double* lambda) {
+  const int64_t n = P.A.cols, ml = P.A.rows;
+  if (P.m_global != n) throw_dim("spevd_hermitian: matrix is not square");
+  if (check_sym && !P.dist) {
+    // reference singlepass.hpp:49-53: uncounted precondition read of A
+    check_symmetric(h, P.A, false);
+    check_flags(h, "spevd_hermitian");
+  }
+  if (k < 1) throw_param("spevd_hermitian: k must be >= 1");
+  if (p < 0) throw_param("spevd_hermitian: p must be >= 0");
+  if (k + p > n) throw_dim("spevd_hermitian: k+p exceeds n");
+  const int64_t l = k + p;
+  DMat Omega = h.ws.mat(n, l);
+  gaussian_dev(h, n, l, rng, Omega);
+  DMat Y = h.ws.mat(ml, l);
+  op_apply(h, P, Omega, Y);  // the single pass over A
+  DMat Q = h.ws.mat(ml, l);
+  orthonormalize(h, Y, Q, nullptr, P.dist);
+  DMat Oloc(Omega.p + P.row_off, ml, l, Omega.ld);
+  DMat g = h.ws.mat(l, l), hm = h.ws.mat(l, l);
+  gemm_tn(h, Q, Oloc, g);  // g = Q^T Omega
+  gemm_tn(h, Q, Y, hm);    // h = Q^T Y
+  if (P.dist) {
+    allreduce_mat(h, g);
+    allreduce_mat(h, hm);
+  }
+  DMat gt = h.ws.mat(l, l), ht = h.ws.mat(l, l), X = h.ws.mat(l, l), c = h.ws.mat(l, l);
+  transpose(h, g, gt);
+  transpose(h, hm, ht);
+  solve_ls_impl(h, gt, ht, X);  // C g = h via g^T C^T = h^T
+  sym_part(h, X, c);            // c = X^T; c = (c + c^T)/2
+  DMat Uc = h.ws.mat(l, l);
+  double* lam = h.ws.alloc(l);
+  evd_symmetric_impl(h, c, Uc, lam);
+  gemm_nn(h, Q, DMat(Uc.p, l, k, Uc.ld), U);
+  RSVD_CUDA(cudaMemcpyAsync(lambda, lam, size_t(k) * 8, cudaMemcpyDeviceToDevice, h.stream));
+}
+
+void spsvd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, DMat U,
+                double* sigma, DMat V) {
+  const int64_t n = P.A.cols, ml = P.A.rows, m = P.m_global;
+  if (k < 1) throw_param("spsvd_general: k must be >= 1");
+  if (p < 0) throw_param("spsvd_general: p must be >= 0");
+  if (k + p > std::min(m, n)) throw_dim("spsvd_general: k+p exceeds min(m,n)");
+  const int64_t l = k + p;
+  DMat Oc = h.ws.mat(n, l);
+  gaussian_dev(h, n, l, rng, Oc);  // Omega_c
+  DMat Psi = h.ws.mat(ml, l);
+  gaussian_dev(h, m, l, rng, Psi, P.row_off, P.row_off + ml);  // Omega_r (local rows)
+  DMat Yc = h.ws.mat(ml, l), W = h.ws.mat(n, l);
+  op_apply(h, P, Oc, Yc);     // Y_c = A Omega_c
+  op_adjoint(h, P, Psi, W);   // Y_r = A^T Omega_r
+  DMat Qc = h.ws.mat(ml, l), Qr = h.ws.mat(n, l);
+  orthonormalize(h, Yc, Qc, nullptr, P.dist);
+  orthonormalize(h, W, Qr, nullptr, false);
+  DMat G1 = h.ws.mat(l, l), H1 = h.ws.mat(l, l), G2 = h.ws.mat(l, l), H2 = h.ws.mat(l, l);
+  gemm_tn(h, Psi, Qc, G1);  // Omega_r^T Q_c
+  gemm_tn(h, W, Qr, H1);    // Y_r^T Q_r
+  gemm_tn(h, Qr, Oc, G2);   // Q_r^T Omega_c
+  gemm_tn(h, Qc, Yc, H2);   // Q_c^T Y_c
+  if (P.dist) {
+    allreduce_mat(h, G1);
+    allreduce_mat(h, H2);
+  }
+  DMat C = h.ws.mat(l, l);
+  solve_joint_core_impl(h, G1, H1, G2, H2, C);
+  DMat Uc = h.ws.mat(l, l), Vc = h.ws.mat(l, l);
+  double* s = h.ws.alloc(l);
+  svd_small_impl(h, C, Uc, s, Vc);
+  gemm_nn(h, Qc, DMat(Uc.p, l, k, Uc.ld), U);
+  gemm_nn(h, Qr, DMat(Vc.p, l, k, Vc.ld), V);
+  RSVD_CUDA(cudaMemcpyAsync(sigma, s, size_t(k) * 8, cudaMemcpyDeviceToDevice, h.stream));
+}
+
+}  // namespace rsvdb

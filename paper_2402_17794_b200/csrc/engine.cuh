@@ -1,0 +1,34 @@
+// Pipelines (engine.cu).
+#pragma once
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace rsvdb {
+
+struct Problem {
+  DMat A;              // local row shard (m_local x n)
+  int64_t m_global = 0;
+  int64_t row_off = 0;
+  bool dist = false;
+};
+
+Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda);
+void op_apply(Handle& h, const Problem& P, const DMat& X, DMat Y);
+void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z);
+void check_symmetric(Handle& h, const DMat& C, bool dist);
+
+void svd_small_impl(Handle& h, const DMat& M, DMat U, double* s, DMat V);
+void solve_ls_impl(Handle& h, const DMat& G, const DMat& Hm, DMat X);
+void evd_symmetric_impl(Handle& h, const DMat& C, DMat U, double* lambda);
+void solve_joint_core_impl(Handle& h, const DMat& G1, const DMat& H1, const DMat& G2,
+                           const DMat& H2, DMat C);
+void range_basis_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, int mode,
+                      DevRng& rng, DMat Q);
+void rsvd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, int mode, DevRng& rng,
+               DMat U, double* sigma, DMat V);
+void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, bool check_sym,
+                DMat U, double* lambda);
+void spsvd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, DMat U,
+                double* sigma, DMat V);
+
+}  // namespace rsvdb

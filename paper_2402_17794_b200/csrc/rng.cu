@@ -1,0 +1,352 @@
+// On-device Gaussian test matrices reproducing the reference's seeded stream.
+//
+// Reference: gaussian(n, l, rng) (sketch.hpp:48-59) fills column-major with
+// Rng::normal() (sketch.hpp:27) = std::normal_distribution<double> over
+// std::mt19937_64:
+//   * mt19937_64: 312-word state, lazy regeneration (_M_gen_rand) when the
+//     index reaches 312, tempering on output (libstdc++ random.tcc);
+//   * generate_canonical<double,53>: u = RN((double)x) / 2^64, clamped below 1
+//     (libstdc++ random.tcc:3346-3381);
+//   * Marsaglia polar (libstdc++ random.tcc:1810-1843): x = 2u-1, y = 2u'-1,
+//     r2 = x*x + y*y (no FMA), reject r2 > 1 or r2 == 0, mult =
+//     sqrt(-2 log r2 / r2), return y*mult and CACHE x*mult for the next call.
+//
+// Device pipeline (all exact integer / correctly rounded IEEE arithmetic,
+// except log, see ddlog.cuh):
+//   1. mt_blocks: regenerate the untempered MT word sequence past the current
+//      position (twist = two 156-wide parallel phases per 312 words).
+//   2. polar_count: accept flags of every attempt (pair of draws), per-tile
+//      counts; scan_counts: exclusive prefix over tiles.
+//   3. polar_write: ranks inside each tile by ballot/popc; accepted attempt of
+//      rank a writes normals 2a and 2a+1 of the output stream (column-major
+//      placement), the attempt that completes the stream records how many
+//      draws were consumed and the cached second variate.
+//   4. rng_finish: the new MT state (312 words of the block holding the last
+//      consumed draw + index, libstdc++'s lazy convention) and the cache.
+// The host Rng state is passed in and returned advanced by exactly the draws
+// consumed, so a host rsvd::Rng continues bit-identically.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "ddlog.cuh"
+#include "rng.cuh"
+#include "small.cuh"
+
+namespace rsvdb {
+
+__constant__ ddlog::Entry c_log_table[ddlog::kTableSize];
+
+namespace {
+
+constexpr uint64_t kMatA = 0xB5026F5AA96619E9ULL;
+constexpr uint64_t kUpper = 0xFFFFFFFF80000000ULL;
+constexpr uint64_t kLower = 0x000000007FFFFFFFULL;
+constexpr int kN = 312, kM = 156;
+
+__device__ __forceinline__ uint64_t twist(uint64_t xk, uint64_t xk1) {
+  const uint64_t y = (xk & kUpper) | (xk1 & kLower);
+  return (y >> 1) ^ ((y & 1ULL) ? kMatA : 0ULL);
+}
+__device__ __forceinline__ uint64_t temper(uint64_t z) {
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+  z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+  z ^= (z >> 43);
+  return z;
+}
+// generate_canonical<double, 53> for a 64-bit engine.
+__device__ __forceinline__ double canonical(uint64_t z) {
+  double u = __ull2double_rn(z) * 0x1p-64;
+  if (u >= 1.0) u = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
+  return u;
+}
+struct Pair {
+  double x, y, r2;
+  bool ok;
+};
+__device__ __forceinline__ Pair polar_pair(uint64_t w1, uint64_t w2) {
+  Pair p;
+  p.x = __dsub_rn(__dmul_rn(2.0, canonical(temper(w1))), 1.0);
+  p.y = __dsub_rn(__dmul_rn(2.0, canonical(temper(w2))), 1.0);
+  p.r2 = __dadd_rn(__dmul_rn(p.x, p.x), __dmul_rn(p.y, p.y));
+  p.ok = !(p.r2 > 1.0 || p.r2 == 0.0);
+  return p;
+}
+__device__ __forceinline__ double polar_mult(double r2) {
+  const double lg = ddlog::log_cr(r2, c_log_table);
+  return __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, lg), r2));
+}
+
+// 1. sequential block generator (one CTA).  out[0..312) = initial block.
+__global__ void mt_blocks_kernel(const uint64_t* __restrict__ init, int64_t nb,
+                                 uint64_t* __restrict__ out) {
+  __shared__ uint64_t S[2][kN];
+  const int t = threadIdx.x;
+  if (t < kN) {
+    S[0][t] = init[t];
+    out[t] = init[t];
+  }
+  __syncthreads();
+  for (int64_t k = 1; k <= nb; ++k) {
+    const uint64_t* c = S[(k - 1) & 1];
+    uint64_t* n = S[k & 1];
+    if (t < kN - kM) n[t] = c[t + kM] ^ twist(c[t], c[t + 1]);
+    __syncthreads();
+    if (t >= kN - kM && t < kN - 1) n[t] = n[t - (kN - kM)] ^ twist(c[t], c[t + 1]);
+    if (t == kN - 1) n[t] = n[kM - 1] ^ twist(c[kN - 1], n[0]);
+    __syncthreads();
+    if (t < kN) out[k * kN + t] = n[t];
+  }
+}
+
+struct DevState {
+  uint64_t mt[kN];
+  uint64_t pos;
+  int32_t has_cached, pad;
+  double cached;
+};
+
+constexpr int kTile = 1024;  // attempts per tile (= 256 threads x 4)
+
+// 2a. accepted-attempt count per tile.
+__global__ void polar_count_kernel(const uint64_t* __restrict__ words, const uint64_t* p0p,
+                                   int64_t attempts, int* __restrict__ tile_count) {
+  const int64_t p0 = int64_t(*p0p);
+  const int64_t base = int64_t(blockIdx.x) * kTile;
+  int c = 0;
+  for (int k = 0; k < kTile / 256; ++k) {
+    const int64_t j = base + k * 256 + threadIdx.x;
+    if (j < attempts) {
+      const Pair p = polar_pair(words[p0 + 2 * j], words[p0 + 2 * j + 1]);
+      c += p.ok ? 1 : 0;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ int ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 8; ++w) s += ws[w];
+    tile_count[blockIdx.x] = s;
+  }
+}
+
+// 2b. exclusive scan of tile counts (single CTA, sequential chunks).
+__global__ void scan_counts_kernel(const int* __restrict__ cnt, int64_t ntiles,
+                                   int64_t* __restrict__ off, int64_t* __restrict__ total) {
+  __shared__ int64_t carry;
+  __shared__ int64_t wsum[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t b0 = 0; b0 < ntiles; b0 += blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;
+    const int64_t v = i < ntiles ? cnt[i] : 0;
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < int(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int64_t incl = x + (warp > 0 ? wsum[warp - 1] : 0);
+    if (i < ntiles) off[i] = carry + incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+struct GaussOut {
+  double* out;
+  int64_t n, ld;      // rows of the output, leading dimension
+  int64_t total;      // n * l normals
+  int64_t first;      // 1 if the cached variate was placed at element 0
+  int64_t pairs;      // accepted attempts needed
+  int64_t row_lo, row_hi;  // only rows in [row_lo, row_hi) are stored (sharded Psi)
+};
+
+// 3. write normals; record the completing attempt.
+__global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uint64_t* p0p,
+                                   int64_t attempts, const int64_t* __restrict__ tile_off,
+                                   GaussOut g, int64_t* __restrict__ done_attempt,
+                                   double* __restrict__ cache_val) {
+  const int64_t p0 = int64_t(*p0p);
+  const int64_t base = int64_t(blockIdx.x) * kTile;
+  __shared__ int wcnt[8];
+  __shared__ int64_t run;
+  if (threadIdx.x == 0) run = tile_off[blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < kTile / 256; ++k) {
+    const int64_t j = base + k * 256 + threadIdx.x;
+    Pair p{0, 0, 0, false};
+    if (j < attempts) p = polar_pair(words[p0 + 2 * j], words[p0 + 2 * j + 1]);
+    const unsigned bal = __ballot_sync(0xffffffffu, p.ok);
+    if (lane == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+    for (int w = 0; w < warp; ++w) before += wcnt[w];
+    const int64_t rank = run + before + __popc(bal & ((1u << lane) - 1u));
+    if (p.ok && rank < g.pairs) {
+      const double mult = polar_mult(p.r2);
+      const double vy = __dadd_rn(__dmul_rn(p.y, mult), 0.0);
+      const double vx = __dadd_rn(__dmul_rn(p.x, mult), 0.0);
+      const int64_t e0 = g.first + 2 * rank;
+      {
+        const int64_t r = e0 % g.n, c = e0 / g.n;
+        if (r >= g.row_lo && r < g.row_hi) g.out[c * g.ld + (r - g.row_lo)] = vy;
+      }
+      if (e0 + 1 < g.total) {
+        const int64_t r = (e0 + 1) % g.n, c = (e0 + 1) / g.n;
+        if (r >= g.row_lo && r < g.row_hi) g.out[c * g.ld + (r - g.row_lo)] = vx;
+      }
+      if (rank == g.pairs - 1) {
+        *done_attempt = j;
+        *cache_val = (e0 + 1 < g.total) ? 0.0 : vx;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int w = 0; w < 8; ++w) s += wcnt[w];
+      run += s;
+    }
+    __syncthreads();
+  }
+}
+
+// 4. new state: block holding draw index T-1, pos = T - 312*b (lazy twist).
+__global__ void rng_finish_kernel(const uint64_t* __restrict__ words,
+                                  const int64_t* __restrict__ done_attempt,
+                                  const double* __restrict__ cache_val, int64_t pairs,
+                                  int cache_out, DevState* st, int* flags) {
+  if (pairs == 0) {
+    if (threadIdx.x == 0) {
+      st->has_cached = cache_out ? 1 : 0;
+      if (!cache_out) st->cached = 0.0;
+    }
+    return;
+  }
+  const int64_t p0 = int64_t(st->pos);
+  const int64_t J = *done_attempt;
+  __syncthreads();  // every thread read st->pos before thread 0 rewrites it
+  if (J < 0) {
+    if (threadIdx.x == 0) atomicOr(flags, kFlagRngExhausted);
+    return;
+  }
+  const int64_t T = p0 + 2 * (J + 1);
+  const int64_t b = (T - 1) / kN;
+  for (int t = threadIdx.x; t < kN; t += blockDim.x) st->mt[t] = words[b * kN + t];
+  if (threadIdx.x == 0) {
+    st->pos = uint64_t(T - b * kN);
+    st->has_cached = cache_out ? 1 : 0;
+    st->cached = cache_out ? *cache_val : 0.0;
+  }
+}
+
+std::once_flag g_table_once;
+ddlog::Entry g_host_table[ddlog::kTableSize];
+
+}  // namespace
+
+const ddlog::Entry* host_log_table() {
+  std::call_once(g_table_once, [] { ddlog::build_table(g_host_table); });
+  return g_host_table;
+}
+
+void rng_init_device(Handle& h) {
+  (void)h;
+  RSVD_CUDA(cudaMemcpyToSymbol(c_log_table, host_log_table(), sizeof(g_host_table)));
+}
+
+DevRng rng_upload(Handle& h, const rsvd_rng_state* st) {
+  if (st->pos > uint64_t(kN)) throw_param("rng: invalid state index");
+  DevRng r;
+  r.d = h.ws.alloc_bytes(sizeof(DevState));
+  r.has_cached = st->has_cached ? 1 : 0;
+  static_assert(sizeof(DevState) == sizeof(rsvd_rng_state), "state layout");
+  RSVD_CUDA(cudaMemcpyAsync(r.d, st, sizeof(DevState), cudaMemcpyHostToDevice, h.stream));
+  return r;
+}
+
+void rng_download(Handle& h, const DevRng& r, rsvd_rng_state* user) {
+  RSVD_CUDA(cudaMemcpyAsync(h.h_rng, r.d, sizeof(DevState), cudaMemcpyDeviceToHost, h.stream));
+  h.rng_user_out = user;  // filled from h.h_rng at the call's final synchronization
+}
+
+namespace {
+__global__ void place_cached_kernel(const DevState* st, double* out) { out[0] = st->cached; }
+
+}  // namespace
+
+void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_t row_lo,
+                  int64_t row_hi) {
+  if (n < 1 || l < 1) throw_param("gaussian: dimensions must be positive");
+  if (row_hi < 0) {
+    row_lo = 0;
+    row_hi = n;
+  }
+  DevState* dst = static_cast<DevState*>(rng.d);
+  const int64_t total = n * l;
+  const int64_t first = rng.has_cached ? 1 : 0;
+  const int64_t remaining = total - first;
+  const int64_t pairs = (remaining + 1) / 2;
+  const int cache_out = (remaining % 2 == 1) ? 1 : 0;
+  // the cached variate (if any) is element 0 of the stream
+  if (first && row_lo == 0 && row_hi > 0) {
+    place_cached_kernel<<<1, 1, 0, h.stream>>>(dst, out.p);
+    RSVD_LAUNCHED(h);
+  }
+  if (pairs > 0) {
+    // attempt budget: mean pairs/(pi/4) plus > 10 standard deviations
+    const double p = 0.78539816339744831;
+    const int64_t attempts =
+        int64_t(double(pairs) / p + 10.0 * 0.59 * std::sqrt(double(pairs)) + 64.0);
+    const int64_t words_needed = kN + 2 * attempts;  // worst-case start index 312
+    const int64_t nb = ceil_div(words_needed, kN) - 1;
+    uint64_t* words = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nb + 1) * kN * 8));
+    mt_blocks_kernel<<<1, 320, 0, h.stream>>>(dst->mt, nb, words);
+    RSVD_LAUNCHED(h);
+    const int64_t ntiles = ceil_div(attempts, kTile);
+    int* cnt = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(ntiles) * 4 + 16));
+    int64_t* off = reinterpret_cast<int64_t*>(h.ws.alloc_bytes(size_t(ntiles + 4) * 8));
+    int64_t* done = off + ntiles;  // [done_attempt, total]
+    double* cache = reinterpret_cast<double*>(done + 2);
+    RSVD_CUDA(cudaMemsetAsync(done, 0xff, sizeof(int64_t), h.stream));
+    polar_count_kernel<<<unsigned(ntiles), 256, 0, h.stream>>>(words, &dst->pos, attempts, cnt);
+    RSVD_LAUNCHED(h);
+    scan_counts_kernel<<<1, 1024, 0, h.stream>>>(cnt, ntiles, off, done + 1);
+    RSVD_LAUNCHED(h);
+    GaussOut g{out.p, n, out.ld, total, first, pairs, row_lo, row_hi};
+    polar_write_kernel<<<unsigned(ntiles), 256, 0, h.stream>>>(words, &dst->pos, attempts, off, g,
+                                                               done, cache);
+    RSVD_LAUNCHED(h);
+    rng_finish_kernel<<<1, 320, 0, h.stream>>>(words, done, cache, pairs, cache_out, dst,
+                                               h.d_flags);
+    RSVD_LAUNCHED(h);
+  } else {
+    rng_finish_kernel<<<1, 32, 0, h.stream>>>(nullptr, nullptr, nullptr, 0, 0, dst, h.d_flags);
+    RSVD_LAUNCHED(h);
+  }
+  rng.has_cached = cache_out;
+}
+
+}  // namespace rsvdb
+
+extern "C" double rsvd_debug_log_cr(double x) {
+  return rsvdb::ddlog::log_cr(x, rsvdb::host_log_table());
+}

@@ -1,0 +1,868 @@
+// Small dense kernels: orthonormalization, l x l Jacobi SVD / EVD, sign rule.
+//
+// Reference counterparts (core.hpp): orthonormalize :96-105 (Eigen
+// HouseholderQR), svd_small :111-124 (Eigen BDCSVD + sign rule), evd_symmetric
+// :130-162 (SelfAdjointEigenSolver + |lambda| sort).
+//
+// B200 design:
+//  * Householder TSQR for l <= 64: every CTA factors a 128/256-row block in
+//    shared memory (warp-per-column reflector updates), the R factors are
+//    stacked and factored again until one block remains, and Q is formed
+//    top-down by applying each level's reflectors to the parent's Q rows.
+//    Householder keeps the reference's numerics (any conditioning, exact rank
+//    deficiency padded to full width) with only l x l data between blocks.
+//  * CholeskyQR2 for l > 64 (well-conditioned sketches, BASELINE C3-C5): Gram
+//    X^T X on the DMMA pass engine, Cholesky + triangular inverse of the l x l
+//    factor on chip, Q = X R^-1 on the pass engine, repeated twice; a shifted
+//    first pass (shifted CholeskyQR3) when the Gram is not numerically SPD.
+//  * One-sided Jacobi (Hestenes) on the l x l R factor for svd_small: round-
+//    robin parallel ordering, one warp per column pair, whole matrix resident
+//    in shared memory for l <= 112, L2-resident otherwise.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "dist.cuh"
+#include "pass.cuh"
+#include "small.cuh"
+
+namespace rsvdb {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------ Householder
+// Factor one block of `rows_blk` rows (zero padded to b) of X in shared
+// memory.  Writes Householder vectors (unit diagonal implied) to V (ld b, one
+// b x l panel per block), tau (l per block) and the l x l R into Rstack rows
+// [blk*l, blk*l + l) (ld ldr).
+__global__ void hh_factor_kernel(const double* __restrict__ X, int64_t rows, int l, int64_t ldx,
+                                 int b, double* __restrict__ V, double* __restrict__ tau,
+                                 double* __restrict__ Rs, int64_t ldr, int* flags) {
+  extern __shared__ double sm[];
+  double* A = sm;                  // b x l, ld = b
+  double* red = sm + int64_t(b) * l;  // scratch: tau/beta broadcast
+  const int blk = blockIdx.x;
+  const int64_t r0 = int64_t(blk) * b;
+  const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = nthr >> 5;
+  bool bad = false;
+  for (int64_t e = tid; e < int64_t(b) * l; e += nthr) {
+    const int i = int(e % b), j = int(e / b);
+    double v = 0.0;
+    if (r0 + i < rows) {
+      v = X[j * ldx + r0 + i];
+      if (!isfinite(v)) bad = true;
+    }
+    A[e] = v;
+  }
+  if (bad) atomicOr(flags, kFlagNonFinite);
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    if (warp == 0) {
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < b; i += 32) {
+        const double v = A[j * b + i];
+        s += v * v;
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        const double alpha = A[j * b + j];
+        double t = 0.0, beta = alpha, scal = 0.0;
+        if (s > 0.0) {
+          const double nrm = sqrt(alpha * alpha + s);
+          beta = alpha >= 0.0 ? -nrm : nrm;
+          t = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        red[0] = t;
+        red[1] = beta;
+        red[2] = scal;
+      }
+    }
+    __syncthreads();
+    const double t = red[0], beta = red[1], scal = red[2];
+    if (t != 0.0)
+      for (int i = j + 1 + tid; i < b; i += nthr) A[j * b + i] *= scal;
+    __syncthreads();
+    if (tid == 0) A[j * b + j] = beta;
+    if (t != 0.0) {
+      for (int c = j + 1 + warp; c < l; c += nwarps) {
+        double w = (lane == 0) ? A[c * b + j] : 0.0;
+        for (int i = j + 1 + lane; i < b; i += 32) w += A[j * b + i] * A[c * b + i];
+        w = warp_sum(w) * t;
+        if (lane == 0) A[c * b + j] -= w;
+        for (int i = j + 1 + lane; i < b; i += 32) A[c * b + i] -= w * A[j * b + i];
+      }
+    }
+    if (tid == 0) tau[int64_t(blk) * l + j] = t;
+    __syncthreads();
+  }
+  // outputs
+  double* Vb = V + int64_t(blk) * b * l;
+  for (int64_t e = tid; e < int64_t(b) * l; e += nthr) Vb[e] = A[e];
+  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+    const int i = int(e % l), j = int(e / l);
+    Rs[j * ldr + int64_t(blk) * l + i] = (i <= j) ? A[j * b + i] : 0.0;
+  }
+}
+
+// Q_blk = H_1 ... H_l [C_blk; 0], C_blk = rows [blk*l, blk*l+l) of the parent
+// Q (ld ldc) or the identity when C == nullptr.  Writes the real rows of the
+// block into Q (ld ldq).
+__global__ void hh_apply_kernel(const double* __restrict__ V, const double* __restrict__ tau,
+                                int64_t rows, int l, int b, const double* __restrict__ C,
+                                int64_t ldc, double* __restrict__ Q, int64_t ldq) {
+  extern __shared__ double sm[];
+  double* M = sm;                  // b x l
+  double* Vs = sm + int64_t(b) * l;  // b x l
+  const int blk = blockIdx.x;
+  const int64_t r0 = int64_t(blk) * b;
+  const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = nthr >> 5;
+  const double* Vb = V + int64_t(blk) * b * l;
+  for (int64_t e = tid; e < int64_t(b) * l; e += nthr) {
+    const int i = int(e % b), j = int(e / b);
+    Vs[e] = Vb[e];
+    double v = 0.0;
+    if (i < l) v = C ? C[j * ldc + int64_t(blk) * l + i] : (i == j ? 1.0 : 0.0);
+    M[e] = v;
+  }
+  __syncthreads();
+  for (int j = l - 1; j >= 0; --j) {
+    const double t = tau[int64_t(blk) * l + j];
+    if (t != 0.0) {
+      for (int c = warp; c < l; c += nwarps) {
+        double w = (lane == 0) ? M[c * b + j] : 0.0;
+        for (int i = j + 1 + lane; i < b; i += 32) w += Vs[j * b + i] * M[c * b + i];
+        w = warp_sum(w) * t;
+        if (lane == 0) M[c * b + j] -= w;
+        for (int i = j + 1 + lane; i < b; i += 32) M[c * b + i] -= w * Vs[j * b + i];
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t e = tid; e < int64_t(b) * l; e += nthr) {
+    const int i = int(e % b), j = int(e / b);
+    if (r0 + i < rows) Q[j * ldq + r0 + i] = M[e];
+  }
+}
+
+int tsqr_block_rows(int l) { return l <= 32 ? 256 : 128; }
+
+// ---------------------------------------------------------- one-sided Jacobi
+// Rm J = W diag(sigma) for square l x l Rm.  Single CTA; X, J in smem when
+// `in_smem`, otherwise in the global scratch buffers gX / gJ (L2 resident).
+__global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, int l,
+                                  double* __restrict__ Jout, int64_t ldj,
+                                  double* __restrict__ Wout, int64_t ldw,
+                                  double* __restrict__ sigma, double* gX, double* gJ,
+                                  int in_smem, int* flags) {
+  extern __shared__ double sm[];
+  double* X = in_smem ? sm : gX;
+  double* J = in_smem ? sm + int64_t(l) * l : gJ;
+  __shared__ int changed;
+  __shared__ int order[1024];
+  __shared__ double nrm[1024];
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = nthr >> 5;
+  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+    const int i = int(e % l), j = int(e / l);
+    X[e] = Rm[j * ldr + i];
+    J[e] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int lp = l + (l & 1);  // even number of slots (one dummy if odd)
+  const double tol = 1e-15;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (int round = 0; round < lp - 1; ++round) {
+      // circle method: slot 0 fixed, others rotate
+      for (int pr = warp; pr < lp / 2; pr += nwarps) {
+        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (lp - 1);
+        int bq = 1 + (lp - 2 - pr + round) % (lp - 1);
+        int pcol = min(a, bq), qcol = max(a, bq);
+        if (qcol >= l) continue;  // dummy slot
+        double al = 0, be = 0, ga = 0;
+        for (int i = lane; i < l; i += 32) {
+          const double xp = X[pcol * l + i], xq = X[qcol * l + i];
+          al += xp * xp;
+          be += xq * xq;
+          ga += xp * xq;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (fabs(zeta) > 1e150)
+                               ? 0.5 / zeta
+                               : copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int i = lane; i < l; i += 32) {
+            const double xp = X[pcol * l + i], xq = X[qcol * l + i];
+            X[pcol * l + i] = c * xp - s * xq;
+            X[qcol * l + i] = s * xp + c * xq;
+            const double jp = J[pcol * l + i], jq = J[qcol * l + i];
+            J[pcol * l + i] = c * jp - s * jq;
+            J[qcol * l + i] = s * jp + c * jq;
+          }
+          if (lane == 0) changed = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!changed) break;
+    __syncthreads();
+  }
+  if (sweep >= 60 && tid == 0) atomicOr(flags, kFlagJacobiNoConv);
+  // column norms and stable descending order
+  for (int j = warp; j < l; j += nwarps) {
+    double s = 0;
+    for (int i = lane; i < l; i += 32) s += X[j * l + i] * X[j * l + i];
+    s = warp_sum(s);
+    if (lane == 0) nrm[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < l; j += nthr) {
+    int rank = 0;
+    const double v = nrm[j];
+    for (int k = 0; k < l; ++k) {
+      const double u = nrm[k];
+      if (u > v || (u == v && k < j)) ++rank;
+    }
+    order[rank] = j;
+  }
+  __syncthreads();
+  const double smax = nrm[order[0]];
+  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+    const int i = int(e % l), jn = int(e / l);
+    const int src = order[jn];
+    Jout[jn * ldj + i] = J[src * l + i];
+    const double s = nrm[src];
+    Wout[jn * ldw + i] = (s > 0.0 && s > smax * 1e-300) ? X[src * l + i] / s : 0.0;
+  }
+  for (int j = tid; j < l; j += nthr) sigma[j] = nrm[order[j]];
+  __syncthreads();
+  // Complete zero columns of W to an orthonormal set (rank-deficient input).
+  if (warp == 0) {
+    for (int jn = 0; jn < l; ++jn) {
+      const double s = nrm[order[jn]];
+      if (s > 0.0 && s > smax * 1e-300) continue;
+      double bestn = -1.0;
+      int besti = 0;
+      for (int cand = 0; cand < l; ++cand) {
+        // residual norm of e_cand after projecting out valid columns
+        double r2 = 1.0;
+        for (int k = 0; k < l; ++k) {
+          if (k == jn) continue;
+          const double sk = nrm[order[k]];
+          const bool valid = (k < jn) || (sk > 0.0 && sk > smax * 1e-300);
+          if (!valid) continue;
+          const double w = Wout[k * ldw + cand];
+          r2 -= w * w;
+        }
+        if (r2 > bestn + 1e-12) {
+          bestn = r2;
+          besti = cand;
+        }
+      }
+      for (int i = lane; i < l; i += 32) Wout[jn * ldw + i] = (i == besti) ? 1.0 : 0.0;
+      __syncwarp();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int k = 0; k < l; ++k) {
+          if (k == jn) continue;
+          const double sk = nrm[order[k]];
+          const bool valid = (k < jn) || (sk > 0.0 && sk > smax * 1e-300);
+          if (!valid) continue;
+          double d = 0;
+          for (int i = lane; i < l; i += 32) d += Wout[k * ldw + i] * Wout[jn * ldw + i];
+          d = warp_sum(d);
+          for (int i = lane; i < l; i += 32) Wout[jn * ldw + i] -= d * Wout[k * ldw + i];
+          __syncwarp();
+        }
+        double nn = 0;
+        for (int i = lane; i < l; i += 32) nn += Wout[jn * ldw + i] * Wout[jn * ldw + i];
+        nn = sqrt(warp_sum(nn));
+        for (int i = lane; i < l; i += 32) Wout[jn * ldw + i] /= nn;
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------ symmetric Jacobi EVD
+// Two-sided cyclic Jacobi with round-robin ordering; single CTA.
+__global__ void jacobi_evd_kernel(const double* __restrict__ Cin, int64_t ldc, int l,
+                                  double* __restrict__ Uout, int64_t ldu,
+                                  double* __restrict__ lam, double* gA, double* gV, int in_smem,
+                                  double* rot, int* flags) {
+  extern __shared__ double sm[];
+  double* A = in_smem ? sm : gA;
+  double* V = in_smem ? sm + int64_t(l) * l : gV;
+  __shared__ int changed;
+  __shared__ int order[1024];
+  __shared__ int pp[512], qq[512];
+  __shared__ double cs[512], sn[512];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  __shared__ double wsum[32];
+  double part = 0.0;
+  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+    const int i = int(e % l), j = int(e / l);
+    const double v = Cin[j * ldc + i];
+    A[e] = v;
+    part += v * v;
+    V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  part = warp_sum(part);
+  if ((tid & 31) == 0) wsum[tid >> 5] = part;
+  __syncthreads();
+  double fro2 = 0.0;
+  for (int w = 0; w < (nthr >> 5); ++w) fro2 += wsum[w];
+  // rotations below this magnitude are backward-stable no-ops (eps * ||C||_F)
+  const double abs_tol = 1e-17 * sqrt(fro2);
+  const int lp = l + (l & 1);
+  const int npairs = lp / 2;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (int round = 0; round < lp - 1; ++round) {
+      for (int pr = tid; pr < npairs; pr += nthr) {
+        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (lp - 1);
+        int b = 1 + (lp - 2 - pr + round) % (lp - 1);
+        int p = min(a, b), q = max(a, b);
+        double c = 1.0, s = 0.0;
+        if (q < l) {
+          const double apq = A[q * l + p];
+          const double app = A[p * l + p], aqq = A[q * l + q];
+          if (fabs(apq) > abs_tol && fabs(apq) > 1e-300 &&
+              fabs(apq) > 1e-16 * sqrt(fabs(app)) * sqrt(fabs(aqq)) * 0.5) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (fabs(theta) > 1e150)
+                                 ? 0.5 / theta
+                                 : copysign(1.0, theta) / (fabs(theta) + sqrt(1.0 + theta * theta));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            changed = 1;
+          }
+        } else {
+          q = -1;
+        }
+        pp[pr] = p;
+        qq[pr] = q;
+        cs[pr] = c;
+        sn[pr] = s;
+      }
+      __syncthreads();
+      // A <- A J (columns), V <- V J
+      for (int64_t e = tid; e < int64_t(npairs) * l; e += nthr) {
+        const int pr = int(e / l), i = int(e % l);
+        const int p = pp[pr], q = qq[pr];
+        if (q < 0 || sn[pr] == 0.0) continue;
+        const double c = cs[pr], s = sn[pr];
+        const double ap = A[p * l + i], aq = A[q * l + i];
+        A[p * l + i] = c * ap - s * aq;
+        A[q * l + i] = s * ap + c * aq;
+        const double vp = V[p * l + i], vq = V[q * l + i];
+        V[p * l + i] = c * vp - s * vq;
+        V[q * l + i] = s * vp + c * vq;
+      }
+      __syncthreads();
+      // A <- J^T A (rows)
+      for (int64_t e = tid; e < int64_t(npairs) * l; e += nthr) {
+        const int pr = int(e / l), j = int(e % l);
+        const int p = pp[pr], q = qq[pr];
+        if (q < 0 || sn[pr] == 0.0) continue;
+        const double c = cs[pr], s = sn[pr];
+        const double ap = A[j * l + p], aq = A[j * l + q];
+        A[j * l + p] = c * ap - s * aq;
+        A[j * l + q] = s * ap + c * aq;
+      }
+      __syncthreads();
+    }
+    if (!changed) break;
+    __syncthreads();
+  }
+  if (sweep >= 60 && tid == 0) atomicOr(flags, kFlagJacobiNoConv);
+  (void)rot;
+  // order by |lambda| descending, ties by ascending lambda value then index
+  // (reference: stable sort of an ascending eigenvalue list).
+  for (int j = tid; j < l; j += nthr) {
+    const double v = A[j * l + j];
+    int rank = 0;
+    for (int k = 0; k < l; ++k) {
+      const double u = A[k * l + k];
+      // |lambda| descending; exact ties: positive first, then index (the
+      // reference's Eigen solver returns (-1+d, 1) for [[0,1],[1,0]], so its
+      // stable |lambda| sort yields (1, -1); test_core.cpp:148-162)
+      const bool before = (fabs(u) > fabs(v)) || (fabs(u) == fabs(v) && (u > v || (u == v && k < j)));
+      if (before) ++rank;
+    }
+    order[rank] = j;
+  }
+  __syncthreads();
+  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+    const int i = int(e % l), jn = int(e / l);
+    Uout[jn * ldu + i] = V[order[jn] * l + i];
+  }
+  for (int j = tid; j < l; j += nthr) lam[j] = A[order[j] * l + order[j]];
+}
+
+// -------------------------------------------------------------- sign rule
+__global__ void sign_rule_kernel(double* U, int64_t rows, int64_t ldu, double* V, int64_t vrows,
+                                 int64_t ldv) {
+  const int j = blockIdx.x;
+  __shared__ double bv[32];
+  __shared__ long long bi[32];
+  double best = -1.0;
+  long long bidx = 0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double a = fabs(U[j * ldu + i]);
+    if (a > best) {
+      best = a;
+      bidx = i;
+    }
+  }
+  // warp argmax, lowest index on ties
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ob > best || (ob == best && oi < bidx)) {
+      best = ob;
+      bidx = oi;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    bv[warp] = best;
+    bi[warp] = bidx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < int(blockDim.x >> 5); ++w)
+      if (bv[w] > best || (bv[w] == best && bi[w] < bidx)) {
+        best = bv[w];
+        bidx = bi[w];
+      }
+    bi[0] = bidx;
+  }
+  __syncthreads();
+  const bool flip = U[j * ldu + bi[0]] < 0.0;
+  __syncthreads();
+  if (!flip) return;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) U[j * ldu + i] = -U[j * ldu + i];
+  if (V)
+    for (int64_t i = threadIdx.x; i < vrows; i += blockDim.x) V[j * ldv + i] = -V[j * ldv + i];
+}
+
+__global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, int64_t cols,
+                                 int64_t ldi, double* __restrict__ out, int64_t ldo) {
+  __shared__ double t[32][33];
+  const int64_t i0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, j = j0 + k;
+    if (i < rows && j < cols) t[k][threadIdx.x] = in[j * ldi + i];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t j = j0 + threadIdx.x, i = i0 + k;  // out(j, i) = in(i, j)
+    if (i < rows && j < cols) out[i * ldo + j] = t[threadIdx.x][k];
+  }
+}
+
+__global__ void scale_cols_kernel(double* X, int64_t rows, int64_t cols, int64_t ld,
+                                  const double* s, int inv) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    X[j * ld + i] = inv ? X[j * ld + i] / s[j] : X[j * ld + i] * s[j];
+  }
+}
+
+__global__ void sym_part_kernel(const double* A, int64_t n, int64_t lda, double* C, int64_t ldc) {
+  const int64_t tot = n * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    C[j * ldc + i] = 0.5 * (A[j * lda + i] + A[i * lda + j]);
+  }
+}
+
+__global__ void finite_kernel(const double* X, int64_t rows, int64_t cols, int64_t ld, int* flags,
+                              int bit) {
+  const int64_t n = rows * cols;
+  bool bad = false;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    if (!isfinite(X[j * ld + i])) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, bit);
+}
+
+// ---------------------------------------------------------- Cholesky (l x l)
+// Right-looking, single CTA, in place on G (ld l) in shared or global memory.
+// Produces upper R (G = R^T R) and its inverse Rinv.  Sets breakdown flag when
+// a pivot is not positive (relative to the largest diagonal).
+__global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l, double shift,
+                                double* __restrict__ R, int64_t ldr, double* __restrict__ Rinv,
+                                int64_t ldri, double* gA, int in_smem, int* flags) {
+  extern __shared__ double sm[];
+  double* A = in_smem ? sm : gA;  // lower-triangular working copy (col-major, ld l)
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = nthr >> 5;
+  __shared__ double dmax;
+  __shared__ int broke;
+  if (tid == 0) {
+    broke = 0;
+    dmax = 0;
+  }
+  __syncthreads();
+  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+    const int i = int(e % l), j = int(e / l);
+    double v = G[j * ldg + i];
+    if (i == j) v += shift;
+    A[e] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0;
+    for (int j = 0; j < l; ++j) m = fmax(m, A[j * l + j]);
+    dmax = m;
+  }
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    // A(j,j) final; column below
+    const double d = A[j * l + j];
+    if (!(d > 1e-30 * dmax) || !(d > 0.0)) {
+      if (tid == 0) broke = 1;
+      __syncthreads();
+      break;
+    }
+    const double rd = sqrt(d);
+    __syncthreads();
+    for (int i = j + 1 + tid; i < l; i += nthr) A[j * l + i] /= rd;
+    if (tid == 0) A[j * l + j] = rd;
+    __syncthreads();
+    // trailing update: A(i,k) -= L(i,j) L(k,j), k in (j, l), i >= k
+    for (int k = j + 1 + warp; k < l; k += nwarps) {
+      const double lkj = A[j * l + k];
+      for (int i = k + lane; i < l; i += 32) A[k * l + i] -= A[j * l + i] * lkj;
+    }
+    __syncthreads();
+  }
+  if (broke) {
+    if (tid == 0) atomicOr(flags, kFlagCholBreakdown);
+    return;
+  }
+  // R = L^T
+  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+    const int i = int(e % l), j = int(e / l);
+    R[j * ldr + i] = (i <= j) ? A[i * l + j] : 0.0;
+  }
+  // Rinv: solve R x = e_c for each column c by back substitution; R(i,k) = L(k,i)
+  for (int c = warp; c < l; c += nwarps) {
+    // x_i for i > c is 0; x_c = 1/R(c,c); x_i = -(sum_{k=i+1..c} R(i,k) x_k)/R(i,i)
+    for (int i = lane; i < l; i += 32) Rinv[c * ldri + i] = 0.0;
+    __syncwarp();
+    for (int i = c; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1 + lane; k <= c; k += 32) s += A[i * l + k] * Rinv[c * ldri + k];
+      s = warp_sum(s);
+      if (lane == 0) Rinv[c * ldri + i] = ((i == c ? 1.0 : 0.0) - s) / A[i * l + i];
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace
+
+// =================================================================== host
+// Opt a kernel into `bytes` of dynamic shared memory (idempotent, grows only).
+template <class K>
+static void ensure_smem(K kernel, size_t bytes, size_t& current) {
+  if (bytes > 48 * 1024 && bytes > current) {
+    RSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    current = bytes;
+  }
+}
+
+void check_flags(Handle& h, const char* what) {
+  RSVD_CUDA(cudaMemcpyAsync(h.h_flags, h.d_flags, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  const int f = *h.h_flags;
+  if (f) {
+    clear_flags(h);
+    std::string m = std::string(what) + ": ";
+    if (f & kFlagNonFinite) throw_numeric(m + "input has non-finite entries");
+    if (f & kFlagAsymmetric) throw_numeric(m + "input is not symmetric");
+    if (f & kFlagJacobiNoConv) throw_numeric(m + "Jacobi iteration did not converge");
+    if (f & kFlagCholBreakdown) throw_numeric(m + "Cholesky breakdown");
+    if (f & kFlagRngExhausted) throw Error(RSVD_ERR_INTERNAL, m + "rng attempt budget exhausted");
+    throw Error(RSVD_ERR_INTERNAL, m + "device flag set");
+  }
+}
+
+void clear_flags(Handle& h) {
+  RSVD_CUDA(cudaMemsetAsync(h.d_flags, 0, sizeof(int), h.stream));
+}
+
+void check_finite(Handle& h, const DMat& X, int bit) {
+  if (X.rows * X.cols == 0) return;
+  const int64_t n = X.rows * X.cols;
+  const int blocks = int(std::min<int64_t>(ceil_div(n, 256), 4 * h.sm_count));
+  finite_kernel<<<blocks, 256, 0, h.stream>>>(X.p, X.rows, X.cols, X.ld, h.d_flags, bit);
+  RSVD_LAUNCHED(h);
+}
+
+void transpose(Handle& h, const DMat& in, DMat out) {
+  if (in.rows * in.cols == 0) return;
+  dim3 grid(unsigned(ceil_div(in.rows, 32)), unsigned(ceil_div(in.cols, 32)));
+  transpose_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(in.p, in.rows, in.cols, in.ld, out.p,
+                                                       out.ld);
+  RSVD_LAUNCHED(h);
+}
+
+void copy(Handle& h, const DMat& X, DMat Y) {
+  if (X.rows * X.cols == 0 || X.p == Y.p) return;
+  RSVD_CUDA(cudaMemcpy2DAsync(Y.p, Y.ld * 8, X.p, X.ld * 8, X.rows * 8, X.cols,
+                              cudaMemcpyDeviceToDevice, h.stream));
+}
+
+void scale_cols(Handle& h, DMat X, const double* s, bool inv) {
+  const int64_t n = X.rows * X.cols;
+  if (!n) return;
+  const int blocks = int(std::min<int64_t>(ceil_div(n, 256), 4 * h.sm_count));
+  scale_cols_kernel<<<blocks, 256, 0, h.stream>>>(X.p, X.rows, X.cols, X.ld, s, inv ? 1 : 0);
+  RSVD_LAUNCHED(h);
+}
+
+void sym_part(Handle& h, const DMat& A, DMat C) {
+  const int64_t n = A.rows;
+  if (!n) return;
+  const int blocks = int(std::min<int64_t>(ceil_div(n * n, 256), 4 * h.sm_count));
+  sym_part_kernel<<<blocks, 256, 0, h.stream>>>(A.p, n, A.ld, C.p, C.ld);
+  RSVD_LAUNCHED(h);
+}
+
+void sign_rule(Handle& h, DMat U, DMat* V) {
+  if (U.cols == 0) return;
+  sign_rule_kernel<<<unsigned(U.cols), 256, 0, h.stream>>>(
+      U.p, U.rows, U.ld, V ? V->p : nullptr, V ? V->rows : 0, V ? V->ld : 0);
+  RSVD_LAUNCHED(h);
+}
+
+namespace {
+struct TsqrLevel {
+  int64_t rows;
+  int nblk;
+  double* V;
+  double* tau;
+};
+
+// Factor levels until one block remains; returns the l x l R (view into ws).
+DMat tsqr_factor(Handle& h, const DMat& X, std::vector<TsqrLevel>& lv) {
+  const int l = int(X.cols);
+  const int b = tsqr_block_rows(l);
+  const size_t smem_f = (size_t(b) * l + 4) * 8;
+  static size_t cur_f = 0;
+  ensure_smem(hh_factor_kernel, smem_f, cur_f);
+  DMat cur = X;
+  while (true) {
+    TsqrLevel L;
+    L.rows = cur.rows;
+    L.nblk = int(ceil_div(cur.rows, b));
+    L.V = h.ws.alloc(int64_t(L.nblk) * b * l);
+    L.tau = h.ws.alloc(int64_t(L.nblk) * l);
+    DMat Rs = h.ws.mat(int64_t(L.nblk) * l, l);
+    hh_factor_kernel<<<L.nblk, 256, smem_f, h.stream>>>(cur.p, cur.rows, l, cur.ld, b, L.V, L.tau,
+                                                        Rs.p, Rs.ld, h.d_flags);
+    RSVD_LAUNCHED(h);
+    lv.push_back(L);
+    if (L.nblk == 1) return DMat(Rs.p, l, l, Rs.ld);
+    cur = Rs;
+  }
+}
+
+// Form Q top-down; the top level applies its reflectors to C_top (l x l, the
+// identity when null).
+void tsqr_form(Handle& h, const std::vector<TsqrLevel>& lv, int l, const double* c_top,
+               int64_t ld_top, DMat Q) {
+  const int b = tsqr_block_rows(l);
+  const size_t smem_a = size_t(2) * b * l * 8;
+  static size_t cur_a = 0;
+  ensure_smem(hh_apply_kernel, smem_a, cur_a);
+  const double* parent = c_top;
+  int64_t ldp = ld_top;
+  for (int t = int(lv.size()) - 1; t >= 0; --t) {
+    const TsqrLevel& L = lv[t];
+    DMat out = (t == 0) ? Q : h.ws.mat(L.rows, l);
+    hh_apply_kernel<<<L.nblk, 256, smem_a, h.stream>>>(L.V, L.tau, L.rows, l, b, parent, ldp,
+                                                       out.p, out.ld);
+    RSVD_LAUNCHED(h);
+    parent = out.p;
+    ldp = out.ld;
+  }
+}
+}  // namespace
+
+void tsqr(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist) {
+  const int l = int(X.cols);
+  std::vector<TsqrLevel> lv;
+  DMat Rloc = tsqr_factor(h, X, lv);
+  if (!dist || h.nranks <= 1) {
+    if (R) copy(h, Rloc, *R);
+    tsqr_form(h, lv, l, nullptr, 0, Q);
+    return;
+  }
+  // Row-sharded: gather every rank's l x l R, factor the stack redundantly,
+  // and seed this rank's tree with its l rows of the stacked Q.
+  const int P = h.nranks;
+  double* packed = h.ws.alloc(int64_t(l) * l);
+  DMat Rp(packed, l, l, l);
+  copy(h, Rloc, Rp);
+  double* gath = h.ws.alloc(int64_t(P) * l * l);
+  allgather(h, packed, gath, int64_t(l) * l);
+  // gath holds P column-major l x l blocks; restack as (P l) x l
+  DMat S = h.ws.mat(int64_t(P) * l, l);
+  for (int r = 0; r < P; ++r)
+    RSVD_CUDA(cudaMemcpy2DAsync(S.p + int64_t(r) * l, S.ld * 8, gath + int64_t(r) * l * l, l * 8,
+                                l * 8, l, cudaMemcpyDeviceToDevice, h.stream));
+  std::vector<TsqrLevel> lv2;
+  DMat Rtop = tsqr_factor(h, S, lv2);
+  if (R) copy(h, Rtop, *R);
+  DMat Qs = h.ws.mat(int64_t(P) * l, l);
+  tsqr_form(h, lv2, l, nullptr, 0, Qs);
+  tsqr_form(h, lv, l, Qs.p + int64_t(h.rank) * l, Qs.ld, Q);
+}
+
+namespace {
+size_t small_smem_limit() { return 200 * 1024; }
+}  // namespace
+
+
+// CholeskyQR2 (shifted CholeskyQR3 when the first Gram is not numerically SPD).
+static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
+  const int l = int(X.cols);
+  DMat G = h.ws.mat(l, l), R1 = h.ws.mat(l, l), Ri = h.ws.mat(l, l);
+  const bool in_smem = size_t(l) * l * 8 <= small_smem_limit();
+  double* gA = in_smem ? nullptr : h.ws.alloc(int64_t(l) * l);
+  static size_t cur_c = 0;
+  ensure_smem(chol_inv_kernel, in_smem ? size_t(l) * l * 8 : 0, cur_c);
+  auto chol = [&](const DMat& Gm, double shift) {
+    chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
+        Gm.p, Gm.ld, l, shift, R1.p, R1.ld, Ri.p, Ri.ld, gA, in_smem ? 1 : 0, h.d_flags);
+    RSVD_LAUNCHED(h);
+  };
+  check_finite(h, X, kFlagNonFinite);
+  check_flags(h, "orthonormalize");
+  int64_t m_global = X.rows, row_off = 0;
+  if (dist) shard_rows(h, X.rows, &m_global, &row_off);
+  auto gram = [&](const DMat& Y) {
+    gemm_tn(h, Y, Y, G);
+    if (dist) allreduce_mat(h, G);
+  };
+  // pass 1
+  gram(X);
+  chol(G, 0.0);
+  RSVD_CUDA(cudaMemcpyAsync(h.h_flags, h.d_flags, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  DMat Rtot = h.ws.mat(l, l), Rtmp = h.ws.mat(l, l);
+  bool have_rtot = false;
+  int passes = 2;
+  if (*h.h_flags & kFlagCholBreakdown) {
+    clear_flags(h);
+    // shifted CholeskyQR: s = 11 (m l + l (l+1)) u ||X||_2^2, ||X||_2^2 <= trace(G)
+    std::vector<double> hg(size_t(l) * l);
+    RSVD_CUDA(cudaMemcpy2DAsync(hg.data(), l * 8, G.p, G.ld * 8, l * 8, l, cudaMemcpyDeviceToHost,
+                                h.stream));
+    RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    double tr = 0;
+    for (int i = 0; i < l; ++i) tr += hg[size_t(i) * l + i];
+    const double u = 1.1102230246251565e-16;
+    const double shift = 11.0 * (double(m_global) * l + double(l) * (l + 1)) * u * tr;
+    chol(G, shift);
+    passes = 3;
+  }
+  if (X.p == Q.p) {
+    DMat Qt = h.ws.mat(Q.rows, l);
+    gemm_nn(h, X, Ri, Qt);
+    copy(h, Qt, Q);
+  } else {
+    gemm_nn(h, X, Ri, Q);
+  }
+  copy(h, R1, Rtot);
+  have_rtot = true;
+  for (int pass = 1; pass < passes; ++pass) {
+    gram(Q);
+    chol(G, 0.0);
+    DMat Qt = h.ws.mat(Q.rows, l);
+    gemm_nn(h, Q, Ri, Qt);
+    copy(h, Qt, Q);
+    if (Rout) {  // Rtot = R1 * Rtot
+      gemm_nn(h, R1, Rtot, Rtmp);
+      copy(h, Rtmp, Rtot);
+    }
+  }
+  check_flags(h, "orthonormalize");
+  if (Rout && have_rtot) copy(h, Rtot, *Rout);
+}
+
+void orthonormalize(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist) {
+  if (X.cols > X.rows && !dist)
+    throw_dim("orthonormalize: more columns than rows (" + std::to_string(X.cols) + " > " +
+              std::to_string(X.rows) + ")");
+  if (X.cols == 0) return;
+  if (X.cols <= 64)
+    tsqr(h, X, Q, R, dist);
+  else
+    cholqr(h, X, Q, R, dist);
+}
+
+void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) {
+  const int l = int(Rm.rows);
+  if (l > 1024) throw_dim("jacobi_svd: l > 1024 not supported");
+  const bool in_smem = size_t(2) * l * l * 8 <= small_smem_limit();
+  double* gX = nullptr;
+  double* gJ = nullptr;
+  if (!in_smem) {
+    gX = h.ws.alloc(int64_t(l) * l);
+    gJ = h.ws.alloc(int64_t(l) * l);
+  }
+  static size_t cur_j = 0;
+  ensure_smem(jacobi_svd_kernel, in_smem ? size_t(2) * l * l * 8 : 0, cur_j);
+  jacobi_svd_kernel<<<1, 1024, in_smem ? size_t(2) * l * l * 8 : 0, h.stream>>>(
+      Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma, gX, gJ, in_smem ? 1 : 0, h.d_flags);
+  RSVD_LAUNCHED(h);
+
+}
+
+void jacobi_evd_sym(Handle& h, const DMat& C, DMat U, double* lambda) {
+  const int l = int(C.rows);
+  if (l > 1024) throw_dim("jacobi_evd: l > 1024 not supported");
+  const bool in_smem = size_t(2) * l * l * 8 <= small_smem_limit();
+  double* gA = nullptr;
+  double* gV = nullptr;
+  if (!in_smem) {
+    gA = h.ws.alloc(int64_t(l) * l);
+    gV = h.ws.alloc(int64_t(l) * l);
+  }
+  static size_t cur_e = 0;
+  ensure_smem(jacobi_evd_kernel, in_smem ? size_t(2) * l * l * 8 : 0, cur_e);
+  jacobi_evd_kernel<<<1, 1024, in_smem ? size_t(2) * l * l * 8 : 0, h.stream>>>(
+      C.p, C.ld, l, U.p, U.ld, lambda, gA, gV, in_smem ? 1 : 0, nullptr, h.d_flags);
+  RSVD_LAUNCHED(h);
+
+}
+
+}  // namespace rsvdb

@@ -1,0 +1,54 @@
+// Small dense kernels of the rsvd hot path (small.cu): orthonormalization
+// (Householder TSQR / CholeskyQR2), the l x l one-sided Jacobi SVD, the
+// symmetric Jacobi EVD, the sign rule, and helpers.
+#pragma once
+#include "common.cuh"
+
+namespace rsvdb {
+
+// Q (m x l) with range(Q) >= range(X), always exactly l orthonormal columns
+// (reference core.hpp:93-105).  If R != nullptr it receives the l x l factor
+// with X = Q R.  X and Q may alias.  dist: X is this rank's row shard of a
+// row-sharded matrix (NCCL exchange of l x l factors only).
+void orthonormalize(Handle& h, const DMat& X, DMat Q, DMat* R = nullptr, bool dist = false);
+
+// Householder TSQR (any conditioning, rank-deficient inputs padded), l <= 64.
+void tsqr(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist);
+
+// One-sided Jacobi on a square l x l matrix Rm:  Rm J = W diag(sigma).
+// sigma descending (stable), J orthogonal, W orthonormal (zero-sigma columns
+// completed to an orthonormal set).  Device outputs.
+void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma);
+
+// Symmetric two-sided Jacobi EVD of an l x l symmetric matrix (device), with
+// eigenvalues reordered by |lambda| descending, stable (core.hpp:148-152).
+void jacobi_evd_sym(Handle& h, const DMat& C, DMat U, double* lambda);
+
+// Reference sign rule (core.hpp:115-122): for each column j of U, the entry of
+// largest magnitude (lowest row on ties) is made >= 0; the flip is applied to
+// column j of V too (V may be null).
+void sign_rule(Handle& h, DMat U, DMat* V);
+
+// out = in^T
+void transpose(Handle& h, const DMat& in, DMat out);
+// Y = X (copy, shapes equal)
+void copy(Handle& h, const DMat& X, DMat Y);
+// columns j of X scaled by s[j] (device vector), or by 1/s[j] when inv
+void scale_cols(Handle& h, DMat X, const double* s, bool inv);
+// C = alpha*(A + B^T) elementwise (square)
+void sym_part(Handle& h, const DMat& A, DMat C);
+// Set device flag if any entry of X is not finite.
+void check_finite(Handle& h, const DMat& X, int flag_bit);
+
+enum FlagBits : int {
+  kFlagNonFinite = 1,
+  kFlagJacobiNoConv = 2,
+  kFlagRngExhausted = 4,
+  kFlagAsymmetric = 8,
+  kFlagCholBreakdown = 16,
+};
+// Raises NumericError if any flag is set (synchronizes the stream).
+void check_flags(Handle& h, const char* what);
+void clear_flags(Handle& h);
+
+}  // namespace rsvdb
