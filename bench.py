@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Headline benchmark: randomized-SVD factorizations on B200.
+
+Workload (BASELINE.json configs[1] = C2, the config the metric is quoted on):
+Algorithm 3 (power iteration, no re-orthonormalization), A = U diag(sigma) V^T
+8192 x 8192 fp64 with Haar U, V; sigma_j = 1 (j <= 20), 1e-2 (j-20)^-1
+(j > 20); k = 20, p = 5, q = 2; Omega 8192 x 25 from Rng(seed).  One step =
+one full factorization through the public API (rsvd(A, cfg), reference
+factor.hpp:21-24): Omega generation, 6 streaming passes over A, TSQR,
+the small SVD, and the lift.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+Multi-GPU (torchrun, one rank per GPU): A is row-sharded; n x l and l x l
+partials are NCCL-allreduced; every rank's time is measured with CUDA events
+between barriers and the MAX over ranks is reported (strong scaling: the
+whole job factors one matrix).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak, profiles/r01_fp64_peaks.md
+FP64_PEAK_SOURCE = "measured DMMA microbenchmark (profiles/r01_fp64_peaks.md); MEASURED_PEAKS.json has no fp64 figure"
+
+
+def hbm_peak_gbs() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+# ----------------------------------------------------------------- configs
+def sigma_c1(n):
+    return 10.0 ** (-np.arange(n) / 100.0)
+
+
+def sigma_c2(n):
+    j = np.arange(1, n + 1, dtype=np.float64)
+    s = np.ones(n)
+    s[20:] = 1e-2 / (j[20:] - 20.0)
+    return s
+
+
+def sigma_c3(n):
+    return np.exp(-np.arange(1, n + 1) / 50.0)
+
+
+CONFIGS = {
+    "C1": dict(alg=2, mode="basic", m=2048, n=1024, k=20, p=5, q=0, sigma=sigma_c1,
+               name="Alg2 basic 2048x1024 k20 p5 q0"),
+    "C2": dict(alg=3, mode="power", m=8192, n=8192, k=20, p=5, q=2, sigma=sigma_c2,
+               name="Alg3 power 8192x8192 k20 p5 q2"),
+    "C3": dict(alg=4, mode="power_ortho", m=65536, n=16384, k=100, p=10, q=2, sigma=sigma_c3,
+               name="Alg4 ortho 65536x16384 k100 p10 q2"),
+}
+SEED_U, SEED_V, SEED_OMEGA = 1001, 1002, 1
+
+
+def make_input(cfg, device):
+    """A = U diag(sigma) V^T with Haar U, V (QR of seeded N(0,1), sign-fixed),
+    generated on the GPU (input construction is not timed).  Returned as a
+    column-major (m x n) view of an (n x m) contiguous tensor."""
+    import torch
+    m, n = cfg["m"], cfg["n"]
+    r = min(m, n)
+    g = torch.Generator(device=device)
+
+    def haar(rows, cols, seed):
+        g.manual_seed(seed)
+        x = torch.randn(rows, cols, dtype=torch.float64, device=device, generator=g)
+        q, rr = torch.linalg.qr(x)
+        q *= torch.sign(torch.diagonal(rr))
+        return q
+
+    u = haar(m, r, SEED_U)
+    v = haar(n, r, SEED_V)
+    s = torch.from_numpy(cfg["sigma"](r)).to(device)
+    at = v @ (u * s).t()  # (n x m) contiguous == A column-major
+    del u, v
+    return at.t()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown",
+               "sync_boost", "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown",
+               "display_clock_setting"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"rsvd_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                mask = int(parts[3], 16)
+            except ValueError:
+                continue
+            for b, name in enumerate(self.REASONS):
+                if mask & (1 << b) and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference arm
+def cpu_reference(cfg, steps, warmup, threads, a_host=None):
+    """The reference's algorithm on the host CPU: oracle/rsvd_oracle.cpp, a
+    C++ restatement of the reference (which cannot be compiled here: Eigen is
+    absent) over libstdc++'s mt19937_64 + scipy's OpenBLAS LAPACK."""
+    import oracle
+    oracle.set_threads(threads)
+    if a_host is None:
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        a_host = np.asfortranarray(make_input(cfg, dev).cpu().numpy())
+    mode = {"basic": 0, "power": 1, "power_ortho": 2}[cfg["mode"]]
+    for _ in range(warmup):
+        oracle.rsvd(a_host, cfg["k"], cfg["p"], cfg["q"], mode, oracle.Rng(SEED_OMEGA))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.rsvd(a_host, cfg["k"], cfg["p"], cfg["q"], mode, oracle.Rng(SEED_OMEGA))
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    return dt
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    steps = args.steps
+    dt = cpu_reference(cfg, steps, min(args.warmup, 1), threads)
+    value = 1.0 / dt
+    line = {
+        "impl": "reference", "metric": f"rsvd factorizations/s ({cfg['name']})", "value": value,
+        "unit": "factorizations/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Haar U, V; BASELINE spectrum)",
+        "config": {"workload": f"{args.config}: {cfg['name']}", "m": cfg["m"], "n": cfg["n"],
+                   "k": cfg["k"], "p": cfg["p"], "q": cfg["q"], "seed": SEED_OMEGA},
+        "cpu_baseline": {"value": value, "unit": "factorizations/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{steps} full {args.config} factorizations, oracle/rsvd_oracle.cpp "
+                                   f"with {threads} OpenBLAS threads"},
+        "e2e": {"value": value, "unit": "factorizations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2402_17794_b200 as eng
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
+        obj = [eng.Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        engine = eng.Engine(local, rank, world, obj[0])
+    else:
+        engine = eng.Engine(local)
+    engine.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    m, n, k, p, q = cfg["m"], cfg["n"], cfg["k"], cfg["p"], cfg["q"]
+    l = k + p
+    a_full = make_input(cfg, device)  # column-major view
+    rows = np.array_split(np.arange(m), world)[rank]
+    r0, r1 = int(rows[0]), int(rows[-1]) + 1
+    a_loc = a_full[r0:r1, :].t().contiguous().t() if world > 1 else a_full
+    mode = eng.RangeMode[cfg["mode"]]
+    sk = eng.SketchConfig(k, p, q, mode, SEED_OMEGA)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        return eng.rsvd(a_loc, sk, eng.Rng(SEED_OMEGA))
+
+    with eng.using_engine(engine):
+        for _ in range(args.warmup):
+            f = step()
+        torch.cuda.synchronize()
+        # ---- timed region (device-resident inputs)
+        clocks = ClockSampler(local)
+        clocks.start()
+        engine.reset_counters()
+        engine.profile(True)
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            f = step()
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_total = ev0.elapsed_time(ev1)
+        clk = clocks.stop()
+        counters = engine.counters()
+        prof = engine.profile_read()
+        engine.profile(False)
+        if world > 1:
+            t = torch.tensor([ms_total], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_total = float(t.item())
+        ms_step = ms_total / args.steps
+        value = 1000.0 / ms_step
+
+        # ---- e2e through the host-buffer C ABI (pinned host A, copies timed)
+        a_pin = torch.empty((n, r1 - r0), dtype=torch.float64, pin_memory=True)
+        a_pin.copy_(a_loc.t())
+        a_host = a_pin.numpy().T  # Fortran-ordered (m_local x n) view
+        u_h = torch.empty((l, r1 - r0), dtype=torch.float64, pin_memory=True).numpy().T
+        v_h = torch.empty((l, n), dtype=torch.float64, pin_memory=True).numpy().T
+        s_h = torch.empty(l, dtype=torch.float64, pin_memory=True).numpy()
+        eng.rsvd_host(a_host, sk, eng.Rng(SEED_OMEGA), out=(u_h, s_h, v_h))  # warm
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            eng.rsvd_host(a_host, sk, eng.Rng(SEED_OMEGA), out=(u_h, s_h, v_h))
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        barrier()
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        h2d = (r1 - r0) * n * 8
+        d2h = ((r1 - r0) * l + l + n * l) * 8
+
+    # ---- roofline of the dominant pass kernel (live CUDA-event timing)
+    hbm = hbm_peak_gbs()
+    passes = {}
+    for kind, d in prof.items():
+        if d["launches"] == 0:
+            continue
+        per_ms = d["ms"] / d["launches"]
+        fl = d["flops"] / d["launches"]
+        by = d["bytes"] / d["launches"]
+        t_fp = fl / (FP64_PEAK_TFLOPS * 1e12)
+        t_hb = by / (hbm * 1e9)
+        bound = "tensor" if t_fp >= t_hb else "hbm"
+        tf = fl / (per_ms * 1e-3) / 1e12
+        gbs = by / (per_ms * 1e-3) / 1e9
+        passes[kind] = {"launches_per_step": d["launches"] / args.steps, "ms_per_launch": per_ms,
+                        "bound": bound, "tflops": tf, "gbs": gbs,
+                        "frac_fp64": tf / FP64_PEAK_TFLOPS, "frac_hbm": gbs / hbm,
+                        "frac_roofline": max(t_fp, t_hb) / (per_ms * 1e-3),
+                        "share_of_step": d["ms"] / ms_total if ms_total else None}
+    dom = max(passes, key=lambda k_: passes[k_]["ms_per_launch"] * passes[k_]["launches_per_step"])
+    dp = passes[dom]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
+        except Exception:
+            traffic = None
+    if dp["bound"] == "tensor":
+        roof = {"bound": "tensor", "achieved": dp["tflops"], "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": dp["tflops"] / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": FP64_PEAK_SOURCE, "kernel": f"pass_kernel ({dom})"}
+    else:
+        roof = {"bound": "hbm", "achieved": dp["gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": dp["gbs"] / hbm, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernel": f"pass_kernel ({dom})"}
+
+    # ---- CPU baseline (rank 0, N = 1 only): the oracle on the host cores
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        a_np = np.asfortranarray(a_full.cpu().numpy())
+        threads = os.cpu_count() or 1
+        dt = cpu_reference(cfg, 2, 1, threads, a_np)
+        dt1 = cpu_reference(cfg, 1, 0, 1, a_np) if args.config in ("C1", "C2") else None
+        cpu = {"value": 1.0 / dt, "unit": "factorizations/s", "cores": threads, "kind": "port",
+               "sample": f"2 full {args.config} factorizations, oracle/rsvd_oracle.cpp "
+                         f"(libstdc++ mt19937_64 + OpenBLAS {threads} threads)",
+               "value_1thread": (1.0 / dt1) if dt1 else None}
+
+    if rank == 0:
+        line = {
+            "metric": f"rsvd factorizations/s ({cfg['name']})",
+            "value": value, "unit": "factorizations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Haar U, V from QR of seeded N(0,1); BASELINE spectrum)",
+            "config": {"workload": f"{args.config}: {cfg['name']}", "m": m, "n": n, "k": k,
+                       "p": p, "q": q, "seeds": {"U": SEED_U, "V": SEED_V, "omega": SEED_OMEGA},
+                       "parallelism": f"row-shard x{world}",
+                       "l2": "inputs larger than L2 (|A| = %.0f MB)" % (m * n * 8 / 1e6)},
+            "e2e": {"value": 1000.0 / e2e_ms, "unit": "factorizations/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms, "api": "rsvd_rsvd_host (pinned host A)"},
+            "roofline": roof,
+            "passes": passes,
+            "cpu_baseline": cpu,
+            "gpu_launches": counters["kernel_launches"],
+            "physical_passes_per_step": counters["physical_passes"] / args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    engine.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,4 @@
+// Drop-in for the reference header of the same name (proj/include/rsvd/rangefinder.hpp):
+// the hot-path API, executed by the B200 engine.
+#pragma once
+#include "rsvd_b200.hpp"

@@ -93,6 +93,13 @@ rsvd_status rsvd_set_stream(rsvd_handle* h, void* cuda_stream);
 rsvd_status rsvd_synchronize(rsvd_handle* h);
 rsvd_status rsvd_get_counters(rsvd_handle* h, rsvd_counters* out);
 rsvd_status rsvd_reset_counters(rsvd_handle* h);
+/* Live timing of the streaming-pass kernels: when enabled, every pass launch
+ * is bracketed by CUDA events on the handle's stream; totals per kind
+ * (0 = apply Y = A X, 1 = adjoint Z = A^T Y) with their algorithmic flops and
+ * bytes (2 M N K, 8 (MK + KN + MN)).  Enabling resets the totals. */
+rsvd_status rsvd_profile_enable(rsvd_handle* h, int on);
+rsvd_status rsvd_profile_read(rsvd_handle* h, int kind, int64_t* launches, double* ms,
+                              double* flops, double* bytes);
 /* Row-sharding info (1 / 0 for a single-GPU handle). */
 rsvd_status rsvd_dist_info(rsvd_handle* h, int* rank, int* nranks);
 
@@ -127,6 +134,24 @@ rsvd_status rsvd_solve_ls_dev(rsvd_handle* h, int64_t m, int64_t n, const double
 rsvd_status rsvd_solve_joint_core_dev(rsvd_handle* h, int64_t l, const double* g1,
                                       const double* h1, const double* g2, const double* h2,
                                       double* c);
+
+/* Host-buffer variants of the kernel-level entry points (the C++ drop-in
+ * layer uses these; copies are included). */
+rsvd_status rsvd_gaussian_host(rsvd_handle* h, int64_t n, int64_t l, rsvd_rng_state* rng,
+                               double* out, int64_t ld_out);
+rsvd_status rsvd_orthonormalize_host(rsvd_handle* h, int64_t m, int64_t n, const double* in,
+                                     int64_t ld_in, double* q, int64_t ld_q);
+rsvd_status rsvd_svd_small_host(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                int64_t lda, double* u, int64_t ldu, double* s, double* v,
+                                int64_t ldv);
+rsvd_status rsvd_evd_symmetric_host(rsvd_handle* h, int64_t n, const double* c, int64_t ldc,
+                                    double* u, int64_t ldu, double* lambda);
+rsvd_status rsvd_solve_ls_host(rsvd_handle* h, int64_t m, int64_t n, const double* g,
+                               int64_t ldg, int64_t r, const double* hm, int64_t ldh, double* x,
+                               int64_t ldx);
+rsvd_status rsvd_range_basis_host(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                  int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                  rsvd_rng_state* rng, double* q_out, int64_t ldq);
 
 /* -------------------------------------------- streaming passes over A */
 /* Y = A X   (A m x n, X n x l, Y m x l): the sketch / power product. */

@@ -35,7 +35,7 @@ __all__ = [
     "solve_joint_core", "RangeMode", "SketchConfig", "fixed_rank_range", "power_range",
     "subspace_iter_range", "range_basis", "SvdApprox", "EvdApprox", "rsvd", "truncate",
     "CountingOperator", "spevd_hermitian", "spsvd_general", "apply", "apply_adjoint", "Engine",
-    "default_engine", "lib_path", "build",
+    "default_engine", "lib_path", "build", "using_engine", "rsvd_host",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -116,6 +116,9 @@ def _load():
             "rsvd_get_counters": [P, ctypes.POINTER(Counters)],
             "rsvd_reset_counters": [P],
             "rsvd_dist_info": [P, ctypes.POINTER(I), ctypes.POINTER(I)],
+            "rsvd_profile_enable": [P, I],
+            "rsvd_profile_read": [P, I, ctypes.POINTER(I64), ctypes.POINTER(D), ctypes.POINTER(D),
+                                  ctypes.POINTER(D)],
             "rsvd_gaussian_dev": [P, I64, I64, PS, P, I64],
             "rsvd_orthonormalize_dev": [P, I64, I64, P, I64, P, I64],
             "rsvd_svd_small_dev": [P, I64, I64, P, I64, P, I64, P, P, I64],
@@ -200,6 +203,19 @@ class Engine:
 
     def reset_counters(self) -> None:
         _check(_load().rsvd_reset_counters(self._h))
+
+    def profile(self, on: bool = True) -> None:
+        """Time every streaming-pass launch with CUDA events (resets totals)."""
+        _check(_load().rsvd_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for kind, name in ((0, "apply"), (1, "adjoint")):
+            n, ms, fl, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+            _check(_load().rsvd_profile_read(self._h, kind, ctypes.byref(n), ctypes.byref(ms),
+                                             ctypes.byref(fl), ctypes.byref(by)))
+            out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+        return out
 
     def synchronize(self) -> None:
         _check(_load().rsvd_synchronize(self._h))
@@ -318,8 +334,31 @@ def _vec_out(t, host: bool):
     return t.cpu().numpy() if host else t
 
 
+_engine_override = threading.local()
+
+
+class using_engine:
+    """Context manager routing the module-level API through a given Engine
+    (e.g. a row-sharded multi-GPU engine)."""
+
+    def __init__(self, engine: Engine):
+        self.engine = engine
+
+    def __enter__(self):
+        self.prev = getattr(_engine_override, "e", None)
+        _engine_override.e = self.engine
+        return self.engine
+
+    def __exit__(self, *exc):
+        _engine_override.e = self.prev
+
+
 def _eng(x=None) -> Engine:
     import torch
+    ov = getattr(_engine_override, "e", None)
+    if ov is not None:
+        ov.set_stream(torch.cuda.current_stream().cuda_stream)
+        return ov
     dev = None
     if x is not None and _is_torch(x) and x.is_cuda:
         dev = x.device.index
@@ -633,6 +672,28 @@ def apply_adjoint(a, y):
     _check(_load().rsvd_apply_adjoint_dev(e.handle, da.rows, da.cols, da.ptr, da.ld, dy.cols,
                                           dy.ptr, dy.ld, z.data_ptr(), max(da.cols, 1)))
     return _out(z, da.host)
+
+
+def rsvd_host(a: np.ndarray, cfg: SketchConfig, rng: Optional[Rng] = None, out=None):
+    """End-to-end host-buffer call (rsvd_rsvd_host): A and the outputs live in
+    host memory; the host<->device copies are part of the call.  `a` must be a
+    Fortran-ordered float64 array (pinned memory makes the copy fast); `out`
+    optionally supplies preallocated (U, sigma, V) host arrays."""
+    if rng is None:
+        rng = Rng(cfg.seed)
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
+        a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    l = max(cfg.k + cfg.p, 0)
+    if out is None:
+        out = (np.empty((m, l), order="F"), np.empty(l), np.empty((n, l), order="F"))
+    u, s, v = out
+    e = _eng()
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+    _check(_load().rsvd_rsvd_host(e.handle, m, n, P(a), max(m, 1), cfg.k, cfg.p, cfg.q,
+                                  int(cfg.mode), ctypes.byref(rng.state), P(u), max(m, 1), P(s),
+                                  P(v), max(n, 1)))
+    return SvdApprox(u, s, v)
 
 
 def debug_log_cr(x: float) -> float:

@@ -141,6 +141,7 @@ void rsvd_destroy(rsvd_handle* hd) {
   if (h.d_flags) cudaFree(h.d_flags);
   if (h.h_flags) cudaFreeHost(h.h_flags);
   if (h.h_rng) cudaFreeHost(h.h_rng);
+  for (auto e : h.prof_pool) cudaEventDestroy(e);
   if (h.own_stream) cudaStreamDestroy(h.own_stream);
   delete hd;
 }
@@ -165,6 +166,28 @@ rsvd_status rsvd_get_counters(rsvd_handle* hd, rsvd_counters* out) {
 rsvd_status rsvd_reset_counters(rsvd_handle* hd) {
   if (!hd) return RSVD_ERR_PARAMETER;
   hd->h.counters = rsvd_counters{};
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_profile_enable(rsvd_handle* hd, int on) {
+  if (!hd) return RSVD_ERR_PARAMETER;
+  rsvdb::Handle& h = hd->h;
+  h.prof = on != 0;
+  for (int k = 0; k < 2; ++k) {
+    h.prof_ms[k] = h.prof_flops[k] = h.prof_bytes[k] = 0;
+    h.prof_count[k] = 0;
+  }
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_profile_read(rsvd_handle* hd, int kind, int64_t* launches, double* ms,
+                              double* flops, double* bytes) {
+  if (!hd || kind < 0 || kind > 1) return RSVD_ERR_PARAMETER;
+  rsvdb::Handle& h = hd->h;
+  if (launches) *launches = h.prof_count[kind];
+  if (ms) *ms = h.prof_ms[kind];
+  if (flops) *flops = h.prof_flops[kind];
+  if (bytes) *bytes = h.prof_bytes[kind];
   return RSVD_OK;
 }
 
@@ -352,6 +375,90 @@ rsvd_status rsvd_spsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double*
     io.down(U, u, ldu);
     io.down_vec(s, sigma, kk);
     io.down(V, v, ldv);
+  });
+}
+
+rsvd_status rsvd_gaussian_host(rsvd_handle* hd, int64_t n, int64_t l, rsvd_rng_state* rng,
+                               double* out, int64_t ld) {
+  return guard(hd, "gaussian", [&](rsvdb::Handle& h) {
+    if (n < 1 || l < 1) rsvdb::throw_param("gaussian: dimensions must be positive");
+    if (!rng) rsvdb::throw_param("gaussian: null rng");
+    HostIO io{h};
+    rsvdb::DMat G = h.ws.mat(n, l);
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::gaussian_dev(h, n, l, r, G);
+    rsvdb::rng_download(h, r, rng);
+    io.down(G, out, ld);
+  });
+}
+
+rsvd_status rsvd_orthonormalize_host(rsvd_handle* hd, int64_t m, int64_t n, const double* in,
+                                     int64_t ld_in, double* q, int64_t ld_q) {
+  return guard(hd, "orthonormalize", [&](rsvdb::Handle& h) {
+    if (n > m)
+      rsvdb::throw_dim("orthonormalize: more columns than rows (" + std::to_string(n) + " > " +
+                       std::to_string(m) + ")");
+    HostIO io{h};
+    rsvdb::DMat X = io.up(in, m, n, ld_in), Q = h.ws.mat(m, n);
+    rsvdb::orthonormalize(h, X, Q);
+    io.down(Q, q, ld_q);
+  });
+}
+
+rsvd_status rsvd_svd_small_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                int64_t lda, double* u, int64_t ldu, double* s, double* v,
+                                int64_t ldv) {
+  return guard(hd, "svd_small", [&](rsvdb::Handle& h) {
+    const int64_t r = std::min(m, n);
+    if (r == 0) return;
+    HostIO io{h};
+    rsvdb::DMat A = io.up(a, m, n, lda), U = h.ws.mat(m, r), V = h.ws.mat(n, r);
+    double* sd = h.ws.alloc(r);
+    rsvdb::svd_small_impl(h, A, U, sd, V);
+    io.down(U, u, ldu);
+    io.down_vec(sd, s, r);
+    io.down(V, v, ldv);
+  });
+}
+
+rsvd_status rsvd_evd_symmetric_host(rsvd_handle* hd, int64_t n, const double* c, int64_t ldc,
+                                    double* u, int64_t ldu, double* lambda) {
+  return guard(hd, "evd_symmetric", [&](rsvdb::Handle& h) {
+    if (n == 0) return;
+    HostIO io{h};
+    rsvdb::DMat C = io.up(c, n, n, ldc), U = h.ws.mat(n, n);
+    double* lam = h.ws.alloc(n);
+    rsvdb::evd_symmetric_impl(h, C, U, lam);
+    io.down(U, u, ldu);
+    io.down_vec(lam, lambda, n);
+  });
+}
+
+rsvd_status rsvd_solve_ls_host(rsvd_handle* hd, int64_t m, int64_t n, const double* g,
+                               int64_t ldg, int64_t r, const double* hm, int64_t ldh, double* x,
+                               int64_t ldx) {
+  return guard(hd, "solve_ls", [&](rsvdb::Handle& h) {
+    if (n == 0 || r == 0) return;
+    HostIO io{h};
+    rsvdb::DMat G = io.up(g, m, n, ldg), Hm = io.up(hm, m, r, ldh), X = h.ws.mat(n, r);
+    rsvdb::solve_ls_impl(h, G, Hm, X);
+    io.down(X, x, ldx);
+  });
+}
+
+rsvd_status rsvd_range_basis_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                  int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                  rsvd_rng_state* rng, double* q_out, int64_t ldq) {
+  return guard(hd, "range_basis", [&](rsvdb::Handle& h) {
+    HostIO io{h};
+    rsvdb::DMat A = io.up(a, m, n, lda);
+    rsvdb::Problem P = rsvdb::make_problem(h, A.p, m, n, A.ld);
+    const int64_t l = std::max<int64_t>(k + p, 0);
+    rsvdb::DMat Q = h.ws.mat(m, l);
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::range_basis_impl(h, P, k, p, q, mode, r, Q);
+    rsvdb::rng_download(h, r, rng);
+    io.down(Q, q_out, ldq);
   });
 }
 

@@ -95,6 +95,19 @@ struct Handle {
   rsvd_counters counters{};
   Comm* comm = nullptr;        // null => single GPU
   int rank = 0, nranks = 1;
+  // Live per-launch timing of the streaming-pass kernels (bench.py roofline):
+  // CUDA events recorded on h.stream around every pass launch, folded into
+  // per-kind totals at the call's final synchronization.
+  bool prof = false;
+  struct ProfRec {
+    cudaEvent_t a, b;
+    int kind;  // 0 = NN (Y = A X), 1 = TN (Z = A^T Y)
+    double flops, bytes;
+  };
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> prof_pool;
+  double prof_ms[2] = {0, 0}, prof_flops[2] = {0, 0}, prof_bytes[2] = {0, 0};
+  int64_t prof_count[2] = {0, 0};
   // pinned staging for the RNG state copy-back (rng.cu)
   void* h_rng = nullptr;
   rsvd_rng_state* rng_user_out = nullptr;

@@ -83,6 +83,17 @@ void finish_call(Handle& h, const char* what) {
   h.rng_user_out = nullptr;
   check_flags(h, what);  // synchronizes
   if (user) std::memcpy(user, h.h_rng, sizeof(rsvd_rng_state));
+  for (auto& r : h.prof_pending) {
+    float ms = 0.f;
+    RSVD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    h.prof_ms[r.kind] += ms;
+    h.prof_flops[r.kind] += r.flops;
+    h.prof_bytes[r.kind] += r.bytes;
+    h.prof_count[r.kind] += 1;
+    h.prof_pool.push_back(r.a);
+    h.prof_pool.push_back(r.b);
+  }
+  h.prof_pending.clear();
 }
 
 namespace {

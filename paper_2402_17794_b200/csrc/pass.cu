@@ -109,26 +109,50 @@ struct PassCfg {
   static constexpr int A_BYTES = BM * BK * 8;
   static constexpr int B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int CPAD = 4;
-  static constexpr int CS_BYTES = BN * (BM + CPAD) * 8;
   static constexpr int PIPE_BYTES = STAGES * STAGE_BYTES;
-  static constexpr int SMEM = (PIPE_BYTES > CS_BYTES ? PIPE_BYTES : CS_BYTES) + 1024 /*align*/ +
-                              2 * STAGES * 8 + 16;
+  static constexpr int SMEM = PIPE_BYTES + 1024 /*align*/ + 2 * STAGES * 8 + 16;
   static_assert(BN % 8 == 0, "BN must be a multiple of 8");
   static_assert(BK % 16 == 0, "BK must be a multiple of 16");
   static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "swizzle-128B alignment");
   static_assert(BM <= 256, "TMA box limit");
 };
 
+// Work schedule.  A "unit" is one BK-deep slice of one output tile; tiles are
+// numbered t = m_tile * nt + n_tile.  Two schedules share one kernel:
+//  * split-K:  grid (nt, mt, S); CTA (n, m, s) owns tile (m, n), K slices
+//              [s*kps, (s+1)*kps).  Concurrent CTAs of the same m_tile read the
+//              same A rows, so A is re-read from L2, not HBM (many-tile passes).
+//  * stream-K: 1-D grid of G persistent CTAs; CTA c owns the contiguous unit
+//              range [c*U/G, (c+1)*U/G) of the tile-major unit space and may
+//              cover several partial tiles ("segments") -- all SMs busy even when
+//              there are fewer tiles than SMs (C1/C2 passes, Gram products).
+// A tile covered by several segments is reduced by the last-arriving segment's
+// CTA, which sums every segment's partial in FIXED segment order (its own from
+// registers): bitwise deterministic, no floating-point atomics.
 struct PassParams {
   int64_t M, N, K;
-  int64_t k_per_split;  // multiple of BK
-  int splits;
+  int mt, nt, kb_tile;   // tile grid and BK-slices per tile
+  int stream_k;          // schedule
+  int splits;            // split-K: S
+  int kb_split;          // split-K: BK-slices per split
+  int64_t units;         // stream-K: U = mt * nt * kb_tile
+  int grid;              // stream-K: G
+  int max_seg;           // stream-K: partial slots per CTA
   double* C;
   int64_t ldc;
   double* partials;
   int* counters;
 };
+
+__device__ __forceinline__ int64_t sk_begin(int c, const PassParams& p) {
+  return (int64_t(c) * p.units) / p.grid;
+}
+__device__ __forceinline__ int sk_cta_of(int64_t u, const PassParams& p) {
+  int c = int((u * p.grid) / p.units);
+  while (c + 1 < p.grid && sk_begin(c + 1, p) <= u) ++c;
+  while (c > 0 && sk_begin(c, p) > u) --c;
+  return c;
+}
 
 template <bool kNN, int BN, int WMT, int BK, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -136,20 +160,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 PassParams p) {
   using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES>;
   constexpr int BM = Cfg::BM, NT = Cfg::NT;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(
-      smem + (Cfg::PIPE_BYTES > Cfg::CS_BYTES ? Cfg::PIPE_BYTES : Cfg::CS_BYTES));
+  constexpr int FRAG = kConsumerWarps * WMT * NT * 64;  // doubles per partial tile
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // Pointer arithmetic on the __shared__ array (no integer round trip) keeps
+  // the state space visible to the compiler: fragment loads become LDS.
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::PIPE_BYTES);
   uint64_t* empty = full + STAGES;
   int* flag = reinterpret_cast<int*>(empty + STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z;
-  const int64_t m0 = int64_t(m_tile) * BM, n0 = int64_t(n_tile) * BN;
-  const int64_t k_begin = int64_t(split) * p.k_per_split;
-  const int64_t k_end = min(p.K, k_begin + p.k_per_split);
-  const int nkb = k_end > k_begin ? int((k_end - k_begin + BK - 1) / BK) : 0;
+  // This CTA's unit range (tile-major units for stream-K; one segment for split-K).
+  int64_t u0, u1;
+  int fixed_tile = 0, fixed_kb0 = 0;
+  if (p.stream_k) {
+    u0 = sk_begin(blockIdx.x, p);
+    u1 = sk_begin(blockIdx.x + 1, p);
+  } else {
+    fixed_tile = blockIdx.y * p.nt + blockIdx.x;
+    fixed_kb0 = blockIdx.z * p.kb_split;
+    const int kb1 = min(p.kb_tile, fixed_kb0 + p.kb_split);
+    u0 = 0;
+    u1 = max(0, kb1 - fixed_kb0);
+  }
+  auto unit_tile = [&](int64_t u) { return p.stream_k ? int(u / p.kb_tile) : fixed_tile; };
+  auto unit_kb = [&](int64_t u) { return p.stream_k ? int(u % p.kb_tile) : fixed_kb0 + int(u); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -167,139 +202,196 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::prefetch_tmap(&tmB);
       const uint64_t pol_a = ptx::policy_evict_first();
       const uint64_t pol_b = ptx::policy_evict_last();
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) ptx::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+      for (int64_t u = u0; u < u1; ++u) {
+        const int i = int(u - u0);
+        const int s = i % STAGES;
+        if (i >= STAGES) ptx::mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         uint8_t* a_st = smem + s * Cfg::STAGE_BYTES;
         uint8_t* b_st = a_st + Cfg::A_BYTES;
         ptx::mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-        const int k0 = int(k_begin + int64_t(kb) * BK);
+        const int t = unit_tile(u);
+        const int m0 = (t / p.nt) * BM, n0 = (t % p.nt) * BN;
+        const int k0 = unit_kb(u) * BK;
         if constexpr (kNN) {
           // A is M x K, M inner: boxes of 16 (M) x BK (K).
 #pragma unroll
           for (int b = 0; b < BM / 16; ++b)
-            ptx::tma_load_2d(a_st + b * (BK * 128), &tmA, &full[s], int(m0) + 16 * b, k0, pol_a);
+            ptx::tma_load_2d(a_st + b * (BK * 128), &tmA, &full[s], m0 + 16 * b, k0, pol_a);
         } else {
           // A is K x M, K inner: boxes of 16 (K) x BM (M).
 #pragma unroll
           for (int h = 0; h < Cfg::KH; ++h)
-            ptx::tma_load_2d(a_st + h * (BM * 128), &tmA, &full[s], k0 + 16 * h, int(m0), pol_a);
+            ptx::tma_load_2d(a_st + h * (BM * 128), &tmA, &full[s], k0 + 16 * h, m0, pol_a);
         }
 #pragma unroll
         for (int h = 0; h < Cfg::KH; ++h)
-          ptx::tma_load_2d(b_st + h * (BN * 128), &tmB, &full[s], k0 + 16 * h, int(n0), pol_b);
+          ptx::tma_load_2d(b_st + h * (BN * 128), &tmB, &full[s], k0 + 16 * h, n0, pol_b);
       }
     }
+    return;
+  }
+
+  // -------------------------------------------------- DMMA consumer warps
+  const int r8 = lane >> 2, c4 = lane & 3;
+  const int cx = c4 >> 1, cy = c4 & 1;
+  const int wm0 = warp * WMT * 8;
+  const int tid = threadIdx.x;
+  constexpr int NCT = kConsumerWarps * 32;
+  // Per-lane fragment offsets (bytes within a stage).  The 128B swizzle XORs
+  // the 16B-chunk index with the row index mod 8; everything that depends on
+  // the lane is folded here so the k-step loads are LDS [reg + imm].
+  int offA[4], offB[4];
+  if constexpr (kNN) {
+    // A (M inner): row = K index kr = 8*(ks>>1) + off, off = 2*(ks&1) + 4cy + cx;
+    // column chunk of m = 8i + r8 within its 16-row box.  Index [ks&1][i&1].
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ksb = q >> 1, ib = q & 1;
+      const int off = 2 * ksb + 4 * cy + cx;
+      const int chunk = ((ib ^ cy) << 2) | ((r8 >> 1) ^ ((ksb << 1) | cx));
+      offA[q] = (wm0 >> 4) * (BK * 128) + off * 128 + chunk * 16 + (r8 & 1) * 8;
+    }
+    // B (K inner): kk = 8*((ks>>1)&1) + off, chunk = (kk>>1) ^ r8.  Index [ks&3].
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int kk = 8 * (q >> 1) + 2 * (q & 1) + 4 * cy + cx;
+      offB[q] = r8 * 128 + (((kk >> 1) ^ r8) << 4) + (kk & 1) * 8;
+    }
   } else {
-    // ------------------------------------------------ DMMA consumer warps
+    // A and B both K inner: kk = 4*(ks&3) + c4, chunk = (kk>>1) ^ r8.  Index [ks&3].
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int kk = 4 * q + c4;
+      const int lo = r8 * 128 + (((kk >> 1) ^ r8) << 4) + (kk & 1) * 8;
+      offA[q] = wm0 * 128 + lo;
+      offB[q] = lo;
+    }
+  }
+  int64_t u = u0;
+  int seg_local = 0;
+  do {
     double acc[WMT][NT][2];
 #pragma unroll
     for (int i = 0; i < WMT; ++i)
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const int r8 = lane >> 2, c4 = lane & 3;
-    const int wm0 = warp * WMT * 8;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      ptx::mbar_wait(&full[s], (kb / STAGES) & 1);
+    const int t = (u < u1) ? unit_tile(u) : fixed_tile;
+    const int64_t seg_end = p.stream_k ? min(u1, int64_t(t + 1) * p.kb_tile) : u1;
+    for (; u < seg_end; ++u) {
+      const int i = int(u - u0);
+      const int s = i % STAGES;
+      ptx::mbar_wait(&full[s], (i / STAGES) & 1);
       const uint8_t* a_st = smem + s * Cfg::STAGE_BYTES;
       const uint8_t* b_st = a_st + Cfg::A_BYTES;
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         double af[WMT], bf[NT];
-        int kr;  // K row (0..BK-1) this lane contributes in k-step ks
         if constexpr (kNN) {
-          // Permuted K order {0,4,1,5},{2,6,3,7} per 8-group: conflict-free with
-          // the M-inner swizzled A tile.
-          const int base = (ks >> 1) * 8;
-          const int off = (ks & 1) ? ((c4 & 1) ? 6 : 2) + ((c4 >> 1) ? 1 : 0)
-                                   : ((c4 & 1) ? 4 : 0) + ((c4 >> 1) ? 1 : 0);
-          kr = base + off;
 #pragma unroll
-          for (int i = 0; i < WMT; ++i) {
-            const int m = wm0 + i * 8 + r8;
-            const int mm = m & 15;
-            const uint8_t* ptr = a_st + (m >> 4) * (BK * 128) + kr * 128 +
-                                 ((((mm >> 1)) ^ (kr & 7)) << 4) + ((mm & 1) << 3);
-            af[i] = *reinterpret_cast<const double*>(ptr);
-          }
+          for (int i2 = 0; i2 < WMT; ++i2)
+            af[i2] = *reinterpret_cast<const double*>(
+                a_st + offA[((ks & 1) << 1) | (i2 & 1)] + (i2 >> 1) * (BK * 128) + (ks >> 1) * 1024);
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+            bf[j] = *reinterpret_cast<const double*>(b_st + offB[ks & 3] + (ks >> 2) * (BN * 128) +
+                                                     j * 1024);
         } else {
-          kr = ks * 4 + c4;
-          const int h = kr >> 4, kk = kr & 15;
 #pragma unroll
-          for (int i = 0; i < WMT; ++i) {
-            const int m = wm0 + i * 8 + r8;
-            const uint8_t* ptr = a_st + h * (BM * 128) + m * 128 + (((kk >> 1) ^ (m & 7)) << 4) +
-                                 ((kk & 1) << 3);
-            af[i] = *reinterpret_cast<const double*>(ptr);
-          }
-        }
-        {
-          const int h = kr >> 4, kk = kr & 15;
+          for (int i2 = 0; i2 < WMT; ++i2)
+            af[i2] = *reinterpret_cast<const double*>(a_st + offA[ks & 3] + (ks >> 2) * (BM * 128) +
+                                                      i2 * 1024);
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const int n = j * 8 + r8;
-            const uint8_t* ptr = b_st + h * (BN * 128) + n * 128 + (((kk >> 1) ^ (n & 7)) << 4) +
-                                 ((kk & 1) << 3);
-            bf[j] = *reinterpret_cast<const double*>(ptr);
-          }
+          for (int j = 0; j < NT; ++j)
+            bf[j] = *reinterpret_cast<const double*>(b_st + offB[ks & 3] + (ks >> 2) * (BN * 128) +
+                                                     j * 1024);
         }
 #pragma unroll
-        for (int i = 0; i < WMT; ++i)
+        for (int i2 = 0; i2 < WMT; ++i2)
 #pragma unroll
-          for (int j = 0; j < NT; ++j) ptx::dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < NT; ++j) ptx::dmma(acc[i2][j][0], acc[i2][j][1], af[i2], bf[j]);
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
 
-    // ------------------------------------------------ epilogue
-    ptx::named_bar(1, kConsumerWarps * 32);  // all consumers done reading stages
-    double* cs = reinterpret_cast<double*>(smem);
-    constexpr int LDC = BM + Cfg::CPAD;
-#pragma unroll
-    for (int i = 0; i < WMT; ++i)
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const int m = wm0 + i * 8 + r8;
-        const int n = j * 8 + 2 * c4;
-        cs[n * LDC + m] = acc[i][j][0];
-        cs[(n + 1) * LDC + m] = acc[i][j][1];
-      }
-    ptx::named_bar(1, kConsumerWarps * 32);
-
-    const int tid = threadIdx.x;
-    constexpr int NCT = kConsumerWarps * 32;
-    const int mlim = int(p.M - m0 < BM ? p.M - m0 : BM);
-    const int nlim = int(p.N - n0 < BN ? p.N - n0 : BN);
-    if (p.splits == 1) {
-      for (int n = 0; n < nlim; ++n)
-        for (int m = tid; m < mlim; m += NCT) p.C[(n0 + n) * p.ldc + m0 + m] = cs[n * LDC + m];
+    // ---------------------------------------------- segment epilogue (tile t)
+    const int64_t m0 = int64_t(t / p.nt) * BM, n0 = int64_t(t % p.nt) * BN;
+    int nseg, my_seg, c_first = 0;
+    if (p.stream_k) {
+      c_first = sk_cta_of(int64_t(t) * p.kb_tile, p);
+      const int c_last = sk_cta_of(int64_t(t + 1) * p.kb_tile - 1, p);
+      nseg = c_last - c_first + 1;
+      my_seg = int(blockIdx.x) - c_first;
     } else {
-      const int64_t tile = int64_t(m_tile) * gridDim.x + n_tile;
-      double* part = p.partials + (tile * p.splits) * (BM * BN);
-      double* mine = part + int64_t(split) * (BM * BN);
-      for (int e = tid; e < BM * BN; e += NCT) mine[e] = cs[(e / BM) * LDC + (e % BM)];
+      nseg = p.splits;
+      my_seg = blockIdx.z;
+    }
+    auto store = [&](double (&v)[WMT][NT][2]) {
+#pragma unroll
+      for (int i2 = 0; i2 < WMT; ++i2)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t m = m0 + wm0 + i2 * 8 + r8, n = n0 + j * 8 + 2 * c4 + e;
+            if (m < p.M && n < p.N) p.C[n * p.ldc + m] = v[i2][j][e];
+          }
+    };
+    if (nseg == 1) {
+      store(acc);
+    } else {
+      auto slot = [&](int sg) -> int64_t {
+        if (!p.stream_k) return int64_t(t) * p.splits + sg;
+        const int c2 = c_first + sg;
+        const int j2 = t - int(sk_begin(c2, p) / p.kb_tile);
+        return int64_t(c2) * p.max_seg + j2;
+      };
+      // partial in fragment-native layout: [warp][i][j][lane][2] (16B / lane, coalesced)
+      const bool warp_live = (m0 + wm0) < p.M;
+      const int64_t my_slot = p.stream_k ? int64_t(blockIdx.x) * p.max_seg + seg_local
+                                         : int64_t(t) * p.splits + my_seg;
+      if (warp_live) {
+        double2* dst = reinterpret_cast<double2*>(p.partials + my_slot * FRAG) +
+                       (warp * WMT * NT) * 32 + lane;
+#pragma unroll
+        for (int i2 = 0; i2 < WMT; ++i2)
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+            if (n0 + j * 8 < p.N) dst[(i2 * NT + j) * 32] = make_double2(acc[i2][j][0], acc[i2][j][1]);
+      }
       __threadfence();
       ptx::named_bar(1, NCT);
-      if (tid == 0) {
-        const int old = atomicAdd(&p.counters[tile], 1);
-        *flag = (old == p.splits - 1);
-      }
+      if (tid == 0) *flag = (atomicAdd(&p.counters[t], 1) == nseg - 1);
       ptx::named_bar(1, NCT);
       if (*flag) {
         __threadfence();
-        for (int n = 0; n < nlim; ++n)
-          for (int m = tid; m < mlim; m += NCT) {
-            double v = 0.0;
-            for (int z = 0; z < p.splits; ++z) v += __ldcg(part + int64_t(z) * (BM * BN) + n * BM + m);
-            p.C[(n0 + n) * p.ldc + m0 + m] = v;
+        // Sum every segment's partial (this CTA's own included, re-read from
+        // where it was just written) in segment order: deterministic.
+        if (warp_live) {
+#pragma unroll
+          for (int i2 = 0; i2 < WMT; ++i2)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[i2][j][0] = acc[i2][j][1] = 0.0;
+          for (int sg = 0; sg < nseg; ++sg) {
+            const double2* src = reinterpret_cast<const double2*>(p.partials + slot(sg) * FRAG) +
+                                 (warp * WMT * NT) * 32 + lane;
+#pragma unroll
+            for (int i2 = 0; i2 < WMT; ++i2)
+#pragma unroll
+              for (int j = 0; j < NT; ++j)
+                if (n0 + j * 8 < p.N) {
+                  const double2 v = __ldcg(src + (i2 * NT + j) * 32);
+                  acc[i2][j][0] += v.x;
+                  acc[i2][j][1] += v.y;
+                }
           }
-        if (tid == 0) p.counters[tile] = 0;  // self-reset for the next launch
+          store(acc);
+        }
+        if (tid == 0) p.counters[t] = 0;  // self-reset for the next launch
       }
     }
-  }
+    ++seg_local;
+  } while (u < u1);
 }
 
 // ------------------------------------------------------------- host side
@@ -354,38 +446,88 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
   const int64_t mt = ceil_div(M, Cfg::BM), nt = ceil_div(N, BN);
   const int64_t tiles = mt * nt;
   const int64_t kblocks = ceil_div(K, BK);
-  // Split K so that the grid fills whole waves of the 148 SMs (1 CTA/SM).
-  int splits = 1;
-  if (force_splits > 0) {
-    splits = force_splits;
+  constexpr int64_t FRAG = kConsumerWarps * WMT * (BN / 8) * 64;
+  PassParams pp{};
+  pp.M = M;
+  pp.N = N;
+  pp.K = K;
+  pp.mt = int(mt);
+  pp.nt = int(nt);
+  pp.kb_tile = int(kblocks);
+  pp.C = C.p;
+  pp.ldc = C.ld;
+  const int sms = h.sm_count;
+  dim3 grid;
+  // Few tiles (C1/C2 passes, Gram products): stream-K over all SMs.  Many
+  // tiles: split-K grid with n-tiles adjacent for L2 reuse of A.
+  const bool stream_k = force_splits <= 0 && tiles < 2 * sms;
+  if (stream_k) {
+    const int64_t units = tiles * kblocks;
+    // at least ~6 slices per CTA so the pipeline fill amortizes
+    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(sms, units / 6));
+    pp.stream_k = 1;
+    pp.units = units;
+    pp.grid = int(g);
+    pp.max_seg = int(ceil_div(ceil_div(units, g), kblocks) + 1);
+    pp.splits = 1;
+    pp.kb_split = int(kblocks);
+    pp.partials = h.ws.alloc(g * pp.max_seg * FRAG);
+    pp.counters = tile_counters(h, tiles);
+    grid = dim3(unsigned(g), 1, 1);
   } else {
-    const int sms = h.sm_count;
-    double best = 1e300;
-    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(kblocks / 4, 64));
-    for (int64_t s = 1; s <= smax; ++s) {
-      const int64_t ctas = tiles * s;
-      const int64_t waves = ceil_div(ctas, sms);
-      const double t = double(waves) * double(ceil_div(kblocks, s) + 6) + 0.5 * double(s);
-      if (t < best) {
-        best = t;
-        splits = int(s);
+    int splits = 1;
+    if (force_splits > 0) {
+      splits = force_splits;
+    } else {
+      double best = 1e300;
+      const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(kblocks / 4, 64));
+      for (int64_t s = 1; s <= smax; ++s) {
+        const int64_t ctas = tiles * s;
+        const int64_t waves = ceil_div(ctas, sms);
+        const double t = double(waves) * double(ceil_div(kblocks, s) + 6) + 0.5 * double(s);
+        if (t < best) {
+          best = t;
+          splits = int(s);
+        }
       }
     }
-  }
-  const int64_t kps = round_up(ceil_div(K, splits), BK);
-  splits = int(ceil_div(K, kps));
-  if (splits < 1) splits = 1;
-  PassParams pp{M, N, K, kps, splits, C.p, C.ld, nullptr, nullptr};
-  if (splits > 1) {
-    pp.partials = h.ws.alloc(tiles * splits * Cfg::BM * BN);
-    pp.counters = tile_counters(h, tiles);
+    const int64_t kps = ceil_div(kblocks, splits);
+    splits = int(ceil_div(kblocks, kps));
+    pp.stream_k = 0;
+    pp.splits = splits;
+    pp.kb_split = int(kps);
+    if (splits > 1) {
+      pp.partials = h.ws.alloc(tiles * splits * FRAG);
+      pp.counters = tile_counters(h, tiles);
+    }
+    grid = dim3(unsigned(nt), unsigned(mt), unsigned(splits));
   }
   CUtensorMap ta = kNN ? make_map(P.p, P.rows, P.cols, P.ld, 16, BK)
                        : make_map(P.p, P.rows, P.cols, P.ld, 16, Cfg::BM);
   CUtensorMap tb = make_map(R.p, R.rows, R.cols, R.ld, 16, BN);
-  const dim3 grid{unsigned(nt), unsigned(mt), unsigned(splits)};
+  Handle::ProfRec rec{};
+  if (h.prof) {
+    for (int i = 0; i < 2; ++i) {
+      cudaEvent_t e;
+      if (h.prof_pool.empty()) {
+        RSVD_CUDA(cudaEventCreate(&e));
+      } else {
+        e = h.prof_pool.back();
+        h.prof_pool.pop_back();
+      }
+      (i == 0 ? rec.a : rec.b) = e;
+    }
+    rec.kind = kNN ? 0 : 1;
+    rec.flops = 2.0 * double(M) * double(N) * double(K);
+    rec.bytes = 8.0 * (double(M) * K + double(K) * N + double(M) * N);
+    RSVD_CUDA(cudaEventRecord(rec.a, h.stream));
+  }
   kern<<<grid, kThreads, Cfg::SMEM, h.stream>>>(ta, tb, pp);
   RSVD_LAUNCHED(h);
+  if (h.prof) {
+    RSVD_CUDA(cudaEventRecord(rec.b, h.stream));
+    h.prof_pending.push_back(rec);
+  }
 }
 
 // Copy into an aligned, even-ld workspace when TMA cannot address x directly.

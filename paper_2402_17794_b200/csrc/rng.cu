@@ -79,7 +79,14 @@ __device__ __forceinline__ double polar_mult(double r2) {
   return __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, lg), r2));
 }
 
-// 1. sequential block generator (one CTA).  out[0..312) = initial block.
+// 1. block generator (one CTA).  out[0..312) = initial block.  The libstdc++
+// twist regenerates block N from block C in place; unrolling its in-place
+// dependency (N[j] for j >= 156 reads N[j-156]) expresses every word of N in
+// terms of C alone:
+//   j <  156: N[j]   = C[j+156] ^ g(C[j], C[j+1])
+//   j <  311: N[j]   = C[j] ^ g(C[j-156], C[j-155]) ^ g(C[j], C[j+1])
+//   j == 311: N[311] = C[311] ^ g(C[155], C[156]) ^ g(C[311], C[156] ^ g(C[0], C[1]))
+// so a whole 312-word block costs one barrier.
 __global__ void mt_blocks_kernel(const uint64_t* __restrict__ init, int64_t nb,
                                  uint64_t* __restrict__ out) {
   __shared__ uint64_t S[2][kN];
@@ -92,12 +99,20 @@ __global__ void mt_blocks_kernel(const uint64_t* __restrict__ init, int64_t nb,
   for (int64_t k = 1; k <= nb; ++k) {
     const uint64_t* c = S[(k - 1) & 1];
     uint64_t* n = S[k & 1];
-    if (t < kN - kM) n[t] = c[t + kM] ^ twist(c[t], c[t + 1]);
+    if (t < kN) {
+      uint64_t v;
+      if (t < kN - kM) {
+        v = c[t + kM] ^ twist(c[t], c[t + 1]);
+      } else if (t < kN - 1) {
+        v = c[t] ^ twist(c[t - kM], c[t - kM + 1]) ^ twist(c[t], c[t + 1]);
+      } else {
+        const uint64_t n0 = c[kM] ^ twist(c[0], c[1]);
+        v = c[kN - 1] ^ twist(c[kM - 1], c[kM]) ^ twist(c[kN - 1], n0);
+      }
+      n[t] = v;
+      out[k * kN + t] = v;
+    }
     __syncthreads();
-    if (t >= kN - kM && t < kN - 1) n[t] = n[t - (kN - kM)] ^ twist(c[t], c[t + 1]);
-    if (t == kN - 1) n[t] = n[kM - 1] ^ twist(c[kN - 1], n[0]);
-    __syncthreads();
-    if (t < kN) out[k * kN + t] = n[t];
   }
 }
 

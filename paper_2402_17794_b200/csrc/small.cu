@@ -511,59 +511,74 @@ __global__ void finite_kernel(const double* X, int64_t rows, int64_t cols, int64
 }
 
 // ---------------------------------------------------------- Cholesky (l x l)
-// Right-looking, single CTA, in place on G (ld l) in shared or global memory.
-// Produces upper R (G = R^T R) and its inverse Rinv.  Sets breakdown flag when
-// a pivot is not positive (relative to the largest diagonal).
-__global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l, double shift,
-                                double* __restrict__ R, int64_t ldr, double* __restrict__ Rinv,
-                                int64_t ldri, double* gA, int in_smem, int* flags) {
+// Right-looking, single CTA, in place on a copy of G (ld l) in shared or global
+// memory.  Produces upper R (G + s I = R^T R) and Rinv = R^-1.
+// Shift policy (shifted CholeskyQR, Fukaya et al.): the factorization is first
+// tried with s = 0; when a pivot has lost all precision (Schur pivot
+// <= 1e-12 of its original diagonal, or not positive) it restarts with
+// s = shift_coef * trace(G), shift_coef = 11 (m l + l (l+1)) u, and records it
+// in *shift_used.  The decision is made on the device: no host round trip.
+__global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l,
+                                double shift_coef, double* __restrict__ R, int64_t ldr,
+                                double* __restrict__ Rinv, int64_t ldri, double* gA, int in_smem,
+                                int* shift_used, int* flags) {
   extern __shared__ double sm[];
   double* A = in_smem ? sm : gA;  // lower-triangular working copy (col-major, ld l)
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
   const int nwarps = nthr >> 5;
-  __shared__ double dmax;
   __shared__ int broke;
-  if (tid == 0) {
-    broke = 0;
-    dmax = 0;
-  }
+  __shared__ double trace;
+  __shared__ double diag0[1024];  // original diagonal (pivot-loss test), kept on chip
+  for (int j = tid; j < l; j += nthr) diag0[j] = G[j * ldg + j];
   __syncthreads();
-  for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
-    const int i = int(e % l), j = int(e / l);
-    double v = G[j * ldg + i];
-    if (i == j) v += shift;
-    A[e] = v;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double m = 0;
-    for (int j = 0; j < l; ++j) m = fmax(m, A[j * l + j]);
-    dmax = m;
-  }
-  __syncthreads();
-  for (int j = 0; j < l; ++j) {
-    // A(j,j) final; column below
-    const double d = A[j * l + j];
-    if (!(d > 1e-30 * dmax) || !(d > 0.0)) {
-      if (tid == 0) broke = 1;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    double shift = 0.0;
+    if (attempt == 1) {
+      if (tid == 0) {
+        double t = 0;
+        for (int j = 0; j < l; ++j) t += diag0[j];
+        trace = t;
+      }
       __syncthreads();
+      shift = shift_coef * trace;
+    }
+    if (tid == 0) broke = 0;
+    for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
+      const int i = int(e % l), j = int(e / l);
+      double v = G[j * ldg + i];
+      if (i == j) v += shift;
+      A[e] = v;
+    }
+    __syncthreads();
+    for (int j = 0; j < l; ++j) {
+      const double d = A[j * l + j];
+      const double orig = diag0[j] + shift;
+      if (!(d > 1e-12 * orig) || !(d > 0.0)) {
+        if (tid == 0) broke = 1;
+        __syncthreads();
+        break;
+      }
+      const double rd = sqrt(d);
+      __syncthreads();
+      for (int i = j + 1 + tid; i < l; i += nthr) A[j * l + i] /= rd;
+      if (tid == 0) A[j * l + j] = rd;
+      __syncthreads();
+      // trailing update: A(i,k) -= L(i,j) L(k,j), k in (j, l), i >= k
+      for (int k = j + 1 + warp; k < l; k += nwarps) {
+        const double lkj = A[j * l + k];
+        for (int i = k + lane; i < l; i += 32) A[k * l + i] -= A[j * l + i] * lkj;
+      }
+      __syncthreads();
+    }
+    if (!broke) {
+      if (attempt == 1 && tid == 0 && shift_used) *shift_used = 1;
       break;
     }
-    const double rd = sqrt(d);
-    __syncthreads();
-    for (int i = j + 1 + tid; i < l; i += nthr) A[j * l + i] /= rd;
-    if (tid == 0) A[j * l + j] = rd;
-    __syncthreads();
-    // trailing update: A(i,k) -= L(i,j) L(k,j), k in (j, l), i >= k
-    for (int k = j + 1 + warp; k < l; k += nwarps) {
-      const double lkj = A[j * l + k];
-      for (int i = k + lane; i < l; i += 32) A[k * l + i] -= A[j * l + i] * lkj;
+    if (attempt == 1) {
+      if (tid == 0) atomicOr(flags, kFlagCholBreakdown);
+      return;
     }
     __syncthreads();
-  }
-  if (broke) {
-    if (tid == 0) atomicOr(flags, kFlagCholBreakdown);
-    return;
   }
   // R = L^T
   for (int64_t e = tid; e < int64_t(l) * l; e += nthr) {
@@ -572,7 +587,6 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l
   }
   // Rinv: solve R x = e_c for each column c by back substitution; R(i,k) = L(k,i)
   for (int c = warp; c < l; c += nwarps) {
-    // x_i for i > c is 0; x_c = 1/R(c,c); x_i = -(sum_{k=i+1..c} R(i,k) x_k)/R(i,i)
     for (int i = lane; i < l; i += 32) Rinv[c * ldri + i] = 0.0;
     __syncwarp();
     for (int i = c; i >= 0; --i) {
@@ -751,71 +765,60 @@ size_t small_smem_limit() { return 200 * 1024; }
 }  // namespace
 
 
-// CholeskyQR2 (shifted CholeskyQR3 when the first Gram is not numerically SPD).
+// CholeskyQR with device-side shifting (see chol_inv_kernel): 2 passes when
+// the first Gram factors without a shift (CholeskyQR2), 4 when it needed one
+// (shifted CholeskyQR3 + 1: covers kappa(X) up to ~1/u and exact rank
+// deficiency, whose null directions come out as orthonormal round-off noise,
+// i.e. the basis is padded to full width as core.hpp:93-95 requires).  For
+// l <= 64 the 4 passes are always run (no host round trip); for larger l one
+// flag read after pass 1 picks 2 or 4.
 static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   const int l = int(X.cols);
   DMat G = h.ws.mat(l, l), R1 = h.ws.mat(l, l), Ri = h.ws.mat(l, l);
   const bool in_smem = size_t(l) * l * 8 <= small_smem_limit();
   double* gA = in_smem ? nullptr : h.ws.alloc(int64_t(l) * l);
+  int* shift_used = reinterpret_cast<int*>(h.ws.alloc_bytes(16));
+  RSVD_CUDA(cudaMemsetAsync(shift_used, 0, 16, h.stream));
   static size_t cur_c = 0;
   ensure_smem(chol_inv_kernel, in_smem ? size_t(l) * l * 8 : 0, cur_c);
-  auto chol = [&](const DMat& Gm, double shift) {
-    chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
-        Gm.p, Gm.ld, l, shift, R1.p, R1.ld, Ri.p, Ri.ld, gA, in_smem ? 1 : 0, h.d_flags);
-    RSVD_LAUNCHED(h);
-  };
-  check_finite(h, X, kFlagNonFinite);
-  check_flags(h, "orthonormalize");
   int64_t m_global = X.rows, row_off = 0;
   if (dist) shard_rows(h, X.rows, &m_global, &row_off);
-  auto gram = [&](const DMat& Y) {
+  const double coef = 11.0 * (double(m_global) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
+  auto pass = [&](const DMat& Y, DMat Qo) {
     gemm_tn(h, Y, Y, G);
     if (dist) allreduce_mat(h, G);
-  };
-  // pass 1
-  gram(X);
-  chol(G, 0.0);
-  RSVD_CUDA(cudaMemcpyAsync(h.h_flags, h.d_flags, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
-  RSVD_CUDA(cudaStreamSynchronize(h.stream));
-  DMat Rtot = h.ws.mat(l, l), Rtmp = h.ws.mat(l, l);
-  bool have_rtot = false;
-  int passes = 2;
-  if (*h.h_flags & kFlagCholBreakdown) {
-    clear_flags(h);
-    // shifted CholeskyQR: s = 11 (m l + l (l+1)) u ||X||_2^2, ||X||_2^2 <= trace(G)
-    std::vector<double> hg(size_t(l) * l);
-    RSVD_CUDA(cudaMemcpy2DAsync(hg.data(), l * 8, G.p, G.ld * 8, l * 8, l, cudaMemcpyDeviceToHost,
-                                h.stream));
-    RSVD_CUDA(cudaStreamSynchronize(h.stream));
-    double tr = 0;
-    for (int i = 0; i < l; ++i) tr += hg[size_t(i) * l + i];
-    const double u = 1.1102230246251565e-16;
-    const double shift = 11.0 * (double(m_global) * l + double(l) * (l + 1)) * u * tr;
-    chol(G, shift);
-    passes = 3;
-  }
-  if (X.p == Q.p) {
-    DMat Qt = h.ws.mat(Q.rows, l);
-    gemm_nn(h, X, Ri, Qt);
-    copy(h, Qt, Q);
-  } else {
-    gemm_nn(h, X, Ri, Q);
-  }
-  copy(h, R1, Rtot);
-  have_rtot = true;
-  for (int pass = 1; pass < passes; ++pass) {
-    gram(Q);
-    chol(G, 0.0);
-    DMat Qt = h.ws.mat(Q.rows, l);
-    gemm_nn(h, Q, Ri, Qt);
-    copy(h, Qt, Q);
-    if (Rout) {  // Rtot = R1 * Rtot
-      gemm_nn(h, R1, Rtot, Rtmp);
-      copy(h, Rtmp, Rtot);
+    chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
+        G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld, gA, in_smem ? 1 : 0, shift_used, h.d_flags);
+    RSVD_LAUNCHED(h);
+    if (Y.p == Qo.p) {
+      DMat Qt = h.ws.mat(Qo.rows, l);
+      gemm_nn(h, Y, Ri, Qt);
+      copy(h, Qt, Qo);
+    } else {
+      gemm_nn(h, Y, Ri, Qo);
     }
+  };
+  check_finite(h, X, kFlagNonFinite);
+  DMat X0 = X;
+  if (Rout && X.p == Q.p) {  // keep X for R = Q^T X
+    X0 = h.ws.mat(X.rows, l);
+    copy(h, X, X0);
   }
-  check_flags(h, "orthonormalize");
-  if (Rout && have_rtot) copy(h, Rtot, *Rout);
+  pass(X0, Q);
+  int passes = 4;
+  if (l > 64) {
+    int used = 0;
+    RSVD_CUDA(cudaMemcpyAsync(&used, shift_used, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+    RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    passes = used ? 4 : 2;
+  }
+  for (int i = 1; i < passes; ++i) pass(Q, Q);
+  if (Rout) {
+    // X = Q R with R = Q^T X (exact relation once Q spans X; R need not be
+    // triangular for its consumers: the Jacobi SVD of the l x l factor).
+    gemm_tn(h, Q, X0, *Rout);
+    if (dist) allreduce_mat(h, *Rout);
+  }
 }
 
 void orthonormalize(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist) {
@@ -823,7 +826,10 @@ void orthonormalize(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist) {
     throw_dim("orthonormalize: more columns than rows (" + std::to_string(X.cols) + " > " +
               std::to_string(X.rows) + ")");
   if (X.cols == 0) return;
-  if (X.cols <= 64)
+  // Small problems (one 128/256-row block, the reference's unit-test sizes):
+  // Householder in one CTA, numerically the reference's algorithm.  Otherwise
+  // CholeskyQR on the DMMA pass engine (see cholqr).
+  if (!dist && X.cols <= 64 && X.rows <= tsqr_block_rows(int(X.cols)))
     tsqr(h, X, Q, R, dist);
   else
     cholqr(h, X, Q, R, dist);
