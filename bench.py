@@ -59,6 +59,15 @@ def sigma_c3(n):
     return np.exp(-np.arange(1, n + 1) / 50.0)
 
 
+def lambda_c4(n):
+    j = np.arange(1, n + 1, dtype=np.float64)
+    return np.where(j % 2 == 0, 1.0, -1.0) * j ** -1.5
+
+
+def sigma_c5(r):
+    return np.exp(-np.arange(1, r + 1) / 200.0)
+
+
 CONFIGS = {
     "C1": dict(alg=2, mode="basic", m=2048, n=1024, k=20, p=5, q=0, sigma=sigma_c1,
                name="Alg2 basic 2048x1024 k20 p5 q0"),
@@ -66,6 +75,10 @@ CONFIGS = {
                name="Alg3 power 8192x8192 k20 p5 q2"),
     "C3": dict(alg=4, mode="power_ortho", m=65536, n=16384, k=100, p=10, q=2, sigma=sigma_c3,
                name="Alg4 ortho 65536x16384 k100 p10 q2"),
+    "C4": dict(alg=5, mode="spevd", m=32768, n=32768, k=200, p=20, q=0, sigma=lambda_c4,
+               name="Alg5 single-pass Hermitian 32768^2 k200 p20"),
+    "C5": dict(alg=6, mode="spsvd", m=262144, n=32768, k=500, p=50, q=0, sigma=sigma_c5, rank=1000,
+               noise=1e-6, name="Alg6 single-pass general 262144x32768 k500 p50"),
 }
 SEED_U, SEED_V, SEED_OMEGA = 1001, 1002, 1
 
@@ -86,6 +99,30 @@ def make_input(cfg, device):
         q *= torch.sign(torch.diagonal(rr))
         return q
 
+    if cfg["alg"] == 5:  # A = U diag(lambda) U^T, exactly symmetric
+        u = haar(n, n, SEED_U)
+        lam = torch.from_numpy(cfg["sigma"](n)).to(device)
+        a = (u * lam) @ u.t()
+        del u
+        a.add_(a.t().clone()).mul_(0.5)
+        return a.t()
+    if cfg["alg"] == 6:  # low rank + noise, generated in row chunks
+        r = cfg["rank"]
+        u = haar(m, r, SEED_U)
+        v = haar(n, r, SEED_V)
+        s = torch.from_numpy(cfg["sigma"](r)).to(device)
+        at = torch.empty((n, m), dtype=torch.float64, device=device)
+        g.manual_seed(1003)
+        step = 8192
+        vs = v * s
+        for c0 in range(0, m, step):
+            c1 = min(m, c0 + step)
+            blk = vs @ u[c0:c1].t()
+            blk.add_(torch.randn(blk.shape, dtype=torch.float64, device=device, generator=g),
+                     alpha=cfg["noise"])
+            at[:, c0:c1] = blk
+        del u, v, vs
+        return at.t()
     u = haar(m, r, SEED_U)
     v = haar(n, r, SEED_V)
     s = torch.from_numpy(cfg["sigma"](r)).to(device)
@@ -154,12 +191,18 @@ def cpu_reference(cfg, steps, warmup, threads, a_host=None):
         import torch
         dev = "cuda" if torch.cuda.is_available() else "cpu"
         a_host = np.asfortranarray(make_input(cfg, dev).cpu().numpy())
-    mode = {"basic": 0, "power": 1, "power_ortho": 2}[cfg["mode"]]
+    def run():
+        if cfg["alg"] == 5:
+            return oracle.spevd_hermitian(a_host, cfg["k"], cfg["p"], oracle.Rng(SEED_OMEGA))
+        if cfg["alg"] == 6:
+            return oracle.spsvd_general(a_host, cfg["k"], cfg["p"], oracle.Rng(SEED_OMEGA))
+        mode = {"basic": 0, "power": 1, "power_ortho": 2}[cfg["mode"]]
+        return oracle.rsvd(a_host, cfg["k"], cfg["p"], cfg["q"], mode, oracle.Rng(SEED_OMEGA))
     for _ in range(warmup):
-        oracle.rsvd(a_host, cfg["k"], cfg["p"], cfg["q"], mode, oracle.Rng(SEED_OMEGA))
+        run()
     t0 = time.perf_counter()
     for _ in range(steps):
-        oracle.rsvd(a_host, cfg["k"], cfg["p"], cfg["q"], mode, oracle.Rng(SEED_OMEGA))
+        run()
     dt = (time.perf_counter() - t0) / max(steps, 1)
     return dt
 
@@ -231,7 +274,7 @@ def main():
     rows = np.array_split(np.arange(m), world)[rank]
     r0, r1 = int(rows[0]), int(rows[-1]) + 1
     a_loc = a_full[r0:r1, :].t().contiguous().t() if world > 1 else a_full
-    mode = eng.RangeMode[cfg["mode"]]
+    mode = eng.RangeMode[cfg["mode"]] if cfg["alg"] <= 4 else eng.RangeMode.basic
     sk = eng.SketchConfig(k, p, q, mode, SEED_OMEGA)
     torch.cuda.synchronize()
 
@@ -240,6 +283,10 @@ def main():
             dist.barrier()
 
     def step():
+        if cfg["alg"] == 5:
+            return eng.spevd_hermitian(a_loc, k, p, eng.Rng(SEED_OMEGA))
+        if cfg["alg"] == 6:
+            return eng.spsvd_general(a_loc, k, p, eng.Rng(SEED_OMEGA))
         return eng.rsvd(a_loc, sk, eng.Rng(SEED_OMEGA))
 
     with eng.using_engine(engine):
@@ -279,12 +326,18 @@ def main():
         u_h = torch.empty((l, r1 - r0), dtype=torch.float64, pin_memory=True).numpy().T
         v_h = torch.empty((l, n), dtype=torch.float64, pin_memory=True).numpy().T
         s_h = torch.empty(l, dtype=torch.float64, pin_memory=True).numpy()
-        eng.rsvd_host(a_host, sk, eng.Rng(SEED_OMEGA), out=(u_h, s_h, v_h))  # warm
+        def host_step():
+            if cfg["alg"] == 5:
+                return eng.spevd_host(a_host, k, p, eng.Rng(SEED_OMEGA))
+            if cfg["alg"] == 6:
+                return eng.spsvd_host(a_host, k, p, eng.Rng(SEED_OMEGA))
+            return eng.rsvd_host(a_host, sk, eng.Rng(SEED_OMEGA), out=(u_h, s_h, v_h))
+        host_step()  # warm
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            eng.rsvd_host(a_host, sk, eng.Rng(SEED_OMEGA), out=(u_h, s_h, v_h))
+            host_step()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
         barrier()
         if world > 1:

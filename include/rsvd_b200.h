@@ -100,6 +100,11 @@ rsvd_status rsvd_reset_counters(rsvd_handle* h);
 rsvd_status rsvd_profile_enable(rsvd_handle* h, int on);
 rsvd_status rsvd_profile_read(rsvd_handle* h, int kind, int64_t* launches, double* ms,
                               double* flops, double* bytes);
+/* Launch-site trace: when enabled, the device time between consecutive
+ * kernel launches (kernel plus any idle gap before it) is accumulated per
+ * source launch site; the report is "site count total_ms" lines. */
+rsvd_status rsvd_trace_enable(rsvd_handle* h, int on);
+rsvd_status rsvd_trace_report(rsvd_handle* h, char* buf, int64_t len);
 /* Row-sharding info (1 / 0 for a single-GPU handle). */
 rsvd_status rsvd_dist_info(rsvd_handle* h, int* rank, int* nranks);
 

@@ -117,6 +117,8 @@ def _load():
             "rsvd_reset_counters": [P],
             "rsvd_dist_info": [P, ctypes.POINTER(I), ctypes.POINTER(I)],
             "rsvd_profile_enable": [P, I],
+            "rsvd_trace_enable": [P, I],
+            "rsvd_trace_report": [P, ctypes.c_char_p, I64],
             "rsvd_profile_read": [P, I, ctypes.POINTER(I64), ctypes.POINTER(D), ctypes.POINTER(D),
                                   ctypes.POINTER(D)],
             "rsvd_gaussian_dev": [P, I64, I64, PS, P, I64],
@@ -216,6 +218,19 @@ class Engine:
                                              ctypes.byref(fl), ctypes.byref(by)))
             out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
         return out
+
+    def trace(self, on: bool = True) -> None:
+        """Charge device time between consecutive launches to launch sites."""
+        _check(_load().rsvd_trace_enable(self._h, 1 if on else 0))
+
+    def trace_report(self) -> list:
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(_load().rsvd_trace_report(self._h, buf, len(buf)))
+        rows = []
+        for line in buf.value.decode().splitlines():
+            site, cnt, ms = line.rsplit(" ", 2)
+            rows.append((site, int(cnt), float(ms)))
+        return sorted(rows, key=lambda r: -r[2])
 
     def synchronize(self) -> None:
         _check(_load().rsvd_synchronize(self._h))
@@ -694,6 +709,34 @@ def rsvd_host(a: np.ndarray, cfg: SketchConfig, rng: Optional[Rng] = None, out=N
                                   int(cfg.mode), ctypes.byref(rng.state), P(u), max(m, 1), P(s),
                                   P(v), max(n, 1)))
     return SvdApprox(u, s, v)
+
+
+def spevd_host(a: np.ndarray, k: int, p: int, rng: Rng):
+    """End-to-end host-buffer spevd_hermitian (rsvd_spevd_host)."""
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
+        a = np.asfortranarray(a, dtype=np.float64)
+    n = a.shape[0]
+    kk = max(k, 0)
+    u, lam = np.empty((n, kk), order="F"), np.empty(max(kk, 1))
+    e = _eng()
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+    _check(_load().rsvd_spevd_host(e.handle, n, P(a), max(n, 1), k, p, ctypes.byref(rng.state),
+                                   P(u), max(n, 1), P(lam)))
+    return EvdApprox(u, lam[:kk])
+
+
+def spsvd_host(a: np.ndarray, k: int, p: int, rng: Rng):
+    """End-to-end host-buffer spsvd_general (rsvd_spsvd_host)."""
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
+        a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    kk = max(k, 0)
+    u, s, v = np.empty((m, kk), order="F"), np.empty(max(kk, 1)), np.empty((n, kk), order="F")
+    e = _eng()
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+    _check(_load().rsvd_spsvd_host(e.handle, m, n, P(a), max(m, 1), k, p, ctypes.byref(rng.state),
+                                   P(u), max(m, 1), P(s), P(v), max(n, 1)))
+    return SvdApprox(u, s[:kk], v)
 
 
 def debug_log_cr(x: float) -> float:

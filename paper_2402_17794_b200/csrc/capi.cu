@@ -26,6 +26,7 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
     RSVD_CUDA(cudaSetDevice(h.device));
     h.ws.reset();
     h.rng_user_out = nullptr;
+    rsvdb::trace_begin(h);
     f(h);
     rsvdb::finish_call(h, what);
     return RSVD_OK;
@@ -138,10 +139,12 @@ void rsvd_destroy(rsvd_handle* hd) {
   cudaStreamSynchronize(h.stream);
   rsvdb::comm_destroy(h);
   if (h.d_counters) cudaFree(h.d_counters);
+  if (h.d_jump) cudaFree(h.d_jump);
   if (h.d_flags) cudaFree(h.d_flags);
   if (h.h_flags) cudaFreeHost(h.h_flags);
   if (h.h_rng) cudaFreeHost(h.h_rng);
   for (auto e : h.prof_pool) cudaEventDestroy(e);
+  for (auto e : h.trace_pool) cudaEventDestroy(e);
   if (h.own_stream) cudaStreamDestroy(h.own_stream);
   delete hd;
 }
@@ -188,6 +191,27 @@ rsvd_status rsvd_profile_read(rsvd_handle* hd, int kind, int64_t* launches, doub
   if (ms) *ms = h.prof_ms[kind];
   if (flops) *flops = h.prof_flops[kind];
   if (bytes) *bytes = h.prof_bytes[kind];
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_trace_enable(rsvd_handle* hd, int on) {
+  if (!hd) return RSVD_ERR_PARAMETER;
+  hd->h.trace = on != 0;
+  hd->h.trace_acc.clear();
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_trace_report(rsvd_handle* hd, char* buf, int64_t len) {
+  if (!hd || !buf || len < 1) return RSVD_ERR_PARAMETER;
+  std::string out;
+  for (auto& kv : hd->h.trace_acc) {
+    const char* site = kv.first.c_str();
+    const char* slash = std::strrchr(site, '/');
+    out += std::string(slash ? slash + 1 : site) + " " + std::to_string(kv.second.first) + " " +
+           std::to_string(kv.second.second) + "\n";
+  }
+  std::strncpy(buf, out.c_str(), size_t(len - 1));
+  buf[len - 1] = 0;
   return RSVD_OK;
 }
 

@@ -36,10 +36,13 @@ struct Error : std::runtime_error {
 #define RSVD_LAUNCH_CHECK() RSVD_CUDA(cudaGetLastError())
 // Every kernel launch of the engine goes through this: error check + count
 // (rsvd_counters.kernel_launches, reported by bench.py as gpu_launches).
-#define RSVD_LAUNCHED(hh)    \
-  do {                       \
-    RSVD_LAUNCH_CHECK();     \
-    (hh).counters.kernel_launches++; \
+#define RSVD_STR2(x) #x
+#define RSVD_STR(x) RSVD_STR2(x)
+#define RSVD_LAUNCHED(hh)                                        \
+  do {                                                           \
+    RSVD_LAUNCH_CHECK();                                         \
+    (hh).counters.kernel_launches++;                             \
+    if ((hh).trace) ::rsvdb::trace_mark((hh), __FILE__ ":" RSVD_STR(__LINE__)); \
   } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -108,6 +111,17 @@ struct Handle {
   std::vector<cudaEvent_t> prof_pool;
   double prof_ms[2] = {0, 0}, prof_flops[2] = {0, 0}, prof_bytes[2] = {0, 0};
   int64_t prof_count[2] = {0, 0};
+  // Launch-site trace (rsvd_trace_enable): an event after every launch; the
+  // time between consecutive events (kernel + any idle gap before it) is
+  // charged to the launch site at the call's final synchronization.
+  bool trace = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> trace_ev;
+  std::vector<cudaEvent_t> trace_pool;
+  std::vector<std::pair<std::string, std::pair<int64_t, double>>> trace_acc;
+  // MT19937-64 jump polynomials on the device (rng.cu / mtjump.cpp)
+  uint64_t* d_jump = nullptr;
+  uint64_t jump_L = 0;
+  int jump_count = 0;
   // pinned staging for the RNG state copy-back (rng.cu)
   void* h_rng = nullptr;
   rsvd_rng_state* rng_user_out = nullptr;
@@ -116,6 +130,10 @@ struct Handle {
 // End of a top-level call: synchronize, raise NumericError on device flags,
 // copy back a pending RNG state.
 void finish_call(Handle& h, const char* what);
+
+void trace_mark(Handle& h, const char* site);
+void trace_begin(Handle& h);
+void trace_collect(Handle& h);
 
 // Split-K semaphores, at least n of them.
 int* tile_counters(Handle& h, int64_t n);

@@ -78,6 +78,49 @@ int* tile_counters(Handle& h, int64_t n) {
   return h.d_counters;
 }
 
+static cudaEvent_t trace_event(Handle& h) {
+  cudaEvent_t e;
+  if (h.trace_pool.empty()) {
+    RSVD_CUDA(cudaEventCreate(&e));
+  } else {
+    e = h.trace_pool.back();
+    h.trace_pool.pop_back();
+  }
+  return e;
+}
+
+void trace_begin(Handle& h) {
+  if (!h.trace) return;
+  cudaEvent_t e = trace_event(h);
+  RSVD_CUDA(cudaEventRecord(e, h.stream));
+  h.trace_ev.push_back({"<call start>", e});
+}
+
+void trace_mark(Handle& h, const char* site) {
+  cudaEvent_t e = trace_event(h);
+  RSVD_CUDA(cudaEventRecord(e, h.stream));
+  h.trace_ev.push_back({site, e});
+}
+
+void trace_collect(Handle& h) {
+  for (size_t i = 1; i < h.trace_ev.size(); ++i) {
+    float ms = 0.f;
+    RSVD_CUDA(cudaEventElapsedTime(&ms, h.trace_ev[i - 1].second, h.trace_ev[i].second));
+    const std::string site = h.trace_ev[i].first;
+    bool found = false;
+    for (auto& kv : h.trace_acc)
+      if (kv.first == site) {
+        kv.second.first += 1;
+        kv.second.second += ms;
+        found = true;
+        break;
+      }
+    if (!found) h.trace_acc.push_back({site, {1, double(ms)}});
+  }
+  for (auto& kv : h.trace_ev) h.trace_pool.push_back(kv.second);
+  h.trace_ev.clear();
+}
+
 void finish_call(Handle& h, const char* what) {
   rsvd_rng_state* user = h.rng_user_out;
   h.rng_user_out = nullptr;
@@ -94,6 +137,7 @@ void finish_call(Handle& h, const char* what) {
     h.prof_pool.push_back(r.b);
   }
   h.prof_pending.clear();
+  if (h.trace) trace_collect(h);
 }
 
 namespace {

@@ -101,10 +101,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
-template <bool kNN, int BN, int WMT, int BK, int STAGES>
+// XC = 1: the last of the BN/8 loaded column groups holds ONE real column,
+// computed with DFMA from the A fragments already in registers instead of a
+// padded DMMA n-tile (l = 25 = 3 x 8 + 1: 24 columns on DMMA + 1 on DFMA does
+// 25/32 of the FP64-pipe work of padding to 32; DMMA and DFMA share the pipe).
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC>
 struct PassCfg {
   static constexpr int BM = kConsumerWarps * WMT * 8;
-  static constexpr int NT = BN / 8;
+  static constexpr int NT = BN / 8 - XC;  // DMMA n-tiles
+  static constexpr int NCOL = NT * 8 + XC;  // output columns per tile
+  static constexpr int FRAG = kConsumerWarps * WMT * NT * 64 + XC * kConsumerWarps * WMT * 32;
   static constexpr int KH = BK / 16;  // 16-wide (128-byte) swizzle boxes along K
   static constexpr int A_BYTES = BM * BK * 8;
   static constexpr int B_BYTES = BN * BK * 8;
@@ -154,13 +160,13 @@ __device__ __forceinline__ int sk_cta_of(int64_t u, const PassParams& p) {
   return c;
 }
 
-template <bool kNN, int BN, int WMT, int BK, int STAGES>
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC>
 __global__ void __launch_bounds__(kThreads, 1)
     pass_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 PassParams p) {
-  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES>;
-  constexpr int BM = Cfg::BM, NT = Cfg::NT;
-  constexpr int FRAG = kConsumerWarps * WMT * NT * 64;  // doubles per partial tile
+  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC>;
+  constexpr int BM = Cfg::BM, NT = Cfg::NT, NCOL = Cfg::NCOL;
+  constexpr int FRAG = Cfg::FRAG;  // doubles per partial tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // Pointer arithmetic on the __shared__ array (no integer round trip) keeps
   // the state space visible to the compiler: fragment loads become LDS.
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* b_st = a_st + Cfg::A_BYTES;
         ptx::mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
         const int t = unit_tile(u);
-        const int m0 = (t / p.nt) * BM, n0 = (t % p.nt) * BN;
+        const int m0 = (t / p.nt) * BM, n0 = (t % p.nt) * NCOL;
         const int k0 = unit_kb(u) * BK;
         if constexpr (kNN) {
           // A is M x K, M inner: boxes of 16 (M) x BK (K).
@@ -267,14 +273,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       offB[q] = lo;
     }
   }
+  // XC column (row NT*8 of the B tile, whose swizzle XOR is 0): lane part of
+  // the byte offset; the k-step part is a compile-time constant.
+  const int offX = kNN ? (32 * cy + 8 * cx) : (16 * cx + 8 * cy);
   int64_t u = u0;
   int seg_local = 0;
   do {
     double acc[WMT][NT][2];
+    double xacc[WMT];
 #pragma unroll
-    for (int i = 0; i < WMT; ++i)
+    for (int i = 0; i < WMT; ++i) {
+      xacc[i] = 0.0;
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
     const int t = (u < u1) ? unit_tile(u) : fixed_tile;
     const int64_t seg_end = p.stream_k ? min(u1, int64_t(t + 1) * p.kb_tile) : u1;
     for (; u < seg_end; ++u) {
@@ -309,13 +321,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i2 = 0; i2 < WMT; ++i2)
 #pragma unroll
           for (int j = 0; j < NT; ++j) ptx::dmma(acc[i2][j][0], acc[i2][j][1], af[i2], bf[j]);
+        if constexpr (XC == 1) {
+          // lane holds A(m = 8i + r8, k = kr): partial dot product with column NT*8
+          const int kconst = kNN ? (64 * ((ks >> 1) & 1) + 16 * (ks & 1)) : 32 * (ks & 3);
+          const double bx = *reinterpret_cast<const double*>(
+              b_st + (ks >> 2) * (BN * 128) + NT * 1024 + offX + kconst);
+#pragma unroll
+          for (int i2 = 0; i2 < WMT; ++i2) xacc[i2] = fma(af[i2], bx, xacc[i2]);
+        }
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
 
     // ---------------------------------------------- segment epilogue (tile t)
-    const int64_t m0 = int64_t(t / p.nt) * BM, n0 = int64_t(t % p.nt) * BN;
+    if constexpr (XC == 1) {
+      // the 4 lanes of a row hold disjoint K subsets: butterfly sum (identical
+      // in all 4 lanes: IEEE addition is commutative)
+#pragma unroll
+      for (int i2 = 0; i2 < WMT; ++i2) {
+        xacc[i2] += __shfl_xor_sync(0xffffffffu, xacc[i2], 1);
+        xacc[i2] += __shfl_xor_sync(0xffffffffu, xacc[i2], 2);
+      }
+    }
+    const int64_t m0 = int64_t(t / p.nt) * BM, n0 = int64_t(t % p.nt) * NCOL;
     int nseg, my_seg, c_first = 0;
     if (p.stream_k) {
       c_first = sk_cta_of(int64_t(t) * p.kb_tile, p);
@@ -326,9 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       nseg = p.splits;
       my_seg = blockIdx.z;
     }
-    auto store = [&](double (&v)[WMT][NT][2]) {
+    auto store = [&](double (&v)[WMT][NT][2], double (&vx)[WMT]) {
 #pragma unroll
-      for (int i2 = 0; i2 < WMT; ++i2)
+      for (int i2 = 0; i2 < WMT; ++i2) {
 #pragma unroll
         for (int j = 0; j < NT; ++j)
 #pragma unroll
@@ -336,9 +365,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t m = m0 + wm0 + i2 * 8 + r8, n = n0 + j * 8 + 2 * c4 + e;
             if (m < p.M && n < p.N) p.C[n * p.ldc + m] = v[i2][j][e];
           }
+        if constexpr (XC == 1) {
+          const int64_t m = m0 + wm0 + i2 * 8 + r8, n = n0 + NT * 8;
+          if (c4 == 0 && m < p.M && n < p.N) p.C[n * p.ldc + m] = vx[i2];
+        }
+      }
     };
     if (nseg == 1) {
-      store(acc);
+      store(acc, xacc);
     } else {
       auto slot = [&](int sg) -> int64_t {
         if (!p.stream_k) return int64_t(t) * p.splits + sg;
@@ -358,6 +392,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < NT; ++j)
             if (n0 + j * 8 < p.N) dst[(i2 * NT + j) * 32] = make_double2(acc[i2][j][0], acc[i2][j][1]);
+        if constexpr (XC == 1) {
+          double* dx = p.partials + my_slot * FRAG + kConsumerWarps * WMT * NT * 64 +
+                       warp * WMT * 32 + lane;
+#pragma unroll
+          for (int i2 = 0; i2 < WMT; ++i2) dx[i2 * 32] = xacc[i2];
+        }
       }
       __threadfence();
       ptx::named_bar(1, NCT);
@@ -369,10 +409,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         // where it was just written) in segment order: deterministic.
         if (warp_live) {
 #pragma unroll
-          for (int i2 = 0; i2 < WMT; ++i2)
+          for (int i2 = 0; i2 < WMT; ++i2) {
+            xacc[i2] = 0.0;
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[i2][j][0] = acc[i2][j][1] = 0.0;
-          for (int sg = 0; sg < nseg; ++sg) {
+          }
+          // RU partials in flight per round trip (summed in order afterwards)
+          constexpr int RU = (WMT * NT <= 4) ? 4 : ((WMT * NT <= 8) ? 2 : 1);
+          int sg = 0;
+          for (; sg + RU <= nseg; sg += RU) {
+            double2 v[RU][WMT][NT];
+            double vx[RU][WMT];
+#pragma unroll
+            for (int r = 0; r < RU; ++r) {
+              const double2* src = reinterpret_cast<const double2*>(p.partials + slot(sg + r) * FRAG) +
+                                   (warp * WMT * NT) * 32 + lane;
+#pragma unroll
+              for (int i2 = 0; i2 < WMT; ++i2) {
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+                  v[r][i2][j] = (n0 + j * 8 < p.N) ? __ldcg(src + (i2 * NT + j) * 32)
+                                                   : make_double2(0.0, 0.0);
+                vx[r][i2] = 0.0;
+                if constexpr (XC == 1)
+                  vx[r][i2] = __ldcg(p.partials + slot(sg + r) * FRAG +
+                                     kConsumerWarps * WMT * NT * 64 + warp * WMT * 32 + lane + i2 * 32);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < RU; ++r)
+#pragma unroll
+              for (int i2 = 0; i2 < WMT; ++i2) {
+                xacc[i2] += vx[r][i2];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                  acc[i2][j][0] += v[r][i2][j].x;
+                  acc[i2][j][1] += v[r][i2][j].y;
+                }
+              }
+          }
+          for (; sg < nseg; ++sg) {
+            if constexpr (XC == 1) {
+              const double* sx = p.partials + slot(sg) * FRAG + kConsumerWarps * WMT * NT * 64 +
+                                 warp * WMT * 32 + lane;
+#pragma unroll
+              for (int i2 = 0; i2 < WMT; ++i2) xacc[i2] += __ldcg(sx + i2 * 32);
+            }
             const double2* src = reinterpret_cast<const double2*>(p.partials + slot(sg) * FRAG) +
                                  (warp * WMT * NT) * 32 + lane;
 #pragma unroll
@@ -385,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   acc[i2][j][1] += v.y;
                 }
           }
-          store(acc);
+          store(acc, xacc);
         }
         if (tid == 0) p.counters[t] = 0;  // self-reset for the next launch
       }
@@ -433,20 +515,20 @@ bool tma_ok(const DMat& x) {
   return (reinterpret_cast<uintptr_t>(x.p) % 16 == 0) && (x.ld % 2 == 0) && x.ld >= x.rows;
 }
 
-template <bool kNN, int BN, int WMT, int BK, int STAGES>
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC = 0>
 void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t N, int64_t K,
             int force_splits) {
-  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES>;
+  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC>;
   static bool attr_set = false;
-  auto kern = pass_kernel<kNN, BN, WMT, BK, STAGES>;
+  auto kern = pass_kernel<kNN, BN, WMT, BK, STAGES, XC>;
   if (!attr_set) {
     RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr_set = true;
   }
-  const int64_t mt = ceil_div(M, Cfg::BM), nt = ceil_div(N, BN);
+  const int64_t mt = ceil_div(M, Cfg::BM), nt = ceil_div(N, Cfg::NCOL);
   const int64_t tiles = mt * nt;
   const int64_t kblocks = ceil_div(K, BK);
-  constexpr int64_t FRAG = kConsumerWarps * WMT * (BN / 8) * 64;
+  constexpr int64_t FRAG = Cfg::FRAG;
   PassParams pp{};
   pp.M = M;
   pp.N = N;
@@ -463,8 +545,10 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
   const bool stream_k = force_splits <= 0 && tiles < 2 * sms;
   if (stream_k) {
     const int64_t units = tiles * kblocks;
-    // at least ~6 slices per CTA so the pipeline fill amortizes
-    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(sms, units / 6));
+    // one CTA per tile at least (short-K products: no partials at all), and
+    // >= 8 K slices per CTA when tiles are few (bounds the partials a tile's
+    // last segment must reduce)
+    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(sms, std::max<int64_t>(tiles, units / 8)));
     pp.stream_k = 1;
     pp.units = units;
     pp.grid = int(g);
@@ -550,12 +634,103 @@ void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
     return;
   }
   DMat Pv = tma_view(h, P), Rv = tma_view(h, R);
-  if (N <= 32)
+  if (N == 25)
+    launch<true, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits);
+  else if (N <= 32)
     launch<true, 32, 2, 32, 4>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 64)
     launch<true, 64, 2, 32, 3>(h, Pv, Rv, C, M, N, K, force_splits);
   else
     launch<true, 56, 4, 16, 4>(h, Pv, Rv, C, M, N, K, force_splits);
+}
+
+// ---------------------------------------------------------------- small Gram
+// C (M x N) = P^T R for tall P (K x M), R (K x N) with M, N <= 64: the l x l
+// inner products of the orthonormalization and single-pass cores (Q^T Q,
+// Q^T Omega, Q^T Y).  A DMMA tile engine would waste >= 4/5 of its work on
+// such outputs.  Each CTA stages one chunk of rows of P and R in shared memory
+// with a single round of coalesced loads, forms its M x N partial with DFMA,
+// and the last CTA to finish (one atomic ticket) sums the partials in CTA
+// order with batched loads: bitwise deterministic, one level, one launch.
+
+__global__ void __launch_bounds__(256) gram_small_kernel(
+    const double* __restrict__ P, int64_t ldp, const double* __restrict__ R, int64_t ldr,
+    int64_t K, int M, int N, int64_t rows_per_cta, double* __restrict__ part,
+    int* __restrict__ counter, double* __restrict__ C, int64_t ldc) {
+  extern __shared__ double sh[];
+  const int RP = int(rows_per_cta);
+  double* Ps = sh;                   // [RP][M+1]
+  double* Rs = sh + RP * (M + 1);    // [RP][N+1]
+  __shared__ int last;
+  const int tid = threadIdx.x;
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per_cta;
+  const int nr = int(K - r0 < rows_per_cta ? K - r0 : rows_per_cta);
+  for (int e = tid; e < RP * M; e += 256) {
+    const int r = e % RP, a = e / RP;
+    Ps[r * (M + 1) + a] = r < nr ? P[int64_t(a) * ldp + r0 + r] : 0.0;
+  }
+  for (int e = tid; e < RP * N; e += 256) {
+    const int r = e % RP, b = e / RP;
+    Rs[r * (N + 1) + b] = r < nr ? R[int64_t(b) * ldr + r0 + r] : 0.0;
+  }
+  __syncthreads();
+  const int MN = M * N;
+  double* mine = part + int64_t(blockIdx.x) * MN;
+  for (int o = tid; o < MN; o += 256) {
+    const int a = o % M, b = o / M;
+    double s0 = 0.0, s1 = 0.0;
+    int r = 0;
+    for (; r + 1 < nr; r += 2) {
+      s0 = fma(Ps[r * (M + 1) + a], Rs[r * (N + 1) + b], s0);
+      s1 = fma(Ps[(r + 1) * (M + 1) + a], Rs[(r + 1) * (N + 1) + b], s1);
+    }
+    if (r < nr) s0 = fma(Ps[r * (M + 1) + a], Rs[r * (N + 1) + b], s0);
+    mine[o] = s0 + s1;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(counter, 1) == int(gridDim.x) - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int G = gridDim.x;
+  for (int o = tid; o < MN; o += 256) {
+    double v = 0.0;
+    int c = 0;
+    for (; c + 8 <= G; c += 8) {
+      double t[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t[q] = __ldcg(part + int64_t(c + q) * MN + o);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v += t[q];
+    }
+    for (; c < G; ++c) v += __ldcg(part + int64_t(c) * MN + o);
+    C[int64_t(o / M) * ldc + (o % M)] = v;
+  }
+  if (tid == 0) *counter = 0;
+}
+
+void gram_small(Handle& h, const DMat& P, const DMat& R, DMat C) {
+  const int64_t K = P.rows;
+  const int M = int(P.cols), N = int(R.cols);
+  // rows per CTA: ~16 partials for the ordered final sum (its latency, not the
+  // DFMA work, dominates these tiny products), at least 64 rows; smem-bounded
+  int64_t rp = std::max<int64_t>(64, ceil_div(K, 16));
+  const int64_t rp_max = (200 * 1024) / (8 * (M + N + 2));
+  rp = std::min(rp, rp_max);
+  const int64_t G = ceil_div(K, rp);
+  double* part = h.ws.alloc(G * M * N);
+  int* cnt = tile_counters(h, 1);
+  const size_t smem = size_t(rp) * (M + N + 2) * 8;
+  static size_t cur = 0;
+  if (smem > cur) {
+    RSVD_CUDA(cudaFuncSetAttribute(gram_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    cur = smem;
+  }
+  gram_small_kernel<<<unsigned(G), 256, smem, h.stream>>>(P.p, P.ld, R.p, R.ld, K, M, N, rp, part,
+                                                          cnt, C.p, C.ld);
+  RSVD_LAUNCHED(h);
 }
 
 void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) {
@@ -566,8 +741,14 @@ void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
     RSVD_CUDA(cudaMemset2DAsync(C.p, C.ld * 8, 0, M * 8, N, h.stream));
     return;
   }
+  if (M <= 64 && N <= 64 && force_splits <= 0) {
+    gram_small(h, P, R, C);
+    return;
+  }
   DMat Pv = tma_view(h, P), Rv = tma_view(h, R);
-  if (N <= 32)
+  if (N == 25)
+    launch<false, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits);
+  else if (N <= 32)
     launch<false, 32, 2, 32, 4>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 64)
     launch<false, 64, 2, 32, 3>(h, Pv, Rv, C, M, N, K, force_splits);

@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "ddlog.cuh"
+#include "mtjump.h"
 #include "rng.cuh"
 #include "small.cuh"
 
@@ -122,6 +123,73 @@ struct DevState {
   int32_t has_cached, pad;
   double cached;
 };
+
+// ------------------------------------------------------- parallel stream
+// Long streams are generated in segments of kSegWords words, all segments at
+// once.  Segment s >= 1 starts from the 312-word window that precedes it,
+// obtained by jump-ahead (mtjump.cpp): window[j] = XOR_{k in poly_s} base[k + j],
+// base[i] = words[1 + i] (the first 19937 + 312 words, generated sequentially).
+constexpr int64_t kSegBlocks = 1024;
+constexpr int64_t kSegWords = kSegBlocks * kN;
+constexpr int kJumpBase = 19937 + kN;  // base words needed by a jump
+constexpr int kPolyWords = 312;
+constexpr int kSegPerCta = 3;          // segments advanced in lockstep per CTA
+
+__global__ void __launch_bounds__(320) mt_jump_kernel(const uint64_t* __restrict__ words,
+                                                      const uint64_t* __restrict__ polys,
+                                                      uint64_t* __restrict__ windows) {
+  extern __shared__ uint64_t base[];  // kJumpBase words
+  __shared__ uint64_t poly[kPolyWords];
+  const int t = threadIdx.x;
+  const int s = blockIdx.x + 1;  // segment
+  for (int i = t; i < kJumpBase; i += blockDim.x) base[i] = words[1 + i];
+  for (int i = t; i < kPolyWords; i += blockDim.x) poly[i] = polys[int64_t(s - 1) * kPolyWords + i];
+  __syncthreads();
+  if (t >= kN) return;
+  uint64_t acc = 0;
+  for (int w = 0; w < kPolyWords; ++w) {
+    uint64_t bits = poly[w];  // warp-uniform
+    while (bits) {
+      const int b = __ffsll(static_cast<long long>(bits)) - 1;
+      bits &= bits - 1;
+      acc ^= base[64 * w + b + t];
+    }
+  }
+  windows[int64_t(s) * kN + t] = acc;
+}
+
+// Segment s generates words [s*kSegWords, (s+1)*kSegWords) from its window
+// (segment 0 from the initial block, which it also writes).
+__global__ void __launch_bounds__(kSegPerCta * kN) mt_segments_kernel(
+    const uint64_t* __restrict__ init, const uint64_t* __restrict__ windows, int64_t nseg,
+    uint64_t* __restrict__ words) {
+  __shared__ uint64_t S[kSegPerCta][2][kN];
+  const int g = threadIdx.x / kN, t = threadIdx.x % kN;
+  const int64_t s = int64_t(blockIdx.x) * kSegPerCta + g;
+  const bool live = s < nseg;
+  if (live) S[g][0][t] = (s == 0) ? init[t] : windows[s * kN + t];
+  if (live && s == 0) words[t] = init[t];
+  __syncthreads();
+  const int64_t first = (s == 0) ? 1 : 0;  // segment 0's block 0 is the initial block
+  for (int64_t k = 0; k < kSegBlocks - first; ++k) {
+    const uint64_t* c = S[g][k & 1];
+    uint64_t* n = S[g][(k + 1) & 1];
+    if (live) {
+      uint64_t v;
+      if (t < kN - kM) {
+        v = c[t + kM] ^ twist(c[t], c[t + 1]);
+      } else if (t < kN - 1) {
+        v = c[t] ^ twist(c[t - kM], c[t - kM + 1]) ^ twist(c[t], c[t + 1]);
+      } else {
+        const uint64_t n0 = c[kM] ^ twist(c[0], c[1]);
+        v = c[kN - 1] ^ twist(c[kM - 1], c[kM]) ^ twist(c[kN - 1], n0);
+      }
+      n[t] = v;
+      words[s * kSegWords + (k + first) * kN + t] = v;
+    }
+    __syncthreads();
+  }
+}
 
 constexpr int kTile = 1024;  // attempts per tile (= 256 threads x 4)
 
@@ -283,6 +351,23 @@ const ddlog::Entry* host_log_table() {
   return g_host_table;
 }
 
+// Jump polynomials on the device, cached per handle (grown on demand).
+static const uint64_t* device_jump_polys(Handle& h, uint64_t L, int count) {
+  if (count <= 0) return nullptr;
+  if (h.jump_L != L || h.jump_count < count) {
+    const uint64_t* hp = mtjump::jump_polys(L, count);
+    if (h.d_jump) {
+      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      RSVD_CUDA(cudaFree(h.d_jump));
+    }
+    RSVD_CUDA(cudaMalloc(&h.d_jump, size_t(count) * kPolyWords * 8));
+    RSVD_CUDA(cudaMemcpy(h.d_jump, hp, size_t(count) * kPolyWords * 8, cudaMemcpyHostToDevice));
+    h.jump_L = L;
+    h.jump_count = count;
+  }
+  return h.d_jump;
+}
+
 void rng_init_device(Handle& h) {
   (void)h;
   RSVD_CUDA(cudaMemcpyToSymbol(c_log_table, host_log_table(), sizeof(g_host_table)));
@@ -332,10 +417,33 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
     const int64_t attempts =
         int64_t(double(pairs) / p + 10.0 * 0.59 * std::sqrt(double(pairs)) + 64.0);
     const int64_t words_needed = kN + 2 * attempts;  // worst-case start index 312
-    const int64_t nb = ceil_div(words_needed, kN) - 1;
-    uint64_t* words = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nb + 1) * kN * 8));
-    mt_blocks_kernel<<<1, 320, 0, h.stream>>>(dst->mt, nb, words);
-    RSVD_LAUNCHED(h);
+    uint64_t* words;
+    if (words_needed <= 2 * kSegWords) {
+      const int64_t nb = ceil_div(words_needed, kN) - 1;
+      words = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nb + 1) * kN * 8));
+      mt_blocks_kernel<<<1, 320, 0, h.stream>>>(dst->mt, nb, words);
+      RSVD_LAUNCHED(h);
+    } else {
+      // parallel: base prefix (sequential), jump windows, all segments at once
+      const int64_t nseg = ceil_div(words_needed, kSegWords);
+      words = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nseg) * kSegWords * 8));
+      uint64_t* windows = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nseg) * kN * 8));
+      const uint64_t* dpolys = device_jump_polys(h, uint64_t(kSegWords), int(nseg - 1));
+      const int64_t nb_base = ceil_div(1 + kJumpBase, kN);
+      mt_blocks_kernel<<<1, 320, 0, h.stream>>>(dst->mt, nb_base, words);
+      RSVD_LAUNCHED(h);
+      static bool attr = false;
+      if (!attr) {
+        RSVD_CUDA(cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kJumpBase * 8));
+        attr = true;
+      }
+      mt_jump_kernel<<<unsigned(nseg - 1), 320, kJumpBase * 8, h.stream>>>(words, dpolys, windows);
+      RSVD_LAUNCHED(h);
+      mt_segments_kernel<<<unsigned(ceil_div(nseg, kSegPerCta)), kSegPerCta * kN, 0, h.stream>>>(
+          dst->mt, windows, nseg, words);
+      RSVD_LAUNCHED(h);
+    }
     const int64_t ntiles = ceil_div(attempts, kTile);
     int* cnt = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(ntiles) * 4 + 16));
     int64_t* off = reinterpret_cast<int64_t*>(h.ws.alloc_bytes(size_t(ntiles + 4) * 8));

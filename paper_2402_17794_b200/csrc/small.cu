@@ -159,6 +159,16 @@ int tsqr_block_rows(int l) { return l <= 32 ? 256 : 128; }
 // ---------------------------------------------------------- one-sided Jacobi
 // Rm J = W diag(sigma) for square l x l Rm.  Single CTA; X, J in smem when
 // `in_smem`, otherwise in the global scratch buffers gX / gJ (L2 resident).
+template <int GS>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// GS lanes per column pair: 32 (one warp) for large l, 8 for l <= 64 (fewer
+// shuffle levels and 4 pairs per warp: the round latency is the bottleneck).
+template <int GS>
 __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, int l,
                                   double* __restrict__ Jout, int64_t ldj,
                                   double* __restrict__ Wout, int64_t ldw,
@@ -186,28 +196,40 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
     __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
       // circle method: slot 0 fixed, others rotate
-      for (int pr = warp; pr < lp / 2; pr += nwarps) {
-        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (lp - 1);
-        int bq = 1 + (lp - 2 - pr + round) % (lp - 1);
-        int pcol = min(a, bq), qcol = max(a, bq);
-        if (qcol >= l) continue;  // dummy slot
-        double al = 0, be = 0, ga = 0;
-        for (int i = lane; i < l; i += 32) {
-          const double xp = X[pcol * l + i], xq = X[qcol * l + i];
-          al += xp * xp;
-          be += xq * xq;
-          ga += xp * xq;
+      const int ngroups = nthr / GS, grp = tid / GS, gl = tid % GS;
+      for (int pr0 = 0; pr0 < lp / 2; pr0 += ngroups) {
+        const int pr = pr0 + grp;
+        int pcol = 0, qcol = l;  // inactive group -> dummy
+        if (pr < lp / 2) {
+          // circle method without runtime modulo: slot (pr - 1 + round) wraps once
+          int ia = pr - 1 + round;
+          if (ia >= lp - 1) ia -= lp - 1;
+          int ib = lp - 2 - pr + round;
+          if (ib >= lp - 1) ib -= lp - 1;
+          const int a = (pr == 0) ? 0 : 1 + ia;
+          const int bq = 1 + ib;
+          pcol = min(a, bq);
+          qcol = max(a, bq);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (fabs(zeta) > 1e150)
-                               ? 0.5 / zeta
-                               : copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int i = lane; i < l; i += 32) {
+        const bool act = qcol < l;
+        double al = 0, be = 0, ga = 0;
+        if (act)
+          for (int i = gl; i < l; i += GS) {
+            const double xp = X[pcol * l + i], xq = X[qcol * l + i];
+            al += xp * xp;
+            be += xq * xq;
+            ga += xp * xq;
+          }
+        al = group_sum<GS>(al);  // all lanes participate (full-mask shuffles)
+        be = group_sum<GS>(be);
+        ga = group_sum<GS>(ga);
+        if (act && fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
+          // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+          // rewritten with one division and one square root
+          const double d = be - al, g2 = 2.0 * ga;
+          const double t = copysign(1.0, d) * g2 / (fabs(d) + sqrt(d * d + g2 * g2));
+          const double c = rsqrt(1.0 + t * t), s = c * t;
+          for (int i = gl; i < l; i += GS) {
             const double xp = X[pcol * l + i], xq = X[qcol * l + i];
             X[pcol * l + i] = c * xp - s * xq;
             X[qcol * l + i] = s * xp + c * xq;
@@ -215,7 +237,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
             J[pcol * l + i] = c * jp - s * jq;
             J[qcol * l + i] = s * jp + c * jq;
           }
-          if (lane == 0) changed = 1;
+          if (gl == 0) changed = 1;
         }
       }
       __syncthreads();
@@ -599,13 +621,96 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l
   }
 }
 
+// l <= 32: the same factorization (and shift policy) in ONE warp, lane i
+// owning row i.  Every step's dependency chain is a few shared-memory loads,
+// one FMA and one reciprocal square root (no divisions on the critical path):
+//  * Cholesky: step j scales column j by rsqrt(d_j), then lane i updates
+//    A(i, j+1..i) with independent FMAs (L(k,j) is a broadcast load);
+//  * inverse: X = L^-1 column by column, lane c owning column c in registers
+//    (fully unrolled, statically indexed), b_i -= L(i,k) x_k with
+//    precomputed 1/L(k,k); R^-1 = X^T.
+__global__ void chol_inv_warp_kernel(const double* __restrict__ G, int64_t ldg, int l,
+                                     double shift_coef, double* __restrict__ R, int64_t ldr,
+                                     double* __restrict__ Rinv, int64_t ldri, int* shift_used,
+                                     int* flags) {
+  constexpr int LD = 33;
+  __shared__ double A[32 * LD];   // A[i + LD*k], lower triangle (L after factorization)
+  __shared__ double G0[32 * LD];  // the Gram, read from global once (coalesced)
+  __shared__ double inv[32];
+  const int lane = threadIdx.x;
+  const bool row = lane < l;
+  for (int e = lane; e < l * l; e += 32) {
+    const int i = e % l, k = e / l;
+    G0[i + LD * k] = G[int64_t(k) * ldg + i];
+  }
+  __syncwarp();
+  const double d0 = row ? G0[lane + LD * lane] : 0.0;
+  const double tr = warp_sum(d0);
+  bool ok = false;
+  for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+    const double shift = attempt ? shift_coef * tr : 0.0;
+    if (row)
+      for (int k = 0; k <= lane; ++k) A[lane + LD * k] = G0[lane + LD * k] + (lane == k ? shift : 0.0);
+    __syncwarp();
+    bool broke = false;
+    for (int j = 0; j < l; ++j) {
+      const double d = A[j + LD * j];
+      const double orig = __shfl_sync(0xffffffffu, d0, j) + shift;
+      if (!(d > 1e-12 * orig) || !(d > 0.0)) {
+        broke = true;
+        break;
+      }
+      const double rs = rsqrt(d);
+      double lij = 0.0;
+      if (row && lane > j) lij = A[lane + LD * j] * rs;
+      __syncwarp();
+      if (row && lane > j) A[lane + LD * j] = lij;
+      if (lane == j) A[j + LD * j] = d * rs;
+      __syncwarp();
+      if (row && lane > j)
+        for (int k = j + 1; k <= lane; ++k) A[lane + LD * k] -= lij * A[k + LD * j];
+      __syncwarp();
+    }
+    ok = !broke;
+    if (ok && attempt == 1 && lane == 0 && shift_used) *shift_used = 1;
+  }
+  if (!ok) {
+    if (lane == 0) atomicOr(flags, kFlagCholBreakdown);
+    return;
+  }
+  if (row) inv[lane] = 1.0 / A[lane + LD * lane];
+  __syncwarp();
+  // R = L^T: column c of R = row c of L
+  if (row)
+    for (int i = 0; i < l; ++i) R[int64_t(lane) * ldr + i] = (i <= lane) ? A[lane + LD * i] : 0.0;
+  // X = L^-1 (column c in lane c): for k: x_k = b_k / L(k,k); b_i -= L(i,k) x_k, i > k
+  double b[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) b[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (k < l) {
+      b[k] *= inv[k];
+#pragma unroll
+      for (int i = k + 1; i < 32; ++i)
+        if (i < l) b[i] = fma(-A[i + LD * k], b[k], b[i]);
+    }
+  }
+  // R^-1 = X^T: R^-1(c, i) = X(i, c) = b[i] in lane c (zero for c > i)
+  if (row)
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < l) Rinv[int64_t(i) * ldri + lane] = (lane <= i) ? b[i] : 0.0;
+}
+
 }  // namespace
 
 // =================================================================== host
 // Opt a kernel into `bytes` of dynamic shared memory (idempotent, grows only).
 template <class K>
 static void ensure_smem(K kernel, size_t bytes, size_t& current) {
-  if (bytes > 48 * 1024 && bytes > current) {
+  // (static shared memory counts toward the 48 KB default too: always opt in)
+  if (bytes > current) {
     RSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     current = bytes;
   }
@@ -787,8 +892,13 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   auto pass = [&](const DMat& Y, DMat Qo) {
     gemm_tn(h, Y, Y, G);
     if (dist) allreduce_mat(h, G);
-    chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
-        G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld, gA, in_smem ? 1 : 0, shift_used, h.d_flags);
+    if (l <= 32)
+      chol_inv_warp_kernel<<<1, 32, 0, h.stream>>>(G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld,
+                                                   shift_used, h.d_flags);
+    else
+      chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
+          G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld, gA, in_smem ? 1 : 0, shift_used,
+          h.d_flags);
     RSVD_LAUNCHED(h);
     if (Y.p == Qo.p) {
       DMat Qt = h.ws.mat(Qo.rows, l);
@@ -845,10 +955,22 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
     gX = h.ws.alloc(int64_t(l) * l);
     gJ = h.ws.alloc(int64_t(l) * l);
   }
-  static size_t cur_j = 0;
-  ensure_smem(jacobi_svd_kernel, in_smem ? size_t(2) * l * l * 8 : 0, cur_j);
-  jacobi_svd_kernel<<<1, 1024, in_smem ? size_t(2) * l * l * 8 : 0, h.stream>>>(
-      Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma, gX, gJ, in_smem ? 1 : 0, h.d_flags);
+  const size_t dyn = in_smem ? size_t(2) * l * l * 8 : 0;
+  const int pairs = (l + 1) / 2;
+  if (l <= 64) {
+    static size_t cur_j8 = 0;
+    ensure_smem(jacobi_svd_kernel<8>, dyn, cur_j8);
+    const int thr = std::max(32, int(round_up(8 * pairs, 32)));
+    jacobi_svd_kernel<8><<<1, thr, dyn, h.stream>>>(Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
+                                                    gX, gJ, in_smem ? 1 : 0, h.d_flags);
+  } else {
+    static size_t cur_j = 0;
+    ensure_smem(jacobi_svd_kernel<32>, dyn, cur_j);
+    // one warp per column pair of a round (no idle warps in the per-round barrier)
+    const int thr = 32 * std::max(1, std::min(32, pairs));
+    jacobi_svd_kernel<32><<<1, thr, dyn, h.stream>>>(Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
+                                                     gX, gJ, in_smem ? 1 : 0, h.d_flags);
+  }
   RSVD_LAUNCHED(h);
 
 }
