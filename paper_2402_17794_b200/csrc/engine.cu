@@ -178,36 +178,52 @@ __global__ void kron_core_kernel(const double* a, const double* b, int64_t l, in
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr), __double_as_longlong(v));
 }
-__global__ void asym_kernel(const double* __restrict__ A, int64_t n, int64_t lda, double* out) {
-  // blockIdx.x enumerates tile pairs (bi <= bj) of the upper triangle
-  const int64_t nt = (n + 31) / 32;
-  int64_t t = blockIdx.x, bi = 0;
-  while (t >= nt - bi) {
-    t -= nt - bi;
-    ++bi;
-  }
-  const int64_t bj = bi + t;
+// Persistent grid over tile pairs (bi <= bj) of the upper triangle: tile
+// (bi, bj) and its mirror (bj, bi) are loaded once each (coalesced columns),
+// running maxima stay in registers, one atomic per CTA at the end.
+__global__ void __launch_bounds__(256) asym_kernel(const double* __restrict__ A, int64_t n,
+                                                   int64_t lda, double* out) {
   __shared__ double T1[32][33], T2[32][33];
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int k = ty; k < 32; k += blockDim.y) {
-    const int64_t r1 = bi * 32 + tx, c1 = bj * 32 + k;  // tile (bi, bj)
-    T1[k][tx] = (r1 < n && c1 < n) ? A[c1 * lda + r1] : 0.0;
-    const int64_t r2 = bj * 32 + tx, c2 = bi * 32 + k;  // tile (bj, bi)
-    T2[k][tx] = (r2 < n && c2 < n) ? A[c2 * lda + r2] : 0.0;
-  }
-  __syncthreads();
+  __shared__ double r_abs[8], r_asym[8];
+  const int64_t nt = (n + 31) / 32;
+  const int64_t npairs = nt * (nt + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double mabs = 0.0, masym = 0.0;
-  for (int k = ty; k < 32; k += blockDim.y) {
-    // element (i = bi*32+tx, j = bj*32+k) vs (j, i) = T2[tx][k]
-    const double a = T1[k][tx], b = T2[tx][k];
-    mabs = fmax(mabs, fmax(fabs(a), fabs(b)));
-    masym = fmax(masym, fabs(a - b));
+  for (int64_t t0 = blockIdx.x; t0 < npairs; t0 += gridDim.x) {
+    // invert t0 -> (bi, bj), bi <= bj, row-major over the upper triangle
+    int64_t bi = int64_t((2.0 * nt + 1.0 - sqrt((2.0 * nt + 1.0) * (2.0 * nt + 1.0) - 8.0 * t0)) / 2.0);
+    if (bi < 0) bi = 0;
+    while (bi > 0 && bi * nt - bi * (bi - 1) / 2 > t0) --bi;
+    while ((bi + 1) * nt - (bi + 1) * bi / 2 <= t0) ++bi;
+    const int64_t bj = bi + (t0 - (bi * nt - bi * (bi - 1) / 2));
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t r1 = bi * 32 + tx, c1 = bj * 32 + k;
+      T1[k][tx] = (r1 < n && c1 < n) ? A[c1 * lda + r1] : 0.0;
+      const int64_t r2 = bj * 32 + tx, c2 = bi * 32 + k;
+      T2[k][tx] = (r2 < n && c2 < n) ? A[c2 * lda + r2] : 0.0;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const double a = T1[k][tx], b = T2[tx][k];  // A(i,j) vs A(j,i)
+      mabs = fmax(mabs, fmax(fabs(a), fabs(b)));
+      masym = fmax(masym, fabs(a - b));
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
     masym = fmax(masym, __shfl_xor_sync(0xffffffffu, masym, o));
   }
   if (tx == 0) {
+    r_abs[ty] = mabs;
+    r_asym[ty] = masym;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      mabs = fmax(mabs, r_abs[w]);
+      masym = fmax(masym, r_asym[w]);
+    }
     atomic_max_nonneg(&out[0], mabs);
     atomic_max_nonneg(&out[1], masym);
   }
@@ -230,7 +246,8 @@ void check_symmetric(Handle& h, const DMat& C, bool dist_unused) {
   double* mm = h.ws.alloc(2);
   RSVD_CUDA(cudaMemsetAsync(mm, 0, 16, h.stream));
   const int64_t nt = ceil_div(n, 32);
-  asym_kernel<<<unsigned(nt * (nt + 1) / 2), dim3(32, 8), 0, h.stream>>>(C.p, n, C.ld, mm);
+  const int64_t grid = std::min<int64_t>(nt * (nt + 1) / 2, 8 * h.sm_count);
+  asym_kernel<<<unsigned(grid), 256, 0, h.stream>>>(C.p, n, C.ld, mm);
   RSVD_LAUNCHED(h);
   asym_flag_kernel<<<1, 1, 0, h.stream>>>(mm, h.d_flags, kFlagAsymmetric);
   RSVD_LAUNCHED(h);

@@ -179,13 +179,18 @@ struct Table {
 
 const uint64_t* jump_polys(uint64_t L, int count) {
   static std::mutex mu;
-  static Table tab;
+  static std::vector<Table> tabs;  // one table per segment length
   std::lock_guard<std::mutex> lk(mu);
-  if (tab.L != L) {
-    tab = Table{};
-    tab.L = L;
-    tab.step = x_pow(L);
+  Table* tp = nullptr;
+  for (auto& t : tabs)
+    if (t.L == L) tp = &t;
+  if (!tp) {
+    tabs.push_back(Table{});
+    tp = &tabs.back();
+    tp->L = L;
+    tp->step = x_pow(L);
   }
+  Table& tab = *tp;
   while (int(tab.polys.size()) < count) {
     if (tab.polys.empty())
       tab.polys.push_back(x_pow(L - 313));

@@ -129,40 +129,54 @@ struct DevState {
 // once.  Segment s >= 1 starts from the 312-word window that precedes it,
 // obtained by jump-ahead (mtjump.cpp): window[j] = XOR_{k in poly_s} base[k + j],
 // base[i] = words[1 + i] (the first 19937 + 312 words, generated sequentially).
-constexpr int64_t kSegBlocks = 1024;
-constexpr int64_t kSegWords = kSegBlocks * kN;
+// Segment lengths (blocks of 312 words): short segments (more, cheaper jumps,
+// short generation chains) up to ~9M words, long ones beyond.
+constexpr int64_t kSegBlocksShort = 64;
+constexpr int64_t kSegBlocksLong = 1024;
 constexpr int kJumpBase = 19937 + kN;  // base words needed by a jump
 constexpr int kPolyWords = 312;
 constexpr int kSegPerCta = 3;          // segments advanced in lockstep per CTA
 
+// grid (nseg - 1, parts): part p XORs the terms of poly words [w0, w1) into
+// the window (XOR is order independent: exact and deterministic).
 __global__ void __launch_bounds__(320) mt_jump_kernel(const uint64_t* __restrict__ words,
                                                       const uint64_t* __restrict__ polys,
-                                                      uint64_t* __restrict__ windows) {
-  extern __shared__ uint64_t base[];  // kJumpBase words
+                                                      int wpp,
+                                                      unsigned long long* __restrict__ windows) {
+  extern __shared__ uint64_t base[];  // 64 * wpp + kN words
   __shared__ uint64_t poly[kPolyWords];
   const int t = threadIdx.x;
   const int s = blockIdx.x + 1;  // segment
-  for (int i = t; i < kJumpBase; i += blockDim.x) base[i] = words[1 + i];
-  for (int i = t; i < kPolyWords; i += blockDim.x) poly[i] = polys[int64_t(s - 1) * kPolyWords + i];
+  const int w0 = blockIdx.y * wpp, w1 = min(kPolyWords, w0 + wpp);
+  if (w0 >= w1) return;
+  const int nbase = 64 * (w1 - w0) + kN;
+  for (int i = t; i < nbase; i += blockDim.x) {
+    const int gi = 64 * w0 + i;
+    base[i] = (gi < kJumpBase) ? words[1 + gi] : 0ULL;
+  }
+  for (int i = t; i < w1 - w0; i += blockDim.x) poly[i] = polys[int64_t(s - 1) * kPolyWords + w0 + i];
   __syncthreads();
   if (t >= kN) return;
-  uint64_t acc = 0;
-  for (int w = 0; w < kPolyWords; ++w) {
-    uint64_t bits = poly[w];  // warp-uniform
-    while (bits) {
-      const int b = __ffsll(static_cast<long long>(bits)) - 1;
-      bits &= bits - 1;
-      acc ^= base[64 * w + b + t];
+  uint64_t acc0 = 0, acc1 = 0;
+  for (int w = 0; w < w1 - w0; ++w) {
+    const uint64_t bits = poly[w];  // warp-uniform
+    const uint64_t* bw = base + 64 * w + t;
+#pragma unroll 16
+    for (int b = 0; b < 64; b += 2) {
+      const uint64_t m0 = 0ULL - ((bits >> b) & 1ULL), m1 = 0ULL - ((bits >> (b + 1)) & 1ULL);
+      acc0 ^= bw[b] & m0;
+      acc1 ^= bw[b + 1] & m1;
     }
   }
-  windows[int64_t(s) * kN + t] = acc;
+  atomicXor(&windows[int64_t(s) * kN + t], static_cast<unsigned long long>(acc0 ^ acc1));
 }
 
 // Segment s generates words [s*kSegWords, (s+1)*kSegWords) from its window
 // (segment 0 from the initial block, which it also writes).
 __global__ void __launch_bounds__(kSegPerCta * kN) mt_segments_kernel(
     const uint64_t* __restrict__ init, const uint64_t* __restrict__ windows, int64_t nseg,
-    uint64_t* __restrict__ words) {
+    int64_t seg_blocks, uint64_t* __restrict__ words) {
+  const int64_t seg_words = seg_blocks * kN;
   __shared__ uint64_t S[kSegPerCta][2][kN];
   const int g = threadIdx.x / kN, t = threadIdx.x % kN;
   const int64_t s = int64_t(blockIdx.x) * kSegPerCta + g;
@@ -171,7 +185,7 @@ __global__ void __launch_bounds__(kSegPerCta * kN) mt_segments_kernel(
   if (live && s == 0) words[t] = init[t];
   __syncthreads();
   const int64_t first = (s == 0) ? 1 : 0;  // segment 0's block 0 is the initial block
-  for (int64_t k = 0; k < kSegBlocks - first; ++k) {
+  for (int64_t k = 0; k < seg_blocks - first; ++k) {
     const uint64_t* c = S[g][k & 1];
     uint64_t* n = S[g][(k + 1) & 1];
     if (live) {
@@ -185,7 +199,7 @@ __global__ void __launch_bounds__(kSegPerCta * kN) mt_segments_kernel(
         v = c[kN - 1] ^ twist(c[kM - 1], c[kM]) ^ twist(c[kN - 1], n0);
       }
       n[t] = v;
-      words[s * kSegWords + (k + first) * kN + t] = v;
+      words[s * seg_words + (k + first) * kN + t] = v;
     }
     __syncthreads();
   }
@@ -355,6 +369,7 @@ const ddlog::Entry* host_log_table() {
 static const uint64_t* device_jump_polys(Handle& h, uint64_t L, int count) {
   if (count <= 0) return nullptr;
   if (h.jump_L != L || h.jump_count < count) {
+    if (h.jump_L == L) count = std::max(count, 2 * h.jump_count);  // grow geometrically
     const uint64_t* hp = mtjump::jump_polys(L, count);
     if (h.d_jump) {
       RSVD_CUDA(cudaStreamSynchronize(h.stream));
@@ -418,6 +433,9 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
         int64_t(double(pairs) / p + 10.0 * 0.59 * std::sqrt(double(pairs)) + 64.0);
     const int64_t words_needed = kN + 2 * attempts;  // worst-case start index 312
     uint64_t* words;
+    const int64_t seg_blocks =
+        (words_needed <= 3 * 148 * kSegBlocksShort * kN) ? kSegBlocksShort : kSegBlocksLong;
+    const int64_t kSegWords = seg_blocks * kN;
     if (words_needed <= 2 * kSegWords) {
       const int64_t nb = ceil_div(words_needed, kN) - 1;
       words = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nb + 1) * kN * 8));
@@ -432,16 +450,22 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
       const int64_t nb_base = ceil_div(1 + kJumpBase, kN);
       mt_blocks_kernel<<<1, 320, 0, h.stream>>>(dst->mt, nb_base, words);
       RSVD_LAUNCHED(h);
-      static bool attr = false;
-      if (!attr) {
+      // split every jump over `parts` CTAs so all SMs share the XOR work
+      const int parts = int(std::max<int64_t>(1, std::min<int64_t>(32, (2 * h.sm_count) / (nseg - 1))));
+      const int wpp = (kPolyWords + parts - 1) / parts;
+      const size_t jsmem = size_t(64 * wpp + kN) * 8;
+      static size_t jcur = 0;
+      if (jsmem > jcur) {
         RSVD_CUDA(cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kJumpBase * 8));
-        attr = true;
+                                       int(jsmem)));
+        jcur = jsmem;
       }
-      mt_jump_kernel<<<unsigned(nseg - 1), 320, kJumpBase * 8, h.stream>>>(words, dpolys, windows);
+      RSVD_CUDA(cudaMemsetAsync(windows, 0, size_t(nseg) * kN * 8, h.stream));
+      mt_jump_kernel<<<dim3(unsigned(nseg - 1), unsigned(parts)), 320, jsmem, h.stream>>>(
+          words, dpolys, wpp, reinterpret_cast<unsigned long long*>(windows));
       RSVD_LAUNCHED(h);
       mt_segments_kernel<<<unsigned(ceil_div(nseg, kSegPerCta)), kSegPerCta * kN, 0, h.stream>>>(
-          dst->mt, windows, nseg, words);
+          dst->mt, windows, nseg, seg_blocks, words);
       RSVD_LAUNCHED(h);
     }
     const int64_t ntiles = ceil_div(attempts, kTile);

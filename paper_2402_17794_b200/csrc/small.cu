@@ -27,6 +27,9 @@
 #include "pass.cuh"
 #include "small.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace rsvdb {
 
 namespace {
@@ -189,7 +192,9 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
   }
   __syncthreads();
   const int lp = l + (l & 1);  // even number of slots (one dummy if odd)
-  const double tol = 1e-15;
+  // rotation threshold: the rounding noise of an l-term dot product is ~sqrt(l) eps,
+  // so a fixed 1e-15 would never report convergence for large l
+  const double tol = fmax(1e-15, 2.0 * sqrt(double(l)) * 1.1102230246251565e-16);
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
     if (tid == 0) changed = 0;
@@ -621,32 +626,28 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l
   }
 }
 
-// l <= 32: the same factorization (and shift policy) in ONE warp, lane i
-// owning row i.  Every step's dependency chain is a few shared-memory loads,
-// one FMA and one reciprocal square root (no divisions on the critical path):
+// l <= 32: the Cholesky factorization of the (possibly shifted) Gram and the
+// inverse of its factor, by ONE warp on shared memory (lane i owns row i).
+// Every step's dependency chain is a few shared-memory loads, one FMA and one
+// reciprocal square root (no divisions on the critical path):
 //  * Cholesky: step j scales column j by rsqrt(d_j), then lane i updates
 //    A(i, j+1..i) with independent FMAs (L(k,j) is a broadcast load);
 //  * inverse: X = L^-1 column by column, lane c owning column c in registers
 //    (fully unrolled, statically indexed), b_i -= L(i,k) x_k with
 //    precomputed 1/L(k,k); R^-1 = X^T.
-__global__ void chol_inv_warp_kernel(const double* __restrict__ G, int64_t ldg, int l,
-                                     double shift_coef, double* __restrict__ R, int64_t ldr,
-                                     double* __restrict__ Rinv, int64_t ldri, int* shift_used,
-                                     int* flags) {
+// Shift policy as chol_inv_kernel.  Returns false on breakdown after shifting.
+// G0 (LD 33) is the Gram; outputs R and Rinv (LD 33) in shared memory.
+__device__ __forceinline__ bool warp_chol_inv(const double* G0, int l, double shift_coef, double* A, double* Rs,
+                              double* Rinvs, double* inv, bool* shifted) {
   constexpr int LD = 33;
-  __shared__ double A[32 * LD];   // A[i + LD*k], lower triangle (L after factorization)
-  __shared__ double G0[32 * LD];  // the Gram, read from global once (coalesced)
-  __shared__ double inv[32];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const bool row = lane < l;
-  for (int e = lane; e < l * l; e += 32) {
-    const int i = e % l, k = e / l;
-    G0[i + LD * k] = G[int64_t(k) * ldg + i];
-  }
-  __syncwarp();
   const double d0 = row ? G0[lane + LD * lane] : 0.0;
-  const double tr = warp_sum(d0);
+  double tr = d0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
   bool ok = false;
+  *shifted = false;
   for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
     const double shift = attempt ? shift_coef * tr : 0.0;
     if (row)
@@ -672,18 +673,14 @@ __global__ void chol_inv_warp_kernel(const double* __restrict__ G, int64_t ldg, 
       __syncwarp();
     }
     ok = !broke;
-    if (ok && attempt == 1 && lane == 0 && shift_used) *shift_used = 1;
+    if (ok && attempt == 1) *shifted = true;
   }
-  if (!ok) {
-    if (lane == 0) atomicOr(flags, kFlagCholBreakdown);
-    return;
-  }
+  if (!ok) return false;
   if (row) inv[lane] = 1.0 / A[lane + LD * lane];
   __syncwarp();
-  // R = L^T: column c of R = row c of L
+  // R = L^T (LD 33): R(i, c) = L(c, i)
   if (row)
-    for (int i = 0; i < l; ++i) R[int64_t(lane) * ldr + i] = (i <= lane) ? A[lane + LD * i] : 0.0;
-  // X = L^-1 (column c in lane c): for k: x_k = b_k / L(k,k); b_i -= L(i,k) x_k, i > k
+    for (int i = 0; i < 32; ++i) Rs[i + LD * lane] = (i <= lane && i < l) ? A[lane + LD * i] : 0.0;
   double b[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) b[i] = (i == lane) ? 1.0 : 0.0;
@@ -696,11 +693,186 @@ __global__ void chol_inv_warp_kernel(const double* __restrict__ G, int64_t ldg, 
         if (i < l) b[i] = fma(-A[i + LD * k], b[k], b[i]);
     }
   }
-  // R^-1 = X^T: R^-1(c, i) = X(i, c) = b[i] in lane c (zero for c > i)
-  if (row)
+  // R^-1(c, i) = X(i, c) = b[i] in lane c; store column i of R^-1 at Rinvs[c + LD*i]
+  if (lane < 32)
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < l) Rinv[int64_t(i) * ldri + lane] = (lane <= i) ? b[i] : 0.0;
+    for (int i = 0; i < 32; ++i) Rinvs[lane + LD * i] = (row && i < l && lane <= i) ? b[i] : 0.0;
+  __syncwarp();
+  return true;
+}
+
+__global__ void chol_inv_warp_kernel(const double* __restrict__ G, int64_t ldg, int l,
+                                     double shift_coef, double* __restrict__ R, int64_t ldr,
+                                     double* __restrict__ Rinv, int64_t ldri, int* shift_used,
+                                     int* flags) {
+  constexpr int LD = 33;
+  __shared__ double G0[32 * LD], A[32 * LD], Rs[32 * LD], Ri[32 * LD], inv[32];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < l * l; e += 32) G0[(e % l) + LD * (e / l)] = G[int64_t(e / l) * ldg + (e % l)];
+  __syncwarp();
+  bool shifted;
+  if (!warp_chol_inv(G0, l, shift_coef, A, Rs, Ri, inv, &shifted)) {
+    if (lane == 0) atomicOr(flags, kFlagCholBreakdown);
+    return;
+  }
+  if (shifted && lane == 0 && shift_used) *shift_used = 1;
+  for (int e = lane; e < l * l; e += 32) {
+    const int i = e % l, c = e / l;
+    R[int64_t(c) * ldr + i] = Rs[i + LD * c];
+    Rinv[int64_t(c) * ldri + i] = Ri[i + LD * c];
+  }
+}
+
+// Whole CholeskyQR orthonormalization of a tall m x l (l <= 32) matrix in ONE
+// cooperative launch.  Each CTA keeps its row block in shared memory for all
+// passes; per pass: register-blocked partial Gram -> grid barrier -> every CTA
+// sums the partials in CTA order (identical in every CTA) and factors the
+// Gram with one warp (warp_chol_inv) -> rows <- rows * R^-1 in place.  The
+// partial buffers alternate between passes so one barrier per pass suffices.
+constexpr int kFqThreads = 256;
+
+__global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
+    const double* __restrict__ Y, int64_t ldy, int64_t m, int l, int64_t rows_per,
+    double* __restrict__ Qo, int64_t ldq, double* __restrict__ part, double* __restrict__ Rout,
+    int64_t ldr, double shift_coef, int passes, int* __restrict__ flags) {
+  constexpr int LD = 33;
+  cg::grid_group grid = cg::this_grid();
+  // dynamic shared memory: red[4][32*33] | Gs | A | Rs | Ri | Rt (32*33 each) | inv[32] | Ys
+  extern __shared__ double fsm[];
+  double (*red)[32 * LD] = reinterpret_cast<double (*)[32 * LD]>(fsm);
+  double* Gs = fsm + 4 * 32 * LD;
+  double* A = Gs + 32 * LD;
+  double* Rs = A + 32 * LD;
+  double* Ri = Rs + 32 * LD;
+  double* Rt = Ri + 32 * LD;
+  double* inv = Rt + 32 * LD;
+  double* Ys = inv + 32;  // rows_per x 33 (row-major, padded)
+  __shared__ int okf;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int RP = int(rows_per);
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per;
+  const int nr = int(m - r0 < rows_per ? m - r0 : rows_per);
+  const int G = gridDim.x;
+  bool bad = false;
+  for (int e = tid; e < RP * 32; e += kFqThreads) {
+    const int r = e % RP, a = e / RP;
+    double v = 0.0;
+    if (r < nr && a < l) {
+      v = Y[int64_t(a) * ldy + r0 + r];
+      if (!isfinite(v)) bad = true;
+    }
+    Ys[r * LD + a] = v;
+  }
+  if (bad) atomicOr(flags, kFlagNonFinite);
+  for (int e = tid; e < 32 * LD; e += kFqThreads) Rt[e] = ((e % LD) == (e / LD)) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int pass = 0; pass < passes; ++pass) {
+    // ---- partial Gram: 64 tiles of 4x4, 4 row slices (256 threads)
+    {
+      const int tile = tid & 63, ks = tid >> 6;
+      const int ta = (tile & 7) * 4, tb = (tile >> 3) * 4;
+      double acc[4][4] = {};
+      for (int r = ks; r < nr; r += 4) {
+        const double* yr = Ys + r * LD;
+        double pa[4], pb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pa[q] = yr[ta + q];
+          pb[q] = yr[tb + q];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(pa[i], pb[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[ks][(ta + i) + LD * (tb + j)] = acc[i][j];
+    }
+    __syncthreads();
+    double* pp = part + (int64_t(pass & 1) * G + blockIdx.x) * 1024;
+    for (int e = tid; e < 1024; e += kFqThreads) {
+      const int a = e & 31, b = e >> 5;
+      const int o = a + LD * b;
+      pp[e] = ((red[0][o] + red[1][o]) + red[2][o]) + red[3][o];
+    }
+    __threadfence();
+    grid.sync();
+    // ---- total Gram, identical in every CTA (fixed CTA order)
+    const double* pb0 = part + int64_t(pass & 1) * G * 1024;
+    for (int e = tid; e < 1024; e += kFqThreads) {
+      double v = 0.0;
+      int c = 0;
+      for (; c + 8 <= G; c += 8) {
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = __ldcg(pb0 + int64_t(c + q) * 1024 + e);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v += t[q];
+      }
+      for (; c < G; ++c) v += __ldcg(pb0 + int64_t(c) * 1024 + e);
+      Gs[(e & 31) + LD * (e >> 5)] = v;
+    }
+    __syncthreads();
+    // Converged: the Gram of the current rows is the identity to rounding
+    // (|G - I| <= 4 l u): the remaining passes would multiply by R^-1 = I.
+    if (pass > 0) {
+      if (tid == 0) okf = 2;
+      __syncthreads();
+      double dev = 0.0;
+      for (int e = tid; e < l * l; e += kFqThreads) {
+        const int i = e % l, j = e / l;
+        dev = fmax(dev, fabs(Gs[i + LD * j] - (i == j ? 1.0 : 0.0)));
+      }
+      if (dev > 4.0 * l * 1.1102230246251565e-16) okf = 1;  // benign race: all write 1
+      __syncthreads();
+      if (okf == 2) break;  // identical decision in every CTA
+      __syncthreads();
+    }
+    if (warp == 0) {
+      bool shifted;
+      const bool ok = warp_chol_inv(Gs, l, shift_coef, A, Rs, Ri, inv, &shifted);
+      if ((threadIdx.x & 31) == 0) okf = ok ? 1 : 0;
+      if (!ok && blockIdx.x == 0 && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagCholBreakdown);
+      // R_total <- R * R_total (both upper triangular)
+      if (ok && Rout && blockIdx.x == 0) {
+        // in place, ascending i: row i needs Rt(k, c) only for k >= i
+        const int c = threadIdx.x & 31;
+        for (int i = 0; i < 32; ++i) {
+          double v = 0.0;
+          for (int k = i; k < 32; ++k) v = fma(Rs[i + LD * k], Rt[k + LD * c], v);
+          Rt[i + LD * c] = v;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (!okf) return;  // identical decision in every CTA
+    // ---- rows <- rows * R^-1 (upper triangular), in place, one row per thread
+    for (int r = tid; r < nr; r += kFqThreads) {
+      double y[32];
+#pragma unroll
+      for (int a = 0; a < 32; ++a) y[a] = Ys[r * LD + a];
+#pragma unroll 1
+      for (int c = 0; c < 32; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v = fma(y[k], Ri[k + LD * c], v);  // Ri(k, c) = 0 for k > c
+        Ys[r * LD + c] = (c < l) ? v : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < RP * l; e += kFqThreads) {
+    const int r = e % RP, a = e / RP;
+    if (r < nr) Qo[int64_t(a) * ldq + r0 + r] = Ys[r * LD + a];
+  }
+  if (Rout && blockIdx.x == 0)
+    for (int e = tid; e < l * l; e += kFqThreads) {
+      const int i = e % l, c = e / l;
+      Rout[int64_t(c) * ldr + i] = Rt[i + LD * c];
+    }
 }
 
 }  // namespace
@@ -877,8 +1049,45 @@ size_t small_smem_limit() { return 200 * 1024; }
 // i.e. the basis is padded to full width as core.hpp:93-95 requires).  For
 // l <= 64 the 4 passes are always run (no host round trip); for larger l one
 // flag read after pass 1 picks 2 or 4.
+// One cooperative launch for l <= 32 on one GPU (see cholqr_fused_kernel).
+static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
+  const int l = int(X.cols);
+  const int64_t m = X.rows;
+  if (l > 32) return false;
+  int64_t G = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(m, 256)));
+  const int64_t rp = ceil_div(m, G);
+  const size_t smem = (size_t(rp) * 33 + 9 * 32 * 33 + 32) * 8;
+  if (smem > 220 * 1024) return false;
+  G = ceil_div(m, rp);
+  static size_t cur = 0;
+  if (smem > cur) {
+    RSVD_CUDA(cudaFuncSetAttribute(cholqr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    cur = smem;
+  }
+  double* part = h.ws.alloc(2 * G * 1024);
+  const double coef = 11.0 * (double(m) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
+  int passes = 4;
+  const double* yp = X.p;
+  int64_t ldy = X.ld;
+  double* qp = Q.p;
+  int64_t ldq = Q.ld;
+  int64_t mm = m, rpp = rp;
+  int lv = l;
+  double* rp_out = Rout ? Rout->p : nullptr;
+  int64_t ldr = Rout ? Rout->ld : 0;
+  double cf = coef;
+  int* fl = h.d_flags;
+  void* args[] = {&yp, &ldy, &mm, &lv, &rpp, &qp, &ldq, &part, &rp_out, &ldr, &cf, &passes, &fl};
+  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cholqr_fused_kernel), dim3(unsigned(G)),
+                                        dim3(kFqThreads), args, smem, h.stream));
+  RSVD_LAUNCHED(h);
+  return true;
+}
+
 static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   const int l = int(X.cols);
+  if (!dist && cholqr_fused(h, X, Q, Rout)) return;
   DMat G = h.ws.mat(l, l), R1 = h.ws.mat(l, l), Ri = h.ws.mat(l, l);
   const bool in_smem = size_t(l) * l * 8 <= small_smem_limit();
   double* gA = in_smem ? nullptr : h.ws.alloc(int64_t(l) * l);
@@ -947,6 +1156,10 @@ void orthonormalize(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist) {
 
 void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) {
   const int l = int(Rm.rows);
+  if (l > 64) {
+    block_jacobi_svd(h, Rm, J, W, sigma);
+    return;
+  }
   if (l > 1024) throw_dim("jacobi_svd: l > 1024 not supported");
   const bool in_smem = size_t(2) * l * l * 8 <= small_smem_limit();
   double* gX = nullptr;
@@ -977,6 +1190,10 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
 
 void jacobi_evd_sym(Handle& h, const DMat& C, DMat U, double* lambda) {
   const int l = int(C.rows);
+  if (l > 64) {
+    evd_shifted(h, C, U, lambda);
+    return;
+  }
   if (l > 1024) throw_dim("jacobi_evd: l > 1024 not supported");
   const bool in_smem = size_t(2) * l * l * 8 <= small_smem_limit();
   double* gA = nullptr;

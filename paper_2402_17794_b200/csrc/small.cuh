@@ -20,6 +20,11 @@ void tsqr(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist);
 // completed to an orthonormal set).  Device outputs.
 void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma);
 
+// Block one-sided Jacobi (cooperative, multi-CTA) for l > 64 (bjacobi.cu).
+void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma);
+// Symmetric EVD for l > 64 via the SVD of C + mu I (bjacobi.cu).
+void evd_shifted(Handle& h, const DMat& C, DMat U, double* lambda);
+
 // Symmetric two-sided Jacobi EVD of an l x l symmetric matrix (device), with
 // eigenvalues reordered by |lambda| descending, stable (core.hpp:148-152).
 void jacobi_evd_sym(Handle& h, const DMat& C, DMat U, double* lambda);

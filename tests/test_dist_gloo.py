@@ -3,8 +3,8 @@
 The engine row-shards A (dist.cu / engine.cu): products with A are local, and
 only these exchanges cross ranks:
   * A^T Y partials (n x l)                        -> allreduce   (op_adjoint)
-  * per-rank TSQR R factors (l x l)               -> allgather   (small.cu tsqr, dist)
   * CholeskyQR Gram partials (l x l)              -> allreduce   (small.cu cholqr, dist)
+  * per-rank TSQR R factors (l x l)               -> allgather   (small.cu tsqr, dist)
   * Alg 5/6 inner products Q^T Omega, Psi^T Q_c   -> allreduce
   * shard sizes                                   -> allgather   (shard_rows)
 This test replays exactly that decomposition with numpy + torch.distributed
@@ -58,13 +58,23 @@ def dist_tsqr(y_loc):
     return q_loc @ c, r_top
 
 
-def dist_cholqr2(y_loc):
-    """small.cu cholqr(dist=True): Gram allreduce, Cholesky, Q = Y R^-1, twice."""
+def dist_cholqr(y_loc, m_global, passes=4):
+    """small.cu cholqr(dist=True): per pass the l x l Gram partials are
+    allreduced, then the (replicated) Cholesky, shifted by
+    11 (m l + l (l+1)) u tr(G) when a pivot loses all precision, and
+    Q_loc = Y_loc R^-1.  4 passes for l <= 64 (shifted CholeskyQR3 + 1)."""
     q = y_loc
-    for _ in range(2):
+    l = y_loc.shape[1]
+    coef = 11.0 * (m_global * l + l * (l + 1)) * 1.1102230246251565e-16
+    for _ in range(passes):
         g = _allreduce(q.T @ q)
-        r = np.linalg.cholesky(g).T
-        q = q @ np.linalg.inv(r)
+        try:
+            L = np.linalg.cholesky(g)
+            if np.any(np.diag(L) ** 2 <= 1e-12 * np.diag(g)):
+                raise np.linalg.LinAlgError
+        except np.linalg.LinAlgError:
+            L = np.linalg.cholesky(g + coef * np.trace(g) * np.eye(l))
+        q = q @ np.linalg.inv(L.T)
     return q
 
 
@@ -83,7 +93,7 @@ def _worker(rank, world, port, a, omega, res_path):
     for _ in range(2):
         z = _allreduce(a_loc.T @ y)
         y = a_loc @ z
-    q_loc, _ = dist_tsqr(y)
+    q_loc = dist_cholqr(y, m)  # kappa(Y) ~ 1e6 here: the shifted passes engage
     # Stage 2 (factor.hpp:14-16): B^T = sum A_g^T Q_g, replicated small SVD
     z = _allreduce(a_loc.T @ q_loc)
     u_b, s, vt = np.linalg.svd(z.T, full_matrices=False)
@@ -92,8 +102,11 @@ def _worker(rank, world, port, a, omega, res_path):
     pad = np.zeros((mx, u_loc.shape[1]))
     pad[:r1 - r0] = u_loc
     u_all = [g[:int(s[0])] for g, s in zip(_allgather(pad), sizes)]
-    q2 = dist_cholqr2(a_loc @ omega)
+    q2 = dist_cholqr(a_loc @ omega, m)
     gram = _allreduce(q2.T @ q2)
+    q3, _ = dist_tsqr(a_loc @ omega)  # the row-sharded TSQR variant (R allgather)
+    gram3 = _allreduce(q3.T @ q3)
+    assert np.max(np.abs(gram3 - np.eye(gram3.shape[0]))) < 1e-12
     if rank == 0:
         np.savez(res_path, s=s, v=vt.T, u=np.vstack(u_all), gram=gram)
     dist.destroy_process_group()
