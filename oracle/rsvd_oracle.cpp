@@ -74,15 +74,23 @@ thread_local std::string g_last_error;
 struct Mat {
   int64_t r = 0, c = 0;
   std::vector<double> d;
+  const double* ext = nullptr;  // non-owning view (large read-only inputs: A)
   Mat() = default;
   Mat(int64_t rows, int64_t cols) : r(rows), c(cols), d(static_cast<size_t>(rows * cols), 0.0) {}
   double& operator()(int64_t i, int64_t j) { return d[static_cast<size_t>(i + j * r)]; }
-  double operator()(int64_t i, int64_t j) const { return d[static_cast<size_t>(i + j * r)]; }
+  double operator()(int64_t i, int64_t j) const { return data()[static_cast<size_t>(i + j * r)]; }
   double* data() { return d.data(); }
-  const double* data() const { return d.data(); }
+  const double* data() const { return ext ? ext : d.data(); }
   static Mat from(int64_t rows, int64_t cols, const double* p) {
     Mat m(rows, cols);
     if (rows * cols > 0) std::memcpy(m.data(), p, sizeof(double) * rows * cols);
+    return m;
+  }
+  static Mat view(int64_t rows, int64_t cols, const double* p) {
+    Mat m;
+    m.r = rows;
+    m.c = cols;
+    m.ext = p;
     return m;
   }
   void to(double* p) const {
@@ -118,8 +126,9 @@ Mat gemm(const Mat& a, bool ta, const Mat& b, bool tb) {
 }
 
 void require_finite(const Mat& m, const char* what) {
-  for (double v : m.d)
-    if (!std::isfinite(v)) throw NumericError(std::string(what) + ": input has non-finite entries");
+  const double* p = m.data();
+  for (int64_t i = 0; i < m.r * m.c; ++i)
+    if (!std::isfinite(p[i])) throw NumericError(std::string(what) + ": input has non-finite entries");
 }
 
 // ---------------------------------------------------------------- sketch.hpp
@@ -596,13 +605,13 @@ int orc_solve_ls(int64_t m, int64_t n, const double* g, int64_t nrhs, const doub
 int orc_range_basis(int64_t m, int64_t n, const double* a, int64_t k, int64_t p, int q, int mode,
                     void* rng, double* qout) {
   return guard(
-      [&] { range_basis(Mat::from(m, n, a), k, p, q, mode, *static_cast<Rng*>(rng)).to(qout); });
+      [&] { range_basis(Mat::view(m, n, a), k, p, q, mode, *static_cast<Rng*>(rng)).to(qout); });
 }
 
 int orc_rsvd(int64_t m, int64_t n, const double* a, int64_t k, int64_t p, int q, int mode,
              void* rng, double* u, double* s, double* v) {
   return guard([&] {
-    Svd f = rsvd(Mat::from(m, n, a), k, p, q, mode, *static_cast<Rng*>(rng));
+    Svd f = rsvd(Mat::view(m, n, a), k, p, q, mode, *static_cast<Rng*>(rng));
     f.U.to(u);
     std::copy(f.s.begin(), f.s.end(), s);
     f.V.to(v);
@@ -612,7 +621,7 @@ int orc_rsvd(int64_t m, int64_t n, const double* a, int64_t k, int64_t p, int q,
 int orc_spevd(int64_t n, const double* a, int64_t k, int64_t p, void* rng, double* u,
               double* lambda, int* applies) {
   return guard([&] {
-    Evd e = spevd_hermitian(Mat::from(n, n, a), k, p, *static_cast<Rng*>(rng), applies);
+    Evd e = spevd_hermitian(Mat::view(n, n, a), k, p, *static_cast<Rng*>(rng), applies);
     e.U.to(u);
     std::copy(e.lambda.begin(), e.lambda.end(), lambda);
   });
@@ -621,7 +630,7 @@ int orc_spevd(int64_t n, const double* a, int64_t k, int64_t p, void* rng, doubl
 int orc_spsvd(int64_t m, int64_t n, const double* a, int64_t k, int64_t p, void* rng, double* u,
               double* s, double* v, int* applies, int* adjoints) {
   return guard([&] {
-    Svd f = spsvd_general(Mat::from(m, n, a), k, p, *static_cast<Rng*>(rng), applies, adjoints);
+    Svd f = spsvd_general(Mat::view(m, n, a), k, p, *static_cast<Rng*>(rng), applies, adjoints);
     f.U.to(u);
     std::copy(f.s.begin(), f.s.end(), s);
     f.V.to(v);

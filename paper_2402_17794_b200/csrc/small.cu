@@ -19,6 +19,8 @@
 //    robin parallel ordering, one warp per column pair, whole matrix resident
 //    in shared memory for l <= 112, L2-resident otherwise.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -251,6 +253,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
     __syncthreads();
   }
   if (sweep >= 60 && tid == 0) atomicOr(flags, kFlagJacobiNoConv);
+  if (tid == 0 && flags) atomicMax(flags + 8, sweep + 1);  // sweep statistics (probe)
   // column norms and stable descending order
   for (int j = warp; j < l; j += nwarps) {
     double s = 0;
@@ -734,9 +737,14 @@ constexpr int kFqThreads = 256;
 __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
     const double* __restrict__ Y, int64_t ldy, int64_t m, int l, int64_t rows_per,
     double* __restrict__ Qo, int64_t ldq, double* __restrict__ part, double* __restrict__ Rout,
-    int64_t ldr, double shift_coef, int passes, int* __restrict__ flags) {
+    int64_t ldr, double shift_coef, int passes, int* __restrict__ flags, long long* probe) {
   constexpr int LD = 33;
   cg::grid_group grid = cg::this_grid();
+  int np_ = 0;
+  auto mark = [&]() {
+    if (probe && blockIdx.x == 0 && threadIdx.x == 0 && np_ < 64) probe[np_++] = clock64();
+  };
+  mark();
   // dynamic shared memory: red[4][32*33] | Gs | A | Rs | Ri | Rt (32*33 each) | inv[32] | Ys
   extern __shared__ double fsm[];
   double (*red)[32 * LD] = reinterpret_cast<double (*)[32 * LD]>(fsm);
@@ -766,6 +774,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
   if (bad) atomicOr(flags, kFlagNonFinite);
   for (int e = tid; e < 32 * LD; e += kFqThreads) Rt[e] = ((e % LD) == (e / LD)) ? 1.0 : 0.0;
   __syncthreads();
+  mark();
   for (int pass = 0; pass < passes; ++pass) {
     // ---- partial Gram: 64 tiles of 4x4, 4 row slices (256 threads)
     {
@@ -798,7 +807,9 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
       pp[e] = ((red[0][o] + red[1][o]) + red[2][o]) + red[3][o];
     }
     __threadfence();
+    mark();
     grid.sync();
+    mark();
     // ---- total Gram, identical in every CTA (fixed CTA order)
     const double* pb0 = part + int64_t(pass & 1) * G * 1024;
     for (int e = tid; e < 1024; e += kFqThreads) {
@@ -815,6 +826,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
       Gs[(e & 31) + LD * (e >> 5)] = v;
     }
     __syncthreads();
+    mark();
     // Converged: the Gram of the current rows is the identity to rounding
     // (|G - I| <= 4 l u): the remaining passes would multiply by R^-1 = I.
     if (pass > 0) {
@@ -848,6 +860,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
       }
     }
     __syncthreads();
+    mark();
     if (!okf) return;  // identical decision in every CTA
     // ---- rows <- rows * R^-1 (upper triangular), in place, one row per thread
     for (int r = tid; r < nr; r += kFqThreads) {
@@ -863,6 +876,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
       }
     }
     __syncthreads();
+    mark();
   }
   for (int e = tid; e < RP * l; e += kFqThreads) {
     const int r = e % RP, a = e / RP;
@@ -1078,10 +1092,24 @@ static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
   int64_t ldr = Rout ? Rout->ld : 0;
   double cf = coef;
   int* fl = h.d_flags;
-  void* args[] = {&yp, &ldy, &mm, &lv, &rpp, &qp, &ldq, &part, &rp_out, &ldr, &cf, &passes, &fl};
+  static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
+  long long* probe = nullptr;
+  if (probe_on) {
+    probe = reinterpret_cast<long long*>(h.ws.alloc_bytes(64 * 8));
+    RSVD_CUDA(cudaMemsetAsync(probe, 0, 64 * 8, h.stream));
+  }
+  void* args[] = {&yp, &ldy, &mm, &lv, &rpp, &qp, &ldq, &part, &rp_out, &ldr, &cf, &passes, &fl, &probe};
   RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cholqr_fused_kernel), dim3(unsigned(G)),
                                         dim3(kFqThreads), args, smem, h.stream));
   RSVD_LAUNCHED(h);
+  if (probe) {
+    long long hp[64];
+    RSVD_CUDA(cudaMemcpyAsync(hp, probe, sizeof hp, cudaMemcpyDeviceToHost, h.stream));
+    RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    std::fprintf(stderr, "cholqr_fused m=%lld l=%d G=%lld:", (long long)m, l, (long long)G);
+    for (int i = 1; i < 64 && hp[i]; ++i) std::fprintf(stderr, " %lld", hp[i] - hp[i - 1]);
+    std::fprintf(stderr, "\n");
+  }
   return true;
 }
 
@@ -1176,6 +1204,13 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
     const int thr = std::max(32, int(round_up(8 * pairs, 32)));
     jacobi_svd_kernel<8><<<1, thr, dyn, h.stream>>>(Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
                                                     gX, gJ, in_smem ? 1 : 0, h.d_flags);
+    static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
+    if (probe_on) {
+      int sw = 0;
+      RSVD_CUDA(cudaMemcpyAsync(&sw, h.d_flags + 8, 4, cudaMemcpyDeviceToHost, h.stream));
+      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      std::fprintf(stderr, "jacobi_svd l=%d sweeps=%d\n", l, sw);
+    }
   } else {
     static size_t cur_j = 0;
     ensure_smem(jacobi_svd_kernel<32>, dyn, cur_j);
