@@ -28,6 +28,7 @@
 #include "dist.cuh"
 #include "pass.cuh"
 #include "small.cuh"
+#include "cholsmall.cuh"
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -35,6 +36,12 @@ namespace cg = cooperative_groups;
 namespace rsvdb {
 
 namespace {
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -629,97 +636,21 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l
   }
 }
 
-// l <= 32: the Cholesky factorization of the (possibly shifted) Gram and the
-// inverse of its factor, by ONE warp on shared memory (lane i owns row i).
-// Every step's dependency chain is a few shared-memory loads, one FMA and one
-// reciprocal square root (no divisions on the critical path):
-//  * Cholesky: step j scales column j by rsqrt(d_j), then lane i updates
-//    A(i, j+1..i) with independent FMAs (L(k,j) is a broadcast load);
-//  * inverse: X = L^-1 column by column, lane c owning column c in registers
-//    (fully unrolled, statically indexed), b_i -= L(i,k) x_k with
-//    precomputed 1/L(k,k); R^-1 = X^T.
-// Shift policy as chol_inv_kernel.  Returns false on breakdown after shifting.
-// G0 (LD 33) is the Gram; outputs R and Rinv (LD 33) in shared memory.
-__device__ __forceinline__ bool warp_chol_inv(const double* G0, int l, double shift_coef, double* A, double* Rs,
-                              double* Rinvs, double* inv, bool* shifted) {
+__global__ void __launch_bounds__(kCholThreads) chol_inv_small_kernel(
+    const double* __restrict__ G, int64_t ldg, int l, double shift_coef, double* __restrict__ R, int64_t ldr,
+    double* __restrict__ Rinv, int64_t ldri, int* shift_used, int* flags) {
   constexpr int LD = 33;
-  const int lane = threadIdx.x & 31;
-  const bool row = lane < l;
-  const double d0 = row ? G0[lane + LD * lane] : 0.0;
-  double tr = d0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
-  bool ok = false;
-  *shifted = false;
-  for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
-    const double shift = attempt ? shift_coef * tr : 0.0;
-    if (row)
-      for (int k = 0; k <= lane; ++k) A[lane + LD * k] = G0[lane + LD * k] + (lane == k ? shift : 0.0);
-    __syncwarp();
-    bool broke = false;
-    for (int j = 0; j < l; ++j) {
-      const double d = A[j + LD * j];
-      const double orig = __shfl_sync(0xffffffffu, d0, j) + shift;
-      if (!(d > 1e-12 * orig) || !(d > 0.0)) {
-        broke = true;
-        break;
-      }
-      const double rs = rsqrt(d);
-      double lij = 0.0;
-      if (row && lane > j) lij = A[lane + LD * j] * rs;
-      __syncwarp();
-      if (row && lane > j) A[lane + LD * j] = lij;
-      if (lane == j) A[j + LD * j] = d * rs;
-      __syncwarp();
-      if (row && lane > j)
-        for (int k = j + 1; k <= lane; ++k) A[lane + LD * k] -= lij * A[k + LD * j];
-      __syncwarp();
-    }
-    ok = !broke;
-    if (ok && attempt == 1) *shifted = true;
-  }
-  if (!ok) return false;
-  if (row) inv[lane] = 1.0 / A[lane + LD * lane];
-  __syncwarp();
-  // R = L^T (LD 33): R(i, c) = L(c, i)
-  if (row)
-    for (int i = 0; i < 32; ++i) Rs[i + LD * lane] = (i <= lane && i < l) ? A[lane + LD * i] : 0.0;
-  double b[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) b[i] = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    if (k < l) {
-      b[k] *= inv[k];
-#pragma unroll
-      for (int i = k + 1; i < 32; ++i)
-        if (i < l) b[i] = fma(-A[i + LD * k], b[k], b[i]);
-    }
-  }
-  // R^-1(c, i) = X(i, c) = b[i] in lane c; store column i of R^-1 at Rinvs[c + LD*i]
-  if (lane < 32)
-#pragma unroll
-    for (int i = 0; i < 32; ++i) Rinvs[lane + LD * i] = (row && i < l && lane <= i) ? b[i] : 0.0;
-  __syncwarp();
-  return true;
-}
-
-__global__ void chol_inv_warp_kernel(const double* __restrict__ G, int64_t ldg, int l,
-                                     double shift_coef, double* __restrict__ R, int64_t ldr,
-                                     double* __restrict__ Rinv, int64_t ldri, int* shift_used,
-                                     int* flags) {
-  constexpr int LD = 33;
-  __shared__ double G0[32 * LD], A[32 * LD], Rs[32 * LD], Ri[32 * LD], inv[32];
-  const int lane = threadIdx.x;
-  for (int e = lane; e < l * l; e += 32) G0[(e % l) + LD * (e / l)] = G[int64_t(e / l) * ldg + (e % l)];
-  __syncwarp();
+  __shared__ double G0[32 * LD], piv[2 * 72], Rs[32 * LD], Ri[32 * LD];
+  for (int e = threadIdx.x; e < l * l; e += kCholThreads)
+    G0[(e % l) + LD * (e / l)] = G[int64_t(e / l) * ldg + (e % l)];
+  __syncthreads();
   bool shifted;
-  if (!warp_chol_inv(G0, l, shift_coef, A, Rs, Ri, inv, &shifted)) {
-    if (lane == 0) atomicOr(flags, kFlagCholBreakdown);
+  if (!cta_chol_inv(G0, l, shift_coef, piv, Rs, Ri, &shifted)) {
+    if (threadIdx.x == 0) atomicOr(flags, kFlagCholBreakdown);
     return;
   }
-  if (shifted && lane == 0 && shift_used) *shift_used = 1;
-  for (int e = lane; e < l * l; e += 32) {
+  if (shifted && threadIdx.x == 0 && shift_used) *shift_used = 1;
+  for (int e = threadIdx.x; e < l * l; e += kCholThreads) {
     const int i = e % l, c = e / l;
     R[int64_t(c) * ldr + i] = Rs[i + LD * c];
     Rinv[int64_t(c) * ldri + i] = Ri[i + LD * c];
@@ -733,6 +664,7 @@ __global__ void chol_inv_warp_kernel(const double* __restrict__ G, int64_t ldg, 
 // Gram with one warp (warp_chol_inv) -> rows <- rows * R^-1 in place.  The
 // partial buffers alternate between passes so one barrier per pass suffices.
 constexpr int kFqThreads = 256;
+static_assert(kFqThreads == kCholThreads, "cta_chol_inv runs on the whole CTA");
 
 __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
     const double* __restrict__ Y, int64_t ldy, int64_t m, int l, int64_t rows_per,
@@ -743,18 +675,17 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
   int np_ = 0;
   auto mark = [&]() {
     if (probe && blockIdx.x == 0 && threadIdx.x == 0 && np_ < 64) probe[np_++] = clock64();
+    if (np_ >= 44) np_ = 43;
   };
   mark();
-  // dynamic shared memory: red[4][32*33] | Gs | A | Rs | Ri | Rt (32*33 each) | inv[32] | Ys
+  // dynamic shared memory: red[8][32*33] | Gs | Rs | Ri | Rt (32*33 each) | Ys
   extern __shared__ double fsm[];
   double (*red)[32 * LD] = reinterpret_cast<double (*)[32 * LD]>(fsm);
-  double* Gs = fsm + 4 * 32 * LD;
-  double* A = Gs + 32 * LD;
-  double* Rs = A + 32 * LD;
+  double* Gs = fsm + 8 * 32 * LD;
+  double* Rs = Gs + 32 * LD;
   double* Ri = Rs + 32 * LD;
   double* Rt = Ri + 32 * LD;
-  double* inv = Rt + 32 * LD;
-  double* Ys = inv + 32;  // rows_per x 33 (row-major, padded)
+  double* Ys = Rt + 32 * LD;  // rows_per x 33 (row-major, padded)
   __shared__ int okf;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int RP = int(rows_per);
@@ -762,6 +693,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
   const int nr = int(m - r0 < rows_per ? m - r0 : rows_per);
   const int G = gridDim.x;
   bool bad = false;
+#pragma unroll 4
   for (int e = tid; e < RP * 32; e += kFqThreads) {
     const int r = e % RP, a = e / RP;
     double v = 0.0;
@@ -776,35 +708,47 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
   __syncthreads();
   mark();
   for (int pass = 0; pass < passes; ++pass) {
-    // ---- partial Gram: 64 tiles of 4x4, 4 row slices (256 threads)
+    // ---- partial Gram Ys^T Ys on DMMA: warp w reduces rows [w*RP/8, (w+1)*RP/8)
+    // into a full 32 x 32 tile (16 m8n8 accumulators); warp tiles summed in order.
     {
-      const int tile = tid & 63, ks = tid >> 6;
-      const int ta = (tile & 7) * 4, tb = (tile >> 3) * 4;
-      double acc[4][4] = {};
-      for (int r = ks; r < nr; r += 4) {
-        const double* yr = Ys + r * LD;
-        double pa[4], pb[4];
+      const int lane = tid & 31, r8 = lane >> 2, c4 = lane & 3;
+      const int wrows = RP / 8, rw0 = warp * wrows;
+      double acc[4][4][2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          pa[q] = yr[ta + q];
-          pb[q] = yr[tb + q];
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int k0 = rw0; k0 < rw0 + wrows; k0 += 4) {
+        const double* yr = Ys + (k0 + c4) * LD;  // row k0 + c4
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          af[i] = yr[i * 8 + r8];  // A(m = a, k = r): Ys[r][a]
+          bf[i] = af[i];           // B(k = r, n = b): Ys[r][b], same fragment shape
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(pa[i], pb[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) red[ks][(ta + i) + LD * (tb + j)] = acc[i][j];
+        for (int j = 0; j < 4; ++j) {
+          const int a0 = i * 8 + r8, b0 = j * 8 + 2 * c4;
+          red[warp][a0 + LD * b0] = acc[i][j][0];
+          red[warp][a0 + LD * (b0 + 1)] = acc[i][j][1];
+        }
     }
     __syncthreads();
     double* pp = part + (int64_t(pass & 1) * G + blockIdx.x) * 1024;
     for (int e = tid; e < 1024; e += kFqThreads) {
       const int a = e & 31, b = e >> 5;
       const int o = a + LD * b;
-      pp[e] = ((red[0][o] + red[1][o]) + red[2][o]) + red[3][o];
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[w][o];
+      pp[e] = v;
     }
     __threadfence();
     mark();
@@ -842,37 +786,68 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
       if (okf == 2) break;  // identical decision in every CTA
       __syncthreads();
     }
-    if (warp == 0) {
+    {
       bool shifted;
-      const bool ok = warp_chol_inv(Gs, l, shift_coef, A, Rs, Ri, inv, &shifted);
-      if ((threadIdx.x & 31) == 0) okf = ok ? 1 : 0;
-      if (!ok && blockIdx.x == 0 && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagCholBreakdown);
-      // R_total <- R * R_total (both upper triangular)
-      if (ok && Rout && blockIdx.x == 0) {
-        // in place, ascending i: row i needs Rt(k, c) only for k >= i
+      long long* pr = (probe && blockIdx.x == 0 && pass < 5) ? probe + 44 + 4 * pass : nullptr;
+      // the Gram partials in red[] are consumed: red[] is the pivot scratch
+      const bool ok = cta_chol_inv(Gs, l, shift_coef, &red[0][0], Rs, Ri, &shifted, pr);
+      if (tid == 0) okf = ok ? 1 : 0;
+      if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(flags, kFlagCholBreakdown);
+      // R_total <- R * R_total (both upper triangular), warp 0 of CTA 0
+      if (ok && Rout && blockIdx.x == 0 && warp == 0) {
+        // lane c: column c of R_total in registers; rows of R are broadcast loads
         const int c = threadIdx.x & 31;
-        for (int i = 0; i < 32; ++i) {
-          double v = 0.0;
-          for (int k = i; k < 32; ++k) v = fma(Rs[i + LD * k], Rt[k + LD * c], v);
-          Rt[i + LD * c] = v;
+        double t[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) t[k] = Rt[k + LD * c];
+#pragma unroll 1
+        for (int i = 0; i < l; ++i) {
+          double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k & 3] = fma(Rs[i + LD * k], t[k], v[k & 3]);
+          Rt[i + LD * c] = (v[0] + v[1]) + (v[2] + v[3]);
         }
         __syncwarp();
       }
+      if (pr && tid == 0) pr[3] = clock64();
     }
     __syncthreads();
     mark();
     if (!okf) return;  // identical decision in every CTA
-    // ---- rows <- rows * R^-1 (upper triangular), in place, one row per thread
-    for (int r = tid; r < nr; r += kFqThreads) {
-      double y[32];
+    // ---- rows <- rows * R^-1 on DMMA, in place: warp w owns rows
+    // [w*RP/8, (w+1)*RP/8) in chunks of 32 (4 m8 tiles x 4 n8 tiles, K = 32)
+    {
+      const int lane = tid & 31, r8 = lane >> 2, c4 = lane & 3;
+      const int wrows = RP / 8, rw0 = warp * wrows;
+      for (int m0 = rw0; m0 < rw0 + wrows; m0 += 32) {
+        double acc[4][4][2];
 #pragma unroll
-      for (int a = 0; a < 32; ++a) y[a] = Ys[r * LD + a];
-#pragma unroll 1
-      for (int c = 0; c < 32; ++c) {
-        double v = 0.0;
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int k = 0; k < 32; ++k) v = fma(y[k], Ri[k + LD * c], v);  // Ri(k, c) = 0 for k > c
-        Ys[r * LD + c] = (c < l) ? v : 0.0;
+          for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const int kk = ks * 4 + c4;
+          double af[4], bf[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) af[i] = Ys[(m0 + i * 8 + r8) * LD + kk];  // A(r, k)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bf[j] = Ri[kk + LD * (j * 8 + r8)];       // B(k, c)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = m0 + i * 8 + r8, c = j * 8 + 2 * c4;
+            Ys[r * LD + c] = (c < l) ? acc[i][j][0] : 0.0;
+            Ys[r * LD + c + 1] = (c + 1 < l) ? acc[i][j][1] : 0.0;
+          }
+        __syncwarp();
       }
     }
     __syncthreads();
@@ -1068,10 +1043,11 @@ static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
   const int l = int(X.cols);
   const int64_t m = X.rows;
   if (l > 32) return false;
-  int64_t G = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(m, 256)));
-  const int64_t rp = ceil_div(m, G);
-  const size_t smem = (size_t(rp) * 33 + 9 * 32 * 33 + 32) * 8;
-  if (smem > 220 * 1024) return false;
+  // rows per CTA: a multiple of 256 (8 warps x 32-row DMMA chunks), <= 512
+  int64_t G = std::max<int64_t>(1, std::min<int64_t>(h.sm_count, ceil_div(m, 256)));
+  const int64_t rp = round_up(ceil_div(m, G), 256);
+  const size_t smem = (size_t(rp) * 33 + 12 * 32 * 33) * 8;
+  if (rp > 512 || smem > 220 * 1024) return false;
   G = ceil_div(m, rp);
   static size_t cur = 0;
   if (smem > cur) {
@@ -1107,7 +1083,10 @@ static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
     RSVD_CUDA(cudaMemcpyAsync(hp, probe, sizeof hp, cudaMemcpyDeviceToHost, h.stream));
     RSVD_CUDA(cudaStreamSynchronize(h.stream));
     std::fprintf(stderr, "cholqr_fused m=%lld l=%d G=%lld:", (long long)m, l, (long long)G);
-    for (int i = 1; i < 64 && hp[i]; ++i) std::fprintf(stderr, " %lld", hp[i] - hp[i - 1]);
+    for (int i = 1; i < 44 && hp[i]; ++i) std::fprintf(stderr, " %lld", hp[i] - hp[i - 1]);
+    std::fprintf(stderr, "\n  chol/inv/rtotal:");
+    for (int i = 44; i < 64 && hp[i]; i += 4)
+      std::fprintf(stderr, " [%lld %lld %lld]", hp[i + 1] - hp[i], hp[i + 2] - hp[i + 1], hp[i + 3] - hp[i + 2]);
     std::fprintf(stderr, "\n");
   }
   return true;
@@ -1130,7 +1109,7 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
     gemm_tn(h, Y, Y, G);
     if (dist) allreduce_mat(h, G);
     if (l <= 32)
-      chol_inv_warp_kernel<<<1, 32, 0, h.stream>>>(G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld,
+      chol_inv_small_kernel<<<1, kCholThreads, 0, h.stream>>>(G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld,
                                                    shift_used, h.d_flags);
     else
       chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
