@@ -352,7 +352,7 @@ def main():
     hbm = hbm_peak_gbs()
     passes = {}
     for kind, d in prof.items():
-        if d["launches"] == 0:
+        if d["launches"] == 0 or kind == "other":
             continue
         per_ms = d["ms"] / d["launches"]
         fl = d["flops"] / d["launches"]

@@ -95,7 +95,8 @@ rsvd_status rsvd_get_counters(rsvd_handle* h, rsvd_counters* out);
 rsvd_status rsvd_reset_counters(rsvd_handle* h);
 /* Live timing of the streaming-pass kernels: when enabled, every pass launch
  * is bracketed by CUDA events on the handle's stream; totals per kind
- * (0 = apply Y = A X, 1 = adjoint Z = A^T Y) with their algorithmic flops and
+ * (0 = apply pass Y = A X, 1 = adjoint pass Z = A^T Y, 2 = other skinny
+ * products such as the lift Q U_B) with their algorithmic flops and
  * bytes (2 M N K, 8 (MK + KN + MN)).  Enabling resets the totals. */
 rsvd_status rsvd_profile_enable(rsvd_handle* h, int on);
 rsvd_status rsvd_profile_read(rsvd_handle* h, int kind, int64_t* launches, double* ms,

@@ -109,8 +109,8 @@ struct Handle {
   };
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> prof_pool;
-  double prof_ms[2] = {0, 0}, prof_flops[2] = {0, 0}, prof_bytes[2] = {0, 0};
-  int64_t prof_count[2] = {0, 0};
+  double prof_ms[3] = {0, 0, 0}, prof_flops[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
+  int64_t prof_count[3] = {0, 0, 0};
   // Launch-site trace (rsvd_trace_enable): an event after every launch; the
   // time between consecutive events (kernel + any idle gap before it) is
   // charged to the launch site at the call's final synchronization.

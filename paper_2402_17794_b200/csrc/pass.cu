@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -98,19 +99,20 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }  // namespace ptx
 
 // ---------------------------------------------------------------- kernel
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+// CW consumer warps (DMMA) + one TMA producer warp per CTA.
 
 // XC = 1: the last of the BN/8 loaded column groups holds ONE real column,
 // computed with DFMA from the A fragments already in registers instead of a
 // padded DMMA n-tile (l = 25 = 3 x 8 + 1: 24 columns on DMMA + 1 on DFMA does
 // 25/32 of the FP64-pipe work of padding to 32; DMMA and DFMA share the pipe).
-template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC>
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW>
 struct PassCfg {
-  static constexpr int BM = kConsumerWarps * WMT * 8;
+  static constexpr int CWARPS = CW;
+  static constexpr int THREADS = (CW + 1) * 32;
+  static constexpr int BM = CW * WMT * 8;
   static constexpr int NT = BN / 8 - XC;  // DMMA n-tiles
   static constexpr int NCOL = NT * 8 + XC;  // output columns per tile
-  static constexpr int FRAG = kConsumerWarps * WMT * NT * 64 + XC * kConsumerWarps * WMT * 32;
+  static constexpr int FRAG = CW * WMT * NT * 64 + XC * CW * WMT * 32;
   static constexpr int KH = BK / 16;  // 16-wide (128-byte) swizzle boxes along K
   static constexpr int A_BYTES = BM * BK * 8;
   static constexpr int B_BYTES = BN * BK * 8;
@@ -160,11 +162,12 @@ __device__ __forceinline__ int sk_cta_of(int64_t u, const PassParams& p) {
   return c;
 }
 
-template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
     pass_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 PassParams p) {
-  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC>;
+  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
+  constexpr int kConsumerWarps = CW;
   constexpr int BM = Cfg::BM, NT = Cfg::NT, NCOL = Cfg::NCOL;
   constexpr int FRAG = Cfg::FRAG;  // doubles per partial tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -243,47 +246,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int wm0 = warp * WMT * 8;
   const int tid = threadIdx.x;
   constexpr int NCT = kConsumerWarps * 32;
-  // Per-lane fragment offsets (bytes within a stage).  The 128B swizzle XORs
-  // the 16B-chunk index with the row index mod 8; everything that depends on
-  // the lane is folded here so the k-step loads are LDS [reg + imm].
-  int offA[4], offB[4];
-  if constexpr (kNN) {
-    // A (M inner): row = K index kr = 8*(ks>>1) + off, off = 2*(ks&1) + 4cy + cx;
-    // column chunk of m = 8i + r8 within its 16-row box.  Index [ks&1][i&1].
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int ksb = q >> 1, ib = q & 1;
-      const int off = 2 * ksb + 4 * cy + cx;
-      const int chunk = ((ib ^ cy) << 2) | ((r8 >> 1) ^ ((ksb << 1) | cx));
-      offA[q] = (wm0 >> 4) * (BK * 128) + off * 128 + chunk * 16 + (r8 & 1) * 8;
-    }
-    // B (K inner): kk = 8*((ks>>1)&1) + off, chunk = (kk>>1) ^ r8.  Index [ks&3].
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int kk = 8 * (q >> 1) + 2 * (q & 1) + 4 * cy + cx;
-      offB[q] = r8 * 128 + (((kk >> 1) ^ r8) << 4) + (kk & 1) * 8;
-    }
-  } else {
-    // A and B both K inner: kk = 4*(ks&3) + c4, chunk = (kk>>1) ^ r8.  Index [ks&3].
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int kk = 4 * q + c4;
-      const int lo = r8 * 128 + (((kk >> 1) ^ r8) << 4) + (kk & 1) * 8;
-      offA[q] = wm0 * 128 + lo;
-      offB[q] = lo;
-    }
-  }
-  // XC column (row NT*8 of the B tile, whose swizzle XOR is 0): lane part of
-  // the byte offset; the k-step part is a compile-time constant.
-  const int offX = kNN ? (32 * cy + 8 * cx) : (16 * cx + 8 * cy);
+  // Per-lane fragment offsets (bytes within a stage).  Shared memory serves a
+  // 64-bit warp load as two half-warp wavefronts, so each HALF warp must hit
+  // 16 distinct 8-byte bank slots (measured: 4 wavefronts instead of 2 per
+  // LDS.64 otherwise).  Inside every 16-wide K block the four DMMA k-steps use
+  // the K sets  {0, 3, 12, 15} ^ t,  t in {0, 1, 4, 5}  (lane c4 takes
+  // base[c4] ^ t; A and B agree, so the contraction is unchanged):
+  //  * K-inner tiles (128B-swizzled rows of 16 K values) need bits 3 and 0 of
+  //    k distinct over c4,
+  //  * the M-inner NN A tile (rows = K index) needs bits 2..1 of k distinct;
+  // {0, 3, 12, 15} satisfies both.  Every lane-dependent term is folded into
+  // one register; the k-step enters as an XOR with a compile-time constant on
+  // bits 3..10 (disjoint from the immediate box/tile offsets).
+  const int kb = (c4 == 0) ? 0 : (c4 == 1) ? 3 : (c4 == 2) ? 12 : 15;
+  int offA0;
+  if constexpr (kNN)
+    offA0 = (wm0 >> 4) * (BK * 128) + kb * 128 + (((r8 >> 1) ^ (kb & 7)) << 4) + (r8 & 1) * 8;
+  else
+    offA0 = wm0 * 128 + r8 * 128 + (((kb >> 1) ^ r8) << 4) + (kb & 1) * 8;
+  const int offB0 = r8 * 128 + (((kb >> 1) ^ r8) << 4) + (kb & 1) * 8;
+  // XC column (row NT*8 of the B tile, swizzle XOR 0): byte k16 * 8
+  const int offX0 = kb * 8;
   int64_t u = u0;
   int seg_local = 0;
   do {
     double acc[WMT][NT][2];
-    double xacc[WMT];
+    double xacc[WMT], xacc2[WMT];  // two K-parity chains for the DFMA column
 #pragma unroll
     for (int i = 0; i < WMT; ++i) {
-      xacc[i] = 0.0;
+      xacc[i] = xacc2[i] = 0.0;
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
@@ -297,37 +288,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint8_t* b_st = a_st + Cfg::A_BYTES;
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
+        constexpr int kT[4] = {0, 1, 4, 5};
+        const int t = kT[ks & 3], kb16 = ks >> 2;
+        const int cB = ((t >> 1) << 4) | ((t & 1) << 3);
         double af[WMT], bf[NT];
         if constexpr (kNN) {
 #pragma unroll
-          for (int i2 = 0; i2 < WMT; ++i2)
-            af[i2] = *reinterpret_cast<const double*>(
-                a_st + offA[((ks & 1) << 1) | (i2 & 1)] + (i2 >> 1) * (BK * 128) + (ks >> 1) * 1024);
-#pragma unroll
-          for (int j = 0; j < NT; ++j)
-            bf[j] = *reinterpret_cast<const double*>(b_st + offB[ks & 3] + (ks >> 2) * (BN * 128) +
-                                                     j * 1024);
+          for (int i2 = 0; i2 < WMT; ++i2) {
+            const int cA = (t << 7) | (((4 * (i2 & 1)) ^ t) << 4);
+            af[i2] = *reinterpret_cast<const double*>(a_st + (offA0 ^ cA) + (i2 >> 1) * (BK * 128) +
+                                                      kb16 * 2048);
+          }
         } else {
 #pragma unroll
           for (int i2 = 0; i2 < WMT; ++i2)
-            af[i2] = *reinterpret_cast<const double*>(a_st + offA[ks & 3] + (ks >> 2) * (BM * 128) +
+            af[i2] = *reinterpret_cast<const double*>(a_st + (offA0 ^ cB) + kb16 * (BM * 128) +
                                                       i2 * 1024);
-#pragma unroll
-          for (int j = 0; j < NT; ++j)
-            bf[j] = *reinterpret_cast<const double*>(b_st + offB[ks & 3] + (ks >> 2) * (BN * 128) +
-                                                     j * 1024);
         }
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          bf[j] = *reinterpret_cast<const double*>(b_st + (offB0 ^ cB) + kb16 * (BN * 128) + j * 1024);
 #pragma unroll
         for (int i2 = 0; i2 < WMT; ++i2)
 #pragma unroll
           for (int j = 0; j < NT; ++j) ptx::dmma(acc[i2][j][0], acc[i2][j][1], af[i2], bf[j]);
         if constexpr (XC == 1) {
           // lane holds A(m = 8i + r8, k = kr): partial dot product with column NT*8
-          const int kconst = kNN ? (64 * ((ks >> 1) & 1) + 16 * (ks & 1)) : 32 * (ks & 3);
           const double bx = *reinterpret_cast<const double*>(
-              b_st + (ks >> 2) * (BN * 128) + NT * 1024 + offX + kconst);
+              b_st + kb16 * (BN * 128) + NT * 1024 + (offX0 ^ (t * 8)));
 #pragma unroll
-          for (int i2 = 0; i2 < WMT; ++i2) xacc[i2] = fma(af[i2], bx, xacc[i2]);
+          for (int i2 = 0; i2 < WMT; ++i2) {
+            if (ks & 1)
+              xacc2[i2] = fma(af[i2], bx, xacc2[i2]);
+            else
+              xacc[i2] = fma(af[i2], bx, xacc[i2]);
+          }
         }
       }
       __syncwarp();
@@ -340,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // in all 4 lanes: IEEE addition is commutative)
 #pragma unroll
       for (int i2 = 0; i2 < WMT; ++i2) {
+        xacc[i2] += xacc2[i2];
         xacc[i2] += __shfl_xor_sync(0xffffffffu, xacc[i2], 1);
         xacc[i2] += __shfl_xor_sync(0xffffffffu, xacc[i2], 2);
       }
@@ -515,12 +511,12 @@ bool tma_ok(const DMat& x) {
   return (reinterpret_cast<uintptr_t>(x.p) % 16 == 0) && (x.ld % 2 == 0) && x.ld >= x.rows;
 }
 
-template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC = 0>
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC = 0, int CW = 8>
 void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t N, int64_t K,
             int force_splits) {
-  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC>;
+  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
   static bool attr_set = false;
-  auto kern = pass_kernel<kNN, BN, WMT, BK, STAGES, XC>;
+  auto kern = pass_kernel<kNN, BN, WMT, BK, STAGES, XC, CW>;
   if (!attr_set) {
     RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr_set = true;
@@ -601,12 +597,15 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
       }
       (i == 0 ? rec.a : rec.b) = e;
     }
-    rec.kind = kNN ? 0 : 1;
+    // kinds: 0 = apply pass over A (A X), 1 = adjoint pass (A^T Y), 2 = other
+    // skinny products (the lift Q U_B): the streamed operand is A exactly when
+    // both of its dimensions dwarf the skinny one
+    rec.kind = (std::min(M, K) > 2 * N) ? (kNN ? 0 : 1) : 2;
     rec.flops = 2.0 * double(M) * double(N) * double(K);
     rec.bytes = 8.0 * (double(M) * K + double(K) * N + double(M) * N);
     RSVD_CUDA(cudaEventRecord(rec.a, h.stream));
   }
-  kern<<<grid, kThreads, Cfg::SMEM, h.stream>>>(ta, tb, pp);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
   RSVD_LAUNCHED(h);
   if (h.prof) {
     RSVD_CUDA(cudaEventRecord(rec.b, h.stream));
@@ -634,8 +633,8 @@ void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
     return;
   }
   DMat Pv = tma_view(h, P), Rv = tma_view(h, R);
-  if (N == 25)
-    launch<true, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits);
+  if (N == 25)  // BK = 48, 3 stages: measured ~2% faster than BK = 32 for NN
+    launch<true, 32, 2, 48, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 32)
     launch<true, 32, 2, 32, 4>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 64)
