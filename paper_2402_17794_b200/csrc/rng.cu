@@ -25,6 +25,7 @@
 //      consumed draw + index, libstdc++'s lazy convention) and the cache.
 // The host Rng state is passed in and returned advanced by exactly the draws
 // consumed, so a host rsvd::Rng continues bit-identically.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -157,15 +158,25 @@ __global__ void __launch_bounds__(320) mt_jump_kernel(const uint64_t* __restrict
   for (int i = t; i < w1 - w0; i += blockDim.x) poly[i] = polys[int64_t(s - 1) * kPolyWords + w0 + i];
   __syncthreads();
   if (t >= kN) return;
+  // Only the set bits of the (warp-uniform) polynomial words contribute:
+  // iterate them in 32-bit halves (find-first-set, clear), ~half of all bits.
   uint64_t acc0 = 0, acc1 = 0;
   for (int w = 0; w < w1 - w0; ++w) {
-    const uint64_t bits = poly[w];  // warp-uniform
+    const uint64_t bits = poly[w];
     const uint64_t* bw = base + 64 * w + t;
-#pragma unroll 16
-    for (int b = 0; b < 64; b += 2) {
-      const uint64_t m0 = 0ULL - ((bits >> b) & 1ULL), m1 = 0ULL - ((bits >> (b + 1)) & 1ULL);
-      acc0 ^= bw[b] & m0;
-      acc1 ^= bw[b + 1] & m1;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      unsigned m = static_cast<unsigned>(bits >> (32 * hf));
+      const uint64_t* bh = bw + 32 * hf;
+      while (m) {
+        const int b0 = __ffs(m) - 1;
+        m &= m - 1;
+        acc0 ^= bh[b0];
+        if (!m) break;
+        const int b1 = __ffs(m) - 1;
+        m &= m - 1;
+        acc1 ^= bh[b1];
+      }
     }
   }
   atomicXor(&windows[int64_t(s) * kN + t], static_cast<unsigned long long>(acc0 ^ acc1));
@@ -179,7 +190,8 @@ __global__ void __launch_bounds__(kSegPerCta * kN) mt_segments_kernel(
   const int64_t seg_words = seg_blocks * kN;
   __shared__ uint64_t S[kSegPerCta][2][kN];
   const int g = threadIdx.x / kN, t = threadIdx.x % kN;
-  const int64_t s = int64_t(blockIdx.x) * kSegPerCta + g;
+  const int spc = int(blockDim.x) / kN;  // segments per CTA (1 .. kSegPerCta)
+  const int64_t s = int64_t(blockIdx.x) * spc + g;
   const bool live = s < nseg;
   if (live) S[g][0][t] = (s == 0) ? init[t] : windows[s * kN + t];
   if (live && s == 0) words[t] = init[t];
@@ -205,7 +217,8 @@ __global__ void __launch_bounds__(kSegPerCta * kN) mt_segments_kernel(
   }
 }
 
-constexpr int kTile = 1024;  // attempts per tile (= 256 threads x 4)
+constexpr int kTile = 256;  // attempts per tile (one per thread): ~4 CTAs per SM
+                            // hide the latency of the correctly rounded log
 
 // 2a. accepted-attempt count per tile.
 __global__ void polar_count_kernel(const uint64_t* __restrict__ words, const uint64_t* p0p,
@@ -436,6 +449,9 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
     const int64_t seg_blocks =
         (words_needed <= 3 * 148 * kSegBlocksShort * kN) ? kSegBlocksShort : kSegBlocksLong;
     const int64_t kSegWords = seg_blocks * kN;
+    // One CTA twists a 312-word block in ~220 ns (measured, latency bound);
+    // beyond two segments the jump-ahead path (base prefix + jump XORs +
+    // parallel segments) is faster.
     if (words_needed <= 2 * kSegWords) {
       const int64_t nb = ceil_div(words_needed, kN) - 1;
       words = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nb + 1) * kN * 8));
@@ -464,7 +480,10 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
       mt_jump_kernel<<<dim3(unsigned(nseg - 1), unsigned(parts)), 320, jsmem, h.stream>>>(
           words, dpolys, wpp, reinterpret_cast<unsigned long long*>(windows));
       RSVD_LAUNCHED(h);
-      mt_segments_kernel<<<unsigned(ceil_div(nseg, kSegPerCta)), kSegPerCta * kN, 0, h.stream>>>(
+      // one segment per CTA while that fits the SMs (a 312-thread CTA twists a
+      // block in ~220 ns; three in lockstep take ~2x longer per block)
+      const int spc = (nseg <= 2 * h.sm_count) ? 1 : kSegPerCta;
+      mt_segments_kernel<<<unsigned(ceil_div(nseg, spc)), spc * kN, 0, h.stream>>>(
           dst->mt, windows, nseg, seg_blocks, words);
       RSVD_LAUNCHED(h);
     }
