@@ -1,6 +1,8 @@
 // extern "C" boundary (include/rsvd_b200.h).  Every entry point: select the
 // handle's device, reset the per-call workspace, run the device pipeline on the
 // handle's stream, synchronize once, map internal errors to rsvd_status.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -45,6 +47,132 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
   }
 }
 
+// Graph-replayed variant of guard() for the top-level device pipelines.
+// `key` identifies everything the host side of the call depends on (entry
+// point, shapes, pointers, the RNG's cached-normal flag); `rng` is the caller's
+// state, re-staged before every launch.  First occurrence: eager (warms the
+// workspace, jump tables, kernel attributes).  Second: captured on the
+// handle's stream, instantiated and launched.  Later: one cudaGraphLaunch plus
+// the counter deltas recorded at capture.  Calls that synchronize with the
+// host mid-way (large-l shift decisions) fail to capture and stay eager.
+// Disabled with RSVD_GRAPHS=0, under profiling/tracing, and with NCCL.
+template <class F>
+rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& key,
+                        rsvd_rng_state* rng, F&& f) {
+  static const bool env_on = [] {
+    const char* e = std::getenv("RSVD_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  if (!hd || !env_on || !hd->h.graphs || hd->h.trace || hd->h.nranks > 1) return guard(hd, what, f);
+  rsvdb::Handle& h = hd->h;
+  auto add = [](rsvd_counters& a, const rsvd_counters& d, int sgn) {
+    a.apply += sgn * d.apply;
+    a.adjoint += sgn * d.adjoint;
+    a.physical_passes += sgn * d.physical_passes;
+    a.kernel_launches += sgn * d.kernel_launches;
+  };
+  try {
+    RSVD_CUDA(cudaSetDevice(h.device));
+    auto gen_now = [&] { return h.generation + h.ws.generation(); };
+    if (h.graph_cache.size() > 256 && !h.graph_cache.count(key)) {  // bound the cache
+      for (auto& kv : h.graph_cache) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        for (auto& r : kv.second.prof) {
+          cudaEventDestroy(r.a);
+          cudaEventDestroy(r.b);
+        }
+      }
+      h.graph_cache.clear();
+    }
+    rsvdb::Handle::GraphEntry& e = h.graph_cache[h.prof ? key + "|prof" : key];
+    if (e.exec && e.gen == gen_now()) {
+      if (rng) std::memcpy(h.h_rng_in, rng, sizeof(rsvd_rng_state));
+      RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
+      add(h.counters, e.delta, 1);
+      h.prof_pending = e.prof;
+      h.rng_user_out = rng;
+      rsvdb::finish_call(h, what);
+      return RSVD_OK;
+    }
+    if (e.exec) {  // stale: a buffer it references was reallocated
+      cudaGraphExecDestroy(e.exec);
+      e.exec = nullptr;
+      for (auto& r : e.prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+      }
+      e.prof.clear();
+    }
+    if (++e.seen >= 2 && !e.bad) {
+      h.ws.reset();
+      h.rng_user_out = nullptr;
+      const rsvd_counters before = h.counters;
+      const uint64_t g0 = gen_now();
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        try {
+          f(h);
+        } catch (...) {
+          ok = false;
+        }
+        const cudaError_t ce = cudaStreamEndCapture(h.stream, &graph);
+        ok = ok && ce == cudaSuccess && graph != nullptr;
+      }
+      const cudaError_t last = cudaGetLastError();
+      const bool same_gen = gen_now() == g0;
+      static const bool dbg = std::getenv("RSVD_GRAPH_DEBUG") != nullptr;
+      if (dbg)
+        std::fprintf(stderr, "graph capture %s: ok=%d same_gen=%d err=%s key=%s\n", what, int(ok),
+                     int(same_gen), cudaGetErrorString(last), key.c_str());
+      if (ok && same_gen) {
+        cudaGraphExec_t exec = nullptr;
+        if (cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+          cudaGraphDestroy(graph);
+          e.exec = exec;
+          e.gen = g0;
+          e.delta = h.counters;
+          add(e.delta, before, -1);
+          for (auto& r : h.prof_pending) r.graph = true;  // the graph keeps these events
+          e.prof = h.prof_pending;
+          RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
+          h.rng_user_out = rng;
+          rsvdb::finish_call(h, what);
+          return RSVD_OK;
+        }
+        cudaGetLastError();
+      }
+      if (graph) cudaGraphDestroy(graph);
+      h.counters = before;
+      for (auto& r : h.prof_pending) {  // events of the failed capture back to the pool
+        h.prof_pool.push_back(r.a);
+        h.prof_pool.push_back(r.b);
+      }
+      h.prof_pending.clear();
+      if (same_gen) e.bad = true;  // genuinely not capturable; a reallocation retries later
+    }
+  } catch (const rsvdb::Error& err) {
+    g_err = err.what();
+    cudaGetLastError();
+    h.rng_user_out = nullptr;
+    cudaStreamSynchronize(h.stream);
+    cudaMemsetAsync(h.d_flags, 0, sizeof(int), h.stream);
+    return err.code;
+  }
+  return guard(hd, what, f);
+}
+
+std::string graph_key(const char* fn, std::initializer_list<int64_t> v) {
+  std::string k(fn);
+  char buf[24];
+  for (int64_t x : v) {
+    std::snprintf(buf, sizeof buf, "|%llx", static_cast<unsigned long long>(x));
+    k += buf;
+  }
+  return k;
+}
+int64_t pv(const void* p) { return static_cast<int64_t>(reinterpret_cast<uintptr_t>(p)); }
+
 rsvdb::DMat dm(const double* p, int64_t r, int64_t c, int64_t ld) {
   if (r < 0 || c < 0) throw rsvdb::Error(RSVD_ERR_DIMENSION, "negative dimension");
   if (r > 0 && c > 0 && ld < r) throw rsvdb::Error(RSVD_ERR_DIMENSION, "leading dimension < rows");
@@ -64,6 +192,7 @@ rsvd_status create_impl(rsvd_handle** out, int device, int rank, int nranks, con
     RSVD_CUDA(cudaMemset(h.d_flags, 0, 64));
     RSVD_CUDA(cudaMallocHost(&h.h_flags, 64));
     RSVD_CUDA(cudaMallocHost(&h.h_rng, sizeof(rsvd_rng_state)));
+    RSVD_CUDA(cudaMallocHost(&h.h_rng_in, sizeof(rsvd_rng_state)));
     RSVD_CUDA(cudaDeviceGetAttribute(&h.sm_count, cudaDevAttrMultiProcessorCount, device));
     rsvdb::rng_init_device(h);
     rsvdb::comm_create(h, rank, nranks, id);
@@ -143,6 +272,14 @@ void rsvd_destroy(rsvd_handle* hd) {
   if (h.d_flags) cudaFree(h.d_flags);
   if (h.h_flags) cudaFreeHost(h.h_flags);
   if (h.h_rng) cudaFreeHost(h.h_rng);
+  if (h.h_rng_in) cudaFreeHost(h.h_rng_in);
+  for (auto& kv : h.graph_cache) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& r : kv.second.prof) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  }
   for (auto e : h.prof_pool) cudaEventDestroy(e);
   for (auto e : h.trace_pool) cudaEventDestroy(e);
   if (h.own_stream) cudaStreamDestroy(h.own_stream);
@@ -300,7 +437,9 @@ rsvd_status rsvd_apply_adjoint_dev(rsvd_handle* hd, int64_t m, int64_t n, const 
 rsvd_status rsvd_range_basis_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
                                  int64_t lda, int64_t k, int64_t p, int q, int mode,
                                  rsvd_rng_state* rng, double* q_out, int64_t ldq) {
-  return guard(hd, "range_basis", [&](rsvdb::Handle& h) {
+  const std::string key = graph_key("range_basis", {m, n, pv(a), lda, k, p, q, mode, pv(q_out), ldq,
+                                                    rng ? rng->has_cached : -1});
+  return guard_graph(hd, "range_basis", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
     rsvdb::range_basis_impl(h, P, k, p, q, mode, r, dm(q_out, m, std::max<int64_t>(k + p, 0), ldq));
@@ -311,7 +450,9 @@ rsvd_status rsvd_range_basis_dev(rsvd_handle* hd, int64_t m, int64_t n, const do
 rsvd_status rsvd_rsvd_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
                           int64_t k, int64_t p, int q, int mode, rsvd_rng_state* rng, double* u,
                           int64_t ldu, double* sigma, double* v, int64_t ldv) {
-  return guard(hd, "rsvd", [&](rsvdb::Handle& h) {
+  const std::string key = graph_key("rsvd", {m, n, pv(a), lda, k, p, q, mode, pv(u), ldu, pv(sigma),
+                                             pv(v), ldv, rng ? rng->has_cached : -1});
+  return guard_graph(hd, "rsvd", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
     const int64_t l = std::max<int64_t>(k + p, 0);
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
@@ -342,7 +483,9 @@ rsvd_status rsvd_rsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* 
 rsvd_status rsvd_spevd_dev(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
                            int64_t p, rsvd_rng_state* rng, int check_symmetry, double* u,
                            int64_t ldu, double* lambda) {
-  return guard(hd, "spevd_hermitian", [&](rsvdb::Handle& h) {
+  const std::string key = graph_key("spevd", {n, pv(a), lda, k, p, check_symmetry, pv(u), ldu,
+                                              pv(lambda), rng ? rng->has_cached : -1});
+  return guard_graph(hd, "spevd_hermitian", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, n, n, lda);
     // local rows: for a single GPU m_local == n
     P.A = dm(a, P.A.rows, n, lda);
@@ -374,7 +517,9 @@ rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t
 rsvd_status rsvd_spsvd_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
                            int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                            double* sigma, double* v, int64_t ldv) {
-  return guard(hd, "spsvd_general", [&](rsvdb::Handle& h) {
+  const std::string key = graph_key("spsvd", {m, n, pv(a), lda, k, p, pv(u), ldu, pv(sigma), pv(v),
+                                              ldv, rng ? rng->has_cached : -1});
+  return guard_graph(hd, "spsvd_general", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
     const int64_t kk = std::max<int64_t>(k, 0);
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
@@ -473,7 +618,9 @@ rsvd_status rsvd_solve_ls_host(rsvd_handle* hd, int64_t m, int64_t n, const doub
 rsvd_status rsvd_range_basis_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
                                   int64_t lda, int64_t k, int64_t p, int q, int mode,
                                   rsvd_rng_state* rng, double* q_out, int64_t ldq) {
-  return guard(hd, "range_basis", [&](rsvdb::Handle& h) {
+  const std::string key = graph_key("range_basis", {m, n, pv(a), lda, k, p, q, mode, pv(q_out), ldq,
+                                                    rng ? rng->has_cached : -1});
+  return guard_graph(hd, "range_basis", key, rng, [&](rsvdb::Handle& h) {
     HostIO io{h};
     rsvdb::DMat A = io.up(a, m, n, lda);
     rsvdb::Problem P = rsvdb::make_problem(h, A.p, m, n, A.ld);

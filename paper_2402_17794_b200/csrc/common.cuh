@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "rsvd_b200.h"
@@ -73,6 +74,8 @@ class Arena {
     return DMat(alloc(ld * c), r, c, ld);
   }
   size_t high_water() const { return high_; }
+  // bumped whenever chunk addresses change (captured CUDA graphs hold them)
+  uint64_t generation() const { return gen_; }
 
  private:
   struct Chunk {
@@ -81,6 +84,7 @@ class Arena {
   };
   std::vector<Chunk> chunks_;
   size_t used_total_ = 0, high_ = 0;
+  uint64_t gen_ = 0;
 };
 
 struct Comm;  // NCCL communicator wrapper (dist.cu)
@@ -106,6 +110,7 @@ struct Handle {
     cudaEvent_t a, b;
     int kind;  // 0 = NN (Y = A X), 1 = TN (Z = A^T Y)
     double flops, bytes;
+    bool graph = false;  // events owned by a captured graph (not pooled)
   };
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> prof_pool;
@@ -125,6 +130,24 @@ struct Handle {
   // pinned staging for the RNG state copy-back (rng.cu)
   void* h_rng = nullptr;
   rsvd_rng_state* rng_user_out = nullptr;
+  // pinned staging for the RNG state upload (the graph-captured H2D source)
+  rsvd_rng_state* h_rng_in = nullptr;
+  // CUDA-graph replay of repeated top-level device calls (capi.cu): a call
+  // is captured on its second occurrence (same shapes, pointers and
+  // host-visible RNG state) and replayed as one graph launch afterwards.
+  // `generation` is bumped whenever a buffer a graph may hold is reallocated
+  // (split-K semaphores, jump polynomials; the arena keeps its own count).
+  bool graphs = true;
+  uint64_t generation = 0;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t gen = 0;
+    rsvd_counters delta{};
+    std::vector<ProfRec> prof;  // pass-timing events recorded inside the graph
+    int seen = 0;
+    bool bad = false;  // not capturable (host synchronization inside the call)
+  };
+  std::unordered_map<std::string, GraphEntry> graph_cache;
 };
 
 // End of a top-level call: synchronize, raise NumericError on device flags,

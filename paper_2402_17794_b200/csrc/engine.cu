@@ -36,6 +36,7 @@ void Arena::reset() {
     Chunk c{nullptr, size_t(round_up(int64_t(high_), int64_t(1) << 20)), 0};
     RSVD_CUDA(cudaMalloc(&c.p, c.cap));
     chunks_.push_back(c);
+    ++gen_;
   }
   for (auto& c : chunks_) c.off = 0;
   used_total_ = 0;
@@ -55,6 +56,7 @@ void* Arena::alloc_bytes(size_t bytes) {
       RSVD_CUDA(cudaMalloc(&c.p, c.cap));
     }
     chunks_.push_back(c);
+    ++gen_;
   }
   Chunk& c = chunks_.back();
   void* p = c.p + c.off;
@@ -72,6 +74,7 @@ int* tile_counters(Handle& h, int64_t n) {
     }
     const int64_t cap = std::max<int64_t>(n, 4096);
     RSVD_CUDA(cudaMalloc(&h.d_counters, size_t(cap) * sizeof(int)));
+    ++h.generation;
     RSVD_CUDA(cudaMemsetAsync(h.d_counters, 0, size_t(cap) * sizeof(int), h.stream));
     h.n_counters = cap;
   }
@@ -133,8 +136,10 @@ void finish_call(Handle& h, const char* what) {
     h.prof_flops[r.kind] += r.flops;
     h.prof_bytes[r.kind] += r.bytes;
     h.prof_count[r.kind] += 1;
-    h.prof_pool.push_back(r.a);
-    h.prof_pool.push_back(r.b);
+    if (!r.graph) {
+      h.prof_pool.push_back(r.a);
+      h.prof_pool.push_back(r.b);
+    }
   }
   h.prof_pending.clear();
   if (h.trace) trace_collect(h);

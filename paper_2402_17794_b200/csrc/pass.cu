@@ -242,7 +242,6 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
 
   // -------------------------------------------------- DMMA consumer warps
   const int r8 = lane >> 2, c4 = lane & 3;
-  const int cx = c4 >> 1, cy = c4 & 1;
   const int wm0 = warp * WMT * 8;
   const int tid = threadIdx.x;
   constexpr int NCT = kConsumerWarps * 32;
@@ -586,6 +585,7 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
                        : make_map(P.p, P.rows, P.cols, P.ld, 16, Cfg::BM);
   CUtensorMap tb = make_map(R.p, R.rows, R.cols, R.ld, 16, BN);
   Handle::ProfRec rec{};
+  unsigned rec_flags = cudaEventRecordDefault;
   if (h.prof) {
     for (int i = 0; i < 2; ++i) {
       cudaEvent_t e;
@@ -603,12 +603,16 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     rec.kind = (std::min(M, K) > 2 * N) ? (kNN ? 0 : 1) : 2;
     rec.flops = 2.0 * double(M) * double(N) * double(K);
     rec.bytes = 8.0 * (double(M) * K + double(K) * N + double(M) * N);
-    RSVD_CUDA(cudaEventRecord(rec.a, h.stream));
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    RSVD_CUDA(cudaStreamIsCapturing(h.stream, &cap));
+    // under capture the event must be an external event-record node to be timeable
+    rec_flags = (cap == cudaStreamCaptureStatusActive) ? cudaEventRecordExternal : cudaEventRecordDefault;
+    RSVD_CUDA(cudaEventRecordWithFlags(rec.a, h.stream, rec_flags));
   }
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
   RSVD_LAUNCHED(h);
   if (h.prof) {
-    RSVD_CUDA(cudaEventRecord(rec.b, h.stream));
+    RSVD_CUDA(cudaEventRecordWithFlags(rec.b, h.stream, rec_flags));
     h.prof_pending.push_back(rec);
   }
 }

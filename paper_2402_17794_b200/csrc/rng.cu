@@ -389,6 +389,7 @@ static const uint64_t* device_jump_polys(Handle& h, uint64_t L, int count) {
       RSVD_CUDA(cudaFree(h.d_jump));
     }
     RSVD_CUDA(cudaMalloc(&h.d_jump, size_t(count) * kPolyWords * 8));
+    ++h.generation;
     RSVD_CUDA(cudaMemcpy(h.d_jump, hp, size_t(count) * kPolyWords * 8, cudaMemcpyHostToDevice));
     h.jump_L = L;
     h.jump_count = count;
@@ -407,7 +408,10 @@ DevRng rng_upload(Handle& h, const rsvd_rng_state* st) {
   r.d = h.ws.alloc_bytes(sizeof(DevState));
   r.has_cached = st->has_cached ? 1 : 0;
   static_assert(sizeof(DevState) == sizeof(rsvd_rng_state), "state layout");
-  RSVD_CUDA(cudaMemcpyAsync(r.d, st, sizeof(DevState), cudaMemcpyHostToDevice, h.stream));
+  // through pinned staging: a graph-capturable copy whose source the replay
+  // path refills with the caller's state before each launch
+  if (h.h_rng_in != st) std::memcpy(h.h_rng_in, st, sizeof(DevState));
+  RSVD_CUDA(cudaMemcpyAsync(r.d, h.h_rng_in, sizeof(DevState), cudaMemcpyHostToDevice, h.stream));
   return r;
 }
 

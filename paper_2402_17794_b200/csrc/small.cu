@@ -238,10 +238,15 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
+        // rotation from two reciprocal square roots (no sqrt/div on the chain):
+        // ir = 1/r, r = |(d, 2g)|; cos 2th = |d|/r; c = sqrt(h), h = (1+cos 2th)/2;
+        // s = sgn(d) sin 2th / (2c) = sgn(d) g ir / sqrt(h)  (c^2 + s^2 = 1)
+        if (ga * ga > tol * tol * (al * be) && ga != 0.0) {
           const double d = be - al, g2 = 2.0 * ga;
-          const double t = copysign(1.0, d) * g2 / (fabs(d) + sqrt(d * d + g2 * g2));
-          const double c = rsqrt(1.0 + t * t), sn = c * t;
+          const double ir = rsqrt(fma(d, d, g2 * g2));
+          const double hh = fma(0.5 * fabs(d), ir, 0.5);
+          const double ih = rsqrt(hh);
+          const double c = hh * ih, sn = copysign(1.0, d) * (ga * ir) * ih;
           if (row) {
             X[pcol * l + lane] = c * xp - sn * xq;
             X[qcol * l + lane] = sn * xp + c * xq;

@@ -297,3 +297,38 @@ def test_spsvd_counts_one_apply_one_adjoint(eng):
     op = eng.CountingOperator(_t(rs.standard_normal((30, 20))))
     eng.spsvd_general(op, 4, 3, eng.Rng(3))
     assert op.apply_count() == 1 and op.adjoint_count() == 1
+
+
+# ------------------------------------------------------- CUDA-graph replay
+def test_graph_replay_matches_eager(eng):
+    """Repeated device calls with identical shapes and pointers are captured
+    (second call) and replayed as one CUDA graph (third call on).  Every call
+    must give bitwise the same factors, RNG state and counter deltas as a
+    fresh handle's eager first call, including after a seed change."""
+    import ctypes
+    import torch
+    L = eng._load()
+    m, n, k, p, q = 1500, 700, 10, 4, 1
+    l = k + p
+    a = _t(haar_test_matrix(m, n, np.logspace(0, -3, 40), 5))
+    u = torch.empty((l, m), dtype=torch.float64, device="cuda").t()
+    v = torch.empty((l, n), dtype=torch.float64, device="cuda").t()
+    s = torch.empty(l, dtype=torch.float64, device="cuda")
+
+    def call(e, seed):
+        r = eng.Rng(seed)
+        c0 = e.counters()
+        eng._check(L.rsvd_rsvd_dev(e.handle, m, n, a.data_ptr(), m, k, p, q, 2, ctypes.byref(r.state),
+                                   u.data_ptr(), m, s.data_ptr(), v.data_ptr(), n))
+        c1 = e.counters()
+        d = {key: c1[key] - c0[key] for key in c1}
+        return u.cpu().numpy().copy(), s.cpu().numpy().copy(), v.cpu().numpy().copy(), bytes(r.state), d
+
+    e1 = eng.Engine(0)
+    runs = [call(e1, 3) for _ in range(4)] + [call(e1, 4)]
+    ref3, ref4 = call(eng.Engine(0), 3), call(eng.Engine(0), 4)
+    for got, ref in zip(runs, [ref3] * 4 + [ref4]):
+        for x, y in zip(got[:3], ref[:3]):
+            assert np.array_equal(x, y)
+        assert got[3] == ref[3]
+        assert got[4] == ref[4]
