@@ -15,8 +15,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
+#include "pass.cuh"
 #include "small.cuh"
 
 namespace cg = cooperative_groups;
@@ -45,21 +48,50 @@ __device__ __forceinline__ void circle(int pr, int round, int np, int& a, int& b
   b = 1 + ib;
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+constexpr int kGL = 33;  // ld of the 32 x 32 Gram in shared memory
+constexpr int kVL = 36;  // ld of V: 36 % 16 == 4 keeps DMMA B-fragment loads conflict-free
+
+// Block pair visit = Gram-based inner step (Hari-Veselic block Jacobi):
+//   G = Xb^T Xb (DMMA), cyclic two-sided Jacobi on the 32 x 32 G accumulating
+//   the rotation V (same rotation rule and threshold as one-sided Jacobi on
+//   the columns), then X(:, pair) <- Xb V and J(:, pair) <- J(:, pair) V (DMMA).
+// The l-long column work is three small GEMMs instead of 31 inner rounds of
+// l-long dot products; the inner rounds touch only the 32 x 32 G.  Outer
+// convergence is measured on the freshly computed G of every visit, so the
+// final orthogonality is that of one-sided Jacobi.
 __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict__ X,
-                                                            double* __restrict__ Jm, int l,
-                                                            int nb, int* __restrict__ changed) {
+                                                            double* __restrict__ Jm, int l, int ldp,
+                                                            int nb, int inner_max,
+                                                            int* __restrict__ changed,
+                                                            long long* __restrict__ probe) {
+  long long pt[6] = {0, 0, 0, 0, 0, 0}, tlast = clock64();
+  auto mark = [&](int ph) {
+    if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
+      const long long t = clock64();
+      pt[ph] += t - tlast;
+      tlast = t;
+    }
+  };
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
-  double* Xb = sm;                            // l x kBJW, ld = l
-  double* V = sm + size_t(l) * kBJW;          // kBJW x kBJW, ld = kBJW
+  double* Xb = sm;                           // kBJW columns x ldp rows (rows >= l are zero)
+  double* G = Xb + size_t(kBJW) * ldp;       // kBJW x kBJW, ld kGL
+  double* V = G + kBJW * kGL;                // kBJW x kBJW, ld kVL (column-major: V[c * kVL + r])
   __shared__ int colmap[kBJW];
-  __shared__ int any;
+  __shared__ double rc[kBJW / 2], rs[kBJW / 2];
+  __shared__ int rp[kBJW / 2], rq[kBJW / 2];
+  __shared__ int any_first, any_inner, any_visit;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nwarps = blockDim.x >> 5;
+  const int r8 = lane >> 2, c4 = lane & 3;
   const int nbp = nb + (nb & 1);
-  // rotation threshold: the rounding noise of an l-term dot product is ~sqrt(l) eps,
-  // so a fixed 1e-15 would never report convergence for large l
   const double tol = fmax(1e-15, 2.0 * sqrt(double(l)) * 1.1102230246251565e-16);
+  const double tol2 = tol * tol;
   for (int sweep = 0; sweep < kBJMaxSweeps; ++sweep) {
     for (int round = 0; round < nbp - 1; ++round) {
       for (int pr = blockIdx.x; pr < nbp / 2; pr += gridDim.x) {
@@ -69,78 +101,166 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
         if (K >= nb) continue;  // dummy block
         const int wI = min(kBJ, l - I * kBJ), wK = min(kBJ, l - K * kBJ);
         const int w = wI + wK;
-        if (tid < w) colmap[tid] = (tid < wI) ? I * kBJ + tid : K * kBJ + (tid - wI);
-        if (tid == 0) any = 0;
+        if (tid < kBJW) colmap[tid] = (tid < wI) ? I * kBJ + tid : (tid < w ? K * kBJ + (tid - wI) : -1);
+        if (tid == 0) any_first = any_visit = 0;
         __syncthreads();
-        for (int e = tid; e < l * w; e += blockDim.x) {
-          const int r = e % l, c = e / l;
-          Xb[c * l + r] = X[int64_t(colmap[c]) * l + r];
+        // ---- panel load (zero padded to kBJW columns x ldp rows)
+        for (int e = tid; e < kBJW * ldp; e += blockDim.x) {
+          const int c = e / ldp, r = e - c * ldp;
+          const int gc = colmap[c];
+          Xb[e] = (gc >= 0 && r < l) ? X[int64_t(gc) * l + r] : 0.0;
         }
-        for (int e = tid; e < kBJW * kBJW; e += blockDim.x)
-          V[e] = ((e % kBJW) == (e / kBJW)) ? 1.0 : 0.0;
+        for (int e = tid; e < kBJW * kVL; e += blockDim.x) V[e] = ((e % kVL) == (e / kVL)) ? 1.0 : 0.0;
         __syncthreads();
-        // one inner sweep over the w columns, one warp per column pair
-        const int wp = w + (w & 1);
-        for (int r2 = 0; r2 < wp - 1; ++r2) {
-          for (int q = warp; q < wp / 2; q += nwarps) {
-            int pa, pb;
-            circle(q, r2, wp, pa, pb);
-            const int p0 = min(pa, pb), q0 = max(pa, pb);
-            if (q0 >= w) continue;
-            double al = 0, be = 0, ga = 0;
-            for (int i = lane; i < l; i += 32) {
-              const double xp = Xb[p0 * l + i], xq = Xb[q0 * l + i];
-              al = fma(xp, xp, al);
-              be = fma(xq, xq, be);
-              ga = fma(xp, xq, ga);
-            }
-            al = wsum(al);
-            be = wsum(be);
-            ga = wsum(ga);
-            if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
-              const double d = be - al, g2 = 2.0 * ga;
-              const double t = copysign(1.0, d) * g2 / (fabs(d) + sqrt(d * d + g2 * g2));
-              const double c = rsqrt(1.0 + t * t), s = c * t;
-              for (int i = lane; i < l; i += 32) {
-                const double xp = Xb[p0 * l + i], xq = Xb[q0 * l + i];
-                Xb[p0 * l + i] = c * xp - s * xq;
-                Xb[q0 * l + i] = s * xp + c * xq;
+        mark(0);
+        // ---- G = Xb^T Xb: warp -> 8 x 8 tile (ti, tj) of the 4 x 4 tile grid, K = ldp
+        {
+          const int ti = warp >> 2, tj = warp & 3;
+          double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
+          const double* pa = Xb + (ti * 8 + r8) * ldp + c4;  // A(m = col, k = row)
+          const double* pb = Xb + (tj * 8 + r8) * ldp + c4;  // B(k = row, n = col)
+          int k0 = 0;
+          for (; k0 + 8 <= ldp; k0 += 8) {
+            dmma884(g0, g1, pa[k0], pb[k0]);
+            dmma884(h0, h1, pa[k0 + 4], pb[k0 + 4]);
+          }
+          if (k0 < ldp) dmma884(g0, g1, pa[k0], pb[k0]);
+          const int gi = ti * 8 + r8, gj = tj * 8 + 2 * c4;
+          G[gi + kGL * gj] = g0 + h0;
+          G[gi + kGL * (gj + 1)] = g1 + h1;
+        }
+        __syncthreads();
+        mark(1);
+        // ---- cyclic two-sided Jacobi on G (w active columns), accumulating V.
+        // Per round: the wp/2 rotations (one thread each), then G <- R^T G R as
+        // independent 2 x 2 blocks (pair i rows x pair j columns) and V <- V R:
+        // two barriers per round.  (A warp-per-pair variant with rows in
+        // registers and shuffled column rotations measured 2x slower.)
+        const int wp = w + (w & 1), np2 = wp / 2;
+        for (int it = 0; it < inner_max; ++it) {
+          if (tid == 0) any_inner = 0;
+          for (int r2 = 0; r2 < wp - 1; ++r2) {
+            if (tid < np2) {
+              int pa, pb;
+              circle(tid, r2, wp, pa, pb);
+              const int p0 = min(pa, pb), q0 = max(pa, pb);
+              double c = 1.0, sn = 0.0;
+              const double al = G[p0 + kGL * p0], be = G[q0 + kGL * q0], ga = G[p0 + kGL * q0];
+              if (q0 < w && ga * ga > tol2 * (al * be) && ga != 0.0) {
+                // rotation zeroing the (p, q) inner product (X' = X R, R = [[c, s], [-s, c]]),
+                // tan(theta) = sgn(d) 2g / (|d| + r), r = |(d, 2g)|, d = G_qq - G_pp,
+                // from two reciprocal square roots: c = sqrt(h), h = (1 + |d|/r) / 2,
+                // s = sgn(d) g / (r c)
+                const double d = be - al, g2 = 2.0 * ga;
+                const double ir = rsqrt(fma(d, d, g2 * g2));
+                const double hh = fma(0.5 * fabs(d), ir, 0.5);
+                const double ih = rsqrt(hh);
+                c = hh * ih;
+                sn = copysign(1.0, d) * (ga * ir) * ih;
+                any_inner = 1;
               }
-              if (lane < w) {
-                const double vp = V[p0 * kBJW + lane], vq = V[q0 * kBJW + lane];
-                V[p0 * kBJW + lane] = c * vp - s * vq;
-                V[q0 * kBJW + lane] = s * vp + c * vq;
-              }
-              if (lane == 0) any = 1;
+              rc[tid] = c;
+              rs[tid] = sn;
+              rp[tid] = p0;
+              rq[tid] = q0;
             }
+            __syncthreads();
+            if (tid < 256) {
+              const int bi = tid >> 4, bj = tid & 15;
+              if (bi < np2 && bj < np2 && (rs[bi] != 0.0 || rs[bj] != 0.0)) {
+                const int pi = rp[bi], qi = rq[bi], pj = rp[bj], qj = rq[bj];
+                const double ci = rc[bi], si = rs[bi], cj = rc[bj], sj = rs[bj];
+                const double b00 = G[pi + kGL * pj], b01 = G[pi + kGL * qj];
+                const double b10 = G[qi + kGL * pj], b11 = G[qi + kGL * qj];
+                // rows: R_i^T B
+                const double m00 = ci * b00 - si * b10, m01 = ci * b01 - si * b11;
+                const double m10 = si * b00 + ci * b10, m11 = si * b01 + ci * b11;
+                // columns: (R_i^T B) R_j
+                G[pi + kGL * pj] = cj * m00 - sj * m01;
+                G[pi + kGL * qj] = sj * m00 + cj * m01;
+                G[qi + kGL * pj] = cj * m10 - sj * m11;
+                G[qi + kGL * qj] = sj * m10 + cj * m11;
+              }
+            } else {
+              const int k = (tid - 256) >> 4, i0 = (tid - 256) & 15;
+              if (k < np2 && rs[k] != 0.0) {
+                const int p0 = rp[k], q0 = rq[k];
+                const double c = rc[k], sn = rs[k];
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                  const int i = i0 + 16 * h2;
+                  const double vp = V[i + kVL * p0], vq = V[i + kVL * q0];
+                  V[i + kVL * p0] = c * vp - sn * vq;
+                  V[i + kVL * q0] = sn * vp + c * vq;
+                }
+              }
+            }
+            __syncthreads();
+          }
+          const int rot = any_inner;
+          if (tid == 0) {
+            if (it == 0) any_first = rot;
+            any_visit |= rot;
           }
           __syncthreads();
+          if (!rot) break;
         }
-        for (int e = tid; e < l * w; e += blockDim.x) {
-          const int r = e % l, c = e / l;
-          X[int64_t(colmap[c]) * l + r] = Xb[c * l + r];
-        }
-        // J(:, block cols) <- J(:, block cols) * V, one row per thread
-        for (int r = tid; r < l; r += blockDim.x) {
-          double jr[kBJW];
+        mark(2);
+        if (any_visit) {
+          // ---- X(:, pair) <- Xb V and J(:, pair) <- J(:, pair) V: warp -> 8-row tiles
+          double vb[4][8];  // B fragments of V: [n tile][k step]
 #pragma unroll
-          for (int c = 0; c < kBJW; ++c) jr[c] = (c < w) ? Jm[int64_t(colmap[c]) * l + r] : 0.0;
-#pragma unroll 4
-          for (int c = 0; c < kBJW; ++c) {
-            if (c >= w) break;
-            double acc = 0.0;
+          for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-            for (int k = 0; k < kBJW; ++k) acc = fma(jr[k], V[c * kBJW + k], acc);
-            Jm[int64_t(colmap[c]) * l + r] = acc;
+            for (int ks = 0; ks < 8; ++ks) vb[nt][ks] = V[(nt * 8 + r8) * kVL + ks * 4 + c4];
+          const int ntiles = (l + 7) / 8;
+          for (int mt = warp; mt < 2 * ntiles; mt += 16) {
+            const bool isJ = mt >= ntiles;
+            const int m0 = (isJ ? mt - ntiles : mt) * 8;
+            double af[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const int k = ks * 4 + c4, row = m0 + r8;
+              if (!isJ) {
+                af[ks] = Xb[k * ldp + row];
+              } else {
+                const int gc = colmap[k];
+                af[ks] = (gc >= 0 && row < l) ? Jm[int64_t(gc) * l + row] : 0.0;
+              }
+            }
+            double acc[4][2];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks) dmma884(acc[nt][0], acc[nt][1], af[ks], vb[nt][ks]);
+            }
+            double* dst = isJ ? Jm : X;
+            const int row = m0 + r8;
+            if (row < l) {
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int gc = colmap[nt * 8 + 2 * c4 + e];
+                  if (gc >= 0) dst[int64_t(gc) * l + row] = acc[nt][e];
+                }
+            }
           }
         }
-        if (tid == 0 && any) atomicOr(&changed[sweep], 1);
+        if (tid == 0 && any_first) atomicOr(&changed[sweep], 1);
         __syncthreads();
+        mark(3);
       }
       grid.sync();
+      mark(4);
     }
     const int done = (*reinterpret_cast<volatile int*>(&changed[sweep]) == 0);
-    if (done) return;
+    if (done) {
+      if (probe && blockIdx.x == 0 && threadIdx.x == 0)
+        for (int i = 0; i < 6; ++i) probe[i] = pt[i];
+      return;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) changed[kBJMaxSweeps] = 1;  // no convergence
 }
@@ -287,18 +407,36 @@ __global__ void shift_copy_kernel(const double* __restrict__ C, int64_t ldc, int
   }
 }
 
-// lambda = sigma - mu, reordered by |lambda| descending; exact ties: positive
-// first (see evd_symmetric in small.cu / the oracle).
-__global__ void evd_order_kernel(const double* __restrict__ sigma, const double* __restrict__ mu,
-                                 const double* __restrict__ Jm, int64_t ldj, int l,
-                                 double* __restrict__ U, int64_t ldu, double* __restrict__ lambda,
-                                 int* __restrict__ order) {
-  const double m = *mu;
+// Rayleigh quotients lambda_j = u_j^T (C u_j) of the computed eigenvectors (one
+// CTA per column).  Second-order accurate in the eigenvector error, unlike
+// sigma_j - mu, whose absolute error carries the shift mu and the rounding
+// of every accumulated rotation.
+__global__ void rayleigh_kernel(const double* __restrict__ Jm, int64_t ldj,
+                                const double* __restrict__ CJ, int64_t ldc, int l,
+                                double* __restrict__ lam) {
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < l; i += blockDim.x) s = fma(Jm[int64_t(c) * ldj + i], CJ[int64_t(c) * ldc + i], s);
+  __shared__ double red[8];
+  s = wsum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+    lam[c] = t;
+  }
+}
+
+// eigenvalues (Rayleigh quotients) reordered by |lambda| descending; exact
+// ties: positive first (see evd_symmetric in small.cu / the oracle).
+__global__ void evd_order_kernel(const double* __restrict__ lam_in, int l,
+                                 double* __restrict__ lambda, int* __restrict__ order) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < l; j += gridDim.x * blockDim.x) {
-    const double v = sigma[j] - m;
+    const double v = lam_in[j];
     int rank = 0;
     for (int k = 0; k < l; ++k) {
-      const double u = sigma[k] - m;
+      const double u = lam_in[k];
       if (fabs(u) > fabs(v) || (fabs(u) == fabs(v) && (u > v || (u == v && k < j)))) ++rank;
     }
     order[rank] = j;
@@ -328,7 +466,11 @@ void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) 
   bj_init_kernel<<<std::max(1, std::min(4 * h.sm_count, (l * l + 255) / 256)), 256, 0, h.stream>>>(
       Rm.p, Rm.ld, l, X, Jm);
   RSVD_LAUNCHED(h);
-  const size_t smem = (size_t(l) * kBJW + kBJW * kBJW) * 8;
+  // panel rows padded to ldp = l rounded up to 8 with ldp % 16 in {4, 12}... use the
+  // smallest ldp >= l, ldp % 4 == 0, (ldp / 4) odd: conflict-free DMMA fragment loads
+  int ldp = (l + 3) / 4 * 4;
+  if ((ldp / 4) % 2 == 0) ldp += 4;
+  const size_t smem = (size_t(ldp) * kBJW + kBJW * kGL + kBJW * kVL) * 8;
   if (smem > 227 * 1024) throw_dim("block_jacobi_svd: l too large for one block pair in shared memory");
   static size_t cur = 0;
   if (smem > cur) {
@@ -337,13 +479,48 @@ void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) 
     cur = smem;
   }
   int nbv = nb;
-  int lv = l;
+  int lv = l, ldpv = ldp;
+  // one inner sweep per visit: more inner sweeps do not reduce the outer sweep
+  // count measurably (C3-C5 shapes)
+  static const int inner_env = std::getenv("RSVD_BJ_INNER") ? std::atoi(std::getenv("RSVD_BJ_INNER")) : 1;
+  int inner = inner_env;
   const int nbp = nb + (nb & 1);
   int grid = std::max(1, std::min(nbp / 2, h.sm_count));
-  void* args[] = {&X, &Jm, &lv, &nbv, &changed};
+  long long* probe = nullptr;
+  static const bool probe_env = std::getenv("RSVD_PROBE_FQ") != nullptr;
+  if (probe_env) {
+    probe = reinterpret_cast<long long*>(h.ws.alloc_bytes(8 * 8));
+    RSVD_CUDA(cudaMemsetAsync(probe, 0, 64, h.stream));
+  }
+  void* args[] = {&X, &Jm, &lv, &ldpv, &nbv, &inner, &changed, &probe};
+  static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (probe_on) {
+    cudaEventCreate(&pe0);
+    cudaEventCreate(&pe1);
+    cudaEventRecord(pe0, h.stream);
+  }
   RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bjacobi_kernel), dim3(grid),
                                         dim3(kBJThreads), args, smem, h.stream));
   RSVD_LAUNCHED(h);
+  if (probe_on) {
+    cudaEventRecord(pe1, h.stream);
+    int hc[kBJMaxSweeps + 1];
+    RSVD_CUDA(cudaMemcpyAsync(hc, changed, sizeof hc, cudaMemcpyDeviceToHost, h.stream));
+    RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pe0, pe1);
+    int sw = 0;
+    while (sw < kBJMaxSweeps && hc[sw]) ++sw;
+    long long hp[6];
+    RSVD_CUDA(cudaMemcpy(hp, probe, sizeof hp, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr,
+                 "bjacobi l=%d nb=%d grid=%d sweeps=%d (+1 clean) %.3f ms  cycles load %lld gram %lld "
+                 "inner %lld update %lld gridsync %lld\n",
+                 l, nb, grid, sw, ms, hp[0], hp[1], hp[2], hp[3], hp[4]);
+    cudaEventDestroy(pe0);
+    cudaEventDestroy(pe1);
+  }
   bj_flag_kernel<<<1, 1, 0, h.stream>>>(changed, h.d_flags);
   RSVD_LAUNCHED(h);
   bj_norms_kernel<<<l, 256, 0, h.stream>>>(X, l, nrm);
@@ -372,8 +549,12 @@ void evd_shifted(Handle& h, const DMat& C, DMat U, double* lambda) {
   double* sg = h.ws.alloc(l);
   block_jacobi_svd(h, DMat(T.p, l, l, l), Jm, W, sg);
   int* order = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(l) * 4 + 16));
-  evd_order_kernel<<<(l + 255) / 256, 256, 0, h.stream>>>(sg, mu, Jm.p, Jm.ld, l, U.p, U.ld, lambda,
-                                                         order);
+  DMat CJ = h.ws.mat(l, l);
+  gemm_nn(h, C, Jm, CJ);
+  double* rq = h.ws.alloc(l);
+  rayleigh_kernel<<<l, 128, 0, h.stream>>>(Jm.p, Jm.ld, CJ.p, CJ.ld, l, rq);
+  RSVD_LAUNCHED(h);
+  evd_order_kernel<<<(l + 255) / 256, 256, 0, h.stream>>>(rq, l, lambda, order);
   RSVD_LAUNCHED(h);
   evd_permute_kernel<<<l, 128, 0, h.stream>>>(Jm.p, Jm.ld, l, order, U.p, U.ld);
   RSVD_LAUNCHED(h);
