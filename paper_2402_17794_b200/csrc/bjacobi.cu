@@ -105,10 +105,13 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
         if (tid == 0) any_first = any_visit = 0;
         __syncthreads();
         // ---- panel load (zero padded to kBJW columns x ldp rows)
-        for (int e = tid; e < kBJW * ldp; e += blockDim.x) {
-          const int c = e / ldp, r = e - c * ldp;
+        // warp w: columns w and w + 16, lanes along rows, 4 loads in flight
+        for (int c = warp; c < kBJW; c += 16) {
           const int gc = colmap[c];
-          Xb[e] = (gc >= 0 && r < l) ? X[int64_t(gc) * l + r] : 0.0;
+          const double* src = X + int64_t(gc < 0 ? 0 : gc) * l;
+          double* dst = Xb + c * ldp;
+#pragma unroll 4
+          for (int r = lane; r < ldp; r += 32) dst[r] = (gc >= 0 && r < l) ? src[r] : 0.0;
         }
         for (int e = tid; e < kBJW * kVL; e += blockDim.x) V[e] = ((e % kVL) == (e / kVL)) ? 1.0 : 0.0;
         __syncthreads();
@@ -116,18 +119,21 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
         // ---- G = Xb^T Xb: warp -> 8 x 8 tile (ti, tj) of the 4 x 4 tile grid, K = ldp
         {
           const int ti = warp >> 2, tj = warp & 3;
-          double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
+          // four independent accumulator chains, K = ldp (multiple of 4)
+          double g[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
           const double* pa = Xb + (ti * 8 + r8) * ldp + c4;  // A(m = col, k = row)
           const double* pb = Xb + (tj * 8 + r8) * ldp + c4;  // B(k = row, n = col)
           int k0 = 0;
-          for (; k0 + 8 <= ldp; k0 += 8) {
-            dmma884(g0, g1, pa[k0], pb[k0]);
-            dmma884(h0, h1, pa[k0 + 4], pb[k0 + 4]);
+          for (; k0 + 16 <= ldp; k0 += 16) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dmma884(g[u][0], g[u][1], pa[k0 + 4 * u], pb[k0 + 4 * u]);
           }
-          if (k0 < ldp) dmma884(g0, g1, pa[k0], pb[k0]);
+#pragma unroll
+          for (int u = 0; u < 3; ++u)
+            if (k0 + 4 * u < ldp) dmma884(g[u][0], g[u][1], pa[k0 + 4 * u], pb[k0 + 4 * u]);
           const int gi = ti * 8 + r8, gj = tj * 8 + 2 * c4;
-          G[gi + kGL * gj] = g0 + h0;
-          G[gi + kGL * (gj + 1)] = g1 + h1;
+          G[gi + kGL * gj] = (g[0][0] + g[1][0]) + (g[2][0] + g[3][0]);
+          G[gi + kGL * (gj + 1)] = (g[0][1] + g[1][1]) + (g[2][1] + g[3][1]);
         }
         __syncthreads();
         mark(1);
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) vb[nt][ks] = V[(nt * 8 + r8) * kVL + ks * 4 + c4];
           const int ntiles = (l + 7) / 8;
+#pragma unroll 2
           for (int mt = warp; mt < 2 * ntiles; mt += 16) {
             const bool isJ = mt >= ntiles;
             const int m0 = (isJ ? mt - ntiles : mt) * 8;
