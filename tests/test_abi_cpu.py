@@ -80,3 +80,17 @@ def test_device_log_agreement_with_glibc_is_measured(orc):
     r2s = _polar_r2(orc, 3, 20000)
     mism = sum(eng.debug_log_cr(v) != math.log(v) for v in r2s)
     assert mism / len(r2s) < 2e-3
+
+
+def test_library_loads_before_torch_without_breaking_it():
+    """The engine links PyTorch's NCCL (same SONAME as the system copy): loading
+    it first must not break a later `import torch` (the build() -> smoke()
+    order of __graft_entry__)."""
+    import subprocess
+    import sys
+    code = ("import ctypes, paper_2402_17794_b200 as e; ctypes.CDLL(e._LIB); "
+            "import torch; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(
+                           __import__("os").path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
