@@ -24,8 +24,12 @@ namespace rsvdb {
 // Must be called by all threads of a 256-thread block.
 constexpr int kCholThreads = 256;
 
+// `orig` (optional, shared): the reference diagonal of the breakdown test
+// (default: G0's diagonal + shift); `attempts` = 1 disables the shifted retry
+// (the blocked factorization of chol_blocked_kernel decides shifts globally).
 __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shift_coef, double* piv, double* Rs,
-                                             double* Rinvs, bool* shifted, long long* pr = nullptr) {
+                                             double* Rinvs, bool* shifted, long long* pr = nullptr,
+                                             const double* orig = nullptr, int attempts = 2) {
   constexpr int LD = 33;
   constexpr unsigned kFull = 0xffffffffu;
   const int t = threadIdx.x, i = t >> 3, c = t & 7, base = (t & 31) & ~7;
@@ -37,7 +41,7 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
   bool ok = false;
   *shifted = false;
 #pragma unroll 1
-  for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+  for (int attempt = 0; attempt < attempts && !ok; ++attempt) {
     const double shift = attempt ? shift_coef * tr : 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -70,7 +74,8 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
           }
           __syncthreads();
           const double d = pv[65];
-          if (!(d > 1e-12 * (G0[j + LD * j] + shift)) || !(d > 0.0)) {
+          const double oj = orig ? orig[j] : G0[j + LD * j] + shift;
+          if (!(d > 1e-12 * oj) || !(d > 0.0)) {
             broke = true;  // identical in every thread
           } else {
             const double wij = __shfl_sync(kFull, w[jj], base + jb);

@@ -1162,17 +1162,25 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   int64_t m_global = X.rows, row_off = 0;
   if (dist) shard_rows(h, X.rows, &m_global, &row_off);
   const double coef = 11.0 * (double(m_global) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
+  // l > 32: blocked multi-CTA Cholesky (cholblk.cu); RSVD_CHOL_BLOCKED=0 keeps
+  // the one-CTA kernel (comparison)
+  static const bool use_blocked = [] {
+    const char* e = std::getenv("RSVD_CHOL_BLOCKED");
+    return !(e && e[0] == '0');
+  }();
   auto pass = [&](const DMat& Y, DMat Qo) {
     gemm_tn(h, Y, Y, G);
     if (dist) allreduce_mat(h, G);
     if (l <= 32)
       chol_inv_small_kernel<<<1, kCholThreads, 0, h.stream>>>(G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld,
                                                    shift_used, h.d_flags);
+    else if (use_blocked)
+      chol_inv_blocked(h, G, l, coef, R1, Ri, shift_used);
     else
       chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
           G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld, gA, in_smem ? 1 : 0, shift_used,
           h.d_flags);
-    RSVD_LAUNCHED(h);
+    if (l <= 32 || !use_blocked) RSVD_LAUNCHED(h);
     if (Y.p == Qo.p) {
       DMat Qt = h.ws.mat(Qo.rows, l);
       gemm_nn(h, Y, Ri, Qt);

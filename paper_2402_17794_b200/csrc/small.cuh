@@ -19,6 +19,9 @@ void tsqr(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist);
 // sigma descending (stable), J orthogonal, W orthonormal (zero-sigma columns
 // completed to an orthonormal set).  Device outputs.
 void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma);
+// Cholesky G + s I = R^T R and R^-1 of an l x l Gram on the whole GPU (cholblk.cu).
+void chol_inv_blocked(Handle& h, const DMat& G, int l, double shift_coef, DMat R, DMat Rinv,
+                      int* shift_used);
 
 // Block one-sided Jacobi (cooperative, multi-CTA) for l > 64 (bjacobi.cu).
 void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma);

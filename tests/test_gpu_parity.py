@@ -135,6 +135,21 @@ def test_orthonormalize_matches_householder_span(eng, orc, m, l):
     assert np.max(np.abs(y - q @ (q.T @ y))) < 1e-10 * np.max(np.abs(y))
 
 
+@pytest.mark.parametrize("m,l,cond", [(4000, 110, 1e12), (3000, 220, 1e10), (6000, 550, 1e6),
+                                      (2000, 40, 1e14)])
+def test_orthonormalize_ill_conditioned_wide(eng, orc, m, l, cond):
+    """Blocked multi-CTA CholeskyQR (l > 32) incl. the shifted restart: an
+    ill-conditioned Y (graded singular values down to 1/cond) must come out
+    orthonormal and spanning Y."""
+    rs = np.random.default_rng(l)
+    u, _ = np.linalg.qr(rs.standard_normal((m, l)))
+    v, _ = np.linalg.qr(rs.standard_normal((l, l)))
+    y = np.asfortranarray((u * np.logspace(0, -np.log10(cond), l)) @ v)
+    q = _np(eng.orthonormalize(_t(y)))
+    assert np.max(np.abs(q.T @ q - np.eye(l))) < 1e-12
+    assert np.max(np.abs(y - q @ (q.T @ y))) < 1e-10 * np.max(np.abs(y))
+
+
 def test_orthonormalize_pads_rank_deficient(eng):
     rs = np.random.default_rng(3)
     c = rs.standard_normal((5, 1))
