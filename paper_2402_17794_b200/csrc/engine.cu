@@ -185,35 +185,57 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 }
 // Persistent grid over tile pairs (bi <= bj) of the upper triangle: tile
 // (bi, bj) and its mirror (bj, bi) are loaded once each (coalesced columns),
-// running maxima stay in registers, one atomic per CTA at the end.
+// running maxima stay in registers, one atomic per CTA at the end.  The next
+// pair's loads are issued before the current pair is compared (register
+// double buffering): one read of A at close to streaming bandwidth.
+__device__ __forceinline__ void asym_pair(int64_t t0, int64_t nt, int64_t& bi, int64_t& bj) {
+  bi = int64_t((2.0 * nt + 1.0 - sqrt((2.0 * nt + 1.0) * (2.0 * nt + 1.0) - 8.0 * t0)) / 2.0);
+  if (bi < 0) bi = 0;
+  while (bi > 0 && bi * nt - bi * (bi - 1) / 2 > t0) --bi;
+  while ((bi + 1) * nt - (bi + 1) * bi / 2 <= t0) ++bi;
+  bj = bi + (t0 - (bi * nt - bi * (bi - 1) / 2));
+}
+
 __global__ void __launch_bounds__(256) asym_kernel(const double* __restrict__ A, int64_t n,
                                                    int64_t lda, double* out) {
-  __shared__ double T1[32][33], T2[32][33];
+  __shared__ double T2[32][33];
   __shared__ double r_abs[8], r_asym[8];
   const int64_t nt = (n + 31) / 32;
   const int64_t npairs = nt * (nt + 1) / 2;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double mabs = 0.0, masym = 0.0;
-  for (int64_t t0 = blockIdx.x; t0 < npairs; t0 += gridDim.x) {
-    // invert t0 -> (bi, bj), bi <= bj, row-major over the upper triangle
-    int64_t bi = int64_t((2.0 * nt + 1.0 - sqrt((2.0 * nt + 1.0) * (2.0 * nt + 1.0) - 8.0 * t0)) / 2.0);
-    if (bi < 0) bi = 0;
-    while (bi > 0 && bi * nt - bi * (bi - 1) / 2 > t0) --bi;
-    while ((bi + 1) * nt - (bi + 1) * bi / 2 <= t0) ++bi;
-    const int64_t bj = bi + (t0 - (bi * nt - bi * (bi - 1) / 2));
+  double a[4], b[4];
+  auto load = [&](int64_t t0) {
+    int64_t bi, bj;
+    asym_pair(t0, nt, bi, bj);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = ty + 8 * q;
+      const int64_t r1 = bi * 32 + tx, c1 = bj * 32 + k;  // A(bi*32 + tx, bj*32 + k)
+      a[q] = (r1 < n && c1 < n) ? __ldcs(A + c1 * lda + r1) : 0.0;
+      const int64_t r2 = bj * 32 + tx, c2 = bi * 32 + k;  // A(bj*32 + tx, bi*32 + k)
+      b[q] = (r2 < n && c2 < n) ? __ldcs(A + c2 * lda + r2) : 0.0;
+    }
+  };
+  int64_t t0 = blockIdx.x;
+  if (t0 < npairs) load(t0);
+  for (; t0 < npairs; t0 += gridDim.x) {
+    double ca[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ca[q] = a[q];
+      T2[ty + 8 * q][tx] = b[q];
+    }
+    if (t0 + gridDim.x < npairs) load(t0 + gridDim.x);  // in flight during the compare
     __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-      const int64_t r1 = bi * 32 + tx, c1 = bj * 32 + k;
-      T1[k][tx] = (r1 < n && c1 < n) ? A[c1 * lda + r1] : 0.0;
-      const int64_t r2 = bj * 32 + tx, c2 = bi * 32 + k;
-      T2[k][tx] = (r2 < n && c2 < n) ? A[c2 * lda + r2] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = ty + 8 * q;
+      const double x = ca[q], y = T2[tx][k];  // A(i, j) vs A(j, i)
+      mabs = fmax(mabs, fmax(fabs(x), fabs(y)));
+      masym = fmax(masym, fabs(x - y));
     }
     __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-      const double a = T1[k][tx], b = T2[tx][k];  // A(i,j) vs A(j,i)
-      mabs = fmax(mabs, fmax(fabs(a), fabs(b)));
-      masym = fmax(masym, fabs(a - b));
-    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
