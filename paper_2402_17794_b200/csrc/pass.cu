@@ -88,6 +88,9 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -260,7 +263,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   const int kb = (c4 == 0) ? 0 : (c4 == 1) ? 3 : (c4 == 2) ? 12 : 15;
   int offA0;
   if constexpr (kNN)
-    offA0 = (wm0 >> 4) * (BK * 128) + kb * 128 + (((r8 >> 1) ^ (kb & 7)) << 4) + (r8 & 1) * 8;
+    // the warp's 8-row tile index parity selects the 16-row box half (WMT odd)
+    offA0 = (wm0 >> 4) * (BK * 128) + kb * 128 +
+            (((((wm0 >> 3) & 1) << 2 | (r8 >> 1)) ^ (kb & 7)) << 4) + (r8 & 1) * 8;
   else
     offA0 = wm0 * 128 + r8 * 128 + (((kb >> 1) ^ r8) << 4) + (kb & 1) * 8;
   const int offB0 = r8 * 128 + (((kb >> 1) ^ r8) << 4) + (kb & 1) * 8;
@@ -394,12 +399,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
           for (int i2 = 0; i2 < WMT; ++i2) dx[i2 * 32] = xacc[i2];
         }
       }
-      __threadfence();
+      ptx::fence_acq_rel_gpu();  // release the partial before the ticket
       ptx::named_bar(1, NCT);
       if (tid == 0) *flag = (atomicAdd(&p.counters[t], 1) == nseg - 1);
       ptx::named_bar(1, NCT);
       if (*flag) {
-        __threadfence();
+        ptx::fence_acq_rel_gpu();  // acquire the other segments' partials
         // Sum every segment's partial (this CTA's own included, re-read from
         // where it was just written) in segment order: deterministic.
         if (warp_live) {
