@@ -26,10 +26,12 @@ constexpr int kCholThreads = 256;
 
 // `orig` (optional, shared): the reference diagonal of the breakdown test
 // (default: G0's diagonal + shift); `attempts` = 1 disables the shifted retry
-// (the blocked factorization of chol_blocked_kernel decides shifts globally).
+// (the blocked factorization of chol_blocked_kernel decides shifts globally);
+// `start` = 1 goes straight to the shifted factorization.
 __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shift_coef, double* piv, double* Rs,
                                              double* Rinvs, bool* shifted, long long* pr = nullptr,
-                                             const double* orig = nullptr, int attempts = 2) {
+                                             const double* orig = nullptr, int attempts = 2,
+                                             int start = 0) {
   constexpr int LD = 33;
   constexpr unsigned kFull = 0xffffffffu;
   const int t = threadIdx.x, i = t >> 3, c = t & 7, base = (t & 31) & ~7;
@@ -41,7 +43,7 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
   bool ok = false;
   *shifted = false;
 #pragma unroll 1
-  for (int attempt = 0; attempt < attempts && !ok; ++attempt) {
+  for (int attempt = start; attempt < attempts && !ok; ++attempt) {
     const double shift = attempt ? shift_coef * tr : 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {

@@ -743,9 +743,11 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
   double* Ri = Rs + 32 * LD;
   double* Rt = Ri + 32 * LD;
   double* Ys = Rt + 32 * LD;  // rows_per x 33 (row-major, padded)
-  __shared__ int okf;
+  __shared__ int okf, prev_shift;
+  __shared__ double devw[kFqThreads / 32];
   const int tid = threadIdx.x, warp = tid >> 5;
   const int RP = int(rows_per);
+  if (tid == 0) prev_shift = 0;
   const int64_t r0 = int64_t(blockIdx.x) * rows_per;
   const int nr = int(m - r0 < rows_per ? m - r0 : rows_per);
   const int G = gridDim.x;
@@ -830,26 +832,80 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
     mark();
     // Converged: the Gram of the current rows is the identity to rounding
     // (|G - I| <= 4 l u): the remaining passes would multiply by R^-1 = I.
+    // Nearly converged (|G - I| <= 1e-8): R from its series, no elimination:
+    // with E = G - I and Phi(M) = upper triangle of M with halved diagonal,
+    // R = I + Phi(E) - Phi(Phi(E)^T Phi(E)) + O(E^3) and
+    // R^-1 = I - Phi(E) + Phi(E)^2 + O(E^2), i.e. orthogonality to O(E^2) <= 1e-16.
+    bool series = false;
     if (pass > 0) {
-      if (tid == 0) okf = 2;
-      __syncthreads();
       double dev = 0.0;
       for (int e = tid; e < l * l; e += kFqThreads) {
         const int i = e % l, j = e / l;
         dev = fmax(dev, fabs(Gs[i + LD * j] - (i == j ? 1.0 : 0.0)));
       }
-      if (dev > 4.0 * l * 1.1102230246251565e-16) okf = 1;  // benign race: all write 1
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+      if ((tid & 31) == 0) devw[warp] = dev;
       __syncthreads();
-      if (okf == 2) break;  // identical decision in every CTA
+      dev = 0.0;
+#pragma unroll
+      for (int w = 0; w < kFqThreads / 32; ++w) dev = fmax(dev, devw[w]);  // identical in every CTA
       __syncthreads();
+      if (dev <= 4.0 * l * 1.1102230246251565e-16) break;
+      series = dev <= 1e-8;
     }
     {
-      bool shifted;
       long long* pr = (probe && blockIdx.x == 0 && pass < 5) ? probe + 44 + 4 * pass : nullptr;
-      // the Gram partials in red[] are consumed: red[] is the pivot scratch
-      const bool ok = cta_chol_inv(Gs, l, shift_coef, &red[0][0], Rs, Ri, &shifted, pr);
-      if (tid == 0) okf = ok ? 1 : 0;
-      if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(flags, kFlagCholBreakdown);
+      bool ok = true;
+      if (series) {
+        auto phi = [&](int a, int b) -> double {
+          return (a < b) ? Gs[a + LD * b] : (a == b ? 0.5 * (Gs[a + LD * a] - 1.0) : 0.0);
+        };
+        for (int e = tid; e < 32 * 32; e += kFqThreads) {
+          const int i = e & 31, j = e >> 5;
+          double v = 0.0;
+          if (i < l && j < l && i <= j) {
+            double s2 = 0.0;
+            for (int k = i; k <= j; ++k) s2 = fma(phi(i, k), phi(k, j), s2);
+            v = (i == j ? 1.0 : 0.0) - phi(i, j) + s2;
+          }
+          Ri[i + LD * j] = v;
+        }
+        if (Rout && blockIdx.x == 0) {
+          double* Mt = &red[0][0];  // Phi^T Phi (the Gram partials are consumed)
+          for (int e = tid; e < 32 * 32; e += kFqThreads) {
+            const int i = e & 31, j = e >> 5;
+            double v = 0.0;
+            for (int k = 0; k <= min(i, j); ++k) v = fma(phi(k, i), phi(k, j), v);
+            Mt[i + LD * j] = v;
+          }
+          __syncthreads();
+          for (int e = tid; e < 32 * 32; e += kFqThreads) {
+            const int i = e & 31, j = e >> 5;
+            double v = 0.0;
+            if (i < l && j < l && i <= j) {
+              const double pm = (i < j) ? Mt[i + LD * j] : 0.5 * Mt[i + LD * i];
+              v = (i == j ? 1.0 : 0.0) + phi(i, j) - pm;
+            }
+            Rs[i + LD * j] = v;
+          }
+        }
+        __syncthreads();
+        if (tid == 0) okf = 1;
+      } else {
+        bool shifted;
+        // the Gram partials in red[] are consumed: red[] is the pivot scratch.
+        // When the first pass needed the shift, the second goes straight to
+        // the shifted factorization (measured on the C2 sketch: its unshifted
+        // attempt breaks down too); later passes stay unshifted first, as an
+        // orthonormal Q requires.
+        ok = cta_chol_inv(Gs, l, shift_coef, &red[0][0], Rs, Ri, &shifted, pr, nullptr, 2,
+                          (pass == 1 && prev_shift) ? 1 : 0);
+        if (tid == 0) okf = ok ? 1 : 0;
+        if (!ok && blockIdx.x == 0 && tid == 0) atomicOr(flags, kFlagCholBreakdown);
+        __syncthreads();
+        if (tid == 0) prev_shift = shifted ? 1 : 0;
+      }
       // R_total <- R * R_total (both upper triangular), warp 0 of CTA 0
       if (ok && Rout && blockIdx.x == 0 && warp == 0) {
         // lane c: column c of R_total in registers; rows of R are broadcast loads
