@@ -149,6 +149,9 @@ struct PassParams {
   int64_t units;         // stream-K: U = mt * nt * kb_tile
   int grid;              // stream-K: G
   int max_seg;           // stream-K: partial slots per CTA
+  int nsub;              // stream-K: CTAs c with equal c / nsub walk the same
+                         // m-tile / K-slice range, one n-tile each (c % nsub):
+                         // the n-tiles of an A block are read at the same time
   double* C;
   int64_t ldc;
   double* partials;
@@ -165,7 +168,7 @@ __device__ __forceinline__ int sk_cta_of(int64_t u, const PassParams& p) {
   return c;
 }
 
-template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW>
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW, bool kGroup>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     pass_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 PassParams p) {
@@ -185,9 +188,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   // This CTA's unit range (tile-major units for stream-K; one segment for split-K).
   int64_t u0, u1;
   int fixed_tile = 0, fixed_kb0 = 0;
+  // kGroup: stream-K with nsub > 1 n-tile CTAs per unit range (compile-time,
+  // so the common nsub = 1 schedule carries no extra integer work)
+  const int grp = (p.stream_k && kGroup) ? int(blockIdx.x) / p.nsub : int(blockIdx.x);
+  const int sub = (p.stream_k && kGroup) ? int(blockIdx.x) % p.nsub : 0;
   if (p.stream_k) {
-    u0 = sk_begin(blockIdx.x, p);
-    u1 = sk_begin(blockIdx.x + 1, p);
+    u0 = sk_begin(grp, p);
+    u1 = sk_begin(grp + 1, p);
   } else {
     fixed_tile = blockIdx.y * p.nt + blockIdx.x;
     fixed_kb0 = blockIdx.z * p.kb_split;
@@ -195,7 +202,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     u0 = 0;
     u1 = max(0, kb1 - fixed_kb0);
   }
-  auto unit_tile = [&](int64_t u) { return p.stream_k ? int(u / p.kb_tile) : fixed_tile; };
+  // stream-K unit u: m-tile-major (u / kb_tile = m-tile when nsub = nt, else
+  // the tile itself), K slice u % kb_tile; this CTA's n-tile is `sub`
+  auto unit_tile = [&](int64_t u) {
+    if constexpr (kGroup) return p.stream_k ? int(u / p.kb_tile) * p.nsub + sub : fixed_tile;
+    return p.stream_k ? int(u / p.kb_tile) : fixed_tile;
+  };
   auto unit_kb = [&](int64_t u) { return p.stream_k ? int(u % p.kb_tile) : fixed_kb0 + int(u); };
 
   if (threadIdx.x == 0) {
@@ -283,7 +295,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
     const int t = (u < u1) ? unit_tile(u) : fixed_tile;
-    const int64_t seg_end = p.stream_k ? min(u1, int64_t(t + 1) * p.kb_tile) : u1;
+    const int tg = (p.stream_k && kGroup) ? t / p.nsub : t;  // unit-space tile (group of n-tiles)
+    const int64_t seg_end = p.stream_k ? min(u1, int64_t(tg + 1) * p.kb_tile) : u1;
     for (; u < seg_end; ++u) {
       const int i = int(u - u0);
       const int s = i % STAGES;
@@ -347,10 +360,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     const int64_t m0 = int64_t(t / p.nt) * BM, n0 = int64_t(t % p.nt) * NCOL;
     int nseg, my_seg, c_first = 0;
     if (p.stream_k) {
-      c_first = sk_cta_of(int64_t(t) * p.kb_tile, p);
-      const int c_last = sk_cta_of(int64_t(t + 1) * p.kb_tile - 1, p);
+      c_first = sk_cta_of(int64_t(tg) * p.kb_tile, p);  // CTA groups
+      const int c_last = sk_cta_of(int64_t(tg + 1) * p.kb_tile - 1, p);
       nseg = c_last - c_first + 1;
-      my_seg = int(blockIdx.x) - c_first;
+      my_seg = grp - c_first;
     } else {
       nseg = p.splits;
       my_seg = blockIdx.z;
@@ -376,9 +389,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     } else {
       auto slot = [&](int sg) -> int64_t {
         if (!p.stream_k) return int64_t(t) * p.splits + sg;
-        const int c2 = c_first + sg;
-        const int j2 = t - int(sk_begin(c2, p) / p.kb_tile);
-        return int64_t(c2) * p.max_seg + j2;
+        const int c2 = c_first + sg;  // group
+        const int j2 = tg - int(sk_begin(c2, p) / p.kb_tile);
+        return int64_t(kGroup ? c2 * p.nsub + sub : c2) * p.max_seg + j2;
       };
       // partial in fragment-native layout: [warp][i][j][lane][2] (16B / lane, coalesced)
       const bool warp_live = (m0 + wm0) < p.M;
@@ -520,9 +533,11 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
             int force_splits) {
   using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
   static bool attr_set = false;
-  auto kern = pass_kernel<kNN, BN, WMT, BK, STAGES, XC, CW>;
+  auto kern1 = pass_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, false>;
+  auto kernG = pass_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, true>;
   if (!attr_set) {
-    RSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    RSVD_CUDA(cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    RSVD_CUDA(cudaFuncSetAttribute(kernG, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr_set = true;
   }
   const int64_t mt = ceil_div(M, Cfg::BM), nt = ceil_div(N, Cfg::NCOL);
@@ -544,20 +559,26 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
   // tiles: split-K grid with n-tiles adjacent for L2 reuse of A.
   const bool stream_k = force_splits <= 0 && tiles < 2 * sms;
   if (stream_k) {
-    const int64_t units = tiles * kblocks;
+    // n-tiles of one m-tile go to nt adjacent CTAs walking the same unit range
+    // (A read once from DRAM; measured 2.44x the algorithmic bytes on C3's
+    // adjoint when one CTA swept the n-tiles one after the other)
+    const int64_t nsub = (nt > 1 && nt <= sms) ? nt : 1;
+    const int64_t units = (tiles / nsub) * kblocks;
     // one CTA per tile at least (short-K products: no partials at all), and
     // >= 8 K slices per CTA when tiles are few (bounds the partials a tile's
     // last segment must reduce)
-    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(sms, std::max<int64_t>(tiles, units / 8)));
+    const int64_t g = std::max<int64_t>(
+        1, std::min<int64_t>(sms / nsub, std::max<int64_t>(tiles / nsub, units / 8)));
     pp.stream_k = 1;
+    pp.nsub = int(nsub);
     pp.units = units;
     pp.grid = int(g);
     pp.max_seg = int(ceil_div(ceil_div(units, g), kblocks) + 1);
     pp.splits = 1;
     pp.kb_split = int(kblocks);
-    pp.partials = h.ws.alloc(g * pp.max_seg * FRAG);
+    pp.partials = h.ws.alloc(g * nsub * pp.max_seg * FRAG);
     pp.counters = tile_counters(h, tiles);
-    grid = dim3(unsigned(g), 1, 1);
+    grid = dim3(unsigned(g * nsub), 1, 1);
   } else {
     int splits = 1;
     if (force_splits > 0) {
@@ -614,7 +635,10 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     rec_flags = (cap == cudaStreamCaptureStatusActive) ? cudaEventRecordExternal : cudaEventRecordDefault;
     RSVD_CUDA(cudaEventRecordWithFlags(rec.a, h.stream, rec_flags));
   }
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
+  if (pp.stream_k && pp.nsub > 1)
+    kernG<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
+  else
+    kern1<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
   RSVD_LAUNCHED(h);
   if (h.prof) {
     RSVD_CUDA(cudaEventRecordWithFlags(rec.b, h.stream, rec_flags));
