@@ -39,7 +39,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "lib", "librsvd_b200.so")
+# RSVD_B200_LIB: an alternative build of the same library (A/B experiments)
+_LIB = os.environ.get("RSVD_B200_LIB") or os.path.join(_HERE, "lib", "librsvd_b200.so")
 
 
 def lib_path() -> str:
