@@ -5,6 +5,9 @@
 //   core.hpp:18-66        DenseMatrix / Vector / Index, DimensionError,
 //                         ParameterError, NumericError, SvdApprox, EvdApprox
 //   core.hpp:96-177       orthonormalize, svd_small, evd_symmetric, solve_ls
+//   core.hpp:180-221      singular_values, spectral_norm
+//   bounds.hpp:107-120    computed_range_error
+//   angles.hpp:11-78      AngleReport, canonical_sines, subspace_quality
 //   sketch.hpp:19-59      Rng (std::mt19937_64 + std::normal_distribution), gaussian
 //   rangefinder.hpp:13-105 RangeMode, SketchConfig, fixed_rank_range,
 //                         power_range, subspace_iter_range, range_basis

@@ -208,4 +208,71 @@ inline SvdApprox spsvd_general(const DenseMatrix& a, Index k, Index p, Rng& rng)
   return spsvd_general(op, k, p, rng);
 }
 
+// ------------------------------------- diagnostics (core / bounds / angles)
+/// Singular values, descending (reference core.hpp:180-183).
+inline Vector singular_values(const DenseMatrix& m) {
+  const Index r = std::min(m.rows(), m.cols());
+  Vector s = b200::make_vec(r);
+  b200::check(rsvd_singular_values_host(b200::handle(), m.rows(), m.cols(), m.data(),
+                                        b200::ld(m), s.data()));
+  return s;
+}
+
+/// Largest singular value (reference core.hpp:188-221): dense SVD when
+/// min(rows, cols) <= 512, else power iteration on M^T M (tol 1e-10, cap 5000).
+inline double spectral_norm(const DenseMatrix& m) {
+  double out = 0.0;
+  b200::check(rsvd_spectral_norm_host(b200::handle(), m.rows(), m.cols(), m.data(), b200::ld(m),
+                                      &out));
+  return out;
+}
+
+/// Measured Stage-1 residual ||A - Q Q^T A||_2 (reference bounds.hpp:107-120).
+inline double computed_range_error(const DenseMatrix& a, const DenseMatrix& q) {
+  if (q.rows() != a.rows()) throw DimensionError("computed_range_error: row counts differ");
+  double out = 0.0;
+  b200::check(rsvd_computed_range_error_host(b200::handle(), a.rows(), a.cols(), a.data(),
+                                             b200::ld(a), q.cols(), q.data(), b200::ld(q), &out));
+  return out;
+}
+
+/// Per-index canonical-angle record (reference angles.hpp:11-22).
+struct AngleReport {
+  Index k = 0;
+  Index p = 0;
+  int q = 0;
+  std::uint64_t seed = 0;
+  double gap = 0.0;
+  Vector sin_theta;
+  Vector sin_nu;
+  Vector bound_theta;
+  Vector bound_nu;
+};
+
+/// Sines of the principal angles between range(X) and range(Y), ascending,
+/// clamped to [0, 1] (reference angles.hpp:42-60, projection route).
+inline Vector canonical_sines(const DenseMatrix& x, const DenseMatrix& y) {
+  if (x.rows() != y.rows()) throw DimensionError("canonical_sines: ambient dimensions differ");
+  Vector out = b200::make_vec(std::min(x.cols(), y.cols()));
+  b200::check(rsvd_canonical_sines_host(b200::handle(), x.rows(), x.cols(), x.data(), b200::ld(x),
+                                        y.cols(), y.data(), b200::ld(y), out.data()));
+  return out;
+}
+
+/// Angles between the oracle's rank-k singular subspaces and the first k
+/// computed factors (reference angles.hpp:62-78).
+inline AngleReport subspace_quality(const SvdApprox& oracle, Index k, const SvdApprox& result) {
+  if (k < 1) throw ParameterError("subspace_quality: k must be >= 1");
+  if (oracle.factor_count() < k || result.factor_count() < k)
+    throw DimensionError("subspace_quality: fewer than k factors available");
+  AngleReport report;
+  report.k = k;
+  report.sin_theta = canonical_sines(oracle.U.leftCols(k), result.U.leftCols(k));
+  report.sin_nu = canonical_sines(oracle.V.leftCols(k), result.V.leftCols(k));
+  return report;
+}
+inline AngleReport subspace_quality(const DenseMatrix& a, Index k, const SvdApprox& result) {
+  return subspace_quality(svd_small(a), k, result);
+}
+
 }  // namespace rsvd

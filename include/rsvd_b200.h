@@ -141,6 +141,50 @@ rsvd_status rsvd_solve_joint_core_dev(rsvd_handle* h, int64_t l, const double* g
                                       const double* h1, const double* g2, const double* h2,
                                       double* c);
 
+/* ------------------------------------- diagnostics */
+/* singular_values(M): min(m,n) values, descending (reference core.hpp:180-183).
+ * NumericError on non-finite input.  s: device. */
+rsvd_status rsvd_singular_values_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                     int64_t lda, double* s);
+/* spectral_norm(M) (reference core.hpp:188-221): dense SVD when
+ * min(m,n) <= 512, else power iteration on M^T M from the reference's LCG
+ * start vector (tol 1e-10, NumericError after 5000 steps).  *out: HOST scalar. */
+rsvd_status rsvd_spectral_norm_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                   int64_t lda, double* out);
+/* computed_range_error(A, Q) = ||A - Q Q^T A||_2 (reference bounds.hpp:107-120):
+ * DimensionError if Q has a different row count, NumericError if
+ * max|Q^T Q - I| > 1e-8.  A m x n, Q m x l (device); *out: HOST scalar. */
+rsvd_status rsvd_computed_range_error_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                          int64_t lda, int64_t l, const double* q, int64_t ldq,
+                                          double* out);
+/* canonical_sines(X, Y) (reference angles.hpp:42-60): the min(kx, ky)
+ * largest singular values of (I - X X^T) Y, ascending, clamped to [0, 1].
+ * DimensionError if the row counts differ, NumericError if X or Y is not
+ * orthonormal to 1e-8.  X m x kx, Y m x ky, out (device). */
+rsvd_status rsvd_canonical_sines_dev(rsvd_handle* h, int64_t m, int64_t kx, const double* x,
+                                     int64_t ldx, int64_t ky, const double* y, int64_t ldy,
+                                     double* out);
+/* run_svd's error report (reference drivers.hpp:145-151) for A ~ U diag(s) V^T
+ * (an EVD passes V = U, s = lambda): *rel_fro = ||A - recon||_F / ||A||_F and
+ * *rel_spec = ||A - recon||_2 / ||A||_2, the spectral norms by spectral_norm's
+ * rules (dense SVD when min(m,n) <= 512, as the reference's
+ * singular_values; power iteration above).  A m x n, U m x r, s r, V n x r
+ * (device); rel_fro / rel_spec: HOST scalars. */
+rsvd_status rsvd_reconstruction_error_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                          int64_t lda, int64_t r, const double* u, int64_t ldu,
+                                          const double* s, const double* v, int64_t ldv,
+                                          double* rel_fro, double* rel_spec);
+rsvd_status rsvd_singular_values_host(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                      int64_t lda, double* s);
+rsvd_status rsvd_spectral_norm_host(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                    int64_t lda, double* out);
+rsvd_status rsvd_computed_range_error_host(rsvd_handle* h, int64_t m, int64_t n,
+                                           const double* a, int64_t lda, int64_t l,
+                                           const double* q, int64_t ldq, double* out);
+rsvd_status rsvd_canonical_sines_host(rsvd_handle* h, int64_t m, int64_t kx, const double* x,
+                                      int64_t ldx, int64_t ky, const double* y, int64_t ldy,
+                                      double* out);
+
 /* Host-buffer variants of the kernel-level entry points (the C++ drop-in
  * layer uses these; copies are included). */
 rsvd_status rsvd_gaussian_host(rsvd_handle* h, int64_t n, int64_t l, rsvd_rng_state* rng,
@@ -196,7 +240,8 @@ rsvd_status rsvd_spevd_host(rsvd_handle* h, int64_t n, const double* a, int64_t 
                             int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                             double* lambda);
 /* spsvd_general(A, k, p, rng) (reference singlepass.hpp:109-137): Y_c = A
- * Omega_c and W = A^T Psi in ONE fused pass.  U m x k, sigma k, V n x k. */
+ * Omega_c and W = A^T Psi (one apply, one adjoint; two streaming passes, see
+ * DESIGN.md section 6).  U m x k, sigma k, V n x k. */
 rsvd_status rsvd_spsvd_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a, int64_t lda,
                            int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                            double* sigma, double* v, int64_t ldv);

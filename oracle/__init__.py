@@ -82,6 +82,10 @@ def lib():
         L.orc_spevd.argtypes = [I64, P, I64, I64, P, P, P, ctypes.POINTER(I)]
         L.orc_spsvd.argtypes = [I64, I64, P, I64, I64, P, P, P, P, ctypes.POINTER(I), ctypes.POINTER(I)]
         L.orc_solve_joint_core.argtypes = [I64, P, P, P, P, I, P]
+        L.orc_singular_values.argtypes = [I64, I64, P, P]
+        L.orc_spectral_norm.argtypes = [I64, I64, P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)]
+        L.orc_computed_range_error.argtypes = [I64, I64, P, I64, P, ctypes.POINTER(ctypes.c_double)]
+        L.orc_canonical_sines.argtypes = [I64, I64, P, I64, P, P]
         _lib = L
     return _lib
 
@@ -239,3 +243,41 @@ def solve_joint_core(g1, h1, g2, h2, route: int = 2):
     c = np.empty((l, l), order="F")
     _check(lib().orc_solve_joint_core(l, _p(g1), _p(h1), _p(g2), _p(h2), route, _p(c)))
     return c
+
+
+# ------------------------------------------------ diagnostics (core/bounds/angles)
+def singular_values(m):
+    """reference core.hpp:180-183"""
+    m = _f(m)
+    s = np.empty(min(m.shape))
+    _check(lib().orc_singular_values(m.shape[0], m.shape[1], _p(m), _p(s)))
+    return s
+
+
+def spectral_norm(m, with_iterations=False):
+    """reference core.hpp:188-221"""
+    m = _f(m)
+    out, it = ctypes.c_double(0.0), ctypes.c_int(0)
+    _check(lib().orc_spectral_norm(m.shape[0], m.shape[1], _p(m), ctypes.byref(out), ctypes.byref(it)))
+    return (out.value, it.value) if with_iterations else out.value
+
+
+def computed_range_error(a, q):
+    """reference bounds.hpp:107-120"""
+    a, q = _f(a), _f(q)
+    if a.shape[0] != q.shape[0]:
+        raise DimensionError("computed_range_error: row counts differ")
+    out = ctypes.c_double(0.0)
+    _check(lib().orc_computed_range_error(a.shape[0], a.shape[1], _p(a), q.shape[1], _p(q),
+                                          ctypes.byref(out)))
+    return out.value
+
+
+def canonical_sines(x, y):
+    """reference angles.hpp:42-60"""
+    x, y = _f(x), _f(y)
+    if x.shape[0] != y.shape[0]:
+        raise DimensionError("canonical_sines: ambient dimensions differ")
+    out = np.empty(min(x.shape[1], y.shape[1]))
+    _check(lib().orc_canonical_sines(x.shape[0], x.shape[1], _p(x), y.shape[1], _p(y), _p(out)))
+    return out

@@ -56,6 +56,8 @@ void scipy_dgesdd_(const char*, const int*, const int*, double*, const int*, dou
                    const int*, double*, const int*, double*, const int*, int*, int*, size_t);
 void scipy_dsyevd_(const char*, const char*, const int*, double*, const int*, double*, double*,
                    const int*, int*, const int*, int*, size_t, size_t);
+void scipy_dgemv_(const char*, const int*, const int*, const double*, const double*, const int*,
+                  const double*, const int*, const double*, double*, const int*, size_t);
 void scipy_openblas_set_num_threads(int);
 int scipy_openblas_get_num_threads(void);
 }
@@ -481,6 +483,121 @@ Svd spsvd_general(const Mat& a, int64_t k, int64_t p, Rng& rng, int* applies, in
   return out;
 }
 
+// ------------------------------------------------- diagnostics (§8(f) rows 1, 3)
+// singular_values: reference core.hpp:180-183 (dense_singular_values :77-79,
+// BDCSVD values only -> dgesdd jobz = 'N').
+std::vector<double> singular_values(const Mat& m) {
+  require_finite(m, "singular_values");
+  const int mi = static_cast<int>(m.r), ni = static_cast<int>(m.c);
+  const int r = std::min(mi, ni);
+  std::vector<double> s(static_cast<size_t>(std::max(r, 0)));
+  if (r == 0) return s;
+  Mat a = Mat::from(m.r, m.c, m.data());
+  std::vector<int> iwork(static_cast<size_t>(8 * r));
+  int info = 0, lwork = -1, one = 1;
+  double wq = 0, dummy = 0;
+  scipy_dgesdd_("N", &mi, &ni, a.data(), &mi, s.data(), &dummy, &one, &dummy, &one, &wq, &lwork,
+                iwork.data(), &info, 1);
+  lwork = std::max(1, static_cast<int>(wq));
+  std::vector<double> work(static_cast<size_t>(lwork));
+  scipy_dgesdd_("N", &mi, &ni, a.data(), &mi, s.data(), &dummy, &one, &dummy, &one, work.data(),
+                &lwork, iwork.data(), &info, 1);
+  if (info != 0) throw NumericError("singular_values: dgesdd did not converge");
+  return s;
+}
+
+// Eigen's Vector::norm(): sqrt of the plain sum of squares.
+double vnorm(const std::vector<double>& v) {
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return std::sqrt(s);
+}
+
+// spectral_norm: reference core.hpp:188-221, statement by statement (dense
+// route for min <= 512; LCG start vector; power iteration on M^T M with
+// |est - sigma| <= 1e-10 est; NumericError after 5000 steps).
+double spectral_norm(const Mat& m, int* iterations) {
+  require_finite(m, "spectral_norm");
+  if (iterations) *iterations = 0;
+  if (std::min(m.r, m.c) <= 512) {
+    std::vector<double> s = singular_values(m);
+    return s.empty() ? 0.0 : s[0];
+  }
+  std::vector<double> x(static_cast<size_t>(m.c)), y(static_cast<size_t>(m.r));
+  std::uint64_t state = 0x9e3779b97f4a7c15ULL;
+  for (auto& xi : x) {
+    state = state * 6364136223846793005ULL + 1442695040888963407ULL;
+    xi = static_cast<double>(state >> 11) / 9007199254740992.0 - 0.5;
+  }
+  const double xn = vnorm(x);
+  if (xn == 0.0) return 0.0;
+  for (auto& xi : x) xi /= xn;
+  const int mi = static_cast<int>(m.r), ni = static_cast<int>(m.c), inc = 1;
+  const double one = 1.0, zero = 0.0;
+  double sigma = 0.0;
+  for (int iter = 0; iter < 5000; ++iter) {
+    if (iterations) *iterations = iter + 1;
+    scipy_dgemv_("N", &mi, &ni, &one, m.data(), &mi, x.data(), &inc, &zero, y.data(), &inc, 1);
+    const double estimate = vnorm(y);
+    if (estimate == 0.0) return 0.0;
+    if (iter > 0 && std::abs(estimate - sigma) <= 1e-10 * estimate) return estimate;
+    sigma = estimate;
+    scipy_dgemv_("T", &mi, &ni, &one, m.data(), &mi, y.data(), &inc, &zero, x.data(), &inc, 1);
+    const double nx = vnorm(x);
+    if (nx == 0.0) return estimate;
+    for (auto& xi : x) xi /= nx;
+  }
+  throw NumericError("spectral_norm: power iteration hit the 5000-step cap");
+}
+
+// max |X^T X - I| (reference angles.hpp:24-35, bounds.hpp:111-117)
+double orthonormal_deviation(const Mat& x) {
+  const Mat g = gemm(x, true, x, false);
+  double dev = 0.0;
+  for (int64_t j = 0; j < g.c; ++j)
+    for (int64_t i = 0; i < g.r; ++i) dev = std::max(dev, std::abs(g(i, j) - (i == j ? 1.0 : 0.0)));
+  return dev;
+}
+
+// computed_range_error: reference bounds.hpp:107-120.
+double computed_range_error(const Mat& a, const Mat& q) {
+  if (q.r != a.r) throw DimensionError("computed_range_error: row counts differ");
+  const double dev = orthonormal_deviation(q);
+  if (dev > 1e-8)
+    throw NumericError("computed_range_error: Q is not orthonormal (deviation " +
+                       std::to_string(dev) + ")");
+  Mat resid = Mat::from(a.r, a.c, a.data());
+  if (q.c > 0) {
+    const Mat qa = gemm(q, true, a, false);
+    const Mat qqa = gemm(q, false, qa, false);
+    for (size_t i = 0; i < resid.d.size(); ++i) resid.d[i] -= qqa.d[i];
+  }
+  return spectral_norm(resid, nullptr);
+}
+
+// canonical_sines: reference angles.hpp:42-60 (projection route).
+std::vector<double> canonical_sines(const Mat& x, const Mat& y) {
+  if (x.r != y.r) throw DimensionError("canonical_sines: ambient dimensions differ");
+  for (int w = 0; w < 2; ++w) {
+    const double dev = orthonormal_deviation(w ? y : x);
+    if (dev > 1e-8)
+      throw NumericError(std::string("canonical_sines: ") + (w ? "Y" : "X") +
+                         ": columns are not orthonormal (deviation " + std::to_string(dev) + ")");
+  }
+  Mat resid = Mat::from(y.r, y.c, y.data());
+  if (x.c > 0) {
+    const Mat xy = gemm(x, true, y, false);
+    const Mat xxy = gemm(x, false, xy, false);
+    for (size_t i = 0; i < resid.d.size(); ++i) resid.d[i] -= xxy.d[i];
+  }
+  const std::vector<double> sv = singular_values(resid);
+  const int64_t count = std::min(x.c, y.c);
+  std::vector<double> out(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i)
+    out[static_cast<size_t>(i)] = std::clamp(sv[static_cast<size_t>(count - 1 - i)], 0.0, 1.0);
+  return out;
+}
+
 // The RNG state exchanged with the engine (same layout as include/rsvd_b200.h).
 struct RngState {
   uint64_t mt[312];
@@ -646,6 +763,30 @@ int orc_solve_joint_core(int64_t l, const double* g1, const double* h1, const do
             : route == 1 ? solve_joint_core_kron(G1, H1, G2, H2)
                          : solve_joint_core(G1, H1, G2, H2);
     r.to(c);
+  });
+}
+
+int orc_singular_values(int64_t m, int64_t n, const double* a, double* s) {
+  return guard([&] {
+    const std::vector<double> v = singular_values(Mat::view(m, n, a));
+    std::copy(v.begin(), v.end(), s);
+  });
+}
+
+int orc_spectral_norm(int64_t m, int64_t n, const double* a, double* out, int* iterations) {
+  return guard([&] { *out = spectral_norm(Mat::view(m, n, a), iterations); });
+}
+
+int orc_computed_range_error(int64_t m, int64_t n, const double* a, int64_t l, const double* q,
+                             double* out) {
+  return guard([&] { *out = computed_range_error(Mat::view(m, n, a), Mat::view(m, l, q)); });
+}
+
+int orc_canonical_sines(int64_t m, int64_t kx, const double* x, int64_t ky, const double* y,
+                        double* out) {
+  return guard([&] {
+    const std::vector<double> v = canonical_sines(Mat::view(m, kx, x), Mat::view(m, ky, y));
+    std::copy(v.begin(), v.end(), out);
   });
 }
 

@@ -7,6 +7,9 @@ argument meaning and exception types as the reference:
 
     Rng(seed), gaussian(n, l, rng)                        sketch.hpp:19-59
     orthonormalize, svd_small, evd_symmetric, solve_ls    core.hpp:96-177
+    singular_values, spectral_norm                        core.hpp:180-221
+    computed_range_error                                  bounds.hpp:107-120
+    canonical_sines, subspace_quality, AngleReport        angles.hpp:11-78
     fixed_rank_range, power_range, subspace_iter_range,
     range_basis, SketchConfig, RangeMode                  rangefinder.hpp:13-105
     rsvd, truncate, SvdApprox                             factor.hpp:12-34
@@ -35,7 +38,8 @@ __all__ = [
     "solve_joint_core", "RangeMode", "SketchConfig", "fixed_rank_range", "power_range",
     "subspace_iter_range", "range_basis", "SvdApprox", "EvdApprox", "rsvd", "truncate",
     "CountingOperator", "spevd_hermitian", "spsvd_general", "apply", "apply_adjoint", "Engine",
-    "default_engine", "lib_path", "build", "using_engine", "rsvd_host",
+    "default_engine", "lib_path", "build", "using_engine", "rsvd_host", "singular_values",
+    "spectral_norm", "computed_range_error", "canonical_sines", "subspace_quality", "AngleReport",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -137,6 +141,14 @@ def _load():
             "rsvd_spevd_host": [P, I64, P, I64, I64, I64, PS, P, I64, P],
             "rsvd_spsvd_dev": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
             "rsvd_spsvd_host": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
+            "rsvd_singular_values_dev": [P, I64, I64, P, I64, P],
+            "rsvd_spectral_norm_dev": [P, I64, I64, P, I64, ctypes.POINTER(D)],
+            "rsvd_computed_range_error_dev": [P, I64, I64, P, I64, I64, P, I64, ctypes.POINTER(D)],
+            "rsvd_canonical_sines_dev": [P, I64, I64, P, I64, I64, P, I64, P],
+            "rsvd_singular_values_host": [P, I64, I64, P, I64, P],
+            "rsvd_spectral_norm_host": [P, I64, I64, P, I64, ctypes.POINTER(D)],
+            "rsvd_computed_range_error_host": [P, I64, I64, P, I64, I64, P, I64, ctypes.POINTER(D)],
+            "rsvd_canonical_sines_host": [P, I64, I64, P, I64, I64, P, I64, P],
         }
         for name, argt in sigs.items():
             f = getattr(L, name)
@@ -752,3 +764,84 @@ def spsvd_host(a: np.ndarray, k: int, p: int, rng: Rng):
 def debug_log_cr(x: float) -> float:
     """Host evaluation of the device polar-sampler log (ddlog.cuh), for tests."""
     return _load().rsvd_debug_log_cr(float(x))
+
+
+# ------------------------------------------------ diagnostics (core/bounds/angles)
+def singular_values(m):
+    """Singular values, descending (reference core.hpp:180-183)."""
+    import torch
+    d = _Dev(m, "singular_values")
+    e = _eng(None if d.host else m)
+    r = min(d.rows, d.cols)
+    s = torch.empty(max(r, 1), dtype=torch.float64, device="cuda")
+    if r:
+        _check(_load().rsvd_singular_values_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, s.data_ptr()))
+    return _vec_out(s[:r], d.host)
+
+
+def spectral_norm(m) -> float:
+    """||M||_2: dense SVD when min(m, n) <= 512, else power iteration on M^T M
+    from the reference's LCG start vector, tol 1e-10, cap 5000
+    (reference core.hpp:188-221)."""
+    d = _Dev(m, "spectral_norm")
+    e = _eng(None if d.host else m)
+    out = ctypes.c_double(0.0)
+    _check(_load().rsvd_spectral_norm_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, ctypes.byref(out)))
+    return out.value
+
+
+def computed_range_error(a, q) -> float:
+    """Measured Stage-1 residual ||A - Q Q^T A||_2 (reference bounds.hpp:107-120)."""
+    da, dq = _Dev(a, "computed_range_error"), _Dev(q, "computed_range_error")
+    if dq.rows != da.rows:
+        raise DimensionError("computed_range_error: row counts differ")
+    e = _eng(None if da.host else a)
+    out = ctypes.c_double(0.0)
+    _check(_load().rsvd_computed_range_error_dev(e.handle, da.rows, da.cols, da.ptr, da.ld,
+                                                 dq.cols, dq.ptr, dq.ld, ctypes.byref(out)))
+    return out.value
+
+
+def canonical_sines(x, y):
+    """Sines of the principal angles between range(X) and range(Y), ascending,
+    clamped to [0, 1] (reference angles.hpp:42-60, projection route)."""
+    import torch
+    dx, dy = _Dev(x, "canonical_sines"), _Dev(y, "canonical_sines")
+    if dx.rows != dy.rows:
+        raise DimensionError("canonical_sines: ambient dimensions differ")
+    e = _eng(None if dx.host else x)
+    cnt = min(dx.cols, dy.cols)
+    out = torch.empty(max(cnt, 1), dtype=torch.float64, device="cuda")
+    _check(_load().rsvd_canonical_sines_dev(e.handle, dx.rows, dx.cols, dx.ptr, dx.ld, dy.cols,
+                                            dy.ptr, dy.ld, out.data_ptr()))
+    return _vec_out(out[:cnt], dx.host)
+
+
+@dataclass
+class AngleReport:
+    """Per-index canonical-angle record (reference angles.hpp:11-22)."""
+    k: int = 0
+    p: int = 0
+    q: int = 0
+    seed: int = 0
+    gap: float = 0.0
+    sin_theta: object = None
+    sin_nu: object = None
+    bound_theta: object = None
+    bound_nu: object = None
+
+
+def subspace_quality(oracle, k: int, result: SvdApprox) -> AngleReport:
+    """Angles between the oracle's rank-k singular subspaces and the first k
+    computed factors (reference angles.hpp:62-78).  `oracle` is an SvdApprox
+    or the matrix itself (then svd_small(oracle) is the oracle)."""
+    if k < 1:
+        raise ParameterError("subspace_quality: k must be >= 1")
+    if not isinstance(oracle, SvdApprox):
+        oracle = svd_small(oracle)
+    if oracle.factor_count() < k or result.factor_count() < k:
+        raise DimensionError("subspace_quality: fewer than k factors available")
+    rep = AngleReport(k=k)
+    rep.sin_theta = canonical_sines(oracle.U[:, :k], result.U[:, :k])
+    rep.sin_nu = canonical_sines(oracle.V[:, :k], result.V[:, :k])
+    return rep

@@ -68,6 +68,7 @@ constexpr int kVL = 36;  // ld of V: 36 % 16 == 4 keeps DMMA B-fragment loads co
 __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict__ X,
                                                             double* __restrict__ Jm, int l, int ldp,
                                                             int nb, int inner_max,
+                                                            double graded_ratio,
                                                             int* __restrict__ changed,
                                                             long long* __restrict__ probe) {
   long long pt[6] = {0, 0, 0, 0, 0, 0}, tlast = clock64();
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
   __shared__ int colmap[kBJW];
   __shared__ double rc[kBJW / 2], rs[kBJW / 2];
   __shared__ int rp[kBJW / 2], rq[kBJW / 2];
-  __shared__ int any_first, any_inner, any_visit;
+  __shared__ int any_first, any_inner, any_visit, graded;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r8 = lane >> 2, c4 = lane & 3;
   const int nbp = nb + (nb & 1);
@@ -137,13 +138,81 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
         }
         __syncthreads();
         mark(1);
+        // ---- graded panel?  The Gram route below updates G by rotations, which
+        // inject absolute errors ~u * max G_cc into every entry: columns whose
+        // norm is below ~1e-6 of the panel's largest can then never be
+        // orthogonalized (the next visit's fresh Gram shows it, and the sweep
+        // never ends: rank-deficient or strongly graded factors).  Such panels
+        // take the one-sided inner sweep instead: rotations from fresh dot
+        // products of the panel columns themselves (relative accuracy).
+        if (tid == 0) {
+          double gmax = 0.0, gmin = 1e308;
+          for (int c = 0; c < w; ++c) {
+            const double d = G[c + kGL * c];
+            gmax = fmax(gmax, d);
+            if (d > 0.0) gmin = fmin(gmin, d);
+          }
+          graded = (gmin < graded_ratio * gmax) ? 1 : 0;
+        }
+        __syncthreads();
+        const int wp = w + (w & 1), np2 = wp / 2;
+        if (graded) {
+          for (int it = 0; it < inner_max; ++it) {
+            if (tid == 0) any_inner = 0;
+            __syncthreads();
+            for (int r2 = 0; r2 < wp - 1; ++r2) {
+              if (warp < np2) {  // warp = pair: dot products, rotation, update
+                int pa, pb;
+                circle(warp, r2, wp, pa, pb);
+                const int p0 = min(pa, pb), q0 = max(pa, pb);
+                if (q0 < w) {
+                  double* xp = Xb + p0 * ldp;
+                  double* xq = Xb + q0 * ldp;
+                  double al = 0.0, be = 0.0, ga = 0.0;
+                  for (int r = lane; r < ldp; r += 32) {
+                    const double a = xp[r], b = xq[r];
+                    al = fma(a, a, al);
+                    be = fma(b, b, be);
+                    ga = fma(a, b, ga);
+                  }
+                  al = wsum(al);
+                  be = wsum(be);
+                  ga = wsum(ga);
+                  if (ga * ga > tol2 * (al * be) && ga != 0.0) {
+                    const double d = be - al, g2 = 2.0 * ga;
+                    const double ir = rsqrt(fma(d, d, g2 * g2));
+                    const double hh = fma(0.5 * fabs(d), ir, 0.5);
+                    const double ih = rsqrt(hh);
+                    const double c = hh * ih, sn = copysign(1.0, d) * (ga * ir) * ih;
+                    for (int r = lane; r < ldp; r += 32) {
+                      const double a = xp[r], b = xq[r];
+                      xp[r] = c * a - sn * b;
+                      xq[r] = sn * a + c * b;
+                    }
+                    const double vp = V[lane + kVL * p0], vq = V[lane + kVL * q0];
+                    V[lane + kVL * p0] = c * vp - sn * vq;
+                    V[lane + kVL * q0] = sn * vp + c * vq;
+                    if (lane == 0) any_inner = 1;
+                  }
+                }
+              }
+              __syncthreads();
+            }
+            const int rot = any_inner;
+            if (tid == 0) {
+              if (it == 0) any_first = rot;
+              any_visit |= rot;
+            }
+            __syncthreads();
+            if (!rot) break;
+          }
+        }
         // ---- cyclic two-sided Jacobi on G (w active columns), accumulating V.
         // Per round: the wp/2 rotations (one thread each), then G <- R^T G R as
         // independent 2 x 2 blocks (pair i rows x pair j columns) and V <- V R:
         // two barriers per round.  (A warp-per-pair variant with rows in
         // registers and shuffled column rotations measured 2x slower.)
-        const int wp = w + (w & 1), np2 = wp / 2;
-        for (int it = 0; it < inner_max; ++it) {
+        for (int it = 0; !graded && it < inner_max; ++it) {
           if (tid == 0) any_inner = 0;
           for (int r2 = 0; r2 < wp - 1; ++r2) {
             if (tid < np2) {
@@ -224,6 +293,18 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
           for (int mt = warp; mt < 2 * ntiles; mt += 16) {
             const bool isJ = mt >= ntiles;
             const int m0 = (isJ ? mt - ntiles : mt) * 8;
+            if (graded && !isJ) {  // one-sided route: Xb holds the rotated columns
+              const int row = m0 + r8;
+              if (row < l)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                  for (int e = 0; e < 2; ++e) {
+                    const int cc = nt * 8 + 2 * c4 + e, gc = colmap[cc];
+                    if (gc >= 0) X[int64_t(gc) * l + row] = Xb[cc * ldp + row];
+                  }
+              continue;
+            }
             double af[8];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
@@ -499,7 +580,10 @@ void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) 
     probe = reinterpret_cast<long long*>(h.ws.alloc_bytes(8 * 8));
     RSVD_CUDA(cudaMemsetAsync(probe, 0, 64, h.stream));
   }
-  void* args[] = {&X, &Jm, &lv, &ldpv, &nbv, &inner, &changed, &probe};
+  static const double graded_env =
+      std::getenv("RSVD_BJ_GRADED") ? std::atof(std::getenv("RSVD_BJ_GRADED")) : 1e-12;
+  double graded_ratio = graded_env;
+  void* args[] = {&X, &Jm, &lv, &ldpv, &nbv, &inner, &graded_ratio, &changed, &probe};
   static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   if (probe_on) {

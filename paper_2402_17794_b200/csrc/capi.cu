@@ -7,6 +7,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "diag.cuh"
 #include "dist.cuh"
 #include "engine.cuh"
 #include "pass.cuh"
@@ -630,6 +631,107 @@ rsvd_status rsvd_range_basis_host(rsvd_handle* hd, int64_t m, int64_t n, const d
     rsvdb::range_basis_impl(h, P, k, p, q, mode, r, Q);
     rsvdb::rng_download(h, r, rng);
     io.down(Q, q_out, ldq);
+  });
+}
+
+// ------------------------------------------------------------- diagnostics
+namespace {
+void single_gpu_only(const rsvdb::Handle& h, const char* what) {
+  if (h.nranks > 1)
+    throw rsvdb::Error(RSVD_ERR_PARAMETER, std::string(what) + ": needs a single-GPU handle");
+}
+}  // namespace
+
+rsvd_status rsvd_singular_values_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                     int64_t lda, double* s) {
+  return guard(hd, "singular_values", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "singular_values");
+    rsvdb::singular_values_impl(h, dm(a, m, n, lda), s);
+  });
+}
+
+rsvd_status rsvd_spectral_norm_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                   int64_t lda, double* out) {
+  return guard(hd, "spectral_norm", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "spectral_norm");
+    *out = rsvdb::spectral_norm_impl(h, dm(a, m, n, lda), nullptr);
+  });
+}
+
+rsvd_status rsvd_computed_range_error_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                          int64_t lda, int64_t l, const double* q, int64_t ldq,
+                                          double* out) {
+  return guard(hd, "computed_range_error", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "computed_range_error");
+    *out = rsvdb::computed_range_error_impl(h, dm(a, m, n, lda), dm(q, m, l, ldq));
+  });
+}
+
+rsvd_status rsvd_canonical_sines_dev(rsvd_handle* hd, int64_t m, int64_t kx, const double* x,
+                                     int64_t ldx, int64_t ky, const double* y, int64_t ldy,
+                                     double* out) {
+  return guard(hd, "canonical_sines", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "canonical_sines");
+    rsvdb::canonical_sines_impl(h, dm(x, m, kx, ldx), dm(y, m, ky, ldy), out);
+  });
+}
+
+rsvd_status rsvd_reconstruction_error_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                          int64_t lda, int64_t r, const double* u, int64_t ldu,
+                                          const double* s, const double* v, int64_t ldv,
+                                          double* rel_fro, double* rel_spec) {
+  return guard(hd, "reconstruction_error", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "reconstruction_error");
+    rsvdb::reconstruction_error_impl(h, dm(a, m, n, lda), dm(u, m, r, ldu), s, dm(v, n, r, ldv),
+                                     rel_fro, rel_spec);
+  });
+}
+
+rsvd_status rsvd_singular_values_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                      int64_t lda, double* s) {
+  return guard(hd, "singular_values", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "singular_values");
+    const int64_t r = std::min(m, n);
+    if (r <= 0) return;
+    HostIO io{h};
+    rsvdb::DMat A = io.up(a, m, n, lda);
+    double* sd = h.ws.alloc(r);
+    rsvdb::singular_values_impl(h, A, sd);
+    io.down_vec(sd, s, r);
+  });
+}
+
+rsvd_status rsvd_spectral_norm_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                    int64_t lda, double* out) {
+  return guard(hd, "spectral_norm", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "spectral_norm");
+    HostIO io{h};
+    *out = rsvdb::spectral_norm_impl(h, io.up(a, m, n, lda), nullptr);
+  });
+}
+
+rsvd_status rsvd_computed_range_error_host(rsvd_handle* hd, int64_t m, int64_t n,
+                                           const double* a, int64_t lda, int64_t l,
+                                           const double* q, int64_t ldq, double* out) {
+  return guard(hd, "computed_range_error", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "computed_range_error");
+    HostIO io{h};
+    rsvdb::DMat A = io.up(a, m, n, lda), Q = io.up(q, m, l, ldq);
+    *out = rsvdb::computed_range_error_impl(h, A, Q);
+  });
+}
+
+rsvd_status rsvd_canonical_sines_host(rsvd_handle* hd, int64_t m, int64_t kx, const double* x,
+                                      int64_t ldx, int64_t ky, const double* y, int64_t ldy,
+                                      double* out) {
+  return guard(hd, "canonical_sines", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "canonical_sines");
+    const int64_t cnt = std::min(kx, ky);
+    HostIO io{h};
+    rsvdb::DMat X = io.up(x, m, kx, ldx), Y = io.up(y, m, ky, ldy);
+    double* o = h.ws.alloc(std::max<int64_t>(cnt, 1));
+    rsvdb::canonical_sines_impl(h, X, Y, o);
+    io.down_vec(o, out, cnt);
   });
 }
 

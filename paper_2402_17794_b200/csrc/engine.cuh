@@ -17,6 +17,8 @@ void op_apply(Handle& h, const Problem& P, const DMat& X, DMat Y);
 void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z);
 void check_symmetric(Handle& h, const DMat& C, bool dist);
 
+// thin SVD without the sign rule (engine.cu)
+void svd_core(Handle& h, const DMat& M, DMat U, double* s, DMat V);
 void svd_small_impl(Handle& h, const DMat& M, DMat U, double* s, DMat V);
 void solve_ls_impl(Handle& h, const DMat& G, const DMat& Hm, DMat X);
 void evd_symmetric_impl(Handle& h, const DMat& C, DMat U, double* lambda);

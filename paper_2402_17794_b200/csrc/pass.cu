@@ -655,6 +655,12 @@ DMat tma_view(Handle& h, const DMat& x) {
   return y;
 }
 
+// Kernel-variant override for tuning experiments (tools/pass_bench.py); 0 = default.
+int env_variant(const char* name) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : 0;
+}
+
 }  // namespace
 
 void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) {
@@ -666,9 +672,20 @@ void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
     return;
   }
   DMat Pv = tma_view(h, P), Rv = tma_view(h, R);
-  if (N == 25)  // BK = 48, 3 stages: measured ~2% faster than BK = 32 for NN
-    launch<true, 32, 2, 48, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits);
-  else if (N <= 32)
+  static const int v25 = env_variant("RSVD_PASS25_NN");
+  if (N == 25) {  // BK = 48, 3 stages: measured ~2% faster than BK = 32 for NN
+    switch (v25) {
+      case 1: launch<true, 32, 4, 32, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 2: launch<true, 32, 3, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 3: launch<true, 32, 4, 16, 6, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 4: launch<true, 32, 4, 32, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 5: launch<true, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 6: launch<true, 32, 4, 32, 3, 1, 6>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 7: launch<true, 32, 4, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 8: launch<true, 32, 2, 32, 4, 1, 7>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      default: launch<true, 32, 2, 48, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits);
+    }
+  } else if (N <= 32)
     launch<true, 32, 2, 32, 4>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 64)
     launch<true, 64, 2, 32, 3>(h, Pv, Rv, C, M, N, K, force_splits);
@@ -778,9 +795,20 @@ void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
     return;
   }
   DMat Pv = tma_view(h, P), Rv = tma_view(h, R);
-  if (N == 25)
-    launch<false, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits);
-  else if (N <= 32)
+  static const int v25 = env_variant("RSVD_PASS25_TN");
+  if (N == 25) {
+    switch (v25) {
+      case 1: launch<false, 32, 4, 32, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 2: launch<false, 32, 3, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 3: launch<false, 32, 4, 16, 6, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 4: launch<false, 32, 4, 32, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 5: launch<false, 32, 2, 48, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 6: launch<false, 32, 4, 32, 3, 1, 6>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 7: launch<false, 32, 4, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 8: launch<false, 32, 2, 32, 4, 1, 7>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      default: launch<false, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits);
+    }
+  } else if (N <= 32)
     launch<false, 32, 2, 32, 4>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 64)
     launch<false, 64, 2, 32, 3>(h, Pv, Rv, C, M, N, K, force_splits);

@@ -28,6 +28,7 @@
 #include "dist.cuh"
 #include "pass.cuh"
 #include "small.cuh"
+#include "diag.cuh"
 #include "cholsmall.cuh"
 
 #include <cooperative_groups.h>
@@ -180,6 +181,14 @@ __device__ __forceinline__ double group_sum(double v) {
 
 // GS lanes per column pair: 32 (one warp) for large l, 8 for l <= 64 (fewer
 // shuffle levels and 4 pairs per warp: the round latency is the bottleneck).
+// Rotation threshold of the one-sided Jacobi sweeps (|g| > tol sqrt(a b)):
+// the rounding noise of an l-term dot product is ~sqrt(l) u, so a fixed 1e-15
+// would never report convergence for large l.  (Measured: l u instead of
+// 2 sqrt(l) u changes neither the sweep count nor the time on C1/C2.)
+__device__ __forceinline__ double jacobi_tol(int l) {
+  return fmax(1e-15, 2.0 * sqrt(double(l)) * 1.1102230246251565e-16);
+}
+
 template <int GS>
 __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, int l,
                                   double* __restrict__ Jout, int64_t ldj,
@@ -203,7 +212,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
   const int lp = l + (l & 1);  // even number of slots (one dummy if odd)
   // rotation threshold: the rounding noise of an l-term dot product is ~sqrt(l) eps,
   // so a fixed 1e-15 would never report convergence for large l
-  const double tol = fmax(1e-15, 2.0 * sqrt(double(l)) * 1.1102230246251565e-16);
+  const double tol = jacobi_tol(l);
   int sweep = 0;
   // l <= 32 with one warp per pair: lane i holds row i of both columns in
   // registers; the three inner products are warp-shuffle trees computed side
@@ -1001,6 +1010,7 @@ void check_flags(Handle& h, const char* what) {
     if (f & kFlagAsymmetric) throw_numeric(m + "input is not symmetric");
     if (f & kFlagJacobiNoConv) throw_numeric(m + "Jacobi iteration did not converge");
     if (f & kFlagCholBreakdown) throw_numeric(m + "Cholesky breakdown");
+    if (f & kFlagPowerCap) throw_numeric(m + "power iteration hit the 5000-step cap");
     if (f & kFlagRngExhausted) throw Error(RSVD_ERR_INTERNAL, m + "rng attempt budget exhausted");
     throw Error(RSVD_ERR_INTERNAL, m + "device flag set");
   }
@@ -1170,7 +1180,9 @@ static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
   }
   double* part = h.ws.alloc(2 * G * 1024);
   const double coef = 11.0 * (double(m) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
-  int passes = 4;
+  // the kernel stops as soon as Q^T Q = I to 4 l u; numerically rank-deficient
+  // inputs need up to ~6 shifted passes to lift their null directions
+  int passes = 8;
   const double* yp = X.p;
   int64_t ldy = X.ld;
   double* qp = Q.p;
@@ -1224,9 +1236,11 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
     const char* e = std::getenv("RSVD_CHOL_BLOCKED");
     return !(e && e[0] == '0');
   }();
-  auto pass = [&](const DMat& Y, DMat Qo) {
-    gemm_tn(h, Y, Y, G);
-    if (dist) allreduce_mat(h, G);
+  auto pass = [&](const DMat& Y, DMat Qo, bool have_gram = false) {
+    if (!have_gram) {
+      gemm_tn(h, Y, Y, G);
+      if (dist) allreduce_mat(h, G);
+    }
     if (l <= 32)
       chol_inv_small_kernel<<<1, kCholThreads, 0, h.stream>>>(G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld,
                                                    shift_used, h.d_flags);
@@ -1260,6 +1274,23 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
     passes = used ? 4 : 2;
   }
   for (int i = 1; i < passes; ++i) pass(Q, Q);
+  // Numerically rank-deficient input (the shift was needed): each shifted
+  // pass lifts the null-space directions by ~1/sqrt(shift) until they are
+  // unit vectors, which can take more than the fixed passes.  Continue until
+  // Q^T Q = I to working accuracy (the padded basis of core.hpp:93-95); the
+  // check's Gram is the next pass's Gram.
+  int used = 0;
+  RSVD_CUDA(cudaMemcpyAsync(&used, shift_used, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  if (used) {
+    const double tol = 8.0 * l * 1.1102230246251565e-16;
+    for (int extra = 0; extra < 8; ++extra) {
+      gemm_tn(h, Q, Q, G);
+      if (dist) allreduce_mat(h, G);
+      if (gram_deviation(h, G) <= tol) break;
+      pass(Q, Q, true);
+    }
+  }
   if (Rout) {
     // X = Q R with R = Q^T X (exact relation once Q spans X; R need not be
     // triangular for its consumers: the Jacobi SVD of the l x l factor).

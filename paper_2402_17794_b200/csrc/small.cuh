@@ -54,6 +54,7 @@ enum FlagBits : int {
   kFlagRngExhausted = 4,
   kFlagAsymmetric = 8,
   kFlagCholBreakdown = 16,
+  kFlagPowerCap = 32,
 };
 // Raises NumericError if any flag is set (synchronizes the stream).
 void check_flags(Handle& h, const char* what);

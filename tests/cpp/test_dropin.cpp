@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <string>
 
+#include "rsvd/angles.hpp"
+#include "rsvd/bounds.hpp"
 #include "rsvd/factor.hpp"
 #include "rsvd/singlepass.hpp"
 
@@ -139,6 +141,33 @@ int main() {
     REQUIRE(op2.adjoint_count() == 1);
     REQUIRE_THROWS_AS(rsvd::spevd_hermitian(random_matrix(6, 6, 2), 2, 1, rng),
                       rsvd::NumericError);
+  }
+  // diagnostics: spectral_norm (core.hpp:188-221), computed_range_error
+  // (bounds.hpp:107-120), canonical_sines / subspace_quality (angles.hpp:42-78)
+  {
+    DenseMatrix d(600, 600);
+    for (int i = 0; i < 600; ++i) d(i, i) = (i == 7) ? 3.0 : 1.0 / (1.0 + i);
+    REQUIRE(std::abs(rsvd::spectral_norm(d) - 3.0) <= 1e-9 * 3.0);  // power route
+    const DenseMatrix small = random_matrix(40, 30, 4);
+    const auto sv = rsvd::singular_values(small);
+    REQUIRE(std::abs(rsvd::spectral_norm(small) - sv(0)) <= 1e-14 * sv(0));  // dense route
+    const DenseMatrix a = random_matrix(60, 40, 5);
+    Rng rng(6);
+    const DenseMatrix q = rsvd::fixed_rank_range(a, 10, 5, rng);
+    const double err = rsvd::computed_range_error(a, q);
+    REQUIRE(err >= sv(0) * 0.0 && err <= rsvd::spectral_norm(a));
+    REQUIRE(err >= rsvd::singular_values(a)(15) * (1 - 1e-10));  // Eckart-Young floor
+    REQUIRE_THROWS_AS(rsvd::computed_range_error(random_matrix(50, 40, 1), q),
+                      rsvd::DimensionError);
+    const auto same = rsvd::canonical_sines(q, q);
+    REQUIRE(same.rows() == 15);
+    for (int i = 0; i < 15; ++i) REQUIRE(std::abs(same(i)) < 1e-13);
+    const rsvd::SvdApprox f = rsvd::rsvd(a, rsvd::SketchConfig{5, 5, 2, rsvd::RangeMode::power, 1});
+    const rsvd::AngleReport rep = rsvd::subspace_quality(a, 5, f);
+    REQUIRE(rep.k == 5 && rep.sin_theta.rows() == 5 && rep.sin_nu.rows() == 5);
+    for (int i = 0; i + 1 < 5; ++i) REQUIRE(rep.sin_theta(i) <= rep.sin_theta(i + 1));
+    REQUIRE_THROWS_AS(rsvd::subspace_quality(a, 0, f), rsvd::ParameterError);
+    REQUIRE_THROWS_AS(rsvd::canonical_sines(a, q), rsvd::NumericError);
   }
   std::printf(g_fail ? "drop-in: %d failures\n" : "drop-in: all passed\n", g_fail);
   return g_fail ? 1 : 0;

@@ -342,3 +342,34 @@ def test_joint_core_residual_vs_bruteforce(orc):
     def res(x):
         return np.sqrt(np.sum((g1 @ x - h1) ** 2) + np.sum((x @ g2 - h2) ** 2))
     assert res(c) <= res(brute) + 1e-9
+
+
+# ------------------------------------------------- diagnostics (§8(f) rows 1, 3)
+def test_oracle_spectral_norm_routes(orc):
+    """core.hpp:188-221: dense route <= 512 equals sigma_max exactly; the power
+    route converges to sigma_max (relative test 1e-10 between successive
+    estimates) and is a lower bound."""
+    rs = np.random.default_rng(0)
+    a = rs.standard_normal((300, 200))
+    assert abs(orc.spectral_norm(a) - np.linalg.norm(a, 2)) <= 1e-13 * np.linalg.norm(a, 2)
+    u = np.linalg.qr(rs.standard_normal((700, 3)))[0]
+    v = np.linalg.qr(rs.standard_normal((600, 3)))[0]
+    b = (u * [5.0, 2.0, 1.0]) @ v.T
+    s, it = orc.spectral_norm(b, with_iterations=True)
+    assert it > 1 and abs(s - 5.0) <= 1e-12 * 5.0
+    assert orc.spectral_norm(np.zeros((600, 600))) == 0.0
+
+
+def test_oracle_range_error_and_sines(orc):
+    """bounds.hpp:107-120 and angles.hpp:42-60 against numpy/scipy restatements."""
+    import scipy.linalg as sl
+    rs = np.random.default_rng(1)
+    a = rs.standard_normal((120, 90))
+    q = np.linalg.qr(rs.standard_normal((120, 10)))[0]
+    assert abs(orc.computed_range_error(a, q) - np.linalg.norm(a - q @ (q.T @ a), 2)) < 1e-12
+    with pytest.raises(orc.NumericError):
+        orc.computed_range_error(a, 1.01 * q)
+    x = np.linalg.qr(rs.standard_normal((80, 6)))[0]
+    y = np.linalg.qr(x + 1e-2 * rs.standard_normal((80, 6)))[0]
+    ref = np.sort(np.sin(sl.subspace_angles(x, y)))
+    assert np.abs(orc.canonical_sines(x, y) - ref).max() < 1e-13
