@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak, profiles/r01_fp64_peaks.md
-L2_FLUSH_BELOW = 1 << 30     # A below this is L2-flushed between timed steps
+L2_FLUSH_BELOW = 256 << 20   # A below 2x L2 is L2-flushed between timed steps
 L2_FLUSH_BYTES = 512 << 20   # > 4x the 126 MB L2
 FP64_PEAK_SOURCE = "measured DMMA microbenchmark (profiles/r01_fp64_peaks.md); MEASURED_PEAKS.json has no fp64 figure"
 
@@ -310,31 +310,40 @@ def main():
         # the per-step events) so every step reads A from HBM.
         flush = a_loc.numel() * 8 < L2_FLUSH_BELOW
         fbuf = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device) if flush else None
+        def timed_region():
+            barrier()
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps if flush else 1)]
+            if not flush:
+                evs[0][0].record()
+            for i in range(args.steps):
+                if flush:
+                    fbuf.sum()  # read-only flush: evicts A, leaves no dirty lines
+                    evs[i][0].record()
+                    step()
+                    evs[i][1].record()
+                else:
+                    step()
+            if not flush:
+                evs[0][1].record()
+            torch.cuda.synchronize()
+            barrier()
+            return sum(a_.elapsed_time(b_) for a_, b_ in evs)
+
         clocks = ClockSampler(local)
         clocks.start()
         engine.reset_counters()
-        engine.profile(True)
-        barrier()
-        torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps if flush else 1)]
-        if not flush:
-            evs[0][0].record()
-        for i in range(args.steps):
-            if flush:
-                fsum = fbuf.sum()  # read-only flush: evicts A, leaves no dirty lines
-                evs[i][0].record()
-                f = step()
-                evs[i][1].record()
-            else:
-                f = step()
-        if not flush:
-            evs[0][1].record()
-        torch.cuda.synchronize()
-        barrier()
-        ms_total = sum(a_.elapsed_time(b_) for a_, b_ in evs)
+        # (1) the headline: K steps exactly as a user runs them
+        ms_total = timed_region()
         clk = clocks.stop()
         counters = engine.counters()
+        # (2) the same K steps again with a CUDA-event pair around every pass
+        # launch (rsvd_profile_enable) for the per-kernel roofline; the event
+        # nodes cost ~10 us each inside the replayed graph, so this run is
+        # not the headline
+        engine.profile(True)
+        ms_prof = timed_region()
         prof = engine.profile_read()
         engine.profile(False)
         if world > 1:
@@ -391,7 +400,7 @@ def main():
                         "bound": bound, "tflops": tf, "gbs": gbs,
                         "frac_fp64": tf / FP64_PEAK_TFLOPS, "frac_hbm": gbs / hbm,
                         "frac_roofline": max(t_fp, t_hb) / (per_ms * 1e-3),
-                        "share_of_step": d["ms"] / ms_total if ms_total else None}
+                        "share_of_step": d["ms"] / ms_prof if ms_prof else None}
     dom = max(passes, key=lambda k_: passes[k_]["ms_per_launch"] * passes[k_]["launches_per_step"])
     dp = passes[dom]
     traffic = None
@@ -440,6 +449,7 @@ def main():
                     "ms_per_step": e2e_ms, "api": "rsvd_rsvd_host (pinned host A)"},
             "roofline": roof,
             "passes": passes,
+            "profiled_run_ms_per_step": ms_prof / args.steps,
             "cpu_baseline": cpu,
             "gpu_launches": counters["kernel_launches"],
             "physical_passes_per_step": counters["physical_passes"] / args.steps,

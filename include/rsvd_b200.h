@@ -185,6 +185,27 @@ rsvd_status rsvd_canonical_sines_host(rsvd_handle* h, int64_t m, int64_t kx, con
                                       int64_t ldx, int64_t ky, const double* y, int64_t ldy,
                                       double* out);
 
+/* ----------------------------------- batched trials */
+/* The trial loops of the reference's run_bounds / run_angles
+ * (drivers.hpp:340-356, 400-431): trial t runs with Rng(seed_base + t)
+ * (sketch.hpp:37-39).  Every streaming pass over A is shared by all trials
+ * (one pass of width trials * (k + p)); block t of each output is trial t's
+ * result.  range_basis_trials: Q m x (trials (k+p)).  rsvd_trials: U m x
+ * (trials (k+p)), sigma trials (k+p), V n x (trials (k+p)), each block as
+ * rsvd(A, cfg, Rng(seed_base + t)).  range_error_trials: errors[t] =
+ * computed_range_error(A, Q_t) (HOST array, single-GPU handle). */
+rsvd_status rsvd_range_basis_trials_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                        int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                        uint64_t seed_base, int64_t trials, double* q_out,
+                                        int64_t ldq);
+rsvd_status rsvd_rsvd_trials_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                 int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                 uint64_t seed_base, int64_t trials, double* u, int64_t ldu,
+                                 double* sigma, double* v, int64_t ldv);
+rsvd_status rsvd_range_error_trials_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
+                                        int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                        uint64_t seed_base, int64_t trials, double* errors);
+
 /* Host-buffer variants of the kernel-level entry points (the C++ drop-in
  * layer uses these; copies are included). */
 rsvd_status rsvd_gaussian_host(rsvd_handle* h, int64_t n, int64_t l, rsvd_rng_state* rng,

@@ -10,6 +10,8 @@ argument meaning and exception types as the reference:
     singular_values, spectral_norm                        core.hpp:180-221
     computed_range_error                                  bounds.hpp:107-120
     canonical_sines, subspace_quality, AngleReport        angles.hpp:11-78
+    reconstruction_error                                  drivers.hpp:145-151
+    range_basis_trials, rsvd_trials, range_error_trials   drivers.hpp:340-356, 400-431
     fixed_rank_range, power_range, subspace_iter_range,
     range_basis, SketchConfig, RangeMode                  rangefinder.hpp:13-105
     rsvd, truncate, SvdApprox                             factor.hpp:12-34
@@ -40,6 +42,7 @@ __all__ = [
     "CountingOperator", "spevd_hermitian", "spsvd_general", "apply", "apply_adjoint", "Engine",
     "default_engine", "lib_path", "build", "using_engine", "rsvd_host", "singular_values",
     "spectral_norm", "computed_range_error", "canonical_sines", "subspace_quality", "AngleReport",
+    "reconstruction_error", "range_basis_trials", "rsvd_trials", "range_error_trials",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -149,6 +152,14 @@ def _load():
             "rsvd_spectral_norm_host": [P, I64, I64, P, I64, ctypes.POINTER(D)],
             "rsvd_computed_range_error_host": [P, I64, I64, P, I64, I64, P, I64, ctypes.POINTER(D)],
             "rsvd_canonical_sines_host": [P, I64, I64, P, I64, I64, P, I64, P],
+            "rsvd_reconstruction_error_dev": [P, I64, I64, P, I64, I64, P, I64, P, P, I64,
+                                              ctypes.POINTER(D), ctypes.POINTER(D)],
+            "rsvd_range_basis_trials_dev": [P, I64, I64, P, I64, I64, I64, I, I, ctypes.c_uint64,
+                                            I64, P, I64],
+            "rsvd_rsvd_trials_dev": [P, I64, I64, P, I64, I64, I64, I, I, ctypes.c_uint64, I64, P,
+                                     I64, P, P, I64],
+            "rsvd_range_error_trials_dev": [P, I64, I64, P, I64, I64, I64, I, I, ctypes.c_uint64,
+                                            I64, P],
         }
         for name, argt in sigs.items():
             f = getattr(L, name)
@@ -845,3 +856,73 @@ def subspace_quality(oracle, k: int, result: SvdApprox) -> AngleReport:
     rep.sin_theta = canonical_sines(oracle.U[:, :k], result.U[:, :k])
     rep.sin_nu = canonical_sines(oracle.V[:, :k], result.V[:, :k])
     return rep
+
+
+def reconstruction_error(a, f):
+    """run_svd's error report (reference drivers.hpp:145-151) for an SvdApprox
+    (or EvdApprox): (||A - recon||_F / ||A||_F, ||A - recon||_2 / ||A||_2)."""
+    da = _Dev(a, "reconstruction_error")
+    e = _eng(None if da.host else a)
+    if isinstance(f, EvdApprox):
+        du, dv, s = _Dev(f.U), _Dev(f.U), f.lambda_
+    else:
+        du, dv, s = _Dev(f.U), _Dev(f.V), f.sigma
+    import torch
+    sd = torch.as_tensor(np.asarray(s) if not _is_torch(s) else s, dtype=torch.float64).cuda().contiguous()
+    fro, spec = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(_load().rsvd_reconstruction_error_dev(e.handle, da.rows, da.cols, da.ptr, da.ld, du.cols,
+                                                 du.ptr, du.ld, sd.data_ptr(), dv.ptr, dv.ld,
+                                                 ctypes.byref(fro), ctypes.byref(spec)))
+    return fro.value, spec.value
+
+
+# ------------------------------------------------------------ batched trials
+def _trial_args(cfg: SketchConfig, trials: int):
+    if trials < 1:
+        raise ParameterError("trials must be >= 1")
+    return cfg.k, cfg.p, cfg.q, int(cfg.mode), ctypes.c_uint64(cfg.seed & (2**64 - 1)), int(trials)
+
+
+def range_basis_trials(a, cfg: SketchConfig, trials: int):
+    """Stage-1 bases of `trials` runs, trial t with Rng(cfg.seed + t) (the
+    run_bounds loop, drivers.hpp:340-346): every pass over A shared by all
+    trials.  Returns a list of m x (k+p) bases."""
+    d = _Dev(a, "range_basis_trials")
+    e = _eng(None if d.host else a)
+    k, p, q, mode, seed, T = _trial_args(cfg, trials)
+    l = max(k + p, 0)
+    qall = _empty(d.rows, l * T, d.host)
+    _check(_load().rsvd_range_basis_trials_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, k, p, q, mode,
+                                               seed, T, qall.data_ptr(), max(d.rows, 1)))
+    qall = _out(qall, d.host)
+    return [qall[:, t * l:(t + 1) * l] for t in range(T)]
+
+
+def rsvd_trials(a, cfg: SketchConfig, trials: int):
+    """rsvd(A, cfg, Rng(cfg.seed + t)) for t < trials (the run_angles loop,
+    drivers.hpp:400-408) with the passes over A shared by all trials."""
+    import torch
+    d = _Dev(a, "rsvd_trials")
+    e = _eng(None if d.host else a)
+    k, p, q, mode, seed, T = _trial_args(cfg, trials)
+    l = max(k + p, 0)
+    u, v = _empty(d.rows, l * T, d.host), _empty(d.cols, l * T, d.host)
+    s = torch.empty(max(l * T, 1), dtype=torch.float64, device="cuda")
+    _check(_load().rsvd_rsvd_trials_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, k, p, q, mode, seed, T,
+                                        u.data_ptr(), max(d.rows, 1), s.data_ptr(), v.data_ptr(),
+                                        max(d.cols, 1)))
+    u, v, s = _out(u, d.host), _out(v, d.host), _vec_out(s[:l * T], d.host)
+    return [SvdApprox(u[:, t * l:(t + 1) * l], s[t * l:(t + 1) * l], v[:, t * l:(t + 1) * l])
+            for t in range(T)]
+
+
+def range_error_trials(a, cfg: SketchConfig, trials: int) -> np.ndarray:
+    """computed_range_error(A, range_basis(A, cfg, Rng(cfg.seed + t))) for
+    t < trials (the run_bounds loop, drivers.hpp:340-346)."""
+    d = _Dev(a, "range_error_trials")
+    e = _eng(None if d.host else a)
+    k, p, q, mode, seed, T = _trial_args(cfg, trials)
+    out = np.zeros(T)
+    _check(_load().rsvd_range_error_trials_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, k, p, q, mode,
+                                               seed, T, out.ctypes.data_as(ctypes.c_void_p)))
+    return out

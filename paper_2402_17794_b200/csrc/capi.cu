@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "diag.cuh"
+#include "trials.cuh"
 #include "dist.cuh"
 #include "engine.cuh"
 #include "pass.cuh"
@@ -274,6 +275,7 @@ void rsvd_destroy(rsvd_handle* hd) {
   if (h.h_flags) cudaFreeHost(h.h_flags);
   if (h.h_rng) cudaFreeHost(h.h_rng);
   if (h.h_rng_in) cudaFreeHost(h.h_rng_in);
+  if (h.h_rng_batch) cudaFreeHost(h.h_rng_batch);
   for (auto& kv : h.graph_cache) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (auto& r : kv.second.prof) {
@@ -732,6 +734,41 @@ rsvd_status rsvd_canonical_sines_host(rsvd_handle* hd, int64_t m, int64_t kx, co
     double* o = h.ws.alloc(std::max<int64_t>(cnt, 1));
     rsvdb::canonical_sines_impl(h, X, Y, o);
     io.down_vec(o, out, cnt);
+  });
+}
+
+// ------------------------------------------------------------ batched trials
+rsvd_status rsvd_range_basis_trials_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                        int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                        uint64_t seed_base, int64_t trials, double* q_out,
+                                        int64_t ldq) {
+  return guard(hd, "range_basis_trials", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
+    const int64_t l = std::max<int64_t>(k + p, 0);
+    rsvdb::range_basis_trials_impl(h, P, k, p, q, mode, seed_base, trials,
+                                   dm(q_out, m, l * std::max<int64_t>(trials, 0), ldq));
+  });
+}
+
+rsvd_status rsvd_rsvd_trials_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                 int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                 uint64_t seed_base, int64_t trials, double* u, int64_t ldu,
+                                 double* sigma, double* v, int64_t ldv) {
+  return guard(hd, "rsvd_trials", [&](rsvdb::Handle& h) {
+    rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
+    const int64_t L = std::max<int64_t>(k + p, 0) * std::max<int64_t>(trials, 0);
+    rsvdb::rsvd_trials_impl(h, P, k, p, q, mode, seed_base, trials, dm(u, m, L, ldu), sigma,
+                            dm(v, n, L, ldv));
+  });
+}
+
+rsvd_status rsvd_range_error_trials_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
+                                        int64_t lda, int64_t k, int64_t p, int q, int mode,
+                                        uint64_t seed_base, int64_t trials, double* errors) {
+  return guard(hd, "range_error_trials", [&](rsvdb::Handle& h) {
+    single_gpu_only(h, "range_error_trials");
+    rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
+    rsvdb::range_error_trials_impl(h, P, k, p, q, mode, seed_base, trials, errors);
   });
 }
 

@@ -132,6 +132,9 @@ struct Handle {
   rsvd_rng_state* rng_user_out = nullptr;
   // pinned staging for the RNG state upload (the graph-captured H2D source)
   rsvd_rng_state* h_rng_in = nullptr;
+  // pinned staging for the per-trial seeded states of batched trials (trials.cu)
+  rsvd_rng_state* h_rng_batch = nullptr;
+  int64_t h_rng_batch_cap = 0;
   // CUDA-graph replay of repeated top-level device calls (capi.cu): a call
   // is captured on its second occurrence (same shapes, pointers and
   // host-visible RNG state) and replayed as one graph launch afterwards.

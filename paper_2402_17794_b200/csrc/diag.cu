@@ -445,7 +445,7 @@ double spectral_norm_impl(Handle& h, const DMat& M, int64_t* iterations) {
   return out[0];
 }
 
-double computed_range_error_impl(Handle& h, const DMat& A, const DMat& Q) {
+double computed_range_error_impl(Handle& h, const DMat& A, const DMat& Q, DMat* resid) {
   if (Q.rows != A.rows) throw_dim("computed_range_error: row counts differ");
   const double dev = orthonormal_deviation(h, Q);
   if (dev > 1e-8 || dev != dev) {
@@ -453,7 +453,7 @@ double computed_range_error_impl(Handle& h, const DMat& A, const DMat& Q) {
     std::snprintf(buf, sizeof buf, "%f", dev);
     throw_numeric(std::string("computed_range_error: Q is not orthonormal (deviation ") + buf + ")");
   }
-  DMat R = h.ws.mat(A.rows, A.cols);
+  DMat R = resid ? *resid : h.ws.mat(A.rows, A.cols);
   if (Q.cols == 0) {
     copy(h, A, R);
   } else {

@@ -14,8 +14,8 @@ double orthonormal_deviation(Handle& h, const DMat& X);
 void residual_lowrank(Handle& h, const DMat& A, const DMat& Q, const DMat& Z, DMat R);
 // ||M||_2 (core.hpp:188-221); iterations: power steps taken (0 on the dense route)
 double spectral_norm_impl(Handle& h, const DMat& M, int64_t* iterations);
-// ||A - Q Q^T A||_2 (bounds.hpp:107-120)
-double computed_range_error_impl(Handle& h, const DMat& A, const DMat& Q);
+// ||A - Q Q^T A||_2 (bounds.hpp:107-120); resid: optional m x n scratch for the residual
+double computed_range_error_impl(Handle& h, const DMat& A, const DMat& Q, DMat* resid = nullptr);
 // ascending sines of the principal angles between range(X) and range(Y),
 // min(cols X, cols Y) of them, clamped to [0, 1] (angles.hpp:42-60)
 void canonical_sines_impl(Handle& h, const DMat& X, const DMat& Y, double* out);

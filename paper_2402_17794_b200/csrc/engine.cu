@@ -303,8 +303,8 @@ Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t l
 }
 
 // ------------------------------------------------- svd_small / solve_ls
-// Square l x l:  M J = W S  =>  M = W S J^T  (U = W, V = J).
-// Tall m > n:    M = Q R, R^T J = W S  =>  M = (Q J) S W^T: U = Q J, V = W.
+// Square l <= 64: M J = W S  =>  M = W S J^T  (U = W, V = J).
+// Tall m >= n:   M = Q R, R^T J = W S  =>  M = (Q J) S W^T: U = Q J, V = W.
 // Wide m < n:    M^T = Q R, R^T J = W S =>  M = W S (Q J)^T: U = W, V = Q J.
 // One-sided Jacobi runs on the TRANSPOSED triangular factor (Drmac-Veselic
 // preconditioning): on numerically rank-deficient / strongly graded factors
@@ -312,9 +312,9 @@ Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t l
 // with 500 singular values below u: ~40 sweeps on R, 14 on R^T).
 void svd_core(Handle& h, const DMat& M, DMat U, double* s, DMat V) {
   const int64_t m = M.rows, n = M.cols;
-  if (m == n) {
+  if (m == n && n <= 64) {
     jacobi_svd_square(h, M, V, U, s);
-  } else if (m > n) {
+  } else if (m >= n) {  // square n > 64 too: residuals and cores can be graded
     DMat Qm = h.ws.mat(m, n), R = h.ws.mat(n, n), Rt = h.ws.mat(n, n), J = h.ws.mat(n, n);
     orthonormalize(h, M, Qm, &R);
     transpose(h, R, Rt);
