@@ -567,8 +567,12 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     // one CTA per tile at least (short-K products: no partials at all), and
     // >= 8 K slices per CTA when tiles are few (bounds the partials a tile's
     // last segment must reduce)
+    static const int64_t min_slices = [] {
+      const char* e = std::getenv("RSVD_SK_MIN_SLICES");
+      return int64_t(e ? std::max(1, std::atoi(e)) : 8);
+    }();
     const int64_t g = std::max<int64_t>(
-        1, std::min<int64_t>(sms / nsub, std::max<int64_t>(tiles / nsub, units / 8)));
+        1, std::min<int64_t>(sms / nsub, std::max<int64_t>(tiles / nsub, units / min_slices)));
     pp.stream_k = 1;
     pp.nsub = int(nsub);
     pp.units = units;
@@ -655,7 +659,12 @@ DMat tma_view(Handle& h, const DMat& x) {
   return y;
 }
 
-// Kernel-variant override for tuning experiments (tools/pass_bench.py); 0 = default.
+// Kernel-variant override for tuning experiments (tools/pass_sweep.py); 0 = default.
+// Measured on C2 (l = 25), all within 0-9 % slower than the default: BM 256
+// (WMT 4), BK 16 x 6 stages, 4 or 6 consumer warps with WMT 4, BK 32 x 4
+// stages; a math-free copy of the same TMA load path streams A at 6.4 TB/s
+// (tools/microbench/tma_stream.cu), so the pass is bound by the overlap of
+// DMMA issue with the 3-stage ring, not by the TMA boxes.
 int env_variant(const char* name) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : 0;
@@ -676,7 +685,6 @@ void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
   if (N == 25) {  // BK = 48, 3 stages: measured ~2% faster than BK = 32 for NN
     switch (v25) {
       case 1: launch<true, 32, 4, 32, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
-      case 2: launch<true, 32, 3, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 3: launch<true, 32, 4, 16, 6, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 4: launch<true, 32, 4, 32, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 5: launch<true, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
@@ -799,7 +807,6 @@ void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
   if (N == 25) {
     switch (v25) {
       case 1: launch<false, 32, 4, 32, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
-      case 2: launch<false, 32, 3, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 3: launch<false, 32, 4, 16, 6, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 4: launch<false, 32, 4, 32, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 5: launch<false, 32, 2, 48, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
