@@ -372,14 +372,14 @@ __global__ void bj_norms_kernel(const double* __restrict__ X, int l, double* __r
 __global__ void bj_order_kernel(const double* __restrict__ nrm, int l, int* __restrict__ order,
                                 double* __restrict__ sigma) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < l; j += gridDim.x * blockDim.x) {
-    const double v = nrm[j];
+    const double v = order_key(nrm[j]);
     int rank = 0;
     for (int k = 0; k < l; ++k) {
-      const double u = nrm[k];
+      const double u = order_key(nrm[k]);
       if (u > v || (u == v && k < j)) ++rank;
     }
     order[rank] = j;
-    sigma[rank] = v;
+    sigma[rank] = nrm[j];
   }
 }
 
@@ -521,14 +521,14 @@ __global__ void rayleigh_kernel(const double* __restrict__ Jm, int64_t ldj,
 __global__ void evd_order_kernel(const double* __restrict__ lam_in, int l,
                                  double* __restrict__ lambda, int* __restrict__ order) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < l; j += gridDim.x * blockDim.x) {
-    const double v = lam_in[j];
+    const double v0 = lam_in[j], v = (v0 != v0) ? 0.0 : v0, av = order_key(fabs(v0));
     int rank = 0;
     for (int k = 0; k < l; ++k) {
-      const double u = lam_in[k];
-      if (fabs(u) > fabs(v) || (fabs(u) == fabs(v) && (u > v || (u == v && k < j)))) ++rank;
+      const double u0 = lam_in[k], u = (u0 != u0) ? 0.0 : u0, au = order_key(fabs(u0));
+      if (au > av || (au == av && (u > v || (u == v && k < j)))) ++rank;
     }
     order[rank] = j;
-    lambda[rank] = v;
+    lambda[rank] = v0;
   }
 }
 

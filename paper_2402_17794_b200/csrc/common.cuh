@@ -47,6 +47,14 @@ struct Error : std::runtime_error {
   } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+#ifdef __CUDACC__
+// Sort key for the rank-by-counting orderings of singular values / |lambda|:
+// NaN (a non-finite input that is only reported at the call's end) sorts
+// last, so every ordering stays a permutation and no kernel indexes out of
+// bounds before the NumericError is raised.
+__device__ __forceinline__ double order_key(double x) { return x != x ? -1.0 : x; }
+#endif
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // Device matrix view (column-major).

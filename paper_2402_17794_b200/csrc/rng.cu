@@ -76,8 +76,8 @@ __device__ __forceinline__ Pair polar_pair(uint64_t w1, uint64_t w2) {
   p.ok = !(p.r2 > 1.0 || p.r2 == 0.0);
   return p;
 }
-__device__ __forceinline__ double polar_mult(double r2) {
-  const double lg = ddlog::log_cr(r2, c_log_table);
+__device__ __forceinline__ double polar_mult(double r2, const ddlog::Entry* table) {
+  const double lg = ddlog::log_cr(r2, table);
   return __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, lg), r2));
 }
 
@@ -298,6 +298,10 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
   const int64_t base = int64_t(blockIdx.x) * kTile;
   __shared__ int wcnt[8];
   __shared__ int64_t run;
+  // the log table in shared memory: lanes index it at random, which the
+  // constant cache would serialize (measured: the whole kernel 19 us on C2)
+  __shared__ ddlog::Entry tab[ddlog::kTableSize];
+  for (int i = threadIdx.x; i < ddlog::kTableSize; i += blockDim.x) tab[i] = c_log_table[i];
   if (threadIdx.x == 0) run = tile_off[blockIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -312,7 +316,7 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
     for (int w = 0; w < warp; ++w) before += wcnt[w];
     const int64_t rank = run + before + __popc(bal & ((1u << lane) - 1u));
     if (p.ok && rank < g.pairs) {
-      const double mult = polar_mult(p.r2);
+      const double mult = polar_mult(p.r2, tab);
       const double vy = __dadd_rn(__dmul_rn(p.y, mult), 0.0);
       const double vx = __dadd_rn(__dmul_rn(p.x, mult), 0.0);
       const int64_t e0 = g.first + 2 * rank;

@@ -337,9 +337,9 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
   __syncthreads();
   for (int j = tid; j < l; j += nthr) {
     int rank = 0;
-    const double v = nrm[j];
+    const double v = order_key(nrm[j]);
     for (int k = 0; k < l; ++k) {
-      const double u = nrm[k];
+      const double u = order_key(nrm[k]);
       if (u > v || (u == v && k < j)) ++rank;
     }
     order[rank] = j;
@@ -500,14 +500,16 @@ __global__ void jacobi_evd_kernel(const double* __restrict__ Cin, int64_t ldc, i
   // order by |lambda| descending, ties by ascending lambda value then index
   // (reference: stable sort of an ascending eigenvalue list).
   for (int j = tid; j < l; j += nthr) {
-    const double v = A[j * l + j];
+    const double v0 = A[j * l + j], v = (v0 != v0) ? 0.0 : v0;
+    const double av = order_key(fabs(v0));
     int rank = 0;
     for (int k = 0; k < l; ++k) {
-      const double u = A[k * l + k];
+      const double u0 = A[k * l + k], u = (u0 != u0) ? 0.0 : u0;
+      const double au = order_key(fabs(u0));
       // |lambda| descending; exact ties: positive first, then index (the
       // reference's Eigen solver returns (-1+d, 1) for [[0,1],[1,0]], so its
       // stable |lambda| sort yields (1, -1); test_core.cpp:148-162)
-      const bool before = (fabs(u) > fabs(v)) || (fabs(u) == fabs(v) && (u > v || (u == v && k < j)));
+      const bool before = (au > av) || (au == av && (u > v || (u == v && k < j)));
       if (before) ++rank;
     }
     order[rank] = j;
