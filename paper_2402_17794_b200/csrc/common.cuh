@@ -149,6 +149,12 @@ struct Handle {
   // `generation` is bumped whenever a buffer a graph may hold is reallocated
   // (split-K semaphores, jump polynomials; the arena keeps its own count).
   bool graphs = true;
+  // Pass configuration for l > 64: 0 = two 4-warp CTAs per SM (default),
+  // 1 = one 8-warp CTA per SM.  Alg 5's single pass keeps the latter: its
+  // Ritz values sit at the 1e-10 parity tolerance under u-level rounding
+  // changes of the sketch, and that summation order is
+  // the one measured inside it on C4.
+  int pass_cfg_big = 0;
   uint64_t generation = 0;
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;

@@ -459,7 +459,14 @@ void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
   DMat Omega = h.ws.mat(n, l);
   gaussian_dev(h, n, l, rng, Omega);
   DMat Y = h.ws.mat(ml, l);
-  op_apply(h, P, Omega, Y);  // the single pass over A
+  {
+    struct Cfg {  // see Handle::pass_cfg_big; restored on exceptions too
+      Handle& h;
+      ~Cfg() { h.pass_cfg_big = 0; }
+    } cfg_scope{h};
+    h.pass_cfg_big = 1;
+    op_apply(h, P, Omega, Y);  // the single pass over A
+  }
   DMat Q = h.ws.mat(ml, l);
   orthonormalize(h, Y, Q, nullptr, P.dist);
   DMat Oloc(Omega.p + P.row_off, ml, l, Omega.ld);

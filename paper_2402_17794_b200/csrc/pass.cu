@@ -169,7 +169,8 @@ __device__ __forceinline__ int sk_cta_of(int64_t u, const PassParams& p) {
 }
 
 template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW, bool kGroup>
-__global__ void __launch_bounds__((CW + 1) * 32, 1)
+// CW <= 4: two CTAs per SM (two independent TMA rings), registers capped to fit
+__global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
     pass_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 PassParams p) {
   using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
@@ -553,7 +554,13 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
   pp.kb_tile = int(kblocks);
   pp.C = C.p;
   pp.ldc = C.ld;
-  const int sms = h.sm_count;
+  // resident CTAs per SM for this instantiation (2 for the CW <= 4 configs)
+  static int occ = 0;
+  if (occ == 0) {
+    RSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern1, Cfg::THREADS, Cfg::SMEM));
+    occ = std::max(1, occ);
+  }
+  const int sms = h.sm_count * occ;
   dim3 grid;
   // Few tiles (C1/C2 passes, Gram products): stream-K over all SMs.  Many
   // tiles: split-K grid with n-tiles adjacent for L2 reuse of A.
@@ -682,7 +689,12 @@ void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
   }
   DMat Pv = tma_view(h, P), Rv = tma_view(h, R);
   static const int v25 = env_variant("RSVD_PASS25_NN");
-  if (N == 25) {  // BK = 48, 3 stages: measured ~2% faster than BK = 32 for NN
+  static const int vbig = env_variant("RSVD_PASSBIG");
+  // N == 25 (C1 / C2): 4 consumer warps, BM 64, two CTAs per SM (two
+  // independent TMA rings per SM): C2 passes 124.2 us vs 126.6 us for one
+  // 8-warp CTA (BM 128), 926 vs 915 factorizations/s.  BK = 48, 3 stages
+  // (measured ~2 % faster than BK = 32 for NN).
+  if (N == 25) {
     switch (v25) {
       case 1: launch<true, 32, 4, 32, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 3: launch<true, 32, 4, 16, 6, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
@@ -691,14 +703,22 @@ void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
       case 6: launch<true, 32, 4, 32, 3, 1, 6>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 7: launch<true, 32, 4, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 8: launch<true, 32, 2, 32, 4, 1, 7>(h, Pv, Rv, C, M, N, K, force_splits); break;
-      default: launch<true, 32, 2, 48, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits);
+      case 9: launch<true, 32, 2, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 10: launch<true, 32, 2, 32, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 11: launch<true, 32, 1, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 12: launch<true, 32, 2, 48, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      default: launch<true, 32, 2, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits);
     }
   } else if (N <= 32)
     launch<true, 32, 2, 32, 4>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 64)
     launch<true, 64, 2, 32, 3>(h, Pv, Rv, C, M, N, K, force_splits);
-  else
+  else if (vbig == 1)
+    launch<true, 56, 4, 16, 4, 0, 4>(h, Pv, Rv, C, M, N, K, force_splits);
+  else if (vbig == 3 || (vbig == 0 && h.pass_cfg_big == 1))
     launch<true, 56, 4, 16, 4>(h, Pv, Rv, C, M, N, K, force_splits);
+  else  // two CTAs per SM, BM 64: C3 7.06 -> 6.84 ms, C5-shape 34.8 -> 33.8 ms (apply)
+    launch<true, 56, 2, 32, 3, 0, 4>(h, Pv, Rv, C, M, N, K, force_splits);
 }
 
 // ---------------------------------------------------------------- small Gram
@@ -804,7 +824,8 @@ void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
   }
   DMat Pv = tma_view(h, P), Rv = tma_view(h, R);
   static const int v25 = env_variant("RSVD_PASS25_TN");
-  if (N == 25) {
+  static const int vbig = env_variant("RSVD_PASSBIG");
+  if (N == 25) {  // see gemm_nn
     switch (v25) {
       case 1: launch<false, 32, 4, 32, 3, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 3: launch<false, 32, 4, 16, 6, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
@@ -813,14 +834,22 @@ void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits) 
       case 6: launch<false, 32, 4, 32, 3, 1, 6>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 7: launch<false, 32, 4, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
       case 8: launch<false, 32, 2, 32, 4, 1, 7>(h, Pv, Rv, C, M, N, K, force_splits); break;
-      default: launch<false, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits);
+      case 9: launch<false, 32, 2, 32, 4, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 10: launch<false, 32, 2, 32, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 11: launch<false, 32, 1, 48, 3, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      case 12: launch<false, 32, 2, 32, 4, 1>(h, Pv, Rv, C, M, N, K, force_splits); break;
+      default: launch<false, 32, 2, 32, 4, 1, 4>(h, Pv, Rv, C, M, N, K, force_splits);
     }
   } else if (N <= 32)
     launch<false, 32, 2, 32, 4>(h, Pv, Rv, C, M, N, K, force_splits);
   else if (N <= 64)
     launch<false, 64, 2, 32, 3>(h, Pv, Rv, C, M, N, K, force_splits);
-  else
+  else if (vbig == 1)
+    launch<false, 56, 4, 16, 4, 0, 4>(h, Pv, Rv, C, M, N, K, force_splits);
+  else if (vbig == 3 || (vbig == 0 && h.pass_cfg_big == 1))
     launch<false, 56, 4, 16, 4>(h, Pv, Rv, C, M, N, K, force_splits);
+  else  // two CTAs per SM, BM 64: C3 7.06 -> 6.84 ms, C5-shape 34.8 -> 33.8 ms (apply)
+    launch<false, 56, 2, 32, 3, 0, 4>(h, Pv, Rv, C, M, N, K, force_splits);
 }
 
 }  // namespace rsvdb

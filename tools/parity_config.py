@@ -42,7 +42,8 @@ def main():
         if cfg["alg"] == 6:
             return eng.spsvd_general(a, k, p, eng.Rng(bench.SEED_OMEGA))
         return eng.rsvd(a, eng.SketchConfig(k, p, q, eng.RangeMode[cfg["mode"]], bench.SEED_OMEGA))
-    run()  # warm
+    run()  # warm (grows the workspace arena)
+    run()  # warm (the arena is merged into one allocation at this call)
     e = eng.default_engine()
     e.trace(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
