@@ -26,6 +26,8 @@ void solve_joint_core_impl(Handle& h, const DMat& G1, const DMat& H1, const DMat
                            const DMat& H2, DMat C);
 void range_basis_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, int mode,
                       DevRng& rng, DMat Q);
+// Stage 2 of rsvd given Q and Z = A^T Q (engine.cu)
+void rsvd_stage2(Handle& h, const DMat& Q, const DMat& Z, DMat U, double* sigma, DMat V);
 void rsvd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, int mode, DevRng& rng,
                DMat U, double* sigma, DMat V);
 void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, bool check_sym,

@@ -126,15 +126,8 @@ void rsvd_trials_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, 
   range_basis_trials_impl(h, P, k, p, q, mode, seed_base, T, Q);
   DMat Z = h.ws.mat(n, L);
   op_adjoint(h, P, Q, Z);  // B_t^T = A^T Q_t for every trial: one pass
-  DMat Qb = h.ws.mat(n, l), Rb = h.ws.mat(l, l), J = h.ws.mat(l, l), W = h.ws.mat(l, l);
-  for (int64_t t = 0; t < T; ++t) {  // as rsvd_impl (engine.cu), per trial
-    DMat Vt = block(V, t, l);
-    orthonormalize(h, block(Z, t, l), Qb, &Rb, false);
-    jacobi_svd_square(h, Rb, J, W, sigma + t * l);
-    gemm_nn(h, Qb, W, Vt);
-    sign_rule(h, J, &Vt);
-    gemm_nn(h, block(Q, t, l), J, block(U, t, l));
-  }
+  for (int64_t t = 0; t < T; ++t)  // as rsvd_impl (engine.cu), per trial
+    rsvd_stage2(h, block(Q, t, l), block(Z, t, l), block(U, t, l), sigma + t * l, block(V, t, l));
 }
 
 // computed_range_error (bounds.hpp:107-120) of every trial's Stage-1 basis:
