@@ -65,11 +65,22 @@ constexpr int kVL = 36;  // ld of V: 36 % 16 == 4 keeps DMMA B-fragment loads co
 // l-long dot products; the inner rounds touch only the 32 x 32 G.  Outer
 // convergence is measured on the freshly computed G of every visit, so the
 // final orthogonality is that of one-sided Jacobi.
-__global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict__ X,
-                                                            double* __restrict__ Jm, int l, int ldp,
+// Up to two independent problems of the same size share one launch (the
+// two joint-core SVDs of Alg 6): CTAs walk the (problem, pair) items of a
+// round; a converged problem's visits are skipped until both are done.
+struct BJProblem {
+  double* X;
+  double* Jm;
+  int* changed;  // kBJMaxSweeps + 2 ints
+};
+struct BJBatch {
+  BJProblem p[2];
+  int nprob;
+};
+
+__global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int l, int ldp,
                                                             int nb, int inner_max,
                                                             double graded_ratio,
-                                                            int* __restrict__ changed,
                                                             long long* __restrict__ probe) {
   long long pt[6] = {0, 0, 0, 0, 0, 0}, tlast = clock64();
   auto mark = [&](int ph) {
@@ -93,9 +104,16 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
   const int nbp = nb + (nb & 1);
   const double tol = fmax(1e-15, 2.0 * sqrt(double(l)) * 1.1102230246251565e-16);
   const double tol2 = tol * tol;
+  const int npairs = nbp / 2;
+  bool done0 = false, done1 = batch.nprob < 2;  // identical in every thread
   for (int sweep = 0; sweep < kBJMaxSweeps; ++sweep) {
     for (int round = 0; round < nbp - 1; ++round) {
-      for (int pr = blockIdx.x; pr < nbp / 2; pr += gridDim.x) {
+      for (int item = blockIdx.x; item < batch.nprob * npairs; item += gridDim.x) {
+        const int prob = item / npairs, pr = item % npairs;
+        if (prob == 0 ? done0 : done1) continue;
+        double* __restrict__ X = batch.p[prob].X;
+        double* __restrict__ Jm = batch.p[prob].Jm;
+        int* __restrict__ changed = batch.p[prob].changed;
         int a, b;
         circle(pr, round, nbp, a, b);
         const int I = min(a, b), K = max(a, b);
@@ -343,14 +361,17 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(double* __restrict_
       grid.sync();
       mark(4);
     }
-    const int done = (*reinterpret_cast<volatile int*>(&changed[sweep]) == 0);
-    if (done) {
+    if (!done0) done0 = (*reinterpret_cast<volatile int*>(&batch.p[0].changed[sweep]) == 0);
+    if (!done1) done1 = (*reinterpret_cast<volatile int*>(&batch.p[1].changed[sweep]) == 0);
+    if (done0 && done1) {
       if (probe && blockIdx.x == 0 && threadIdx.x == 0)
         for (int i = 0; i < 6; ++i) probe[i] = pt[i];
       return;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) changed[kBJMaxSweeps] = 1;  // no convergence
+  if (blockIdx.x == 0 && threadIdx.x == 0)  // no convergence
+    for (int q = 0; q < batch.nprob; ++q)
+      if (!(q == 0 ? done0 : done1)) batch.p[q].changed[kBJMaxSweeps] = 1;
 }
 
 // column norms (sigma), stable descending order, permuted outputs
@@ -541,19 +562,45 @@ __global__ void evd_permute_kernel(const double* __restrict__ Jm, int64_t ldj, i
 
 }  // namespace
 
-void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) {
+namespace {
+struct BJWork {
+  double *X, *Jm, *nrm;
+  int *order, *changed, *nzero;
+};
+
+BJWork bj_prepare(Handle& h, const DMat& Rm) {
   const int l = int(Rm.rows);
-  const int nb = (l + kBJ - 1) / kBJ;
-  double* X = h.ws.alloc(int64_t(l) * l);
-  double* Jm = h.ws.alloc(int64_t(l) * l);
-  double* nrm = h.ws.alloc(l);
-  int* order = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(l) * 4 + 16));
-  int* changed = reinterpret_cast<int*>(h.ws.alloc_bytes((kBJMaxSweeps + 2) * 4));
-  int* nzero = changed + kBJMaxSweeps + 1;
-  RSVD_CUDA(cudaMemsetAsync(changed, 0, (kBJMaxSweeps + 2) * 4, h.stream));
+  BJWork w;
+  w.X = h.ws.alloc(int64_t(l) * l);
+  w.Jm = h.ws.alloc(int64_t(l) * l);
+  w.nrm = h.ws.alloc(l);
+  w.order = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(l) * 4 + 16));
+  w.changed = reinterpret_cast<int*>(h.ws.alloc_bytes((kBJMaxSweeps + 2) * 4));
+  w.nzero = w.changed + kBJMaxSweeps + 1;
+  RSVD_CUDA(cudaMemsetAsync(w.changed, 0, (kBJMaxSweeps + 2) * 4, h.stream));
   bj_init_kernel<<<std::max(1, std::min(4 * h.sm_count, (l * l + 255) / 256)), 256, 0, h.stream>>>(
-      Rm.p, Rm.ld, l, X, Jm);
+      Rm.p, Rm.ld, l, w.X, w.Jm);
   RSVD_LAUNCHED(h);
+  return w;
+}
+
+void bj_finish(Handle& h, const BJWork& w, int l, DMat J, DMat W, double* sigma) {
+  bj_flag_kernel<<<1, 1, 0, h.stream>>>(w.changed, h.d_flags);
+  RSVD_LAUNCHED(h);
+  bj_norms_kernel<<<l, 256, 0, h.stream>>>(w.X, l, w.nrm);
+  RSVD_LAUNCHED(h);
+  bj_order_kernel<<<(l + 255) / 256, 256, 0, h.stream>>>(w.nrm, l, w.order, sigma);
+  RSVD_LAUNCHED(h);
+  bj_permute_kernel<<<l, 128, 0, h.stream>>>(w.X, w.Jm, w.nrm, w.order, l, J.p, J.ld, W.p, W.ld,
+                                            w.nzero);
+  RSVD_LAUNCHED(h);
+  bj_complete_kernel<<<1, 32, 0, h.stream>>>(sigma, l, W.p, W.ld, w.nzero);
+  RSVD_LAUNCHED(h);
+}
+
+// One cooperative launch over 1 or 2 problems of size l.
+void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
+  const int nb = (l + kBJ - 1) / kBJ;
   // panel rows padded to ldp = l rounded up to 8 with ldp % 16 in {4, 12}... use the
   // smallest ldp >= l, ldp % 4 == 0, (ldp / 4) odd: conflict-free DMMA fragment loads
   int ldp = (l + 3) / 4 * 4;
@@ -566,25 +613,29 @@ void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) 
                                    int(smem)));
     cur = smem;
   }
-  int nbv = nb;
-  int lv = l, ldpv = ldp;
+  BJBatch batch{};
+  batch.nprob = nprob;
+  for (int q = 0; q < 2; ++q) {
+    const BJWork& w = work[q < nprob ? q : 0];
+    batch.p[q] = BJProblem{w.X, w.Jm, w.changed};
+  }
+  int nbv = nb, lv = l, ldpv = ldp;
   // one inner sweep per visit: more inner sweeps do not reduce the outer sweep
   // count measurably (C3-C5 shapes)
   static const int inner_env = std::getenv("RSVD_BJ_INNER") ? std::atoi(std::getenv("RSVD_BJ_INNER")) : 1;
   int inner = inner_env;
   const int nbp = nb + (nb & 1);
-  int grid = std::max(1, std::min(nbp / 2, h.sm_count));
-  long long* probe = nullptr;
-  static const bool probe_env = std::getenv("RSVD_PROBE_FQ") != nullptr;
-  if (probe_env) {
-    probe = reinterpret_cast<long long*>(h.ws.alloc_bytes(8 * 8));
-    RSVD_CUDA(cudaMemsetAsync(probe, 0, 64, h.stream));
-  }
+  int grid = std::max(1, std::min(nprob * (nbp / 2), h.sm_count));
   static const double graded_env =
       std::getenv("RSVD_BJ_GRADED") ? std::atof(std::getenv("RSVD_BJ_GRADED")) : 1e-12;
   double graded_ratio = graded_env;
-  void* args[] = {&X, &Jm, &lv, &ldpv, &nbv, &inner, &graded_ratio, &changed, &probe};
+  long long* probe = nullptr;
   static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
+  if (probe_on) {
+    probe = reinterpret_cast<long long*>(h.ws.alloc_bytes(8 * 8));
+    RSVD_CUDA(cudaMemsetAsync(probe, 0, 64, h.stream));
+  }
+  void* args[] = {&batch, &lv, &ldpv, &nbv, &inner, &graded_ratio, &probe};
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   if (probe_on) {
     cudaEventCreate(&pe0);
@@ -597,7 +648,7 @@ void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) 
   if (probe_on) {
     cudaEventRecord(pe1, h.stream);
     int hc[kBJMaxSweeps + 1];
-    RSVD_CUDA(cudaMemcpyAsync(hc, changed, sizeof hc, cudaMemcpyDeviceToHost, h.stream));
+    RSVD_CUDA(cudaMemcpyAsync(hc, work[0].changed, sizeof hc, cudaMemcpyDeviceToHost, h.stream));
     RSVD_CUDA(cudaStreamSynchronize(h.stream));
     float ms = 0;
     cudaEventElapsedTime(&ms, pe0, pe1);
@@ -606,22 +657,30 @@ void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) 
     long long hp[6];
     RSVD_CUDA(cudaMemcpy(hp, probe, sizeof hp, cudaMemcpyDeviceToHost));
     std::fprintf(stderr,
-                 "bjacobi l=%d nb=%d grid=%d sweeps=%d (+1 clean) %.3f ms  cycles load %lld gram %lld "
-                 "inner %lld update %lld gridsync %lld\n",
-                 l, nb, grid, sw, ms, hp[0], hp[1], hp[2], hp[3], hp[4]);
+                 "bjacobi l=%d nb=%d nprob=%d grid=%d sweeps=%d (+1 clean) %.3f ms  cycles load %lld "
+                 "gram %lld inner %lld update %lld gridsync %lld\n",
+                 l, nb, nprob, grid, sw, ms, hp[0], hp[1], hp[2], hp[3], hp[4]);
     cudaEventDestroy(pe0);
     cudaEventDestroy(pe1);
   }
-  bj_flag_kernel<<<1, 1, 0, h.stream>>>(changed, h.d_flags);
-  RSVD_LAUNCHED(h);
-  bj_norms_kernel<<<l, 256, 0, h.stream>>>(X, l, nrm);
-  RSVD_LAUNCHED(h);
-  bj_order_kernel<<<(l + 255) / 256, 256, 0, h.stream>>>(nrm, l, order, sigma);
-  RSVD_LAUNCHED(h);
-  bj_permute_kernel<<<l, 128, 0, h.stream>>>(X, Jm, nrm, order, l, J.p, J.ld, W.p, W.ld, nzero);
-  RSVD_LAUNCHED(h);
-  bj_complete_kernel<<<1, 32, 0, h.stream>>>(sigma, l, W.p, W.ld, nzero);
-  RSVD_LAUNCHED(h);
+}
+}  // namespace
+
+void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma) {
+  const int l = int(Rm.rows);
+  const BJWork w = bj_prepare(h, Rm);
+  bj_run(h, l, &w, 1);
+  bj_finish(h, w, l, J, W, sigma);
+}
+
+void block_jacobi_svd2(Handle& h, const DMat& R0, DMat J0, DMat W0, double* s0, const DMat& R1,
+                       DMat J1, DMat W1, double* s1) {
+  const int l = int(R0.rows);
+  if (R1.rows != l) throw_dim("block_jacobi_svd2: sizes differ");
+  const BJWork w[2] = {bj_prepare(h, R0), bj_prepare(h, R1)};
+  bj_run(h, l, w, 2);
+  bj_finish(h, w[0], l, J0, W0, s0);
+  bj_finish(h, w[1], l, J1, W1, s1);
 }
 
 // Symmetric EVD for l > 64: the SVD of the positive semidefinite C + mu I

@@ -368,8 +368,12 @@ void solve_joint_core_impl(Handle& h, const DMat& G1, const DMat& H1, const DMat
   DMat U1 = h.ws.mat(l, l), V1 = h.ws.mat(l, l), U2 = h.ws.mat(l, l), V2 = h.ws.mat(l, l);
   double* s1 = h.ws.alloc(l);
   double* s2 = h.ws.alloc(l);
-  jacobi_svd_square(h, G1, V1, U1, s1);  // G1 V1 = U1 S1
-  jacobi_svd_square(h, G2, V2, U2, s2);
+  if (l > 64) {  // the two SVDs are independent: one batched block-Jacobi launch
+    block_jacobi_svd2(h, G1, V1, U1, s1, G2, V2, U2, s2);
+  } else {
+    jacobi_svd_square(h, G1, V1, U1, s1);  // G1 V1 = U1 S1
+    jacobi_svd_square(h, G2, V2, U2, s2);
+  }
   DMat T = h.ws.mat(l, l), a = h.ws.mat(l, l), b = h.ws.mat(l, l), X = h.ws.mat(l, l);
   gemm_tn(h, U1, H1, T);  // U1^T H1
   gemm_nn(h, T, U2, a);   // (U1^T H1) U2

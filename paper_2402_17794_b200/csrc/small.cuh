@@ -25,6 +25,9 @@ void chol_inv_blocked(Handle& h, const DMat& G, int l, double shift_coef, DMat R
 
 // Block one-sided Jacobi (cooperative, multi-CTA) for l > 64 (bjacobi.cu).
 void block_jacobi_svd(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma);
+// Two independent l x l problems (l > 64) in one cooperative launch.
+void block_jacobi_svd2(Handle& h, const DMat& R0, DMat J0, DMat W0, double* s0, const DMat& R1,
+                       DMat J1, DMat W1, double* s1);
 // Symmetric EVD for l > 64 via the SVD of C + mu I (bjacobi.cu).
 void evd_shifted(Handle& h, const DMat& C, DMat U, double* lambda);
 

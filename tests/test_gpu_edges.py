@@ -163,3 +163,14 @@ def test_rng_state_continues_after_device_calls(eng, orc):
     x_e = [r_e.normal() for _ in range(5)]
     x_o = [r_o.normal() for _ in range(5)]
     assert np.allclose(x_e, x_o, rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("l", [70, 150])
+def test_joint_core_batched_block_jacobi(eng, orc, l):
+    """l > 64: the two joint-core SVDs (G1, G2) run as one batched block-Jacobi
+    launch; the result must equal the oracle's Kronecker route."""
+    rs = np.random.default_rng(l)
+    g1, h1, g2, h2 = (np.asfortranarray(rs.standard_normal((l, l))) for _ in range(4))
+    c = eng.solve_joint_core(_t(g1), _t(h1), _t(g2), _t(h2))
+    co = orc.solve_joint_core(g1, h1, g2, h2, route=1)
+    assert np.abs(_np(c) - co).max() <= 1e-9 * np.abs(co).max()
