@@ -197,41 +197,46 @@ __device__ __forceinline__ void asym_pair(int64_t t0, int64_t nt, int64_t& bi, i
   bj = bi + (t0 - (bi * nt - bi * (bi - 1) / 2));
 }
 
+// T x T tiles, 256 threads: thread (tx = row in tile, ty) owns columns ty + (256/T) q.
+// T = 64 reads 512-byte column segments (T = 32: 256 bytes).
+template <int T>
 __global__ void __launch_bounds__(256) asym_kernel(const double* __restrict__ A, int64_t n,
                                                    int64_t lda, double* out) {
-  __shared__ double T2[32][33];
+  constexpr int CS = 256 / T;  // column stride between a thread's elements
+  constexpr int E = T / CS;    // elements per thread per tile
+  __shared__ double T2[T][T + 1];
   __shared__ double r_abs[8], r_asym[8];
-  const int64_t nt = (n + 31) / 32;
+  const int64_t nt = (n + T - 1) / T;
   const int64_t npairs = nt * (nt + 1) / 2;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tx = threadIdx.x % T, ty = threadIdx.x / T;
   double mabs = 0.0, masym = 0.0;
-  double a[4], b[4];
+  double a[E], b[E];
   auto load = [&](int64_t t0) {
     int64_t bi, bj;
     asym_pair(t0, nt, bi, bj);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = ty + 8 * q;
-      const int64_t r1 = bi * 32 + tx, c1 = bj * 32 + k;  // A(bi*32 + tx, bj*32 + k)
+    for (int q = 0; q < E; ++q) {
+      const int k = ty + CS * q;
+      const int64_t r1 = bi * T + tx, c1 = bj * T + k;  // A(bi*T + tx, bj*T + k)
       a[q] = (r1 < n && c1 < n) ? __ldcs(A + c1 * lda + r1) : 0.0;
-      const int64_t r2 = bj * 32 + tx, c2 = bi * 32 + k;  // A(bj*32 + tx, bi*32 + k)
+      const int64_t r2 = bj * T + tx, c2 = bi * T + k;  // A(bj*T + tx, bi*T + k)
       b[q] = (r2 < n && c2 < n) ? __ldcs(A + c2 * lda + r2) : 0.0;
     }
   };
   int64_t t0 = blockIdx.x;
   if (t0 < npairs) load(t0);
   for (; t0 < npairs; t0 += gridDim.x) {
-    double ca[4];
+    double ca[E];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < E; ++q) {
       ca[q] = a[q];
-      T2[ty + 8 * q][tx] = b[q];
+      T2[ty + CS * q][tx] = b[q];
     }
     if (t0 + gridDim.x < npairs) load(t0 + gridDim.x);  // in flight during the compare
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = ty + 8 * q;
+    for (int q = 0; q < E; ++q) {
+      const int k = ty + CS * q;
       const double x = ca[q], y = T2[tx][k];  // A(i, j) vs A(j, i)
       mabs = fmax(mabs, fmax(fabs(x), fabs(y)));
       masym = fmax(masym, fabs(x - y));
@@ -242,15 +247,16 @@ __global__ void __launch_bounds__(256) asym_kernel(const double* __restrict__ A,
     mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
     masym = fmax(masym, __shfl_xor_sync(0xffffffffu, masym, o));
   }
-  if (tx == 0) {
-    r_abs[ty] = mabs;
-    r_asym[ty] = masym;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    r_abs[w] = mabs;
+    r_asym[w] = masym;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) {
-      mabs = fmax(mabs, r_abs[w]);
-      masym = fmax(masym, r_asym[w]);
+    for (int i = 1; i < 8; ++i) {
+      mabs = fmax(mabs, r_abs[i]);
+      masym = fmax(masym, r_asym[i]);
     }
     atomic_max_nonneg(&out[0], mabs);
     atomic_max_nonneg(&out[1], masym);
@@ -273,9 +279,16 @@ void check_symmetric(Handle& h, const DMat& C, bool dist_unused) {
   if (n == 0) return;
   double* mm = h.ws.alloc(2);
   RSVD_CUDA(cudaMemsetAsync(mm, 0, 16, h.stream));
-  const int64_t nt = ceil_div(n, 32);
-  const int64_t grid = std::min<int64_t>(nt * (nt + 1) / 2, 8 * h.sm_count);
-  asym_kernel<<<unsigned(grid), 256, 0, h.stream>>>(C.p, n, C.ld, mm);
+  static const int tile_env = std::getenv("RSVD_ASYM_T") ? std::atoi(std::getenv("RSVD_ASYM_T")) : 64;
+  if (tile_env == 32 || n < 1024) {
+    const int64_t nt = ceil_div(n, 32);
+    const int64_t grid = std::min<int64_t>(nt * (nt + 1) / 2, 8 * h.sm_count);
+    asym_kernel<32><<<unsigned(grid), 256, 0, h.stream>>>(C.p, n, C.ld, mm);
+  } else {
+    const int64_t nt = ceil_div(n, 64);
+    const int64_t grid = std::min<int64_t>(nt * (nt + 1) / 2, 6 * h.sm_count);
+    asym_kernel<64><<<unsigned(grid), 256, 0, h.stream>>>(C.p, n, C.ld, mm);
+  }
   RSVD_LAUNCHED(h);
   asym_flag_kernel<<<1, 1, 0, h.stream>>>(mm, h.d_flags, kFlagAsymmetric);
   RSVD_LAUNCHED(h);
