@@ -300,7 +300,12 @@ def main():
             return eng.spsvd_general(a_loc, k, p, eng.Rng(SEED_OMEGA))
         return eng.rsvd(a_loc, sk, eng.Rng(SEED_OMEGA))
 
-    with eng.using_engine(engine):
+    # the engine runs on torch's current stream (set per call by using_engine):
+    # a dedicated stream, so the step events below are recorded on the stream
+    # the engine's kernels are launched on
+    torch.cuda.synchronize()
+    run_stream = torch.cuda.Stream(device)
+    with eng.using_engine(engine), torch.cuda.stream(run_stream):
         for _ in range(args.warmup):
             f = step()
         torch.cuda.synchronize()

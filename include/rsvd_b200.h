@@ -80,7 +80,9 @@ typedef struct rsvd_handle rsvd_handle;
 /* ---------------------------------------------------------------- handle */
 rsvd_status rsvd_create(rsvd_handle** h, int device);
 /* Multi-GPU: one handle per rank/GPU.  nccl_id is the 128-byte ncclUniqueId
- * produced by rsvd_nccl_unique_id on rank 0 and broadcast by the caller. */
+ * produced by rsvd_nccl_unique_id on rank 0 and broadcast by the caller.
+ * nranks == 1 with a non-null id builds a one-rank communicator: the
+ * row-sharded code path, every NCCL exchange included, on a single GPU. */
 rsvd_status rsvd_nccl_unique_id(void* nccl_id_out128);
 rsvd_status rsvd_create_dist(rsvd_handle** h, int device, int rank, int nranks,
                              const void* nccl_id128);

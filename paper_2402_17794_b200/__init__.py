@@ -190,7 +190,9 @@ class Engine:
         L = _load()
         self._h = ctypes.c_void_p()
         self.device = device
-        if nranks > 1:
+        # nranks == 1 with an id: a one-rank NCCL communicator, i.e. the
+        # row-sharded code path (every exchange included) on one GPU
+        if nranks > 1 or nccl_id is not None:
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             _check(L.rsvd_create_dist(ctypes.byref(self._h), device, rank, nranks, buf))
         else:

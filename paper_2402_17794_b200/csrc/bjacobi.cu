@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
   __shared__ int colmap[kBJW];
   __shared__ double rc[kBJW / 2], rs[kBJW / 2];
   __shared__ int rp[kBJW / 2], rq[kBJW / 2];
-  __shared__ int any_first, any_inner, any_visit, graded;
+  __shared__ int any_first, any_inner, any_visit, graded, big;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r8 = lane >> 2, c4 = lane & 3;
   const int nbp = nb + (nb & 1);
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
         const int wI = min(kBJ, l - I * kBJ), wK = min(kBJ, l - K * kBJ);
         const int w = wI + wK;
         if (tid < kBJW) colmap[tid] = (tid < wI) ? I * kBJ + tid : (tid < w ? K * kBJ + (tid - wI) : -1);
-        if (tid == 0) any_first = any_visit = 0;
+        if (tid == 0) any_first = any_visit = big = 0;
         __syncthreads();
         // ---- panel load (zero padded to kBJW columns x ldp rows)
         // warp w: columns w and w + 16, lanes along rows, 4 loads in flight
@@ -171,6 +171,15 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
             if (d > 0.0) gmin = fmin(gmin, d);
           }
           graded = (gmin < graded_ratio * gmax) ? 1 : 0;
+        }
+        // any relative off-diagonal above kJacobiQuad in the fresh Gram?
+        // (bit 1 of changed[sweep]; no such entry in a whole sweep = converged)
+        for (int e = tid; e < kBJW * kBJW; e += blockDim.x) {
+          const int i = e % kBJW, j = e / kBJW;
+          if (i < j && j < w) {
+            const double gij = G[i + kGL * j];
+            if (gij * gij > kJacobiQuad2 * (G[i + kGL * i] * G[j + kGL * j])) big = 1;
+          }
         }
         __syncthreads();
         const int wp = w + (w & 1), np2 = wp / 2;
@@ -354,15 +363,17 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
             }
           }
         }
-        if (tid == 0 && any_first) atomicOr(&changed[sweep], 1);
+        // graded panels' Gram entries carry absolute rounding: no early stop
+        if (tid == 0 && any_first) atomicOr(&changed[sweep], (big || graded) ? 3 : 1);
         __syncthreads();
         mark(3);
       }
       grid.sync();
       mark(4);
     }
-    if (!done0) done0 = (*reinterpret_cast<volatile int*>(&batch.p[0].changed[sweep]) == 0);
-    if (!done1) done1 = (*reinterpret_cast<volatile int*>(&batch.p[1].changed[sweep]) == 0);
+    // done: no rotation, or none above kJacobiQuad (bit 1) in this sweep
+    if (!done0) done0 = (*reinterpret_cast<volatile int*>(&batch.p[0].changed[sweep]) & 2) == 0;
+    if (!done1) done1 = (*reinterpret_cast<volatile int*>(&batch.p[1].changed[sweep]) & 2) == 0;
     if (done0 && done1) {
       if (probe && blockIdx.x == 0 && threadIdx.x == 0)
         for (int i = 0; i < 6; ++i) probe[i] = pt[i];

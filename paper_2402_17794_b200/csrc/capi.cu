@@ -22,6 +22,18 @@ struct rsvd_handle {
 namespace {
 thread_local std::string g_err;
 
+// A call on the handle's own (non-blocking) stream must not start before the
+// work the caller queued on the legacy default stream -- the kernels that
+// produced its inputs (a framework's default stream) -- has finished: the
+// non-blocking stream does not synchronize with it implicitly.  Measured
+// without this: the inputs of a call issued right after a framework's
+// asynchronous input construction were read before they were complete.
+void join_caller_stream(rsvdb::Handle& h) {
+  if (h.stream != h.own_stream) return;  // caller's stream: ordered already
+  RSVD_CUDA(cudaEventRecord(h.join_ev, cudaStreamLegacy));
+  RSVD_CUDA(cudaStreamWaitEvent(h.own_stream, h.join_ev, 0));
+}
+
 template <class F>
 rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
   try {
@@ -29,6 +41,7 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
     rsvdb::Handle& h = hd->h;
     RSVD_CUDA(cudaSetDevice(h.device));
     h.ws.reset();
+    join_caller_stream(h);
     h.rng_user_out = nullptr;
     rsvdb::trace_begin(h);
     f(h);
@@ -65,7 +78,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     const char* e = std::getenv("RSVD_GRAPHS");
     return !(e && e[0] == '0');
   }();
-  if (!hd || !env_on || !hd->h.graphs || hd->h.trace || hd->h.nranks > 1) return guard(hd, what, f);
+  if (!hd || !env_on || !hd->h.graphs || hd->h.trace || hd->h.dist()) return guard(hd, what, f);
   rsvdb::Handle& h = hd->h;
   auto add = [](rsvd_counters& a, const rsvd_counters& d, int sgn) {
     a.apply += sgn * d.apply;
@@ -75,6 +88,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
   };
   try {
     RSVD_CUDA(cudaSetDevice(h.device));
+    join_caller_stream(h);  // before any replay or capture on the stream
     auto gen_now = [&] { return h.generation + h.ws.generation(); };
     if (h.graph_cache.size() > 256 && !h.graph_cache.count(key)) {  // bound the cache
       for (auto& kv : h.graph_cache) {
@@ -190,6 +204,7 @@ rsvd_status create_impl(rsvd_handle** out, int device, int rank, int nranks, con
     RSVD_CUDA(cudaSetDevice(device));
     RSVD_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamNonBlocking));
     h.stream = h.own_stream;
+    RSVD_CUDA(cudaEventCreateWithFlags(&h.join_ev, cudaEventDisableTiming));
     RSVD_CUDA(cudaMalloc(&h.d_flags, 64));
     RSVD_CUDA(cudaMemset(h.d_flags, 0, 64));
     RSVD_CUDA(cudaMallocHost(&h.h_flags, 64));
@@ -285,6 +300,7 @@ void rsvd_destroy(rsvd_handle* hd) {
   }
   for (auto e : h.prof_pool) cudaEventDestroy(e);
   for (auto e : h.trace_pool) cudaEventDestroy(e);
+  if (h.join_ev) cudaEventDestroy(h.join_ev);
   if (h.own_stream) cudaStreamDestroy(h.own_stream);
   delete hd;
 }
@@ -432,7 +448,7 @@ rsvd_status rsvd_apply_adjoint_dev(rsvd_handle* hd, int64_t m, int64_t n, const 
   return guard(hd, "apply_adjoint", [&](rsvdb::Handle& h) {
     rsvdb::Problem P;
     P.A = dm(a, m, n, lda);
-    P.dist = h.nranks > 1;
+    P.dist = h.dist();
     rsvdb::op_adjoint(h, P, dm(y, m, l, ldy), dm(z, n, l, ldz));
   });
 }
@@ -639,7 +655,7 @@ rsvd_status rsvd_range_basis_host(rsvd_handle* hd, int64_t m, int64_t n, const d
 // ------------------------------------------------------------- diagnostics
 namespace {
 void single_gpu_only(const rsvdb::Handle& h, const char* what) {
-  if (h.nranks > 1)
+  if (h.dist())
     throw rsvdb::Error(RSVD_ERR_PARAMETER, std::string(what) + ": needs a single-GPU handle");
 }
 }  // namespace

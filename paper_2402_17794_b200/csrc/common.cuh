@@ -101,6 +101,10 @@ struct Handle {
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  // own_stream is non-blocking: a call running on it first waits for the work
+  // already queued on the legacy default stream (the caller's inputs, e.g. a
+  // framework's default stream), see join_caller_stream()
+  cudaEvent_t join_ev = nullptr;
   Arena ws;
   int* d_counters = nullptr;   // split-K tile semaphores (kept zeroed)
   int64_t n_counters = 0;
@@ -110,6 +114,9 @@ struct Handle {
   rsvd_counters counters{};
   Comm* comm = nullptr;        // null => single GPU
   int rank = 0, nranks = 1;
+  // the row-sharded (NCCL) code path: also taken by a one-rank communicator,
+  // which runs every exchange of the multi-GPU path on a single device
+  bool dist() const { return comm != nullptr; }
   // Live per-launch timing of the streaming-pass kernels (bench.py roofline):
   // CUDA events recorded on h.stream around every pass launch, folded into
   // per-kind totals at the call's final synchronization.

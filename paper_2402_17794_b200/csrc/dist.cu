@@ -36,7 +36,9 @@ void nccl_unique_id(void* out128) {
 void comm_create(Handle& h, int rank, int nranks, const void* id128) {
   h.rank = rank;
   h.nranks = nranks;
-  if (nranks <= 1) return;
+  // nranks == 1 with an id: a one-rank communicator (the distributed path,
+  // every NCCL call included, on one GPU); without an id: no communicator
+  if (nranks < 1 || !id128) return;
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof id);
   h.comm = new Comm;
@@ -52,17 +54,17 @@ void comm_destroy(Handle& h) {
 }
 
 void allreduce_sum(Handle& h, double* p, int64_t count) {
-  if (h.nranks <= 1 || count == 0) return;
+  if (!h.dist() || count == 0) return;
   RSVD_NCCL(ncclAllReduce(p, p, size_t(count), ncclDouble, ncclSum, h.comm->c, h.stream));
 }
 
 void allreduce_max(Handle& h, double* p, int64_t count) {
-  if (h.nranks <= 1 || count == 0) return;
+  if (!h.dist() || count == 0) return;
   RSVD_NCCL(ncclAllReduce(p, p, size_t(count), ncclDouble, ncclMax, h.comm->c, h.stream));
 }
 
 void allgather(Handle& h, const double* send, double* recv, int64_t count) {
-  if (h.nranks <= 1) {
+  if (!h.dist()) {
     if (send != recv)
       RSVD_CUDA(cudaMemcpyAsync(recv, send, size_t(count) * 8, cudaMemcpyDeviceToDevice, h.stream));
     return;
@@ -72,7 +74,7 @@ void allgather(Handle& h, const double* send, double* recv, int64_t count) {
 
 // Contiguous (sharded) matrix reductions: dense copy when ld != rows.
 void allreduce_mat(Handle& h, DMat X) {
-  if (h.nranks <= 1 || X.rows * X.cols == 0) return;
+  if (!h.dist() || X.rows * X.cols == 0) return;
   if (X.ld == X.rows) {
     allreduce_sum(h, X.p, X.rows * X.cols);
     return;
@@ -88,7 +90,7 @@ void allreduce_mat(Handle& h, DMat X) {
 // Global row count and this rank's row offset (host values; one tiny
 // allgather, synchronizing).
 void shard_rows(Handle& h, int64_t m_local, int64_t* m_global, int64_t* row_offset) {
-  if (h.nranks <= 1) {
+  if (!h.dist()) {
     *m_global = m_local;
     *row_offset = 0;
     return;

@@ -24,6 +24,23 @@
 namespace rsvdb {
 
 // ------------------------------------------------------------------ arena
+// RSVD_POISON=<byte>: fill every workspace chunk with that byte at each reset
+// and allocation (debug: results must not depend on stale workspace contents).
+static int arena_poison() {
+  static const int v = [] {
+    const char* e = std::getenv("RSVD_POISON");
+    return e ? std::atoi(e) & 255 : -1;
+  }();
+  return v;
+}
+
+// RSVD_ARENA_TINY=1: 256 KB chunks, never merged (debug: every call grows
+// the arena mid-call many times).
+static bool arena_tiny() {
+  static const bool v = std::getenv("RSVD_ARENA_TINY") != nullptr;
+  return v;
+}
+
 Arena::~Arena() {
   for (auto& c : chunks_) cudaFree(c.p);
 }
@@ -31,7 +48,7 @@ Arena::~Arena() {
 void Arena::reset() {
   size_t cap = 0;
   for (auto& c : chunks_) cap += c.cap;
-  if (chunks_.size() > 1 || (chunks_.size() == 1 && chunks_[0].cap < high_)) {
+  if (!arena_tiny() && (chunks_.size() > 1 || (chunks_.size() == 1 && chunks_[0].cap < high_))) {
     for (auto& c : chunks_) cudaFree(c.p);
     chunks_.clear();
     Chunk c{nullptr, size_t(round_up(int64_t(high_), int64_t(1) << 20)), 0};
@@ -40,6 +57,9 @@ void Arena::reset() {
     ++gen_;
   }
   for (auto& c : chunks_) c.off = 0;
+  if (arena_poison() >= 0)
+    for (auto& c : chunks_) RSVD_CUDA(cudaMemset(c.p, arena_poison(), c.cap));
+  if (arena_poison() >= 0) RSVD_CUDA(cudaDeviceSynchronize());
   used_total_ = 0;
   (void)cap;
 }
@@ -47,14 +67,18 @@ void Arena::reset() {
 void* Arena::alloc_bytes(size_t bytes) {
   bytes = size_t(round_up(int64_t(std::max<size_t>(bytes, 1)), 256));
   if (chunks_.empty() || chunks_.back().off + bytes > chunks_.back().cap) {
-    size_t want = std::max<size_t>(bytes, size_t(64) << 20);
-    if (!chunks_.empty()) want = std::max(want, 2 * chunks_.back().cap);
+    size_t want = std::max<size_t>(bytes, arena_tiny() ? (size_t(256) << 10) : (size_t(64) << 20));
+    if (!chunks_.empty() && !arena_tiny()) want = std::max(want, 2 * chunks_.back().cap);
     Chunk c{nullptr, want, 0};
     cudaError_t e = cudaMalloc(&c.p, c.cap);
     if (e != cudaSuccess) {
       cudaGetLastError();
       c.cap = bytes;
       RSVD_CUDA(cudaMalloc(&c.p, c.cap));
+    }
+    if (arena_poison() >= 0) {
+      RSVD_CUDA(cudaMemset(c.p, arena_poison(), c.cap));
+      RSVD_CUDA(cudaDeviceSynchronize());
     }
     chunks_.push_back(c);
     ++gen_;
@@ -311,7 +335,7 @@ void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z) {
 Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda) {
   Problem P;
   P.A = DMat(const_cast<double*>(a), m, n, lda);
-  P.dist = h.nranks > 1;
+  P.dist = h.dist();
   shard_rows(h, m, &P.m_global, &P.row_off);
   return P;
 }

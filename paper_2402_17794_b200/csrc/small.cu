@@ -198,7 +198,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
   extern __shared__ double sm[];
   double* X = in_smem ? sm : gX;
   double* J = in_smem ? sm + int64_t(l) * l : gJ;
-  __shared__ int changed;
+  __shared__ int changed, big;  // any rotation / any above kJacobiQuad this sweep
   __shared__ int order[1024];
   __shared__ double nrm[1024];
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
@@ -221,7 +221,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
   // looping over rows).
   const bool warp_path = (l <= 32) && (nwarps >= lp / 2);
   for (; warp_path && sweep < 60; ++sweep) {
-    if (tid == 0) changed = 0;
+    if (tid == 0) changed = big = 0;
     __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
       const int pr = warp;
@@ -263,16 +263,19 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
             J[pcol * l + lane] = c * jp - sn * jq;
             J[qcol * l + lane] = sn * jp + c * jq;
           }
-          if (lane == 0) changed = 1;
+          if (lane == 0) {
+            changed = 1;
+            if (ga * ga > kJacobiQuad2 * (al * be)) big = 1;
+          }
         }
       }
       __syncthreads();
     }
-    if (!changed) break;
+    if (!changed || !big) break;
     __syncthreads();
   }
   for (; !warp_path && sweep < 60; ++sweep) {
-    if (tid == 0) changed = 0;
+    if (tid == 0) changed = big = 0;
     __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
       // circle method: slot 0 fixed, others rotate
@@ -317,12 +320,15 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
             J[pcol * l + i] = c * jp - s * jq;
             J[qcol * l + i] = s * jp + c * jq;
           }
-          if (gl == 0) changed = 1;
+          if (gl == 0) {
+            changed = 1;
+            if (ga * ga > kJacobiQuad2 * (al * be)) big = 1;
+          }
         }
       }
       __syncthreads();
     }
-    if (!changed) break;
+    if (!changed || !big) break;
     __syncthreads();
   }
   if (sweep >= 60 && tid == 0) atomicOr(flags, kFlagJacobiNoConv);
@@ -1125,7 +1131,7 @@ void tsqr(Handle& h, const DMat& X, DMat Q, DMat* R, bool dist) {
   const int l = int(X.cols);
   std::vector<TsqrLevel> lv;
   DMat Rloc = tsqr_factor(h, X, lv);
-  if (!dist || h.nranks <= 1) {
+  if (!dist || !h.dist()) {
     if (R) copy(h, Rloc, *R);
     tsqr_form(h, lv, l, nullptr, 0, Q);
     return;

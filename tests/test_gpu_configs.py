@@ -64,6 +64,9 @@ def test_config_parity(config):
     k = cfg["k"]
     rel = np.max(np.abs(s[:k] - so[:k]) / np.abs(so[:k]))
     assert rel < SIG_TOL, f"{config}: top-k relative error {rel:.3e}"
-    assert sin_max(u[:, :k], uo[:, :k]) < ANG_TOL
+    ang = sin_max(u[:, :k], uo[:, :k])
+    orth = float(np.abs(u.T @ u - np.eye(u.shape[1])).max())
+    orth_o = float(np.abs(uo.T @ uo - np.eye(uo.shape[1])).max())
+    assert ang < ANG_TOL, f"{config}: U angle {ang:.3e} (orth gpu {orth:.1e}, oracle {orth_o:.1e})"
     if v is not None:
         assert sin_max(v[:, :k], vo[:, :k]) < ANG_TOL

@@ -81,6 +81,23 @@ def test_gaussian_long_stream_jump_ahead(eng, orc, n, l, seed):
     assert so.has_cached == r_g.state.has_cached
 
 
+def test_gaussian_stream_after_mixed_lengths(eng, orc):
+    """The jump tables are cached per handle and per segment length: streams of
+    other lengths (and so other segment schedules) in between must not change
+    a later stream (the C2 sketch 8192 x 25 seed 1 is checked before and after)."""
+    def check(n, l, seed):
+        r_g, r_o = eng.Rng(seed), orc.Rng(seed)
+        g = eng.gaussian(n, l, r_g)
+        o = orc.gaussian(n, l, r_o)
+        assert (g != o).mean() <= 3e-3, f"{n}x{l} seed {seed}: {(g != o).sum()} entries differ"
+        so = r_o.get_state()
+        assert so.pos == r_g.state.pos and list(so.mt) == list(r_g.state.mt)
+    for n, l, seed in [(8192, 25, 1), (100000, 25, 3), (333333, 7, 11), (8192, 25, 1),
+                       (4097, 11, 12345), (100000, 25, 3), (8192, 25, 1), (1000, 25, 7),
+                       (8192, 25, 1)]:
+        check(n, l, seed)
+
+
 def test_gaussian_consecutive_calls_carry_cached_variate(eng, orc):
     """Alg 6 draws Omega_c then Psi from one Rng (singlepass.hpp:119-120)."""
     r_g, r_o = eng.Rng(8), orc.Rng(8)
@@ -112,6 +129,24 @@ def test_apply_and_adjoint_match_fp64_gemm(eng, m, n, l):
     tol = 1e-13 * np.sqrt(max(n, m))
     assert np.max(np.abs(ya - ref_y)) <= tol * np.max(np.abs(ref_y)) + 1e-300
     assert np.max(np.abs(za - ref_z)) <= tol * np.max(np.abs(ref_z)) + 1e-300
+
+
+def test_call_waits_for_inputs_queued_on_default_stream(eng):
+    """The engine runs on its own non-blocking stream when the caller is on the
+    legacy default stream: it must still wait for the caller's queued kernels
+    that produce its inputs (here a ~30 ms cuBLAS product issued right before
+    the call)."""
+    import torch
+    torch.cuda.synchronize()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    b = torch.randn(6144, 6144, dtype=torch.float64, device="cuda", generator=g)
+    x = torch.randn(25, 6144, dtype=torch.float64, device="cuda", generator=g).t()
+    torch.cuda.synchronize()
+    assert torch.cuda.current_stream().cuda_stream == 0
+    a = b @ b  # asynchronous on the default stream
+    y = eng.apply(a, x)
+    ref = a @ x
+    assert float((y - ref).abs().max() / ref.abs().max()) < 1e-13
 
 
 def test_pass_is_bitwise_deterministic(eng):
