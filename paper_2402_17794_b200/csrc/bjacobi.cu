@@ -72,6 +72,7 @@ struct BJProblem {
   double* X;
   double* Jm;
   int* changed;  // kBJMaxSweeps + 2 ints
+  unsigned long long* smax;  // per sweep: largest g^2/(a b) of the fresh Grams (bits)
 };
 struct BJBatch {
   BJProblem p[2];
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
   __shared__ int colmap[kBJW];
   __shared__ double rc[kBJW / 2], rs[kBJW / 2];
   __shared__ int rp[kBJW / 2], rq[kBJW / 2];
-  __shared__ int any_first, any_inner, any_visit, graded, big;
+  __shared__ int any_first, any_inner, any_visit, graded;
+  __shared__ double vmaxw[32];  // per warp: largest g^2/(a b) of this visit's Gram
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r8 = lane >> 2, c4 = lane & 3;
   const int nbp = nb + (nb & 1);
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
         const int wI = min(kBJ, l - I * kBJ), wK = min(kBJ, l - K * kBJ);
         const int w = wI + wK;
         if (tid < kBJW) colmap[tid] = (tid < wI) ? I * kBJ + tid : (tid < w ? K * kBJ + (tid - wI) : -1);
-        if (tid == 0) any_first = any_visit = big = 0;
+        if (tid == 0) any_first = any_visit = 0;
         __syncthreads();
         // ---- panel load (zero padded to kBJW columns x ldp rows)
         // warp w: columns w and w + 16, lanes along rows, 4 loads in flight
@@ -172,14 +174,18 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
           }
           graded = (gmin < graded_ratio * gmax) ? 1 : 0;
         }
-        // any relative off-diagonal above kJacobiQuad in the fresh Gram?
-        // (bit 1 of changed[sweep]; no such entry in a whole sweep = converged)
-        for (int e = tid; e < kBJW * kBJW; e += blockDim.x) {
-          const int i = e % kBJW, j = e / kBJW;
-          if (i < j && j < w) {
-            const double gij = G[i + kGL * j];
-            if (gij * gij > kJacobiQuad2 * (G[i + kGL * i] * G[j + kGL * j])) big = 1;
+        // largest relative off-diagonal of the fresh Gram (sweep stopping rule)
+        {
+          double vm = 0.0;
+          for (int e = tid; e < kBJW * kBJW; e += blockDim.x) {
+            const int i = e % kBJW, j = e / kBJW;
+            if (i < j && j < w) {
+              const double gij = G[i + kGL * j], dd = G[i + kGL * i] * G[j + kGL * j];
+              if (dd > 0.0) vm = fmax(vm, (gij * gij) / dd);
+            }
           }
+          for (int o = 16; o > 0; o >>= 1) vm = fmax(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+          if (lane == 0) vmaxw[warp] = vm;
         }
         __syncthreads();
         const int wp = w + (w & 1), np2 = wp / 2;
@@ -363,17 +369,34 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
             }
           }
         }
+        if (tid == 0 && any_first) atomicOr(&changed[sweep], 1);
         // graded panels' Gram entries carry absolute rounding: no early stop
-        if (tid == 0 && any_first) atomicOr(&changed[sweep], (big || graded) ? 3 : 1);
+        if (tid == 0) {
+          double vm = 1.0;
+          if (!graded) {
+            vm = 0.0;
+            for (int wi = 0; wi < int(blockDim.x >> 5); ++wi) vm = fmax(vm, vmaxw[wi]);
+          }
+          atomicMax(&batch.p[prob].smax[sweep], static_cast<unsigned long long>(__double_as_longlong(vm)));
+        }
         __syncthreads();
         mark(3);
       }
       grid.sync();
       mark(4);
     }
-    // done: no rotation, or none above kJacobiQuad (bit 1) in this sweep
-    if (!done0) done0 = (*reinterpret_cast<volatile int*>(&batch.p[0].changed[sweep]) & 2) == 0;
-    if (!done1) done1 = (*reinterpret_cast<volatile int*>(&batch.p[1].changed[sweep]) & 2) == 0;
+    // done: no rotation in this sweep, or the quadratic-regime stop
+    auto conv = [&](const BJProblem& P) {
+      if (*reinterpret_cast<volatile int*>(&P.changed[sweep]) == 0) return true;
+      if (sweep == 0) return false;
+      const double mk = __longlong_as_double(static_cast<long long>(
+          *reinterpret_cast<volatile unsigned long long*>(&P.smax[sweep])));
+      const double mp = __longlong_as_double(static_cast<long long>(
+          *reinterpret_cast<volatile unsigned long long*>(&P.smax[sweep - 1])));
+      return jacobi_quad_stop(mk, mp);
+    };
+    if (!done0) done0 = conv(batch.p[0]);
+    if (!done1) done1 = conv(batch.p[1]);
     if (done0 && done1) {
       if (probe && blockIdx.x == 0 && threadIdx.x == 0)
         for (int i = 0; i < 6; ++i) probe[i] = pt[i];
@@ -577,6 +600,7 @@ namespace {
 struct BJWork {
   double *X, *Jm, *nrm;
   int *order, *changed, *nzero;
+  unsigned long long* smax;
 };
 
 BJWork bj_prepare(Handle& h, const DMat& Rm) {
@@ -586,9 +610,11 @@ BJWork bj_prepare(Handle& h, const DMat& Rm) {
   w.Jm = h.ws.alloc(int64_t(l) * l);
   w.nrm = h.ws.alloc(l);
   w.order = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(l) * 4 + 16));
-  w.changed = reinterpret_cast<int*>(h.ws.alloc_bytes((kBJMaxSweeps + 2) * 4));
+  const size_t cb = size_t(kBJMaxSweeps + 2) * 4, mb = size_t(kBJMaxSweeps) * 8;
+  w.changed = reinterpret_cast<int*>(h.ws.alloc_bytes(cb + mb));  // 256-byte aligned
   w.nzero = w.changed + kBJMaxSweeps + 1;
-  RSVD_CUDA(cudaMemsetAsync(w.changed, 0, (kBJMaxSweeps + 2) * 4, h.stream));
+  w.smax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(w.changed) + cb);
+  RSVD_CUDA(cudaMemsetAsync(w.changed, 0, cb + mb, h.stream));
   bj_init_kernel<<<std::max(1, std::min(4 * h.sm_count, (l * l + 255) / 256)), 256, 0, h.stream>>>(
       Rm.p, Rm.ld, l, w.X, w.Jm);
   RSVD_LAUNCHED(h);
@@ -628,7 +654,7 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
   batch.nprob = nprob;
   for (int q = 0; q < 2; ++q) {
     const BJWork& w = work[q < nprob ? q : 0];
-    batch.p[q] = BJProblem{w.X, w.Jm, w.changed};
+    batch.p[q] = BJProblem{w.X, w.Jm, w.changed, w.smax};
   }
   int nbv = nb, lv = l, ldpv = ldp;
   // one inner sweep per visit: more inner sweeps do not reduce the outer sweep
@@ -659,8 +685,13 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
   if (probe_on) {
     cudaEventRecord(pe1, h.stream);
     int hc[kBJMaxSweeps + 1];
+    double hm[kBJMaxSweeps];
     RSVD_CUDA(cudaMemcpyAsync(hc, work[0].changed, sizeof hc, cudaMemcpyDeviceToHost, h.stream));
+    RSVD_CUDA(cudaMemcpyAsync(hm, work[0].smax, sizeof hm, cudaMemcpyDeviceToHost, h.stream));
     RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    std::fprintf(stderr, "bjacobi max rel g per sweep:");
+    for (int i = 0; i < kBJMaxSweeps && hm[i] > 0.0; ++i) std::fprintf(stderr, " %.1e", std::sqrt(hm[i]));
+    std::fprintf(stderr, "\n");
     float ms = 0;
     cudaEventElapsedTime(&ms, pe0, pe1);
     int sw = 0;

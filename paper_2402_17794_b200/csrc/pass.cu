@@ -413,12 +413,20 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
           for (int i2 = 0; i2 < WMT; ++i2) dx[i2 * 32] = xacc[i2];
         }
       }
-      ptx::fence_acq_rel_gpu();  // release the partial before the ticket
+      // Ticket: the consumer warps' partial stores are ordered before thread
+      // 0's GPU-scope fence by the CTA barrier (cumulativity), so ONE fence
+      // releases them all; the last arriver's thread 0 fences again (acquire)
+      // before the barrier that releases its CTA to read the other partials.
+      // (Every thread fencing cost ~10 us per small pass: measured on C1.)
       ptx::named_bar(1, NCT);
-      if (tid == 0) *flag = (atomicAdd(&p.counters[t], 1) == nseg - 1);
+      if (tid == 0) {
+        ptx::fence_acq_rel_gpu();
+        const bool last = (atomicAdd(&p.counters[t], 1) == nseg - 1);
+        if (last) ptx::fence_acq_rel_gpu();
+        *flag = last;
+      }
       ptx::named_bar(1, NCT);
       if (*flag) {
-        ptx::fence_acq_rel_gpu();  // acquire the other segments' partials
         // Sum every segment's partial (this CTA's own included, re-read from
         // where it was just written) in segment order: deterministic.
         if (warp_live) {

@@ -194,11 +194,13 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
                                   double* __restrict__ Jout, int64_t ldj,
                                   double* __restrict__ Wout, int64_t ldw,
                                   double* __restrict__ sigma, double* gX, double* gJ,
-                                  int in_smem, int* flags) {
+                                  int in_smem, int* flags, double* dbg = nullptr) {
   extern __shared__ double sm[];
+  __shared__ double wmax_s[32];  // per warp: largest g^2/(a b) met this sweep
+  double m_prev = 1.0;           // previous sweep's maximum (identical in all threads)
   double* X = in_smem ? sm : gX;
   double* J = in_smem ? sm + int64_t(l) * l : gJ;
-  __shared__ int changed, big;  // any rotation / any above kJacobiQuad this sweep
+  __shared__ int changed;  // any rotation this sweep
   __shared__ int order[1024];
   __shared__ double nrm[1024];
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
@@ -221,7 +223,9 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
   // looping over rows).
   const bool warp_path = (l <= 32) && (nwarps >= lp / 2);
   for (; warp_path && sweep < 60; ++sweep) {
-    if (tid == 0) changed = big = 0;
+    if (tid == 0) changed = 0;
+    // running max of g^2/(a b) as a fraction num/den (no division per round)
+    double mnum = 0.0, mden = 1.0;
     __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
       const int pr = warp;
@@ -250,6 +254,10 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
         // rotation from two reciprocal square roots (no sqrt/div on the chain):
         // ir = 1/r, r = |(d, 2g)|; cos 2th = |d|/r; c = sqrt(h), h = (1+cos 2th)/2;
         // s = sgn(d) sin 2th / (2c) = sgn(d) g ir / sqrt(h)  (c^2 + s^2 = 1)
+        if (ga * ga * mden > mnum * (al * be)) {
+          mnum = ga * ga;
+          mden = al * be;
+        }
         if (ga * ga > tol * tol * (al * be) && ga != 0.0) {
           const double d = be - al, g2 = 2.0 * ga;
           const double ir = rsqrt(fma(d, d, g2 * g2));
@@ -263,19 +271,24 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
             J[pcol * l + lane] = c * jp - sn * jq;
             J[qcol * l + lane] = sn * jp + c * jq;
           }
-          if (lane == 0) {
-            changed = 1;
-            if (ga * ga > kJacobiQuad2 * (al * be)) big = 1;
-          }
+          if (lane == 0) changed = 1;
         }
       }
       __syncthreads();
     }
-    if (!changed || !big) break;
+    if (lane == 0) wmax_s[warp] = mden > 0.0 ? mnum / mden : 0.0;
+    __syncthreads();
+    double m_k = 0.0;
+    for (int w = 0; w < nwarps; ++w) m_k = fmax(m_k, wmax_s[w]);
+    if (dbg && tid == 0 && sweep < 30) dbg[1 + sweep] = sqrt(m_k);
+    if (dbg && tid == 0) dbg[0] = sweep + 1;
+    if (!changed || (sweep > 0 && jacobi_quad_stop(m_k, m_prev))) break;
+    m_prev = m_k;
     __syncthreads();
   }
   for (; !warp_path && sweep < 60; ++sweep) {
-    if (tid == 0) changed = big = 0;
+    if (tid == 0) changed = 0;
+    double mnum = 0.0, mden = 1.0;
     __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
       // circle method: slot 0 fixed, others rotate
@@ -306,6 +319,10 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
         al = group_sum<GS>(al);  // all lanes participate (full-mask shuffles)
         be = group_sum<GS>(be);
         ga = group_sum<GS>(ga);
+        if (act && ga * ga * mden > mnum * (al * be)) {
+          mnum = ga * ga;
+          mden = al * be;
+        }
         if (act && fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
           // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
           // rewritten with one division and one square root
@@ -320,15 +337,21 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
             J[pcol * l + i] = c * jp - s * jq;
             J[qcol * l + i] = s * jp + c * jq;
           }
-          if (gl == 0) {
-            changed = 1;
-            if (ga * ga > kJacobiQuad2 * (al * be)) big = 1;
-          }
+          if (gl == 0) changed = 1;
         }
       }
       __syncthreads();
     }
-    if (!changed || !big) break;
+    {
+      double mw = mden > 0.0 ? mnum / mden : 0.0;
+      for (int o = 16; o > 0; o >>= 1) mw = fmax(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+      if (lane == 0) wmax_s[warp] = mw;
+    }
+    __syncthreads();
+    double m_k = 0.0;
+    for (int w = 0; w < nwarps; ++w) m_k = fmax(m_k, wmax_s[w]);
+    if (!changed || (sweep > 0 && jacobi_quad_stop(m_k, m_prev))) break;
+    m_prev = m_k;
     __syncthreads();
   }
   if (sweep >= 60 && tid == 0) atomicOr(flags, kFlagJacobiNoConv);
@@ -1342,14 +1365,21 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
     ensure_smem(jacobi_svd_kernel<8>, dyn, cur_j8);
     // l <= 32: one warp per column pair (the kernel's register path)
     const int thr = (l <= 32) ? 32 * pairs : std::max(32, int(round_up(8 * pairs, 32)));
-    jacobi_svd_kernel<8><<<1, thr, dyn, h.stream>>>(Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
-                                                    gX, gJ, in_smem ? 1 : 0, h.d_flags);
     static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
+    double* dbg = nullptr;
     if (probe_on) {
-      int sw = 0;
-      RSVD_CUDA(cudaMemcpyAsync(&sw, h.d_flags + 8, 4, cudaMemcpyDeviceToHost, h.stream));
+      dbg = h.ws.alloc(32);
+      RSVD_CUDA(cudaMemsetAsync(dbg, 0, 32 * 8, h.stream));
+    }
+    jacobi_svd_kernel<8><<<1, thr, dyn, h.stream>>>(Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
+                                                    gX, gJ, in_smem ? 1 : 0, h.d_flags, dbg);
+    if (probe_on) {
+      double hd[32];
+      RSVD_CUDA(cudaMemcpyAsync(hd, dbg, sizeof hd, cudaMemcpyDeviceToHost, h.stream));
       RSVD_CUDA(cudaStreamSynchronize(h.stream));
-      std::fprintf(stderr, "jacobi_svd l=%d sweeps=%d\n", l, sw);
+      std::fprintf(stderr, "jacobi_svd l=%d sweeps=%d max rel g per sweep:", l, int(hd[0]));
+      for (int i = 1; i <= int(hd[0]) && i < 31; ++i) std::fprintf(stderr, " %.1e", hd[i]);
+      std::fprintf(stderr, "\n");
     }
   } else {
     static size_t cur_j = 0;

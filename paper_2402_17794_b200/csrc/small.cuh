@@ -51,13 +51,18 @@ void sym_part(Handle& h, const DMat& A, DMat C);
 // Set device flag if any entry of X is not finite.
 void check_finite(Handle& h, const DMat& X, int flag_bit);
 
-// Quadratic-convergence stop of the cyclic Jacobi sweeps: a sweep in which no
-// pair's relative inner product |g| / sqrt(a b) exceeded kJacobiQuad leaves
-// off-diagonal terms of order kJacobiQuad^2 (cyclic Jacobi converges
-// quadratically, also with multiple singular values), far below the rotation
-// threshold, so the next sweep would not rotate: it is skipped instead of run
-// as a rotation-free confirmation sweep (C1: 7 -> 6 sweeps).
-constexpr double kJacobiQuad2 = 1e-22;  // kJacobiQuad = 1e-11, squared
+// Quadratic-convergence stop of the cyclic Jacobi sweeps.  e_k = the largest
+// relative inner product |g| / sqrt(a b) met in sweep k.  Once the sweeps are
+// in the quadratic regime (e_k <= 100 e_{k-1}^2) and e_k <= 1e-7, the next
+// sweep would meet terms ~100 e_k^2 <= 1e-12 relative at most (measured on
+// the C1 / C2 Stage-2 factors: e = .., 4.3e-4, 1.8e-8, 9.4e-16 and
+// .., 2.2e-3, 1.2e-9, 1.1e-15): it is skipped instead of run as a
+// (near) rotation-free confirmation sweep.  Compared in squares.
+constexpr double kJacobiStop2 = 1e-14;   // (1e-7)^2
+constexpr double kJacobiQuadK2 = 1e4;    // 100^2
+__host__ __device__ inline bool jacobi_quad_stop(double m_k, double m_prev) {
+  return m_k <= kJacobiStop2 && m_k <= kJacobiQuadK2 * m_prev * m_prev;
+}
 
 enum FlagBits : int {
   kFlagNonFinite = 1,
