@@ -71,14 +71,55 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
 // the counter deltas recorded at capture.  Calls that synchronize with the
 // host mid-way (large-l shift decisions) fail to capture and stay eager.
 // Disabled with RSVD_GRAPHS=0, under profiling/tracing, and with NCCL.
+// A device output of a graph-cached call: the graph writes a staging buffer
+// in the workspace (stable across replays), copied to the caller's pointer
+// after every launch -- so the cache key does not depend on where the caller
+// put this call's outputs (fresh output tensors every call would otherwise
+// miss the cache and re-capture).
+struct OutBuf {
+  double* user;
+  int64_t rows, cols, ld;
+};
+
+// (rows x cols) view of a staging buffer allocated with >= 1 row / column
+rsvdb::DMat sub_view(const rsvdb::DMat& st, int64_t rows, int64_t cols) {
+  return rsvdb::DMat(st.p, rows, cols, st.ld);
+}
+
+void stage_alloc(rsvdb::Handle& h, const std::vector<OutBuf>& outs) {
+  h.stage.clear();
+  for (const OutBuf& o : outs) h.stage.push_back(h.ws.mat(std::max<int64_t>(o.rows, 1), std::max<int64_t>(o.cols, 1)));
+}
+
+void stage_copy_out(rsvdb::Handle& h, const std::vector<rsvdb::DMat>& st, const std::vector<OutBuf>& outs) {
+  for (size_t i = 0; i < outs.size(); ++i) {
+    const OutBuf& o = outs[i];
+    if (o.rows <= 0 || o.cols <= 0 || !o.user) continue;
+    RSVD_CUDA(cudaMemcpy2DAsync(o.user, size_t(o.ld) * 8, st[i].p, size_t(st[i].ld) * 8, size_t(o.rows) * 8,
+                                size_t(o.cols), cudaMemcpyDeviceToDevice, h.stream));
+  }
+}
+
 template <class F>
 rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& key,
-                        rsvd_rng_state* rng, F&& f) {
+                        rsvd_rng_state* rng, F&& f, const std::vector<OutBuf>& outs = {}) {
+  // eager form: outputs through the same staging as the graph
+  auto check_outs = [&] {
+    for (const OutBuf& o : outs)
+      if (o.rows > 0 && o.cols > 0 && o.ld < o.rows)
+        throw rsvdb::Error(RSVD_ERR_DIMENSION, "leading dimension < rows");
+  };
+  auto eager = [&](rsvdb::Handle& h) {
+    check_outs();
+    stage_alloc(h, outs);
+    f(h);
+    stage_copy_out(h, h.stage, outs);
+  };
   static const bool env_on = [] {
     const char* e = std::getenv("RSVD_GRAPHS");
     return !(e && e[0] == '0');
   }();
-  if (!hd || !env_on || !hd->h.graphs || hd->h.trace || hd->h.dist()) return guard(hd, what, f);
+  if (!hd || !env_on || !hd->h.graphs || hd->h.trace || hd->h.dist()) return guard(hd, what, eager);
   rsvdb::Handle& h = hd->h;
   auto add = [](rsvd_counters& a, const rsvd_counters& d, int sgn) {
     a.apply += sgn * d.apply;
@@ -88,6 +129,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
   };
   try {
     RSVD_CUDA(cudaSetDevice(h.device));
+    check_outs();
     join_caller_stream(h);  // before any replay or capture on the stream
     auto gen_now = [&] { return h.generation + h.ws.generation(); };
     if (h.graph_cache.size() > 256 && !h.graph_cache.count(key)) {  // bound the cache
@@ -104,6 +146,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     if (e.exec && e.gen == gen_now()) {
       if (rng) std::memcpy(h.h_rng_in, rng, sizeof(rsvd_rng_state));
       RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
+      stage_copy_out(h, e.stage, outs);
       add(h.counters, e.delta, 1);
       h.prof_pending = e.prof;
       h.rng_user_out = rng;
@@ -128,6 +171,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
       bool ok = cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
       if (ok) {
         try {
+          stage_alloc(h, outs);
           f(h);
         } catch (...) {
           ok = false;
@@ -151,7 +195,9 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
           add(e.delta, before, -1);
           for (auto& r : h.prof_pending) r.graph = true;  // the graph keeps these events
           e.prof = h.prof_pending;
+          e.stage = h.stage;
           RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
+          stage_copy_out(h, e.stage, outs);
           h.rng_user_out = rng;
           rsvdb::finish_call(h, what);
           return RSVD_OK;
@@ -175,7 +221,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     cudaMemsetAsync(h.d_flags, 0, sizeof(int), h.stream);
     return err.code;
   }
-  return guard(hd, what, f);
+  return guard(hd, what, eager);
 }
 
 std::string graph_key(const char* fn, std::initializer_list<int64_t> v) {
@@ -456,28 +502,29 @@ rsvd_status rsvd_apply_adjoint_dev(rsvd_handle* hd, int64_t m, int64_t n, const 
 rsvd_status rsvd_range_basis_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a,
                                  int64_t lda, int64_t k, int64_t p, int q, int mode,
                                  rsvd_rng_state* rng, double* q_out, int64_t ldq) {
-  const std::string key = graph_key("range_basis", {m, n, pv(a), lda, k, p, q, mode, pv(q_out), ldq,
+  const int64_t lq = std::max<int64_t>(k + p, 0);
+  const std::string key = graph_key("range_basis", {m, n, pv(a), lda, k, p, q, mode,
                                                     rng ? rng->has_cached : -1});
   return guard_graph(hd, "range_basis", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
-    rsvdb::range_basis_impl(h, P, k, p, q, mode, r, dm(q_out, m, std::max<int64_t>(k + p, 0), ldq));
+    rsvdb::range_basis_impl(h, P, k, p, q, mode, r, sub_view(h.stage[0], m, lq));
     rsvdb::rng_download(h, r, rng);
-  });
+  }, {{q_out, m, lq, ldq}});
 }
 
 rsvd_status rsvd_rsvd_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
                           int64_t k, int64_t p, int q, int mode, rsvd_rng_state* rng, double* u,
                           int64_t ldu, double* sigma, double* v, int64_t ldv) {
-  const std::string key = graph_key("rsvd", {m, n, pv(a), lda, k, p, q, mode, pv(u), ldu, pv(sigma),
-                                             pv(v), ldv, rng ? rng->has_cached : -1});
+  const int64_t l = std::max<int64_t>(k + p, 0);
+  const std::string key = graph_key("rsvd", {m, n, pv(a), lda, k, p, q, mode, rng ? rng->has_cached : -1});
   return guard_graph(hd, "rsvd", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
-    const int64_t l = std::max<int64_t>(k + p, 0);
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
-    rsvdb::rsvd_impl(h, P, k, p, q, mode, r, dm(u, m, l, ldu), sigma, dm(v, n, l, ldv));
+    rsvdb::rsvd_impl(h, P, k, p, q, mode, r, sub_view(h.stage[0], m, l), h.stage[1].p,
+                     sub_view(h.stage[2], n, l));
     rsvdb::rng_download(h, r, rng);
-  });
+  }, {{u, m, l, ldu}, {sigma, l, 1, std::max<int64_t>(l, 1)}, {v, n, l, ldv}});
 }
 
 rsvd_status rsvd_rsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
@@ -502,17 +549,18 @@ rsvd_status rsvd_rsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* 
 rsvd_status rsvd_spevd_dev(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
                            int64_t p, rsvd_rng_state* rng, int check_symmetry, double* u,
                            int64_t ldu, double* lambda) {
-  const std::string key = graph_key("spevd", {n, pv(a), lda, k, p, check_symmetry, pv(u), ldu,
-                                              pv(lambda), rng ? rng->has_cached : -1});
+  const int64_t kk = std::max<int64_t>(k, 0);
+  const std::string key = graph_key("spevd", {n, pv(a), lda, k, p, check_symmetry,
+                                              rng ? rng->has_cached : -1});
   return guard_graph(hd, "spevd_hermitian", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, n, n, lda);
     // local rows: for a single GPU m_local == n
     P.A = dm(a, P.A.rows, n, lda);
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
-    rsvdb::spevd_impl(h, P, k, p, r, check_symmetry != 0,
-                      dm(u, P.A.rows, std::max<int64_t>(k, 0), ldu), lambda);
+    rsvdb::spevd_impl(h, P, k, p, r, check_symmetry != 0, sub_view(h.stage[0], P.A.rows, kk),
+                      h.stage[1].p);
     rsvdb::rng_download(h, r, rng);
-  });
+  }, {{u, n, kk, ldu}, {lambda, kk, 1, std::max<int64_t>(kk, 1)}});
 }
 
 rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
@@ -536,15 +584,15 @@ rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t
 rsvd_status rsvd_spsvd_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,
                            int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                            double* sigma, double* v, int64_t ldv) {
-  const std::string key = graph_key("spsvd", {m, n, pv(a), lda, k, p, pv(u), ldu, pv(sigma), pv(v),
-                                              ldv, rng ? rng->has_cached : -1});
+  const int64_t kk = std::max<int64_t>(k, 0);
+  const std::string key = graph_key("spsvd", {m, n, pv(a), lda, k, p, rng ? rng->has_cached : -1});
   return guard_graph(hd, "spsvd_general", key, rng, [&](rsvdb::Handle& h) {
     rsvdb::Problem P = rsvdb::make_problem(h, a, m, n, lda);
-    const int64_t kk = std::max<int64_t>(k, 0);
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
-    rsvdb::spsvd_impl(h, P, k, p, r, dm(u, m, kk, ldu), sigma, dm(v, n, kk, ldv));
+    rsvdb::spsvd_impl(h, P, k, p, r, sub_view(h.stage[0], m, kk), h.stage[1].p,
+                      sub_view(h.stage[2], n, kk));
     rsvdb::rng_download(h, r, rng);
-  });
+  }, {{u, m, kk, ldu}, {sigma, kk, 1, std::max<int64_t>(kk, 1)}, {v, n, kk, ldv}});
 }
 
 rsvd_status rsvd_spsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,

@@ -170,7 +170,10 @@ struct Handle {
     std::vector<ProfRec> prof;  // pass-timing events recorded inside the graph
     int seen = 0;
     bool bad = false;  // not capturable (host synchronization inside the call)
+    std::vector<DMat> stage;  // output staging the graph writes (copied out per call)
   };
+  // output staging of the current graph-cached call (see capi.cu guard_graph)
+  std::vector<DMat> stage;
   std::unordered_map<std::string, GraphEntry> graph_cache;
 };
 

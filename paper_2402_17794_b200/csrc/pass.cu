@@ -24,6 +24,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <string>
+#include <vector>
+#include <cstdio>
 
 #include "common.cuh"
 #include "pass.cuh"
@@ -91,6 +94,11 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -156,6 +164,8 @@ struct PassParams {
   int64_t ldc;
   double* partials;
   int* counters;
+  unsigned long long* probe;  // debug (RSVD_PROBE_PASS): 16 %globaltimer stamps per CTA
+  int defer;             // stream-K: partial tiles are summed by sk_reduce_kernel
 };
 
 __device__ __forceinline__ int64_t sk_begin(int c, const PassParams& p) {
@@ -286,6 +296,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
   const int offX0 = kb * 8;
   int64_t u = u0;
   int seg_local = 0;
+  unsigned long long* pr = (p.probe && tid == 0) ? p.probe + int64_t(blockIdx.x + blockIdx.y * gridDim.x +
+                                                                      blockIdx.z * gridDim.x * gridDim.y) * 16
+                                                 : nullptr;
+  if (pr) pr[0] = ptx::gtime();
   do {
     double acc[WMT][NT][2];
     double xacc[WMT], xacc2[WMT];  // two K-parity chains for the DFMA column
@@ -302,6 +316,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
       const int i = int(u - u0);
       const int s = i % STAGES;
       ptx::mbar_wait(&full[s], (i / STAGES) & 1);
+      if (pr && i == 0) pr[1] = ptx::gtime();
       const uint8_t* a_st = smem + s * Cfg::STAGE_BYTES;
       const uint8_t* b_st = a_st + Cfg::A_BYTES;
 #pragma unroll
@@ -347,6 +362,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
 
+    if (pr && seg_local < 4) pr[2 + 3 * seg_local] = ptx::gtime();
     // ---------------------------------------------- segment epilogue (tile t)
     if constexpr (XC == 1) {
       // the 4 lanes of a row hold disjoint K subsets: butterfly sum (identical
@@ -413,6 +429,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
           for (int i2 = 0; i2 < WMT; ++i2) dx[i2 * 32] = xacc[i2];
         }
       }
+      if (p.defer) {  // the separate reduction kernel sums this tile (stream-K)
+        if (pr && seg_local < 4) pr[3 + 3 * seg_local] = pr[4 + 3 * seg_local] = ptx::gtime();
+        ++seg_local;
+        continue;
+      }
       // Ticket: the consumer warps' partial stores are ordered before thread
       // 0's GPU-scope fence by the CTA barrier (cumulativity), so ONE fence
       // releases them all; the last arriver's thread 0 fences again (acquire)
@@ -426,6 +447,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
         *flag = last;
       }
       ptx::named_bar(1, NCT);
+      if (pr && seg_local < 4) pr[3 + 3 * seg_local] = ptx::gtime() | (*flag ? 1ull : 0ull);
       if (*flag) {
         // Sum every segment's partial (this CTA's own included, re-read from
         // where it was just written) in segment order: deterministic.
@@ -494,8 +516,94 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
         if (tid == 0) p.counters[t] = 0;  // self-reset for the next launch
       }
     }
+    if (pr && seg_local < 4) pr[4 + 3 * seg_local] = ptx::gtime();
     ++seg_local;
   } while (u < u1);
+  if (pr) pr[15] = ptx::gtime();
+}
+
+// Stream-K fixup as its own kernel: one CTA per output tile sums the tile's
+// segment partials in segment order (the order the in-kernel last-arriver
+// reduction used: bitwise the same result) and stores it.  Every partial of
+// every tile is loaded in parallel across CTAs instead of one round trip per
+// partial by the last-arriving CTA, and the pass kernel's CTAs never wait on
+// a ticket (measured with RSVD_PROBE_PASS on C1: ticket 2.1 us per segment,
+// in-kernel reduction 3.5-16 us, chained across consecutive tiles).
+template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW, bool kGroup>
+__global__ void __launch_bounds__(CW * 32) sk_reduce_kernel(PassParams p) {
+  using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
+  constexpr int BM = Cfg::BM, NT = Cfg::NT, NCOL = Cfg::NCOL, FRAG = Cfg::FRAG;
+  const int t = blockIdx.x;
+  const int tg = kGroup ? t / p.nsub : t, sub = kGroup ? t % p.nsub : 0;
+  const int c_first = sk_cta_of(int64_t(tg) * p.kb_tile, p);
+  const int c_last = sk_cta_of(int64_t(tg + 1) * p.kb_tile - 1, p);
+  const int nseg = c_last - c_first + 1;
+  if (nseg == 1) return;  // stored directly by the pass kernel
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r8 = lane >> 2, c4 = lane & 3, wm0 = warp * WMT * 8;
+  const int64_t m0 = int64_t(t / p.nt) * BM, n0 = int64_t(t % p.nt) * NCOL;
+  if (m0 + wm0 >= p.M) return;  // no rows of this warp in the tile
+  auto slot = [&](int sg) -> int64_t {
+    const int c2 = c_first + sg;
+    const int j2 = tg - int(sk_begin(c2, p) / p.kb_tile);
+    return int64_t(kGroup ? c2 * p.nsub + sub : c2) * p.max_seg + j2;
+  };
+  double acc[WMT][NT][2], xacc[WMT];
+#pragma unroll
+  for (int i2 = 0; i2 < WMT; ++i2) {
+    xacc[i2] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i2][j][0] = acc[i2][j][1] = 0.0;
+  }
+  constexpr int RU = 4;  // partials in flight per thread
+  for (int sg0 = 0; sg0 < nseg; sg0 += RU) {
+    double2 v[RU][WMT][NT];
+    double vx[RU][WMT];
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      const bool live = sg0 + r < nseg;
+      const int64_t sl = live ? slot(sg0 + r) : 0;
+      const double2* src =
+          reinterpret_cast<const double2*>(p.partials + sl * FRAG) + (warp * WMT * NT) * 32 + lane;
+#pragma unroll
+      for (int i2 = 0; i2 < WMT; ++i2) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          v[r][i2][j] = (live && n0 + j * 8 < p.N) ? __ldcg(src + (i2 * NT + j) * 32) : make_double2(0.0, 0.0);
+        vx[r][i2] = 0.0;
+        if constexpr (XC == 1)
+          if (live)
+            vx[r][i2] = __ldcg(p.partials + sl * FRAG + CW * WMT * NT * 64 + warp * WMT * 32 + lane + i2 * 32);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      if (sg0 + r >= nseg) break;
+#pragma unroll
+      for (int i2 = 0; i2 < WMT; ++i2) {
+        xacc[i2] += vx[r][i2];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          acc[i2][j][0] += v[r][i2][j].x;
+          acc[i2][j][1] += v[r][i2][j].y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i2 = 0; i2 < WMT; ++i2) {
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t m = m0 + wm0 + i2 * 8 + r8, n = n0 + j * 8 + 2 * c4 + e;
+        if (m < p.M && n < p.N) p.C[n * p.ldc + m] = acc[i2][j][e];
+      }
+    if constexpr (XC == 1) {
+      const int64_t m = m0 + wm0 + i2 * 8 + r8, n = n0 + NT * 8;
+      if (c4 == 0 && m < p.M && n < p.N) p.C[n * p.ldc + m] = xacc[i2];
+    }
+  }
 }
 
 // ------------------------------------------------------------- host side
@@ -537,6 +645,50 @@ bool tma_ok(const DMat& x) {
   return (reinterpret_cast<uintptr_t>(x.p) % 16 == 0) && (x.ld % 2 == 0) && x.ld >= x.rows;
 }
 
+// RSVD_PROBE_PASS: per-CTA %globaltimer stamps of one launch (debug):
+// entry, first stage arrival, per segment (main loop end, ticket, epilogue
+// end), exit; printed as percentiles over the CTAs, in microseconds.
+void probe_report(Handle& h, const unsigned long long* dprobe, int64_t nct, int64_t M, int64_t N,
+                  int64_t K, int stream_k) {
+  std::vector<unsigned long long> v(size_t(nct) * 16);
+  RSVD_CUDA(cudaMemcpyAsync(v.data(), dprobe, v.size() * 8, cudaMemcpyDeviceToHost, h.stream));
+  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  unsigned long long t0 = ~0ull, t1 = 0;
+  for (int64_t c = 0; c < nct; ++c) {
+    t0 = std::min(t0, v[size_t(c) * 16]);
+    t1 = std::max(t1, v[size_t(c) * 16 + 15]);
+  }
+  std::vector<double> entry, first, loop0, tick, red_last, red_other, exitv;
+  for (int64_t c = 0; c < nct; ++c) {
+    const unsigned long long* r = &v[size_t(c) * 16];
+    entry.push_back((r[0] - t0) * 1e-3);
+    first.push_back((r[1] - r[0]) * 1e-3);
+    exitv.push_back((r[15] - t0) * 1e-3);
+    for (int sg = 0; sg < 4; ++sg) {
+      const unsigned long long le = r[2 + 3 * sg], tk = r[3 + 3 * sg], ee = r[4 + 3 * sg];
+      if (!le) break;
+      if (sg == 0) loop0.push_back((le - r[1]) * 1e-3);
+      if (tk) {
+        tick.push_back(((tk & ~1ull) - le) * 1e-3);
+        ((tk & 1ull) ? red_last : red_other).push_back((ee - (tk & ~1ull)) * 1e-3);
+      }
+    }
+  }
+  auto pct = [](std::vector<double> x) {
+    if (x.empty()) return std::string("-");
+    std::sort(x.begin(), x.end());
+    char b[96];
+    std::snprintf(b, sizeof b, "%.2f/%.2f/%.2f", x[x.size() / 10], x[x.size() / 2], x.back());
+    return std::string(b);
+  };
+  std::fprintf(stderr,
+               "pass M=%lld N=%lld K=%lld ctas=%lld sk=%d span %.2f us | entry %s | first-data %s | "
+               "loop0 %s | ticket %s | reduce(last) %s n=%zu | epi(other) %s | exit %s  (p10/p50/max)\n",
+               (long long)M, (long long)N, (long long)K, (long long)nct, stream_k, (t1 - t0) * 1e-3,
+               pct(entry).c_str(), pct(first).c_str(), pct(loop0).c_str(), pct(tick).c_str(),
+               pct(red_last).c_str(), red_last.size(), pct(red_other).c_str(), pct(exitv).c_str());
+}
+
 template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC = 0, int CW = 8>
 void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t N, int64_t K,
             int force_splits) {
@@ -573,6 +725,7 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
   // Few tiles (C1/C2 passes, Gram products): stream-K over all SMs.  Many
   // tiles: split-K grid with n-tiles adjacent for L2 reuse of A.
   const bool stream_k = force_splits <= 0 && tiles < 2 * sms;
+  bool split_tiles = false;
   if (stream_k) {
     // n-tiles of one m-tile go to nt adjacent CTAs walking the same unit range
     // (A read once from DRAM; measured 2.44x the algorithmic bytes on C3's
@@ -580,11 +733,11 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     const int64_t nsub = (nt > 1 && nt <= sms) ? nt : 1;
     const int64_t units = (tiles / nsub) * kblocks;
     // one CTA per tile at least (short-K products: no partials at all), and
-    // >= 8 K slices per CTA when tiles are few (bounds the partials a tile's
+    // >= 4 K slices per CTA when tiles are few (bounds the partials a tile's
     // last segment must reduce)
     static const int64_t min_slices = [] {
       const char* e = std::getenv("RSVD_SK_MIN_SLICES");
-      return int64_t(e ? std::max(1, std::atoi(e)) : 8);
+      return int64_t(e ? std::max(1, std::atoi(e)) : 4);
     }();
     const int64_t g = std::max<int64_t>(
         1, std::min<int64_t>(sms / nsub, std::max<int64_t>(tiles / nsub, units / min_slices)));
@@ -596,7 +749,21 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     pp.splits = 1;
     pp.kb_split = int(kblocks);
     pp.partials = h.ws.alloc(g * nsub * pp.max_seg * FRAG);
-    pp.counters = tile_counters(h, tiles);
+    // partial tiles are summed by sk_reduce_kernel after the pass
+    // (RSVD_SK_INKERNEL=1: the last-arriving CTA sums them, ticket per tile)
+    static const bool inkernel = std::getenv("RSVD_SK_INKERNEL") != nullptr;
+    pp.defer = inkernel ? 0 : 1;
+    if (!pp.defer) pp.counters = tile_counters(h, tiles);
+    // any tile covered by more than one CTA (group)?  (host copy of sk_cta_of)
+    auto begin_of = [&](int64_t c) { return (c * units) / g; };
+    auto cta_of = [&](int64_t u) {
+      int64_t c = (u * g) / units;
+      while (c + 1 < g && begin_of(c + 1) <= u) ++c;
+      while (c > 0 && begin_of(c) > u) --c;
+      return c;
+    };
+    for (int64_t tg = 0; tg < tiles / nsub && !split_tiles; ++tg)
+      split_tiles = cta_of(tg * kblocks) != cta_of((tg + 1) * kblocks - 1);
     grid = dim3(unsigned(g * nsub), 1, 1);
   } else {
     int splits = 1;
@@ -654,11 +821,25 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     rec_flags = (cap == cudaStreamCaptureStatusActive) ? cudaEventRecordExternal : cudaEventRecordDefault;
     RSVD_CUDA(cudaEventRecordWithFlags(rec.a, h.stream, rec_flags));
   }
+  static const bool probe_pass = std::getenv("RSVD_PROBE_PASS") != nullptr;
+  const int64_t nct = int64_t(grid.x) * grid.y * grid.z;
+  if (probe_pass) {
+    pp.probe = reinterpret_cast<unsigned long long*>(h.ws.alloc_bytes(size_t(nct) * 16 * 8));
+    RSVD_CUDA(cudaMemsetAsync(pp.probe, 0, size_t(nct) * 16 * 8, h.stream));
+  }
   if (pp.stream_k && pp.nsub > 1)
     kernG<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
   else
     kern1<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
   RSVD_LAUNCHED(h);
+  if (pp.stream_k && pp.defer && split_tiles) {
+    if (pp.nsub > 1)
+      sk_reduce_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, true><<<unsigned(tiles), CW * 32, 0, h.stream>>>(pp);
+    else
+      sk_reduce_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, false><<<unsigned(tiles), CW * 32, 0, h.stream>>>(pp);
+    RSVD_LAUNCHED(h);
+  }
+  if (probe_pass) probe_report(h, pp.probe, nct, M, N, K, pp.stream_k);
   if (h.prof) {
     RSVD_CUDA(cudaEventRecordWithFlags(rec.b, h.stream, rec_flags));
     h.prof_pending.push_back(rec);
