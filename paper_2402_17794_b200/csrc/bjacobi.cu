@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
                                                             int nb, int inner_max,
                                                             double graded_ratio,
                                                             long long* __restrict__ probe) {
+  RSVD_PDL_ENTRY();
   long long pt[6] = {0, 0, 0, 0, 0, 0}, tlast = clock64();
   auto mark = [&](int ph) {
     if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -410,6 +411,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
 
 // column norms (sigma), stable descending order, permuted outputs
 __global__ void bj_norms_kernel(const double* __restrict__ X, int l, double* __restrict__ nrm) {
+  RSVD_PDL_ENTRY();
   const int c = blockIdx.x;
   double s = 0;
   for (int i = threadIdx.x; i < l; i += blockDim.x) s = fma(X[int64_t(c) * l + i], X[int64_t(c) * l + i], s);
@@ -426,6 +428,7 @@ __global__ void bj_norms_kernel(const double* __restrict__ X, int l, double* __r
 
 __global__ void bj_order_kernel(const double* __restrict__ nrm, int l, int* __restrict__ order,
                                 double* __restrict__ sigma) {
+  RSVD_PDL_ENTRY();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < l; j += gridDim.x * blockDim.x) {
     const double v = order_key(nrm[j]);
     int rank = 0;
@@ -442,6 +445,7 @@ __global__ void bj_permute_kernel(const double* __restrict__ X, const double* __
                                   const double* __restrict__ nrm, const int* __restrict__ order,
                                   int l, double* __restrict__ Jout, int64_t ldj,
                                   double* __restrict__ Wout, int64_t ldw, int* __restrict__ nzero) {
+  RSVD_PDL_ENTRY();
   const int jn = blockIdx.x;
   const int src = order[jn];
   const double smax = nrm[order[0]];
@@ -458,6 +462,7 @@ __global__ void bj_permute_kernel(const double* __restrict__ X, const double* __
 // candidate unit vectors, two Gram-Schmidt passes.  Runs only when needed.
 __global__ void bj_complete_kernel(const double* __restrict__ sigma, int l, double* __restrict__ W,
                                    int64_t ldw, const int* __restrict__ nzero) {
+  RSVD_PDL_ENTRY();
   if (*nzero == 0) return;
   const int lane = threadIdx.x;
   const double smax = sigma[0];
@@ -505,6 +510,7 @@ __global__ void bj_complete_kernel(const double* __restrict__ sigma, int l, doub
 
 __global__ void bj_init_kernel(const double* __restrict__ Rm, int64_t ldr, int l,
                                double* __restrict__ X, double* __restrict__ Jm) {
+  RSVD_PDL_ENTRY();
   const int64_t n = int64_t(l) * l;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -515,12 +521,14 @@ __global__ void bj_init_kernel(const double* __restrict__ Rm, int64_t ldr, int l
 }
 
 __global__ void bj_flag_kernel(const int* changed, int* flags) {
+  RSVD_PDL_ENTRY();
   if (changed[kBJMaxSweeps]) atomicOr(flags, kFlagJacobiNoConv);
 }
 
 // mu >= max_i sum_j |c_ij| >= |lambda|_max (Gershgorin): C + mu I is PSD.
 __global__ void gershgorin_kernel(const double* __restrict__ C, int64_t ldc, int l,
                                   double* __restrict__ mu) {
+  RSVD_PDL_ENTRY();
   __shared__ double red[32];
   double m = 0.0;
   for (int i = threadIdx.x; i < l; i += blockDim.x) {
@@ -541,6 +549,7 @@ __global__ void gershgorin_kernel(const double* __restrict__ C, int64_t ldc, int
 
 __global__ void shift_copy_kernel(const double* __restrict__ C, int64_t ldc, int l,
                                   const double* __restrict__ mu, double* __restrict__ T) {
+  RSVD_PDL_ENTRY();
   const int64_t n = int64_t(l) * l;
   const double m = *mu;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
@@ -557,6 +566,7 @@ __global__ void shift_copy_kernel(const double* __restrict__ C, int64_t ldc, int
 __global__ void rayleigh_kernel(const double* __restrict__ Jm, int64_t ldj,
                                 const double* __restrict__ CJ, int64_t ldc, int l,
                                 double* __restrict__ lam) {
+  RSVD_PDL_ENTRY();
   const int c = blockIdx.x;
   double s = 0.0;
   for (int i = threadIdx.x; i < l; i += blockDim.x) s = fma(Jm[int64_t(c) * ldj + i], CJ[int64_t(c) * ldc + i], s);
@@ -575,6 +585,7 @@ __global__ void rayleigh_kernel(const double* __restrict__ Jm, int64_t ldj,
 // ties: positive first (see evd_symmetric in small.cu / the oracle).
 __global__ void evd_order_kernel(const double* __restrict__ lam_in, int l,
                                  double* __restrict__ lambda, int* __restrict__ order) {
+  RSVD_PDL_ENTRY();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < l; j += gridDim.x * blockDim.x) {
     const double v0 = lam_in[j], v = (v0 != v0) ? 0.0 : v0, av = order_key(fabs(v0));
     int rank = 0;
@@ -590,6 +601,7 @@ __global__ void evd_order_kernel(const double* __restrict__ lam_in, int l,
 __global__ void evd_permute_kernel(const double* __restrict__ Jm, int64_t ldj, int l,
                                    const int* __restrict__ order, double* __restrict__ U,
                                    int64_t ldu) {
+  RSVD_PDL_ENTRY();
   const int jn = blockIdx.x, src = order[jn];
   for (int i = threadIdx.x; i < l; i += blockDim.x) U[int64_t(jn) * ldu + i] = Jm[int64_t(src) * ldj + i];
 }
@@ -615,23 +627,23 @@ BJWork bj_prepare(Handle& h, const DMat& Rm) {
   w.nzero = w.changed + kBJMaxSweeps + 1;
   w.smax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(w.changed) + cb);
   RSVD_CUDA(cudaMemsetAsync(w.changed, 0, cb + mb, h.stream));
-  bj_init_kernel<<<std::max(1, std::min(4 * h.sm_count, (l * l + 255) / 256)), 256, 0, h.stream>>>(
+  launch_k(h, bj_init_kernel, std::max(1, std::min(4 * h.sm_count, (l * l + 255) / 256)), 256, 0, 
       Rm.p, Rm.ld, l, w.X, w.Jm);
   RSVD_LAUNCHED(h);
   return w;
 }
 
 void bj_finish(Handle& h, const BJWork& w, int l, DMat J, DMat W, double* sigma) {
-  bj_flag_kernel<<<1, 1, 0, h.stream>>>(w.changed, h.d_flags);
+  launch_k(h, bj_flag_kernel, 1, 1, 0, w.changed, h.d_flags);
   RSVD_LAUNCHED(h);
-  bj_norms_kernel<<<l, 256, 0, h.stream>>>(w.X, l, w.nrm);
+  launch_k(h, bj_norms_kernel, l, 256, 0, w.X, l, w.nrm);
   RSVD_LAUNCHED(h);
-  bj_order_kernel<<<(l + 255) / 256, 256, 0, h.stream>>>(w.nrm, l, w.order, sigma);
+  launch_k(h, bj_order_kernel, (l + 255) / 256, 256, 0, w.nrm, l, w.order, sigma);
   RSVD_LAUNCHED(h);
-  bj_permute_kernel<<<l, 128, 0, h.stream>>>(w.X, w.Jm, w.nrm, w.order, l, J.p, J.ld, W.p, W.ld,
+  launch_k(h, bj_permute_kernel, l, 128, 0, w.X, w.Jm, w.nrm, w.order, l, J.p, J.ld, W.p, W.ld,
                                             w.nzero);
   RSVD_LAUNCHED(h);
-  bj_complete_kernel<<<1, 32, 0, h.stream>>>(sigma, l, W.p, W.ld, w.nzero);
+  launch_k(h, bj_complete_kernel, 1, 32, 0, sigma, l, W.p, W.ld, w.nzero);
   RSVD_LAUNCHED(h);
 }
 
@@ -732,10 +744,10 @@ void block_jacobi_svd2(Handle& h, const DMat& R0, DMat J0, DMat W0, double* s0, 
 void evd_shifted(Handle& h, const DMat& C, DMat U, double* lambda) {
   const int l = int(C.rows);
   double* mu = h.ws.alloc(1);
-  gershgorin_kernel<<<1, 256, 0, h.stream>>>(C.p, C.ld, l, mu);
+  launch_k(h, gershgorin_kernel, 1, 256, 0, C.p, C.ld, l, mu);
   RSVD_LAUNCHED(h);
   DMat T = h.ws.mat(l, l), Jm = h.ws.mat(l, l), W = h.ws.mat(l, l);
-  shift_copy_kernel<<<std::max(1, std::min(4 * h.sm_count, (l * l + 255) / 256)), 256, 0, h.stream>>>(
+  launch_k(h, shift_copy_kernel, std::max(1, std::min(4 * h.sm_count, (l * l + 255) / 256)), 256, 0, 
       C.p, C.ld, l, mu, T.p);
   RSVD_LAUNCHED(h);
   double* sg = h.ws.alloc(l);
@@ -744,11 +756,11 @@ void evd_shifted(Handle& h, const DMat& C, DMat U, double* lambda) {
   DMat CJ = h.ws.mat(l, l);
   gemm_nn(h, C, Jm, CJ);
   double* rq = h.ws.alloc(l);
-  rayleigh_kernel<<<l, 128, 0, h.stream>>>(Jm.p, Jm.ld, CJ.p, CJ.ld, l, rq);
+  launch_k(h, rayleigh_kernel, l, 128, 0, Jm.p, Jm.ld, CJ.p, CJ.ld, l, rq);
   RSVD_LAUNCHED(h);
-  evd_order_kernel<<<(l + 255) / 256, 256, 0, h.stream>>>(rq, l, lambda, order);
+  launch_k(h, evd_order_kernel, (l + 255) / 256, 256, 0, rq, l, lambda, order);
   RSVD_LAUNCHED(h);
-  evd_permute_kernel<<<l, 128, 0, h.stream>>>(Jm.p, Jm.ld, l, order, U.p, U.ld);
+  launch_k(h, evd_permute_kernel, l, 128, 0, Jm.p, Jm.ld, l, order, U.p, U.ld);
   RSVD_LAUNCHED(h);
 }
 

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kT) chol_blocked_kernel(const double* __restri
                                                          int64_t ldr, double* __restrict__ Rinv, int64_t ldri,
                                                          int* __restrict__ shift_used, int* __restrict__ flags,
                                                          int* __restrict__ status) {
+  RSVD_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   __shared__ double S0[kB * kLD], S1[kB * kLD], Rs[kB * kLD], Ri[kB * kLD], piv[2 * 72], orig[kB];
   __shared__ double red[kT / 32];

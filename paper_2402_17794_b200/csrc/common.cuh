@@ -5,6 +5,8 @@
 // and rethrown as rsvd::DimensionError / ParameterError / NumericError by
 // include/rsvd/*.hpp.
 #pragma once
+#include <cstdlib>
+#include <utility>
 
 #include <cuda_runtime.h>
 
@@ -176,6 +178,50 @@ struct Handle {
   std::vector<DMat> stage;
   std::unordered_map<std::string, GraphEntry> graph_cache;
 };
+
+// Programmatic dependent launch (PDL).  Every engine kernel starts with
+// RSVD_PDL_ENTRY(): griddepcontrol.wait (returns once the previous kernel in
+// the stream has completed and its writes are visible -- a no-op for a kernel
+// not launched as a dependent), then griddepcontrol.launch_dependents (the
+// next kernel's CTAs may now be scheduled and wait at their own entry).  With
+// the wait first in every kernel the stream order is unchanged; what overlaps
+// is the next kernel's launch and CTA rasterization with this kernel's run --
+// the inter-kernel gap of the latency-bound small-matrix chains.
+#ifdef __CUDACC__
+#define RSVD_PDL_ENTRY()                                   \
+  do {                                                     \
+    asm volatile("griddepcontrol.wait;" ::: "memory");     \
+    asm volatile("griddepcontrol.launch_dependents;" :::); \
+  } while (0)
+#endif
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RSVD_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+#ifdef __CUDACC__
+// Every non-cooperative engine launch: on the handle's stream, as a
+// programmatic dependent of the previous kernel (RSVD_PDL=0: plain launch).
+template <typename... KArgs, typename... Args>
+inline void launch_k(Handle& h, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  RSVD_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+#endif
 
 // End of a top-level call: synchronize, raise NumericError on device flags,
 // copy back a pending RNG state.

@@ -46,6 +46,7 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 // max_ij |G_ij - delta_ij|  (reference: (gram - I).cwiseAbs().maxCoeff())
 __global__ void dev_identity_kernel(const double* __restrict__ G, int64_t k, int64_t ld,
                                     double* out) {
+  RSVD_PDL_ENTRY();
   double v = 0.0;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < k * k;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(256) residual_lowrank_kernel(
     const double* __restrict__ A, int64_t lda, const double* __restrict__ Q, int64_t ldq,
     const double* __restrict__ Z, int64_t ldz, int64_t m, int64_t n, int64_t l,
     double* __restrict__ R, int64_t ldr) {
+  RSVD_PDL_ENTRY();
   __shared__ double Qs[kRK][kRT];      // Qs[k][row]
   __shared__ double Zs[kRT][kRK + 1];  // Zs[col][k]
   const int tid = threadIdx.x;
@@ -148,6 +150,7 @@ struct SnParams {
 
 // Power iteration of reference core.hpp:194-220, all iterations in one launch.
 __global__ void __launch_bounds__(kSnThreads) spectral_power_kernel(SnParams p) {
+  RSVD_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[kSnWarps + 2];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -288,6 +291,7 @@ __global__ void __launch_bounds__(kSnThreads) spectral_power_kernel(SnParams p) 
 
 // out[i] = clamp(sv[count - 1 - i], 0, 1): ascending sines (angles.hpp:53-57)
 __global__ void reverse_clamp01_kernel(const double* sv, int64_t count, double* out) {
+  RSVD_PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
        i += int64_t(gridDim.x) * blockDim.x)
     out[i] = fmin(fmax(sv[count - 1 - i], 0.0), 1.0);
@@ -297,6 +301,7 @@ __global__ void reverse_clamp01_kernel(const double* sv, int64_t count, double* 
 // CTA sums them in CTA order -- deterministic.
 __global__ void sumsq_partial_kernel(const double* __restrict__ A, int64_t m, int64_t n,
                                      int64_t lda, double* __restrict__ part) {
+  RSVD_PDL_ENTRY();
   __shared__ double sh[kSnWarps + 2];
   double s = 0.0;
   const int64_t total = m * n;
@@ -309,6 +314,7 @@ __global__ void sumsq_partial_kernel(const double* __restrict__ A, int64_t m, in
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 __global__ void sum_kernel(const double* __restrict__ part, int G, double* out) {
+  RSVD_PDL_ENTRY();
   __shared__ double sh[kSnWarps + 2];
   const double s = cta_fixed_sum(part, G, sh);
   if (threadIdx.x == 0) *out = s;
@@ -346,7 +352,7 @@ double gram_deviation(Handle& h, const DMat& G) {
   double* d = h.ws.alloc(1);
   RSVD_CUDA(cudaMemsetAsync(d, 0, sizeof(double), h.stream));
   const int blocks = int(std::min<int64_t>(ceil_div(k * k, 256), 2 * h.sm_count));
-  dev_identity_kernel<<<blocks, 256, 0, h.stream>>>(G.p, k, G.ld, d);
+  launch_k(h, dev_identity_kernel, blocks, 256, 0, G.p, k, G.ld, d);
   RSVD_LAUNCHED(h);
   return read_scalar(h, d);
 }
@@ -354,7 +360,7 @@ double gram_deviation(Handle& h, const DMat& G) {
 void residual_lowrank(Handle& h, const DMat& A, const DMat& Q, const DMat& Z, DMat R) {
   if (A.rows == 0 || A.cols == 0) return;
   dim3 grid(unsigned(ceil_div(A.rows, kRT)), unsigned(ceil_div(A.cols, kRT)));
-  residual_lowrank_kernel<<<grid, 256, 0, h.stream>>>(A.p, A.ld, Q.p, Q.ld, Z.p, Z.ld, A.rows,
+  launch_k(h, residual_lowrank_kernel, grid, 256, 0, A.p, A.ld, Q.p, Q.ld, Z.p, Z.ld, A.rows,
                                                        A.cols, Q.cols, R.p, R.ld);
   RSVD_LAUNCHED(h);
 }
@@ -363,9 +369,9 @@ double frobenius_impl(Handle& h, const DMat& M) {
   if (M.rows == 0 || M.cols == 0) return 0.0;
   const int G = int(std::min<int64_t>(ceil_div(M.rows * M.cols, 256), 4 * h.sm_count));
   double* part = h.ws.alloc(G + 1);
-  sumsq_partial_kernel<<<G, kSnThreads, 0, h.stream>>>(M.p, M.rows, M.cols, M.ld, part);
+  launch_k(h, sumsq_partial_kernel, G, kSnThreads, 0, M.p, M.rows, M.cols, M.ld, part);
   RSVD_LAUNCHED(h);
-  sum_kernel<<<1, kSnThreads, 0, h.stream>>>(part, G, part + G);
+  launch_k(h, sum_kernel, 1, kSnThreads, 0, part, G, part + G);
   RSVD_LAUNCHED(h);
   return std::sqrt(read_scalar(h, part + G));
 }
@@ -491,7 +497,7 @@ void canonical_sines_impl(Handle& h, const DMat& X, const DMat& Y, double* out) 
   double* sv = h.ws.alloc(std::max<int64_t>(r, 1));
   DMat U = h.ws.mat(Rs.rows, r), V = h.ws.mat(Rs.cols, r);
   svd_core(h, Rs, U, sv, V);
-  reverse_clamp01_kernel<<<unsigned(std::min<int64_t>(ceil_div(count, 256), 64)), 256, 0, h.stream>>>(
+  launch_k(h, reverse_clamp01_kernel, unsigned(std::min<int64_t>(ceil_div(count, 256), 64)), 256, 0, 
       sv, count, out);
   RSVD_LAUNCHED(h);
 }

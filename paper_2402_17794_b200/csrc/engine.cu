@@ -177,6 +177,7 @@ namespace {
 // (Eigen SVDBase::rank threshold as used by solve_ls, core.hpp:164-176).
 __global__ void pinv_rows_kernel(double* T, int64_t rows, int64_t cols, int64_t ld,
                                  const double* s) {
+  RSVD_PDL_ENTRY();
   const double thr = fmax(s[0] * 1e-12, DBL_MIN);
   const int64_t n = rows * cols;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
@@ -191,6 +192,7 @@ __global__ void pinv_rows_kernel(double* T, int64_t rows, int64_t cols, int64_t 
 // zero where sqrt(s1_i^2 + s2_j^2) < 1e-12 * sqrt(s1_0^2 + s2_0^2).
 __global__ void kron_core_kernel(const double* a, const double* b, int64_t l, int64_t lda,
                                  const double* s1, const double* s2, double* X, int64_t ldx) {
+  RSVD_PDL_ENTRY();
   const double smax = sqrt(s1[0] * s1[0] + s2[0] * s2[0]);
   const double thr = fmax(smax * 1e-12, DBL_MIN);
   const int64_t n = l * l;
@@ -226,6 +228,7 @@ __device__ __forceinline__ void asym_pair(int64_t t0, int64_t nt, int64_t& bi, i
 template <int T>
 __global__ void __launch_bounds__(256) asym_kernel(const double* __restrict__ A, int64_t n,
                                                    int64_t lda, double* out) {
+  RSVD_PDL_ENTRY();
   constexpr int CS = 256 / T;  // column stride between a thread's elements
   constexpr int E = T / CS;    // elements per thread per tile
   __shared__ double T2[T][T + 1];
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(256) asym_kernel(const double* __restrict__ A,
   }
 }
 __global__ void asym_flag_kernel(const double* mm, int* flags, int bit) {
+  RSVD_PDL_ENTRY();
   if (!(mm[1] <= 1e-8 * (1.0 + mm[0]))) atomicOr(flags, bit);
 }
 
@@ -307,14 +311,14 @@ void check_symmetric(Handle& h, const DMat& C, bool dist_unused) {
   if (tile_env == 32 || n < 1024) {
     const int64_t nt = ceil_div(n, 32);
     const int64_t grid = std::min<int64_t>(nt * (nt + 1) / 2, 8 * h.sm_count);
-    asym_kernel<32><<<unsigned(grid), 256, 0, h.stream>>>(C.p, n, C.ld, mm);
+    launch_k(h, asym_kernel<32>, unsigned(grid), 256, 0, C.p, n, C.ld, mm);
   } else {
     const int64_t nt = ceil_div(n, 64);
     const int64_t grid = std::min<int64_t>(nt * (nt + 1) / 2, 6 * h.sm_count);
-    asym_kernel<64><<<unsigned(grid), 256, 0, h.stream>>>(C.p, n, C.ld, mm);
+    launch_k(h, asym_kernel<64>, unsigned(grid), 256, 0, C.p, n, C.ld, mm);
   }
   RSVD_LAUNCHED(h);
-  asym_flag_kernel<<<1, 1, 0, h.stream>>>(mm, h.d_flags, kFlagAsymmetric);
+  launch_k(h, asym_flag_kernel, 1, 1, 0, mm, h.d_flags, kFlagAsymmetric);
   RSVD_LAUNCHED(h);
 }
 
@@ -385,7 +389,7 @@ void solve_ls_impl(Handle& h, const DMat& G, const DMat& Hm, DMat X) {
   svd_core(h, G, U, s, V);
   DMat T = h.ws.mat(k, r);
   gemm_tn(h, U, Hm, T);  // U^T H
-  pinv_rows_kernel<<<grid_for(k * r, h), 256, 0, h.stream>>>(T.p, k, r, T.ld, s);
+  launch_k(h, pinv_rows_kernel, grid_for(k * r, h), 256, 0, T.p, k, r, T.ld, s);
   RSVD_LAUNCHED(h);
   gemm_nn(h, V, T, X);
 }
@@ -416,7 +420,7 @@ void solve_joint_core_impl(Handle& h, const DMat& G1, const DMat& H1, const DMat
   gemm_nn(h, T, U2, a);   // (U1^T H1) U2
   gemm_tn(h, V1, H2, T);  // V1^T H2
   gemm_nn(h, T, V2, b);   // (V1^T H2) V2
-  kron_core_kernel<<<grid_for(l * l, h), 256, 0, h.stream>>>(a.p, b.p, l, a.ld, s1, s2, X.p, X.ld);
+  launch_k(h, kron_core_kernel, grid_for(l * l, h), 256, 0, a.p, b.p, l, a.ld, s1, s2, X.p, X.ld);
   RSVD_LAUNCHED(h);
   DMat U2t = h.ws.mat(l, l);
   transpose(h, U2, U2t);

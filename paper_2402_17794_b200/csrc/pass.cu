@@ -183,6 +183,7 @@ template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW, bool kG
 __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
     pass_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 PassParams p) {
+  RSVD_PDL_ENTRY();
   using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
   constexpr int kConsumerWarps = CW;
   constexpr int BM = Cfg::BM, NT = Cfg::NT, NCOL = Cfg::NCOL;
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, (CW <= 4) ? 2 : 1)
 // in-kernel reduction 3.5-16 us, chained across consecutive tiles).
 template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC, int CW, bool kGroup>
 __global__ void __launch_bounds__(CW * 32) sk_reduce_kernel(PassParams p) {
+  RSVD_PDL_ENTRY();
   using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
   constexpr int BM = Cfg::BM, NT = Cfg::NT, NCOL = Cfg::NCOL, FRAG = Cfg::FRAG;
   const int t = blockIdx.x;
@@ -828,15 +830,15 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     RSVD_CUDA(cudaMemsetAsync(pp.probe, 0, size_t(nct) * 16 * 8, h.stream));
   }
   if (pp.stream_k && pp.nsub > 1)
-    kernG<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
+    launch_k(h, kernG, grid, Cfg::THREADS, Cfg::SMEM, ta, tb, pp);
   else
-    kern1<<<grid, Cfg::THREADS, Cfg::SMEM, h.stream>>>(ta, tb, pp);
+    launch_k(h, kern1, grid, Cfg::THREADS, Cfg::SMEM, ta, tb, pp);
   RSVD_LAUNCHED(h);
   if (pp.stream_k && pp.defer && split_tiles) {
     if (pp.nsub > 1)
-      sk_reduce_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, true><<<unsigned(tiles), CW * 32, 0, h.stream>>>(pp);
+      launch_k(h, sk_reduce_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, true>, unsigned(tiles), CW * 32, 0, pp);
     else
-      sk_reduce_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, false><<<unsigned(tiles), CW * 32, 0, h.stream>>>(pp);
+      launch_k(h, sk_reduce_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, false>, unsigned(tiles), CW * 32, 0, pp);
     RSVD_LAUNCHED(h);
   }
   if (probe_pass) probe_report(h, pp.probe, nct, M, N, K, pp.stream_k);
@@ -923,6 +925,7 @@ __global__ void __launch_bounds__(256) gram_small_kernel(
     const double* __restrict__ P, int64_t ldp, const double* __restrict__ R, int64_t ldr,
     int64_t K, int M, int N, int64_t rows_per_cta, double* __restrict__ part,
     int* __restrict__ counter, double* __restrict__ C, int64_t ldc) {
+  RSVD_PDL_ENTRY();
   extern __shared__ double sh[];
   const int RP = int(rows_per_cta);
   double* Ps = sh;                   // [RP][M+1]
@@ -994,7 +997,7 @@ void gram_small(Handle& h, const DMat& P, const DMat& R, DMat C) {
                                    int(smem)));
     cur = smem;
   }
-  gram_small_kernel<<<unsigned(G), 256, smem, h.stream>>>(P.p, P.ld, R.p, R.ld, K, M, N, rp, part,
+  launch_k(h, gram_small_kernel, unsigned(G), 256, smem, P.p, P.ld, R.p, R.ld, K, M, N, rp, part,
                                                           cnt, C.p, C.ld);
   RSVD_LAUNCHED(h);
 }

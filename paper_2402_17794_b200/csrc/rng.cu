@@ -91,6 +91,7 @@ __device__ __forceinline__ double polar_mult(double r2, const ddlog::Entry* tabl
 // so a whole 312-word block costs one barrier.
 __global__ void mt_blocks_kernel(const uint64_t* __restrict__ init, int64_t nb,
                                  uint64_t* __restrict__ out) {
+  RSVD_PDL_ENTRY();
   __shared__ uint64_t S[2][kN];
   const int t = threadIdx.x;
   if (t < kN) {
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(320) mt_jump_kernel(const uint64_t* __restrict
                                                       const uint64_t* __restrict__ polys,
                                                       int wpp,
                                                       unsigned long long* __restrict__ windows) {
+  RSVD_PDL_ENTRY();
   extern __shared__ uint64_t base[];  // 64 * wpp + kN words
   __shared__ uint64_t poly[kPolyWords];
   const int t = threadIdx.x;
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(320) mt_jump_kernel(const uint64_t* __restrict
 __global__ void __launch_bounds__(kSegPerCta * kN) mt_segments_kernel(
     const uint64_t* __restrict__ init, const uint64_t* __restrict__ windows, int64_t nseg,
     int64_t seg_blocks, uint64_t* __restrict__ words) {
+  RSVD_PDL_ENTRY();
   const int64_t seg_words = seg_blocks * kN;
   __shared__ uint64_t S[kSegPerCta][2][kN];
   const int g = threadIdx.x / kN, t = threadIdx.x % kN;
@@ -223,6 +226,7 @@ constexpr int kTile = 256;  // attempts per tile (one per thread): ~4 CTAs per S
 // 2a. accepted-attempt count per tile.
 __global__ void polar_count_kernel(const uint64_t* __restrict__ words, const uint64_t* p0p,
                                    int64_t attempts, int* __restrict__ tile_count) {
+  RSVD_PDL_ENTRY();
   const int64_t p0 = int64_t(*p0p);
   const int64_t base = int64_t(blockIdx.x) * kTile;
   int c = 0;
@@ -247,6 +251,7 @@ __global__ void polar_count_kernel(const uint64_t* __restrict__ words, const uin
 // 2b. exclusive scan of tile counts (single CTA, sequential chunks).
 __global__ void scan_counts_kernel(const int* __restrict__ cnt, int64_t ntiles,
                                    int64_t* __restrict__ off, int64_t* __restrict__ total) {
+  RSVD_PDL_ENTRY();
   __shared__ int64_t carry;
   __shared__ int64_t wsum[32];
   if (threadIdx.x == 0) carry = 0;
@@ -294,6 +299,7 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
                                    int64_t attempts, const int64_t* __restrict__ tile_off,
                                    GaussOut g, int64_t* __restrict__ done_attempt,
                                    double* __restrict__ cache_val) {
+  RSVD_PDL_ENTRY();
   const int64_t p0 = int64_t(*p0p);
   const int64_t base = int64_t(blockIdx.x) * kTile;
   __shared__ int wcnt[8];
@@ -348,6 +354,7 @@ __global__ void rng_finish_kernel(const uint64_t* __restrict__ words,
                                   const int64_t* __restrict__ done_attempt,
                                   const double* __restrict__ cache_val, int64_t pairs,
                                   int cache_out, DevState* st, int* flags) {
+  RSVD_PDL_ENTRY();
   if (pairs == 0) {
     if (threadIdx.x == 0) {
       st->has_cached = cache_out ? 1 : 0;
@@ -425,7 +432,8 @@ void rng_download(Handle& h, const DevRng& r, rsvd_rng_state* user) {
 }
 
 namespace {
-__global__ void place_cached_kernel(const DevState* st, double* out) { out[0] = st->cached; }
+__global__ void place_cached_kernel(const DevState* st, double* out) {
+  RSVD_PDL_ENTRY(); out[0] = st->cached; }
 
 }  // namespace
 
@@ -444,7 +452,7 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
   const int cache_out = (remaining % 2 == 1) ? 1 : 0;
   // the cached variate (if any) is element 0 of the stream
   if (first && row_lo == 0 && row_hi > 0) {
-    place_cached_kernel<<<1, 1, 0, h.stream>>>(dst, out.p);
+    launch_k(h, place_cached_kernel, 1, 1, 0, dst, out.p);
     RSVD_LAUNCHED(h);
   }
   if (pairs > 0) {
@@ -463,7 +471,7 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
     if (words_needed <= 2 * kSegWords) {
       const int64_t nb = ceil_div(words_needed, kN) - 1;
       words = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nb + 1) * kN * 8));
-      mt_blocks_kernel<<<1, 320, 0, h.stream>>>(dst->mt, nb, words);
+      launch_k(h, mt_blocks_kernel, 1, 320, 0, dst->mt, nb, words);
       RSVD_LAUNCHED(h);
     } else {
       // parallel: base prefix (sequential), jump windows, all segments at once
@@ -472,7 +480,7 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
       uint64_t* windows = reinterpret_cast<uint64_t*>(h.ws.alloc_bytes(size_t(nseg) * kN * 8));
       const uint64_t* dpolys = device_jump_polys(h, uint64_t(kSegWords), int(nseg - 1));
       const int64_t nb_base = ceil_div(1 + kJumpBase, kN);
-      mt_blocks_kernel<<<1, 320, 0, h.stream>>>(dst->mt, nb_base, words);
+      launch_k(h, mt_blocks_kernel, 1, 320, 0, dst->mt, nb_base, words);
       RSVD_LAUNCHED(h);
       // split every jump over `parts` CTAs so all SMs share the XOR work
       const int parts = int(std::max<int64_t>(1, std::min<int64_t>(32, (2 * h.sm_count) / (nseg - 1))));
@@ -485,13 +493,13 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
         jcur = jsmem;
       }
       RSVD_CUDA(cudaMemsetAsync(windows, 0, size_t(nseg) * kN * 8, h.stream));
-      mt_jump_kernel<<<dim3(unsigned(nseg - 1), unsigned(parts)), 320, jsmem, h.stream>>>(
+      launch_k(h, mt_jump_kernel, dim3(unsigned(nseg - 1), unsigned(parts)), 320, jsmem, 
           words, dpolys, wpp, reinterpret_cast<unsigned long long*>(windows));
       RSVD_LAUNCHED(h);
       // one segment per CTA while that fits the SMs (a 312-thread CTA twists a
       // block in ~220 ns; three in lockstep take ~2x longer per block)
       const int spc = (nseg <= 2 * h.sm_count) ? 1 : kSegPerCta;
-      mt_segments_kernel<<<unsigned(ceil_div(nseg, spc)), spc * kN, 0, h.stream>>>(
+      launch_k(h, mt_segments_kernel, unsigned(ceil_div(nseg, spc)), spc * kN, 0, 
           dst->mt, windows, nseg, seg_blocks, words);
       RSVD_LAUNCHED(h);
     }
@@ -501,19 +509,19 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
     int64_t* done = off + ntiles;  // [done_attempt, total]
     double* cache = reinterpret_cast<double*>(done + 2);
     RSVD_CUDA(cudaMemsetAsync(done, 0xff, sizeof(int64_t), h.stream));
-    polar_count_kernel<<<unsigned(ntiles), 256, 0, h.stream>>>(words, &dst->pos, attempts, cnt);
+    launch_k(h, polar_count_kernel, unsigned(ntiles), 256, 0, words, &dst->pos, attempts, cnt);
     RSVD_LAUNCHED(h);
-    scan_counts_kernel<<<1, 1024, 0, h.stream>>>(cnt, ntiles, off, done + 1);
+    launch_k(h, scan_counts_kernel, 1, 1024, 0, cnt, ntiles, off, done + 1);
     RSVD_LAUNCHED(h);
     GaussOut g{out.p, n, out.ld, total, first, pairs, row_lo, row_hi};
-    polar_write_kernel<<<unsigned(ntiles), 256, 0, h.stream>>>(words, &dst->pos, attempts, off, g,
+    launch_k(h, polar_write_kernel, unsigned(ntiles), 256, 0, words, &dst->pos, attempts, off, g,
                                                                done, cache);
     RSVD_LAUNCHED(h);
-    rng_finish_kernel<<<1, 320, 0, h.stream>>>(words, done, cache, pairs, cache_out, dst,
+    launch_k(h, rng_finish_kernel, 1, 320, 0, words, done, cache, pairs, cache_out, dst,
                                                h.d_flags);
     RSVD_LAUNCHED(h);
   } else {
-    rng_finish_kernel<<<1, 32, 0, h.stream>>>(nullptr, nullptr, nullptr, 0, 0, dst, h.d_flags);
+    launch_k(h, rng_finish_kernel, 1, 32, 0, nullptr, nullptr, nullptr, 0, 0, dst, h.d_flags);
     RSVD_LAUNCHED(h);
   }
   rng.has_cached = cache_out;

@@ -58,6 +58,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 __global__ void hh_factor_kernel(const double* __restrict__ X, int64_t rows, int l, int64_t ldx,
                                  int b, double* __restrict__ V, double* __restrict__ tau,
                                  double* __restrict__ Rs, int64_t ldr, int* flags) {
+  RSVD_PDL_ENTRY();
   extern __shared__ double sm[];
   double* A = sm;                  // b x l, ld = b
   double* red = sm + int64_t(b) * l;  // scratch: tau/beta broadcast
@@ -132,6 +133,7 @@ __global__ void hh_factor_kernel(const double* __restrict__ X, int64_t rows, int
 __global__ void hh_apply_kernel(const double* __restrict__ V, const double* __restrict__ tau,
                                 int64_t rows, int l, int b, const double* __restrict__ C,
                                 int64_t ldc, double* __restrict__ Q, int64_t ldq) {
+  RSVD_PDL_ENTRY();
   extern __shared__ double sm[];
   double* M = sm;                  // b x l
   double* Vs = sm + int64_t(b) * l;  // b x l
@@ -195,6 +197,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
                                   double* __restrict__ Wout, int64_t ldw,
                                   double* __restrict__ sigma, double* gX, double* gJ,
                                   int in_smem, int* flags, double* dbg = nullptr) {
+  RSVD_PDL_ENTRY();
   extern __shared__ double sm[];
   __shared__ double wmax_s[32];  // per warp: largest g^2/(a b) met this sweep
   double m_prev = 1.0;           // previous sweep's maximum (identical in all threads)
@@ -437,6 +440,7 @@ __global__ void jacobi_evd_kernel(const double* __restrict__ Cin, int64_t ldc, i
                                   double* __restrict__ Uout, int64_t ldu,
                                   double* __restrict__ lam, double* gA, double* gV, int in_smem,
                                   double* rot, int* flags) {
+  RSVD_PDL_ENTRY();
   extern __shared__ double sm[];
   double* A = in_smem ? sm : gA;
   double* V = in_smem ? sm + int64_t(l) * l : gV;
@@ -554,6 +558,7 @@ __global__ void jacobi_evd_kernel(const double* __restrict__ Cin, int64_t ldc, i
 // -------------------------------------------------------------- sign rule
 __global__ void sign_rule_kernel(double* U, int64_t rows, int64_t ldu, double* V, int64_t vrows,
                                  int64_t ldv) {
+  RSVD_PDL_ENTRY();
   const int j = blockIdx.x;
   __shared__ double bv[32];
   __shared__ long long bi[32];
@@ -600,6 +605,7 @@ __global__ void sign_rule_kernel(double* U, int64_t rows, int64_t ldu, double* V
 
 __global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, int64_t cols,
                                  int64_t ldi, double* __restrict__ out, int64_t ldo) {
+  RSVD_PDL_ENTRY();
   __shared__ double t[32][33];
   const int64_t i0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -615,6 +621,7 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, in
 
 __global__ void scale_cols_kernel(double* X, int64_t rows, int64_t cols, int64_t ld,
                                   const double* s, int inv) {
+  RSVD_PDL_ENTRY();
   const int64_t n = rows * cols;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -624,6 +631,7 @@ __global__ void scale_cols_kernel(double* X, int64_t rows, int64_t cols, int64_t
 }
 
 __global__ void sym_part_kernel(const double* A, int64_t n, int64_t lda, double* C, int64_t ldc) {
+  RSVD_PDL_ENTRY();
   const int64_t tot = n * n;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -634,6 +642,7 @@ __global__ void sym_part_kernel(const double* A, int64_t n, int64_t lda, double*
 
 __global__ void finite_kernel(const double* X, int64_t rows, int64_t cols, int64_t ld, int* flags,
                               int bit) {
+  RSVD_PDL_ENTRY();
   const int64_t n = rows * cols;
   bool bad = false;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
@@ -656,6 +665,7 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l
                                 double shift_coef, double* __restrict__ R, int64_t ldr,
                                 double* __restrict__ Rinv, int64_t ldri, double* gA, int in_smem,
                                 int* shift_used, int* flags) {
+  RSVD_PDL_ENTRY();
   extern __shared__ double sm[];
   double* A = in_smem ? sm : gA;  // lower-triangular working copy (col-major, ld l)
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
@@ -736,6 +746,7 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l
 __global__ void __launch_bounds__(kCholThreads) chol_inv_small_kernel(
     const double* __restrict__ G, int64_t ldg, int l, double shift_coef, double* __restrict__ R, int64_t ldr,
     double* __restrict__ Rinv, int64_t ldri, int* shift_used, int* flags) {
+  RSVD_PDL_ENTRY();
   constexpr int LD = 33;
   __shared__ double G0[32 * LD], piv[2 * 72], Rs[32 * LD], Ri[32 * LD];
   for (int e = threadIdx.x; e < l * l; e += kCholThreads)
@@ -767,6 +778,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
     const double* __restrict__ Y, int64_t ldy, int64_t m, int l, int64_t rows_per,
     double* __restrict__ Qo, int64_t ldq, double* __restrict__ part, double* __restrict__ Rout,
     int64_t ldr, double shift_coef, int passes, int* __restrict__ flags, long long* probe) {
+  RSVD_PDL_ENTRY();
   constexpr int LD = 33;
   cg::grid_group grid = cg::this_grid();
   int np_ = 0;
@@ -1055,14 +1067,14 @@ void check_finite(Handle& h, const DMat& X, int bit) {
   if (X.rows * X.cols == 0) return;
   const int64_t n = X.rows * X.cols;
   const int blocks = int(std::min<int64_t>(ceil_div(n, 256), 4 * h.sm_count));
-  finite_kernel<<<blocks, 256, 0, h.stream>>>(X.p, X.rows, X.cols, X.ld, h.d_flags, bit);
+  launch_k(h, finite_kernel, blocks, 256, 0, X.p, X.rows, X.cols, X.ld, h.d_flags, bit);
   RSVD_LAUNCHED(h);
 }
 
 void transpose(Handle& h, const DMat& in, DMat out) {
   if (in.rows * in.cols == 0) return;
   dim3 grid(unsigned(ceil_div(in.rows, 32)), unsigned(ceil_div(in.cols, 32)));
-  transpose_kernel<<<grid, dim3(32, 8), 0, h.stream>>>(in.p, in.rows, in.cols, in.ld, out.p,
+  launch_k(h, transpose_kernel, grid, dim3(32, 8), 0, in.p, in.rows, in.cols, in.ld, out.p,
                                                        out.ld);
   RSVD_LAUNCHED(h);
 }
@@ -1077,7 +1089,7 @@ void scale_cols(Handle& h, DMat X, const double* s, bool inv) {
   const int64_t n = X.rows * X.cols;
   if (!n) return;
   const int blocks = int(std::min<int64_t>(ceil_div(n, 256), 4 * h.sm_count));
-  scale_cols_kernel<<<blocks, 256, 0, h.stream>>>(X.p, X.rows, X.cols, X.ld, s, inv ? 1 : 0);
+  launch_k(h, scale_cols_kernel, blocks, 256, 0, X.p, X.rows, X.cols, X.ld, s, inv ? 1 : 0);
   RSVD_LAUNCHED(h);
 }
 
@@ -1085,13 +1097,13 @@ void sym_part(Handle& h, const DMat& A, DMat C) {
   const int64_t n = A.rows;
   if (!n) return;
   const int blocks = int(std::min<int64_t>(ceil_div(n * n, 256), 4 * h.sm_count));
-  sym_part_kernel<<<blocks, 256, 0, h.stream>>>(A.p, n, A.ld, C.p, C.ld);
+  launch_k(h, sym_part_kernel, blocks, 256, 0, A.p, n, A.ld, C.p, C.ld);
   RSVD_LAUNCHED(h);
 }
 
 void sign_rule(Handle& h, DMat U, DMat* V) {
   if (U.cols == 0) return;
-  sign_rule_kernel<<<unsigned(U.cols), 256, 0, h.stream>>>(
+  launch_k(h, sign_rule_kernel, unsigned(U.cols), 256, 0, 
       U.p, U.rows, U.ld, V ? V->p : nullptr, V ? V->rows : 0, V ? V->ld : 0);
   RSVD_LAUNCHED(h);
 }
@@ -1119,7 +1131,7 @@ DMat tsqr_factor(Handle& h, const DMat& X, std::vector<TsqrLevel>& lv) {
     L.V = h.ws.alloc(int64_t(L.nblk) * b * l);
     L.tau = h.ws.alloc(int64_t(L.nblk) * l);
     DMat Rs = h.ws.mat(int64_t(L.nblk) * l, l);
-    hh_factor_kernel<<<L.nblk, 256, smem_f, h.stream>>>(cur.p, cur.rows, l, cur.ld, b, L.V, L.tau,
+    launch_k(h, hh_factor_kernel, L.nblk, 256, smem_f, cur.p, cur.rows, l, cur.ld, b, L.V, L.tau,
                                                         Rs.p, Rs.ld, h.d_flags);
     RSVD_LAUNCHED(h);
     lv.push_back(L);
@@ -1141,7 +1153,7 @@ void tsqr_form(Handle& h, const std::vector<TsqrLevel>& lv, int l, const double*
   for (int t = int(lv.size()) - 1; t >= 0; --t) {
     const TsqrLevel& L = lv[t];
     DMat out = (t == 0) ? Q : h.ws.mat(L.rows, l);
-    hh_apply_kernel<<<L.nblk, 256, smem_a, h.stream>>>(L.V, L.tau, L.rows, l, b, parent, ldp,
+    launch_k(h, hh_apply_kernel, L.nblk, 256, smem_a, L.V, L.tau, L.rows, l, b, parent, ldp,
                                                        out.p, out.ld);
     RSVD_LAUNCHED(h);
     parent = out.p;
@@ -1273,12 +1285,12 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
       if (dist) allreduce_mat(h, G);
     }
     if (l <= 32)
-      chol_inv_small_kernel<<<1, kCholThreads, 0, h.stream>>>(G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld,
+      launch_k(h, chol_inv_small_kernel, 1, kCholThreads, 0, G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld,
                                                    shift_used, h.d_flags);
     else if (use_blocked)
       chol_inv_blocked(h, G, l, coef, R1, Ri, shift_used);
     else
-      chol_inv_kernel<<<1, 1024, in_smem ? size_t(l) * l * 8 : 0, h.stream>>>(
+      launch_k(h, chol_inv_kernel, 1, 1024, in_smem ? size_t(l) * l * 8 : 0, 
           G.p, G.ld, l, coef, R1.p, R1.ld, Ri.p, Ri.ld, gA, in_smem ? 1 : 0, shift_used,
           h.d_flags);
     if (l <= 32 || !use_blocked) RSVD_LAUNCHED(h);
@@ -1371,7 +1383,7 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
       dbg = h.ws.alloc(32);
       RSVD_CUDA(cudaMemsetAsync(dbg, 0, 32 * 8, h.stream));
     }
-    jacobi_svd_kernel<8><<<1, thr, dyn, h.stream>>>(Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
+    launch_k(h, jacobi_svd_kernel<8>, 1, thr, dyn, Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
                                                     gX, gJ, in_smem ? 1 : 0, h.d_flags, dbg);
     if (probe_on) {
       double hd[32];
@@ -1386,8 +1398,8 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
     ensure_smem(jacobi_svd_kernel<32>, dyn, cur_j);
     // one warp per column pair of a round (no idle warps in the per-round barrier)
     const int thr = 32 * std::max(1, std::min(32, pairs));
-    jacobi_svd_kernel<32><<<1, thr, dyn, h.stream>>>(Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
-                                                     gX, gJ, in_smem ? 1 : 0, h.d_flags);
+    launch_k(h, jacobi_svd_kernel<32>, 1, thr, dyn, Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
+                                                     gX, gJ, in_smem ? 1 : 0, h.d_flags, nullptr);
   }
   RSVD_LAUNCHED(h);
 
@@ -1409,7 +1421,7 @@ void jacobi_evd_sym(Handle& h, const DMat& C, DMat U, double* lambda) {
   }
   static size_t cur_e = 0;
   ensure_smem(jacobi_evd_kernel, in_smem ? size_t(2) * l * l * 8 : 0, cur_e);
-  jacobi_evd_kernel<<<1, 1024, in_smem ? size_t(2) * l * l * 8 : 0, h.stream>>>(
+  launch_k(h, jacobi_evd_kernel, 1, 1024, in_smem ? size_t(2) * l * l * 8 : 0, 
       C.p, C.ld, l, U.p, U.ld, lambda, gA, gV, in_smem ? 1 : 0, nullptr, h.d_flags);
   RSVD_LAUNCHED(h);
 
