@@ -244,16 +244,41 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
         qcol = max(a, bq);
       }
       const bool act = qcol < l;  // warp-uniform
+      // probe: clock stamps of warp 0, sweep 0, rounds 0..7 (dbg[32 + 8 r + k])
+      const bool stamp = dbg && sweep == 0 && round < 8 && warp == 0 && lane == 0;
+      if (stamp) dbg[32 + 8 * round] = double(clock64());
       if (act) {
         const bool row = lane < l;
         double xp = row ? X[pcol * l + lane] : 0.0, xq = row ? X[qcol * l + lane] : 0.0;
-        double al = xp * xp, be = xq * xq, ga = xp * xq;
+        // J rows loaded with X (X and J share the shared buffer: the compiler
+        // cannot move these loads above the X stores below)
+        const double jp = row ? J[pcol * l + lane] : 0.0, jq = row ? J[qcol * l + lane] : 0.0;
+        if (stamp) dbg[33 + 8 * round] = double(clock64()) + 0.0 * (xp + xq);
+        // (a, b, g) = sums of xp^2, xq^2, xp xq over the warp.  The round is
+        // bound by the warp shuffles of the 13 warps (one SHFL.32 per clock
+        // per SM: measured 93 cycles per butterfly level for 3 values), so a
+        // reduce-scatter halves the traffic: at offset 16 lanes with bit 4
+        // clear keep (a, b) and the others keep g, at offset 8 the (a, b)
+        // lanes split a / b, then three levels on one value each and three
+        // broadcasts: 9 64-bit shuffles instead of 15.
+        double al, be, ga;
+        {
+          const bool hi4 = (lane & 16) != 0, hi3 = (lane & 8) != 0;
+          const double a0 = xp * xp, b0 = xq * xq, g0 = xp * xq;
+          const double s1 = __shfl_xor_sync(0xffffffffu, hi4 ? a0 : g0, 16);
+          const double s2 = __shfl_xor_sync(0xffffffffu, hi4 ? b0 : 0.0, 16);
+          const double k1 = hi4 ? g0 + s1 : a0 + s1;  // hi4: g, else: a
+          const double k2 = b0 + s2;                  // !hi4: b
+          const double send = hi4 ? k1 : (hi3 ? k1 : k2);
+          const double r = __shfl_xor_sync(0xffffffffu, send, 8);
+          double v = hi4 ? k1 + r : (hi3 ? k2 + r : k1 + r);  // lane quantity: g | b | a
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          al = __shfl_sync(0xffffffffu, v, 0);
+          be = __shfl_sync(0xffffffffu, v, 8);
+          ga = __shfl_sync(0xffffffffu, v, 16);
         }
+        if (stamp) dbg[34 + 8 * round] = double(clock64()) + 0.0 * (al + be + ga);
         // rotation from two reciprocal square roots (no sqrt/div on the chain):
         // ir = 1/r, r = |(d, 2g)|; cos 2th = |d|/r; c = sqrt(h), h = (1+cos 2th)/2;
         // s = sgn(d) sin 2th / (2c) = sgn(d) g ir / sqrt(h)  (c^2 + s^2 = 1)
@@ -267,17 +292,19 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ Rm, int64_t ldr, in
           const double hh = fma(0.5 * fabs(d), ir, 0.5);
           const double ih = rsqrt(hh);
           const double c = hh * ih, sn = copysign(1.0, d) * (ga * ir) * ih;
+          if (stamp) dbg[35 + 8 * round] = double(clock64()) + 0.0 * (c + sn);
           if (row) {
             X[pcol * l + lane] = c * xp - sn * xq;
             X[qcol * l + lane] = sn * xp + c * xq;
-            const double jp = J[pcol * l + lane], jq = J[qcol * l + lane];
             J[pcol * l + lane] = c * jp - sn * jq;
             J[qcol * l + lane] = sn * jp + c * jq;
           }
           if (lane == 0) changed = 1;
+          if (stamp) dbg[36 + 8 * round] = double(clock64());
         }
       }
       __syncthreads();
+      if (stamp) dbg[37 + 8 * round] = double(clock64());
     }
     if (lane == 0) wmax_s[warp] = mden > 0.0 ? mnum / mden : 0.0;
     __syncthreads();
@@ -1380,17 +1407,23 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
     static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
     double* dbg = nullptr;
     if (probe_on) {
-      dbg = h.ws.alloc(32);
-      RSVD_CUDA(cudaMemsetAsync(dbg, 0, 32 * 8, h.stream));
+      dbg = h.ws.alloc(128);
+      RSVD_CUDA(cudaMemsetAsync(dbg, 0, 128 * 8, h.stream));
     }
     launch_k(h, jacobi_svd_kernel<8>, 1, thr, dyn, Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
                                                     gX, gJ, in_smem ? 1 : 0, h.d_flags, dbg);
     if (probe_on) {
-      double hd[32];
+      double hd[128];
       RSVD_CUDA(cudaMemcpyAsync(hd, dbg, sizeof hd, cudaMemcpyDeviceToHost, h.stream));
       RSVD_CUDA(cudaStreamSynchronize(h.stream));
       std::fprintf(stderr, "jacobi_svd l=%d sweeps=%d max rel g per sweep:", l, int(hd[0]));
       for (int i = 1; i <= int(hd[0]) && i < 31; ++i) std::fprintf(stderr, " %.1e", hd[i]);
+      std::fprintf(stderr, "\n  round phases (cycles: load, reduce, rotation, store, barrier; round total):");
+      for (int r = 0; r < 7; ++r) {
+        const double* q = hd + 32 + 8 * r;
+        std::fprintf(stderr, " [%.0f %.0f %.0f %.0f %.0f; %.0f]", q[1] - q[0], q[2] - q[1], q[3] - q[2],
+                     q[4] - q[3], q[5] - q[4], q[8] - q[0]);
+      }
       std::fprintf(stderr, "\n");
     }
   } else {
