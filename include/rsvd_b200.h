@@ -90,7 +90,8 @@ void rsvd_destroy(rsvd_handle* h);
 const char* rsvd_last_error(void);
 const char* rsvd_version(void);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores
- * the handle's own stream. */
+ * the handle's own non-blocking stream, on which every call first waits for
+ * the work already queued on the legacy default stream (the caller's inputs). */
 rsvd_status rsvd_set_stream(rsvd_handle* h, void* cuda_stream);
 rsvd_status rsvd_synchronize(rsvd_handle* h);
 rsvd_status rsvd_get_counters(rsvd_handle* h, rsvd_counters* out);
