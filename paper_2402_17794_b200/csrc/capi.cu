@@ -53,6 +53,7 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
     if (hd) {
       hd->h.rng_user_out = nullptr;
       cudaStreamSynchronize(hd->h.stream);
+      if (hd->h.copy_stream) cudaStreamSynchronize(hd->h.copy_stream);
       cudaMemsetAsync(hd->h.d_flags, 0, sizeof(int), hd->h.stream);
     }
     return e.code;
@@ -251,6 +252,9 @@ rsvd_status create_impl(rsvd_handle** out, int device, int rank, int nranks, con
     RSVD_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamNonBlocking));
     h.stream = h.own_stream;
     RSVD_CUDA(cudaEventCreateWithFlags(&h.join_ev, cudaEventDisableTiming));
+    RSVD_CUDA(cudaStreamCreateWithFlags(&h.copy_stream, cudaStreamNonBlocking));
+    RSVD_CUDA(cudaEventCreateWithFlags(&h.copy_ev, cudaEventDisableTiming));
+    RSVD_CUDA(cudaEventCreateWithFlags(&h.order_ev, cudaEventDisableTiming));
     RSVD_CUDA(cudaMalloc(&h.d_flags, 64));
     RSVD_CUDA(cudaMemset(h.d_flags, 0, 64));
     RSVD_CUDA(cudaMallocHost(&h.h_flags, 64));
@@ -278,6 +282,21 @@ struct HostIO {
     if (r * c > 0)
       RSVD_CUDA(cudaMemcpy2DAsync(d.p, d.ld * 8, a, ld * 8, r * 8, c, cudaMemcpyHostToDevice,
                                   h.stream));
+    return d;
+  }
+  // A's upload on the copy stream, overlapping the call's first kernels (the
+  // Omega stream): the returned event is waited on before A is first read
+  rsvdb::DMat up_overlapped(const double* a, int64_t r, int64_t c, int64_t ld, cudaEvent_t* ready) {
+    rsvdb::DMat d = h.ws.mat(r, c);
+    *ready = nullptr;
+    if (r * c > 0) {
+      RSVD_CUDA(cudaEventRecord(h.order_ev, h.stream));  // after this call's earlier work
+      RSVD_CUDA(cudaStreamWaitEvent(h.copy_stream, h.order_ev, 0));
+      RSVD_CUDA(cudaMemcpy2DAsync(d.p, d.ld * 8, a, ld * 8, r * 8, c, cudaMemcpyHostToDevice,
+                                  h.copy_stream));
+      RSVD_CUDA(cudaEventRecord(h.copy_ev, h.copy_stream));
+      *ready = h.copy_ev;
+    }
     return d;
   }
   void down(const rsvdb::DMat& d, double* a, int64_t ld) {
@@ -347,6 +366,12 @@ void rsvd_destroy(rsvd_handle* hd) {
   for (auto e : h.prof_pool) cudaEventDestroy(e);
   for (auto e : h.trace_pool) cudaEventDestroy(e);
   if (h.join_ev) cudaEventDestroy(h.join_ev);
+  if (h.copy_stream) {
+    cudaStreamSynchronize(h.copy_stream);
+    cudaStreamDestroy(h.copy_stream);
+  }
+  if (h.copy_ev) cudaEventDestroy(h.copy_ev);
+  if (h.order_ev) cudaEventDestroy(h.order_ev);
   if (h.own_stream) cudaStreamDestroy(h.own_stream);
   delete hd;
 }
@@ -532,8 +557,10 @@ rsvd_status rsvd_rsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* 
                            int64_t ldu, double* sigma, double* v, int64_t ldv) {
   return guard(hd, "rsvd", [&](rsvdb::Handle& h) {
     HostIO io{h};
-    rsvdb::DMat A = io.up(a, m, n, lda);
+    cudaEvent_t a_up = nullptr;
+    rsvdb::DMat A = io.up_overlapped(a, m, n, lda, &a_up);
     rsvdb::Problem P = rsvdb::make_problem(h, A.p, m, n, A.ld);
+    P.ready = a_up;
     const int64_t l = std::max<int64_t>(k + p, 0);
     rsvdb::DMat U = h.ws.mat(m, l), V = h.ws.mat(n, l);
     double* s = h.ws.alloc(std::max<int64_t>(l, 1));
@@ -568,8 +595,10 @@ rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t
                             double* lambda) {
   return guard(hd, "spevd_hermitian", [&](rsvdb::Handle& h) {
     HostIO io{h};
-    rsvdb::DMat A = io.up(a, n, n, lda);
+    cudaEvent_t a_up = nullptr;
+    rsvdb::DMat A = io.up_overlapped(a, n, n, lda, &a_up);
     rsvdb::Problem P = rsvdb::make_problem(h, A.p, n, n, A.ld);
+    P.ready = a_up;
     const int64_t kk = std::max<int64_t>(k, 0);
     rsvdb::DMat U = h.ws.mat(n, kk);
     double* lam = h.ws.alloc(std::max<int64_t>(kk, 1));
@@ -600,8 +629,10 @@ rsvd_status rsvd_spsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double*
                             double* sigma, double* v, int64_t ldv) {
   return guard(hd, "spsvd_general", [&](rsvdb::Handle& h) {
     HostIO io{h};
-    rsvdb::DMat A = io.up(a, m, n, lda);
+    cudaEvent_t a_up = nullptr;
+    rsvdb::DMat A = io.up_overlapped(a, m, n, lda, &a_up);
     rsvdb::Problem P = rsvdb::make_problem(h, A.p, m, n, A.ld);
+    P.ready = a_up;
     const int64_t kk = std::max<int64_t>(k, 0);
     rsvdb::DMat U = h.ws.mat(m, kk), V = h.ws.mat(n, kk);
     double* s = h.ws.alloc(std::max<int64_t>(kk, 1));

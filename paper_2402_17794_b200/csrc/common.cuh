@@ -107,6 +107,10 @@ struct Handle {
   // already queued on the legacy default stream (the caller's inputs, e.g. a
   // framework's default stream), see join_caller_stream()
   cudaEvent_t join_ev = nullptr;
+  // host-buffer entry points upload A on copy_stream while the Omega stream is
+  // generated on `stream`; the first use of A waits on copy_ev (Problem::ready)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_ev = nullptr, order_ev = nullptr;
   Arena ws;
   int* d_counters = nullptr;   // split-K tile semaphores (kept zeroed)
   int64_t n_counters = 0;

@@ -152,6 +152,7 @@ void trace_collect(Handle& h) {
 void finish_call(Handle& h, const char* what) {
   rsvd_rng_state* user = h.rng_user_out;
   h.rng_user_out = nullptr;
+  if (h.copy_stream) RSVD_CUDA(cudaStreamSynchronize(h.copy_stream));  // an upload nothing waited on
   check_flags(h, what);  // synchronizes
   if (user) std::memcpy(user, h.h_rng, sizeof(rsvd_rng_state));
   for (auto& r : h.prof_pending) {
@@ -323,13 +324,19 @@ void check_symmetric(Handle& h, const DMat& C, bool dist_unused) {
 }
 
 // ------------------------------------------------------------ operators
+static void a_ready(Handle& h, const Problem& P) {
+  if (P.ready) RSVD_CUDA(cudaStreamWaitEvent(h.stream, P.ready, 0));
+}
+
 void op_apply(Handle& h, const Problem& P, const DMat& X, DMat Y) {
+  a_ready(h, P);
   gemm_nn(h, P.A, X, Y);
   h.counters.apply++;
   h.counters.physical_passes++;
 }
 
 void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z) {
+  a_ready(h, P);
   gemm_tn(h, P.A, Y, Z);
   if (P.dist) allreduce_mat(h, Z);
   h.counters.adjoint++;
@@ -517,6 +524,7 @@ void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
   if (P.m_global != n) throw_dim("spevd_hermitian: matrix is not square");
   if (check_sym && !P.dist) {
     // reference singlepass.hpp:49-53: uncounted precondition read of A
+    a_ready(h, P);
     check_symmetric(h, P.A, false);
     check_flags(h, "spevd_hermitian");
   }

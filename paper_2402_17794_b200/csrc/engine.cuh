@@ -10,6 +10,7 @@ struct Problem {
   int64_t m_global = 0;
   int64_t row_off = 0;
   bool dist = false;
+  cudaEvent_t ready = nullptr;  // A's upload (host entry points): waited on before first use
 };
 
 Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda);
