@@ -268,7 +268,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
+    # RSVD_BENCH_DIST=1 (under torchrun, one rank): the multi-GPU code path of
+    # this script and of the engine (one-rank NCCL communicator) on one GPU
+    dist_mode = world > 1 or os.environ.get("RSVD_BENCH_DIST") == "1"
+    if dist_mode:
+        # rank 0 prints exactly one JSON line on stdout: NCCL_DEBUG=VERSION
+        # would add NCCL's version banner there
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=device)
         os.environ.setdefault("NCCL_ALGO", "Ring")
         os.environ.setdefault("NCCL_PROTO", "Simple")
@@ -290,7 +297,7 @@ def main():
     torch.cuda.synchronize()
 
     def barrier():
-        if world > 1:
+        if dist_mode:
             dist.barrier()
 
     def step():
@@ -351,7 +358,7 @@ def main():
         ms_prof = timed_region()
         prof = engine.profile_read()
         engine.profile(False)
-        if world > 1:
+        if dist_mode:
             t = torch.tensor([ms_total], dtype=torch.float64, device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_total = float(t.item())
@@ -380,7 +387,7 @@ def main():
             host_step()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
         barrier()
-        if world > 1:
+        if dist_mode:
             t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
@@ -461,7 +468,7 @@ def main():
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_mode:
         dist.destroy_process_group()
     engine.close()
     return 0
