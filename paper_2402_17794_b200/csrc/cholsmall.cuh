@@ -64,6 +64,12 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
 #endif
         if (j < l && !broke) {
           double* pv = piv + (j & 1) * 72;
+          // w_ij is final since step j-1 and the breakdown reference is a
+          // constant: both fetched before the barrier.  After it, the update
+          // runs speculatively next to the breakdown test (a broken attempt
+          // is discarded), so the chain is one load, one multiply, the FMAs.
+          const double wij = __shfl_sync(kFull, w[jj], base + jb);
+          const double oj = orig ? orig[j] : G0[j + LD * j] + shift;
           if (i == j) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) pv[8 * c + q] = w[q];
@@ -76,17 +82,12 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
           }
           __syncthreads();
           const double d = pv[65];
-          const double oj = orig ? orig[j] : G0[j + LD * j] + shift;
-          if (!(d > 1e-12 * oj) || !(d > 0.0)) {
-            broke = true;  // identical in every thread
-          } else {
-            const double wij = __shfl_sync(kFull, w[jj], base + jb);
-            if (i > j) {
-              const double f = wij * pv[64];
+          if (i > j) {
+            const double f = wij * pv[64];
 #pragma unroll
-              for (int q = 0; q < 8; ++q) w[q] = fma(-f, pv[8 * c + q], w[q]);
-            }
+            for (int q = 0; q < 8; ++q) w[q] = fma(-f, pv[8 * c + q], w[q]);
           }
+          if (!(d > 1e-12 * oj) || !(d > 0.0)) broke = true;  // identical in every thread
         }
       }
     }
