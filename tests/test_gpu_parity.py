@@ -382,3 +382,43 @@ def test_graph_replay_matches_eager(eng):
             assert np.array_equal(x, y)
         assert got[3] == ref[3]
         assert got[4] == ref[4]
+
+
+def test_graph_replay_with_fresh_output_buffers(eng):
+    """Graph-cached calls write through workspace staging, so the cache key
+    ignores where the caller puts the outputs: calls alternating between
+    output buffers (and a padded leading dimension) must each fill their own
+    buffers with bitwise the same factors, and leave the other buffers alone."""
+    import ctypes
+    import torch
+    L = eng._load()
+    m, n, k, p, q = 1200, 500, 12, 4, 1
+    l = k + p
+    a = _t(haar_test_matrix(m, n, np.logspace(0, -4, 60), 9))
+    e = eng.Engine(0)
+    bufs = []
+    for ldu in (m, m + 6, m):
+        u = torch.full((l, ldu), -7.0, dtype=torch.float64, device="cuda")
+        v = torch.full((l, n), -7.0, dtype=torch.float64, device="cuda")
+        s = torch.full((l,), -7.0, dtype=torch.float64, device="cuda")
+        bufs.append((u, ldu, s, v))
+
+    def call(b):
+        u, ldu, s, v = b
+        r = eng.Rng(5)
+        eng._check(L.rsvd_rsvd_dev(e.handle, m, n, a.data_ptr(), m, k, p, q, 2, ctypes.byref(r.state),
+                                   u.data_ptr(), ldu, s.data_ptr(), v.data_ptr(), n))
+        torch.cuda.synchronize()
+        return u.t()[:m].cpu().numpy().copy(), s.cpu().numpy().copy(), v.t().cpu().numpy().copy()
+
+    ref = call(bufs[0])
+    for i in (1, 2, 0, 1, 2, 0):  # eager, capture and replays with changing outputs
+        before = [t.clone() for j, b in enumerate(bufs) if j != i for t in (b[0], b[2], b[3])]
+        got = call(bufs[i])
+        for x, y in zip(got, ref):
+            assert np.array_equal(x, y)
+        after = [t for j, b in enumerate(bufs) if j != i for t in (b[0], b[2], b[3])]
+        for x, y in zip(before, after):
+            assert torch.equal(x, y)
+    # the padding rows of the padded buffer are untouched
+    assert bool((bufs[1][0].t()[m:] == -7.0).all())
