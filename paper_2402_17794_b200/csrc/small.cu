@@ -894,18 +894,33 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
     mark();
     // ---- total Gram, identical in every CTA (fixed CTA order)
     const double* pb0 = part + int64_t(pass & 1) * G * 1024;
-    for (int e = tid; e < 1024; e += kFqThreads) {
-      double v = 0.0;
+    {
+      // the thread's four entries together: 32 loads in flight per round
+      // trip instead of 8 (same CTA order per entry: bitwise unchanged)
+      constexpr int EPT = 1024 / kFqThreads;
+      double v[EPT];
+#pragma unroll
+      for (int x = 0; x < EPT; ++x) v[x] = 0.0;
       int c = 0;
       for (; c + 8 <= G; c += 8) {
-        double t[8];
+        double t[EPT][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = __ldcg(pb0 + int64_t(c + q) * 1024 + e);
+        for (int x = 0; x < EPT; ++x)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v += t[q];
+          for (int q = 0; q < 8; ++q) t[x][q] = __ldcg(pb0 + int64_t(c + q) * 1024 + tid + kFqThreads * x);
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[x] += t[x][q];
       }
-      for (; c < G; ++c) v += __ldcg(pb0 + int64_t(c) * 1024 + e);
-      Gs[(e & 31) + LD * (e >> 5)] = v;
+      for (; c < G; ++c)
+#pragma unroll
+        for (int x = 0; x < EPT; ++x) v[x] += __ldcg(pb0 + int64_t(c) * 1024 + tid + kFqThreads * x);
+#pragma unroll
+      for (int x = 0; x < EPT; ++x) {
+        const int e = tid + kFqThreads * x;
+        Gs[(e & 31) + LD * (e >> 5)] = v[x];
+      }
     }
     __syncthreads();
     mark();
