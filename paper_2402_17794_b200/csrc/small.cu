@@ -864,18 +864,23 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
           af[i] = yr[i * 8 + r8];  // A(m = a, k = r): Ys[r][a]
           bf[i] = af[i];           // B(k = r, n = b): Ys[r][b], same fragment shape
         }
+        // the Gram is symmetric: upper tiles only (10 of 16), mirrored below
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = i; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = i; j < 4; ++j) {
           const int a0 = i * 8 + r8, b0 = j * 8 + 2 * c4;
           red[warp][a0 + LD * b0] = acc[i][j][0];
           red[warp][a0 + LD * (b0 + 1)] = acc[i][j][1];
+          if (j > i) {
+            red[warp][b0 + LD * a0] = acc[i][j][0];
+            red[warp][(b0 + 1) + LD * a0] = acc[i][j][1];
+          }
         }
     }
     __syncthreads();
@@ -1032,6 +1037,8 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        // R^-1 is upper triangular: column tile j only meets rows k < 8 (j + 1)
+        // (80 of 128 DMMAs per 32-row chunk)
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           const int kk = ks * 4 + c4;
@@ -1039,11 +1046,11 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
 #pragma unroll
           for (int i = 0; i < 4; ++i) af[i] = Ys[(m0 + i * 8 + r8) * LD + kk];  // A(r, k)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) bf[j] = Ri[kk + LD * (j * 8 + r8)];       // B(k, c)
+          for (int j = ks / 2; j < 4; ++j) bf[j] = Ri[kk + LD * (j * 8 + r8)];  // B(k, c)
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            for (int j = ks / 2; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
         __syncwarp();
 #pragma unroll
