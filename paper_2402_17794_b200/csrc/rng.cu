@@ -290,7 +290,8 @@ struct GaussOut {
 // 3. write normals; record the completing attempt.
 __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uint64_t* p0p,
                                    int64_t attempts, const int64_t* __restrict__ tile_off,
-                                   GaussOut g, int64_t* __restrict__ done_attempt,
+                                   const int* __restrict__ tile_count, GaussOut g,
+                                   int64_t* __restrict__ done_attempt,
                                    double* __restrict__ cache_val) {
   RSVD_PDL_ENTRY();
   const int64_t p0 = int64_t(*p0p);
@@ -301,9 +302,26 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
   // constant cache would serialize (measured: the whole kernel 19 us on C2)
   __shared__ ddlog::Entry tab[ddlog::kTableSize];
   for (int i = threadIdx.x; i < ddlog::kTableSize; i += blockDim.x) tab[i] = c_log_table[i];
-  if (threadIdx.x == 0) run = tile_off[blockIdx.x];
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (tile_off) {
+    if (threadIdx.x == 0) run = tile_off[blockIdx.x];
+  } else {
+    // few tiles: this tile's offset is the sum of the counts before it,
+    // summed here (no separate scan launch)
+    int64_t v = 0;
+    for (int i = threadIdx.x; i < int(blockIdx.x); i += blockDim.x) v += tile_count[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __shared__ int64_t ws[8];
+    if (lane == 0) ws[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) t += ws[w];
+      run = t;
+    }
+  }
+  __syncthreads();
   for (int k = 0; k < kTile / 256; ++k) {
     const int64_t j = base + k * 256 + threadIdx.x;
     Pair p{0, 0, 0, false};
@@ -504,11 +522,17 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
     RSVD_CUDA(cudaMemsetAsync(done, 0xff, sizeof(int64_t), h.stream));
     launch_k(h, polar_count_kernel, unsigned(ntiles), 256, 0, words, &dst->pos, attempts, cnt);
     RSVD_LAUNCHED(h);
-    launch_k(h, scan_counts_kernel, 1, 1024, 0, cnt, ntiles, off, done + 1);
-    RSVD_LAUNCHED(h);
+    // up to 4096 tiles each write CTA sums the counts before its tile itself
+    // (<= 16 loads per thread); beyond, one scan launch
+    const bool self_scan = ntiles <= 4096;
+    if (!self_scan) {
+      launch_k(h, scan_counts_kernel, 1, 1024, 0, cnt, ntiles, off, done + 1);
+      RSVD_LAUNCHED(h);
+    }
     GaussOut g{out.p, n, out.ld, total, first, pairs, row_lo, row_hi};
-    launch_k(h, polar_write_kernel, unsigned(ntiles), 256, 0, words, &dst->pos, attempts, off, g,
-                                                               done, cache);
+    launch_k(h, polar_write_kernel, unsigned(ntiles), 256, 0, words, &dst->pos, attempts,
+             self_scan ? static_cast<const int64_t*>(nullptr) : static_cast<const int64_t*>(off),
+             static_cast<const int*>(cnt), g, done, cache);
     RSVD_LAUNCHED(h);
     launch_k(h, rng_finish_kernel, 1, 320, 0, words, done, cache, pairs, cache_out, dst,
                                                h.d_flags);

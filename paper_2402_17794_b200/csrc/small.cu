@@ -885,13 +885,21 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
     }
     __syncthreads();
     double* pp = part + (int64_t(pass & 1) * G + blockIdx.x) * 1024;
-    for (int e = tid; e < 1024; e += kFqThreads) {
-      const int a = e & 31, b = e >> 5;
-      const int o = a + LD * b;
-      double v = 0.0;
+    {
+      // the thread's four entries interleaved (four independent add chains)
+      constexpr int EPT = 1024 / kFqThreads;
+      double v[EPT];
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v += red[w][o];
-      pp[e] = v;
+      for (int x = 0; x < EPT; ++x) v[x] = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+#pragma unroll
+        for (int x = 0; x < EPT; ++x) {
+          const int e = tid + kFqThreads * x;
+          v[x] += red[w][(e & 31) + LD * (e >> 5)];
+        }
+#pragma unroll
+      for (int x = 0; x < EPT; ++x) pp[tid + kFqThreads * x] = v[x];
     }
     __threadfence();
     mark();
