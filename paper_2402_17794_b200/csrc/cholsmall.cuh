@@ -70,9 +70,11 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
           // is discarded), so the chain is one load, one multiply, the FMAs.
           const double wij = __shfl_sync(kFull, w[jj], base + jb);
           const double oj = orig ? orig[j] : G0[j + LD * j] + shift;
+          // pivot-row column 8c+q lives at pv[8q+c]: the 8 lane groups of a
+          // warp touch 8 consecutive words (at pv[8c+q], 4-way bank conflicts)
           if (i == j) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) pv[8 * c + q] = w[q];
+            for (int q = 0; q < 8; ++q) pv[8 * q + c] = w[q];
             if (c == jb) {
               const double d = w[jj];
               const double rs = rsqrt(d);
@@ -85,7 +87,7 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
           if (i > j) {
             const double f = wij * pv[64];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) w[q] = fma(-f, pv[8 * c + q], w[q]);
+            for (int q = 0; q < 8; ++q) w[q] = fma(-f, pv[8 * q + c], w[q]);
           }
           if (!(d > 1e-12 * oj) || !(d > 0.0)) broke = true;  // identical in every thread
         }
