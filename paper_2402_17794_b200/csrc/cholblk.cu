@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kT) chol_blocked_kernel(const double* __restri
                                                          int* __restrict__ status) {
   RSVD_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
-  __shared__ double S0[kB * kLD], S1[kB * kLD], Rs[kB * kLD], Ri[kB * kLD], piv[2 * 72], orig[kB];
+  __shared__ double S0[kB * kLD], S1[kB * kLD], Rs[kB * kLD], Ri[kB * kLD], piv[2 * 136], orig[kB];
   __shared__ double red[kT / 32];
   const int nb = (l + kB - 1) / kB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -19,8 +19,8 @@ namespace rsvdb {
 // shared-memory round trip and one FMA: a single warp doing the same work is
 // shared-memory and issue bound (~4x slower, measured).
 // Shift policy as chol_inv_kernel.  Returns false (in every thread) on
-// breakdown after shifting.  G0 (LD 33, shared) is the Gram; piv is 2 x 72
-// doubles of shared scratch; outputs R and R^-1 (LD 33, zero outside l x l).
+// breakdown after shifting.  G0 (LD 33, shared) is the Gram; piv is 2 x 136
+// doubles of shared scratch (two pivot rows per barrier, double-buffered); outputs R and R^-1 (LD 33, zero outside l x l).
 // Must be called by all threads of a 256-thread block.
 constexpr int kCholThreads = 256;
 
@@ -57,19 +57,26 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
 #pragma unroll 1
     for (int jb = 0; jb * 8 < l && !broke; ++jb) {
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
+      for (int jj = 0; jj < 8; jj += 2) {
         const int j = 8 * jb + jj;
 #ifdef CHOL_STEP_PROBE
         if (pr && t == 0 && j < l) pr[8 + j] = clock64();
 #endif
         if (j < l && !broke) {
-          double* pv = piv + (j & 1) * 72;
-          // w_ij is final since step j-1 and the breakdown reference is a
-          // constant: both fetched before the barrier.  After it, the update
-          // runs speculatively next to the breakdown test (a broken attempt
-          // is discarded), so the chain is one load, one multiply, the FMAs.
+          // Two pivots (j, j+1) per barrier.  Row j+1 is stored as it stands
+          // before step j (pv[72..]); after the barrier every thread applies
+          // step j to it itself (its 8 columns and the scalars at columns j,
+          // j+1), takes the rsqrt of the updated pivot d1 and applies step
+          // j+1: the same operations in the same order as one step per
+          // barrier, so the factor is bitwise unchanged.  w_ij, w_i,j+1 (final
+          // since step j-1) and the breakdown references are fetched before
+          // the barrier.
+          const bool two = j + 1 < l;  // uniform
+          double* pv = piv + ((j >> 1) & 1) * 136;
           const double wij = __shfl_sync(kFull, w[jj], base + jb);
+          const double wij1 = __shfl_sync(kFull, w[jj + 1], base + jb);
           const double oj = orig ? orig[j] : G0[j + LD * j] + shift;
+          const double oj1 = two ? (orig ? orig[j + 1] : G0[(j + 1) + LD * (j + 1)] + shift) : 1.0;
           // pivot-row column 8c+q lives at pv[8q+c]: the 8 lane groups of a
           // warp touch 8 consecutive words (at pv[8c+q], 4-way bank conflicts)
           if (i == j) {
@@ -82,14 +89,36 @@ __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shi
               pv[65] = d;
             }
           }
+          if (two && i == j + 1) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pv[72 + 8 * q + c] = w[q];
+          }
           __syncthreads();
-          const double d = pv[65];
-          if (i > j) {
-            const double f = wij * pv[64];
+          const double d = pv[65], ivd = pv[64];
+          const double f = wij * ivd;
+          bool bad = !(d > 1e-12 * oj) || !(d > 0.0);
+          if (two) {
+            const double fj = pv[72 + 8 * jj + jb] * ivd;  // f_{j+1,j}
+            const double d1 = fma(-fj, pv[8 * (jj + 1) + jb], pv[72 + 8 * (jj + 1) + jb]);
+            if (i > j + 1) {
+              const double wi1 = fma(-f, pv[8 * (jj + 1) + jb], wij1);  // w_i,j+1 after step j
+              const double rs1 = rsqrt(d1);
+              const double f2 = wi1 * (rs1 * rs1);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const double wq = fma(-f, pv[8 * q + c], w[q]);
+                w[q] = fma(-f2, fma(-fj, pv[8 * q + c], pv[72 + 8 * q + c]), wq);
+              }
+            } else if (i == j + 1) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) w[q] = fma(-f, pv[8 * q + c], w[q]);
+            }
+            bad = bad || !(d1 > 1e-12 * oj1) || !(d1 > 0.0);
+          } else if (i > j) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) w[q] = fma(-f, pv[8 * q + c], w[q]);
           }
-          if (!(d > 1e-12 * oj) || !(d > 0.0)) broke = true;  // identical in every thread
+          if (bad) broke = true;  // identical in every thread
         }
       }
     }

@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(kCholThreads) chol_inv_small_kernel(
     double* __restrict__ Rinv, int64_t ldri, int* shift_used, int* flags) {
   RSVD_PDL_ENTRY();
   constexpr int LD = 33;
-  __shared__ double G0[32 * LD], piv[2 * 72], Rs[32 * LD], Ri[32 * LD];
+  __shared__ double G0[32 * LD], piv[2 * 136], Rs[32 * LD], Ri[32 * LD];
   for (int e = threadIdx.x; e < l * l; e += kCholThreads)
     G0[(e % l) + LD * (e / l)] = G[int64_t(e / l) * ldg + (e % l)];
   __syncthreads();
