@@ -68,6 +68,8 @@ def lib():
         L.orc_rng_normal.argtypes = [P]
         L.orc_rng_raw.restype = U64
         L.orc_rng_raw.argtypes = [P]
+        L.orc_polar_r2_log.argtypes = [P, ctypes.c_int64, P, P]
+        L.orc_polar_r2_log.restype = None
         L.orc_rng_get_state.argtypes = [P, ctypes.POINTER(RngState)]
         L.orc_rng_set_state.argtypes = [P, ctypes.POINTER(RngState)]
         L.orc_set_threads.argtypes = [I]
@@ -129,6 +131,13 @@ class Rng:
 
     def raw(self) -> int:
         return lib().orc_rng_raw(self._h)
+
+    def polar_r2_log(self, count: int):
+        """(r2, glibc log(r2)) of the next `count` accepted polar attempts."""
+        r2 = np.empty(count)
+        lg = np.empty(count)
+        lib().orc_polar_r2_log(self._h, count, _p(r2), _p(lg))
+        return r2, lg
 
     def get_state(self) -> RngState:
         st = RngState()

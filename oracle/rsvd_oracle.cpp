@@ -678,6 +678,22 @@ void* orc_rng_new(uint64_t seed) { return new Rng(seed); }
 void orc_rng_free(void* r) { delete static_cast<Rng*>(r); }
 double orc_rng_normal(void* r) { return static_cast<Rng*>(r)->next_normal(); }
 uint64_t orc_rng_raw(void* r) { return static_cast<Rng*>(r)->engine(); }
+
+// The accepted polar inputs r2 of the next `count` accepted attempts of the
+// reference stream (libstdc++ random.tcc:1827-1834: x, y = 2u - 1 from
+// generate_canonical; reject r2 > 1 or r2 == 0), and glibc's log of each.
+void orc_polar_r2_log(void* r, int64_t count, double* r2_out, double* log_out) {
+  auto& g = static_cast<Rng*>(r)->engine;
+  for (int64_t i = 0; i < count;) {
+    const double x = 2.0 * std::generate_canonical<double, 53>(g) - 1.0;
+    const double y = 2.0 * std::generate_canonical<double, 53>(g) - 1.0;
+    const double r2 = x * x + y * y;
+    if (r2 > 1.0 || r2 == 0.0) continue;
+    r2_out[i] = r2;
+    log_out[i] = std::log(r2);
+    ++i;
+  }
+}
 void orc_rng_get_state(void* r, RngState* st) { get_state(*static_cast<Rng*>(r), st); }
 void orc_rng_set_state(void* r, const RngState* st) { set_state(*static_cast<Rng*>(r), st); }
 

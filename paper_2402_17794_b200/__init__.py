@@ -171,6 +171,8 @@ def _load():
         L.rsvd_version.restype = ctypes.c_char_p
         L.rsvd_debug_log_cr.argtypes = [D]
         L.rsvd_debug_log_cr.restype = D
+        L.rsvd_debug_log_window.argtypes = [ctypes.c_void_p, I64, ctypes.c_void_p, ctypes.c_void_p]
+        L.rsvd_debug_log_window.restype = None
         _lib = L
         return _lib
 
@@ -777,6 +779,17 @@ def spsvd_host(a: np.ndarray, k: int, p: int, rng: Rng):
 def debug_log_cr(x: float) -> float:
     """Host evaluation of the device polar-sampler log (ddlog.cuh), for tests."""
     return _load().rsvd_debug_log_cr(float(x))
+
+
+def debug_log_window(x):
+    """Host evaluation of the exact-mode flag test (ddlog.cuh log_near_midpoint):
+    returns (correctly rounded log(x), flag) arrays; flag marks the inputs whose
+    normals the engine recomputes with the host glibc log."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    cr = np.empty_like(x)
+    fl = np.empty(x.shape, dtype=np.uint8)
+    _load().rsvd_debug_log_window(x.ctypes.data, x.size, cr.ctypes.data, fl.ctypes.data)
+    return cr, fl.astype(bool)
 
 
 # ------------------------------------------------ diagnostics (core/bounds/angles)

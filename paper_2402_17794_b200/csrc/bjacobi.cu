@@ -656,12 +656,7 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
   if ((ldp / 4) % 2 == 0) ldp += 4;
   const size_t smem = (size_t(ldp) * kBJW + kBJW * kGL + kBJW * kVL) * 8;
   if (smem > 227 * 1024) throw_dim("block_jacobi_svd: l too large for one block pair in shared memory");
-  static size_t cur = 0;
-  if (smem > cur) {
-    RSVD_CUDA(cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
-    cur = smem;
-  }
+  smem_attr(bjacobi_kernel, smem);
   BJBatch batch{};
   batch.nprob = nprob;
   for (int q = 0; q < 2; ++q) {

@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -18,6 +20,22 @@
 struct rsvd_handle {
   rsvdb::Handle h;
 };
+
+namespace rsvdb {
+void smem_attr_raw(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> set;
+  int dev = 0;
+  RSVD_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set[{dev, kernel}];
+  // (static shared memory counts toward the 48 KB default too: always opt in)
+  if (bytes > cur || cur == 0) {
+    RSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    cur = std::max<size_t>(bytes, 1);
+  }
+}
+}  // namespace rsvdb
 
 namespace {
 thread_local std::string g_err;
@@ -41,6 +59,7 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
     rsvdb::Handle& h = hd->h;
     RSVD_CUDA(cudaSetDevice(h.device));
     h.ws.reset();
+    h.patch_chunk = h.patch_off = 0;
     join_caller_stream(h);
     h.rng_user_out = nullptr;
     rsvdb::trace_begin(h);
@@ -165,6 +184,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     }
     if (++e.seen >= 2 && !e.bad) {
       h.ws.reset();
+      h.patch_chunk = h.patch_off = 0;
       h.rng_user_out = nullptr;
       const rsvd_counters before = h.counters;
       const uint64_t g0 = gen_now();
@@ -356,6 +376,7 @@ void rsvd_destroy(rsvd_handle* hd) {
   if (h.h_rng) cudaFreeHost(h.h_rng);
   if (h.h_rng_in) cudaFreeHost(h.h_rng_in);
   if (h.h_rng_batch) cudaFreeHost(h.h_rng_batch);
+  for (auto& c : h.patch_chunks) cudaFreeHost(c.first);
   for (auto& kv : h.graph_cache) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (auto& r : kv.second.prof) {

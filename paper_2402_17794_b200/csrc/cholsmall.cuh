@@ -28,6 +28,10 @@ constexpr int kCholThreads = 256;
 // (default: G0's diagonal + shift); `attempts` = 1 disables the shifted retry
 // (the blocked factorization of chol_blocked_kernel decides shifts globally);
 // `start` = 1 goes straight to the shifted factorization.
+// Shared scratch (doubles) cta_chol_inv needs for `piv`: two pivot-row
+// buffers of 136 (64 + 8 row-j words, 64 row-(j+1) words) per barrier pair.
+constexpr int kCholPivScratch = 2 * 136;
+
 __device__ __forceinline__ bool cta_chol_inv(const double* G0, int l, double shift_coef, double* piv, double* Rs,
                                              double* Rinvs, bool* shifted, long long* pr = nullptr,
                                              const double* orig = nullptr, int attempts = 2,

@@ -153,6 +153,12 @@ struct Handle {
   rsvd_rng_state* rng_user_out = nullptr;
   // pinned staging for the RNG state upload (the graph-captured H2D source)
   rsvd_rng_state* h_rng_in = nullptr;
+  // Exact Omega/Psi stream (rng.cu): pinned, device-mapped chunks holding the
+  // near-midpoint polar inputs whose log the host evaluates; bump-allocated per
+  // top-level call (cursor reset with the workspace), never freed before the
+  // handle (captured graphs keep pointers into them).
+  std::vector<std::pair<char*, size_t>> patch_chunks;
+  size_t patch_chunk = 0, patch_off = 0;
   // pinned staging for the per-trial seeded states of batched trials (trials.cu)
   rsvd_rng_state* h_rng_batch = nullptr;
   int64_t h_rng_batch_cap = 0;
@@ -234,6 +240,16 @@ void finish_call(Handle& h, const char* what);
 void trace_mark(Handle& h, const char* site);
 void trace_begin(Handle& h);
 void trace_collect(Handle& h);
+
+// Opt `kernel` into `bytes` of dynamic shared memory on the CURRENT device.
+// The attribute belongs to the device context, so it is tracked per
+// (device, kernel) -- a process with handles on several GPUs sets it on each
+// (thread-safe; capi.cu).
+void smem_attr_raw(const void* kernel, size_t bytes);
+template <class K>
+inline void smem_attr(K* kernel, size_t bytes) {
+  smem_attr_raw(reinterpret_cast<const void*>(kernel), bytes);
+}
 
 // Split-K semaphores, at least n of them.
 int* tile_counters(Handle& h, int64_t n);

@@ -115,8 +115,9 @@ inline void build_table(Entry* t) {
 constexpr double kLn2Hi = 0.6931471805599453094;   // RN(ln 2)
 constexpr double kLn2Lo = 2.319046813846299558e-17; // ln 2 - kLn2Hi
 
-// Natural log of a positive normal double (the polar sampler's r2 in (0,1]).
-RSVD_HD inline double log_cr(double x, const Entry* table) {
+// Natural log of a positive normal double (the polar sampler's r2 in (0,1])
+// as a normalized double-double (|lo| <= ulp(hi)/2).
+RSVD_HD inline dd log_dd(double x, const Entry* table) {
   int e;
   double m = frexp(x, &e);  // x = m * 2^e, m in [0.5, 1)
   m *= 2.0;
@@ -157,7 +158,53 @@ RSVD_HD inline double log_cr(double x, const Entry* table) {
     el = quick_two_sum(el.hi, el.lo);
     s = dd_add(s, el);
   }
+  return s;
+}
+
+// Correctly rounded log.
+RSVD_HD inline double log_cr(double x, const Entry* table) {
+  const dd s = log_dd(x, table);
   return s.hi + s.lo;
+}
+
+// Distance, in ulps of v = RN(s.hi + s.lo), from the exact value s to the
+// nearest rounding midpoint (0.5 = s is representable, 0 = s is a midpoint).
+// A log with error bound 0.5 + w ulps can differ from v only where this
+// distance is below w.  *pow2 is set when |v| is a power of two (the spacing
+// below v is half an ulp; callers treat those as near a midpoint).
+RSVD_HD inline double midpoint_distance(dd s, double v, bool* pow2) {
+  if (v == 0.0) {
+    *pow2 = false;
+    return 0.5;
+  }
+  int e;
+  const double f = frexp(v, &e);  // v = f * 2^e, |f| in [0.5, 1)
+  *pow2 = fabs(f) == 0.5;
+  const double ulp = ldexp(1.0, e - 53);
+  const double resid = (s.hi - v) + s.lo;  // s.hi - v is exact (v in {hi, hi +- ulp})
+  return 0.5 - fabs(resid) / ulp;
+}
+
+// Exact-mode flag test for the polar sampler: true where glibc's log may
+// round log(x) differently from v = RN(s).  glibc 2.39's log (both the FMA and
+// the SSE2 ifunc variants) differs from the correctly rounded value only when
+// the exact value lies within ~0.02 ulp of a rounding midpoint, and that
+// distance bound scales like an ABSOLUTE error near |log x| ~ 1/16 (the
+// table path's largest term), falling by ~2x per binade on either side.
+// Window, in ulps of v, for |v| = f * 2^e (|f| in [0.5, 1)):
+//   w(e) = 0.04 * 2^-|e + 3|
+// i.e. >= 2x the largest midpoint distance of any glibc mismatch observed per
+// binade over 1e9 reference polar inputs per ifunc variant
+// (tools/logwindow.cpp; profiles/r02_logwindow.txt).  Flags ~1.7 % of inputs.
+RSVD_HD inline bool log_near_midpoint(dd s, double v) {
+  bool p2;
+  const double d = midpoint_distance(s, v, &p2);
+  if (p2) return true;
+  int e;
+  frexp(v, &e);
+  const int k = e + 3 < 0 ? -(e + 3) : e + 3;
+  const double w = k > 60 ? 0.0 : ldexp(0.04, -k);
+  return d < w;
 }
 
 }  // namespace ddlog

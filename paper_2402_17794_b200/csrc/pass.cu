@@ -30,84 +30,10 @@
 
 #include "common.cuh"
 #include "pass.cuh"
+#include "ptx.cuh"
 
 namespace rsvdb {
 
-// ------------------------------------------------------------ PTX helpers
-namespace ptx {
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait(bar, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > (20LL << 30)) __trap();
-  }
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel_gpu() {
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
-}
-}  // namespace ptx
 
 // ---------------------------------------------------------------- kernel
 // CW consumer warps (DMMA) + one TMA producer warp per CTA.
@@ -626,6 +552,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+}  // namespace
+
 // 2-D column-major fp64 tensor map: dims {inner=rows, outer=cols}.
 CUtensorMap make_map(const double* p, int64_t rows, int64_t cols, int64_t ld, int box_inner,
                      int box_outer) {
@@ -646,6 +574,8 @@ CUtensorMap make_map(const double* p, int64_t rows, int64_t cols, int64_t ld, in
 bool tma_ok(const DMat& x) {
   return (reinterpret_cast<uintptr_t>(x.p) % 16 == 0) && (x.ld % 2 == 0) && x.ld >= x.rows;
 }
+
+namespace {
 
 // RSVD_PROBE_PASS: per-CTA %globaltimer stamps of one launch (debug):
 // entry, first stage arrival, per segment (main loop end, ticket, epilogue
@@ -695,14 +625,10 @@ template <bool kNN, int BN, int WMT, int BK, int STAGES, int XC = 0, int CW = 8>
 void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t N, int64_t K,
             int force_splits) {
   using Cfg = PassCfg<kNN, BN, WMT, BK, STAGES, XC, CW>;
-  static bool attr_set = false;
   auto kern1 = pass_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, false>;
   auto kernG = pass_kernel<kNN, BN, WMT, BK, STAGES, XC, CW, true>;
-  if (!attr_set) {
-    RSVD_CUDA(cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    RSVD_CUDA(cudaFuncSetAttribute(kernG, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    attr_set = true;
-  }
+  smem_attr(kern1, Cfg::SMEM);
+  smem_attr(kernG, Cfg::SMEM);
   const int64_t mt = ceil_div(M, Cfg::BM), nt = ceil_div(N, Cfg::NCOL);
   const int64_t tiles = mt * nt;
   const int64_t kblocks = ceil_div(K, BK);
@@ -991,12 +917,7 @@ void gram_small(Handle& h, const DMat& P, const DMat& R, DMat C) {
   double* part = h.ws.alloc(G * M * N);
   int* cnt = tile_counters(h, 1);
   const size_t smem = size_t(rp) * (M + N + 2) * 8;
-  static size_t cur = 0;
-  if (smem > cur) {
-    RSVD_CUDA(cudaFuncSetAttribute(gram_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
-    cur = smem;
-  }
+  smem_attr(gram_small_kernel, smem);
   launch_k(h, gram_small_kernel, unsigned(G), 256, smem, P.p, P.ld, R.p, R.ld, K, M, N, rp, part,
                                                           cnt, C.p, C.ld);
   RSVD_LAUNCHED(h);

@@ -1,5 +1,7 @@
 // Streaming-pass GEMMs (pass.cu).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace rsvdb {
@@ -7,4 +9,10 @@ namespace rsvdb {
 void gemm_nn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits = 0);
 // C (M x N) = P^T * R,  P (K x M), R (K x N)   [Z = A^T Y, Gram Q^T Y]
 void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits = 0);
+// 2-D column-major fp64 TMA map (dims {rows, cols}, box {box_inner, box_outer},
+// 128-byte swizzle) and whether x can be addressed by one (16-byte aligned
+// base, even ld).
+CUtensorMap make_map(const double* p, int64_t rows, int64_t cols, int64_t ld, int box_inner,
+                     int box_outer);
+bool tma_ok(const DMat& x);
 }  // namespace rsvdb

@@ -12,7 +12,7 @@
 //     sqrt(-2 log r2 / r2), return y*mult and CACHE x*mult for the next call.
 //
 // Device pipeline (all exact integer / correctly rounded IEEE arithmetic,
-// except log, see ddlog.cuh):
+// except log, see ddlog.cuh and "Exact mode" below):
 //   1. mt_blocks: regenerate the untempered MT word sequence past the current
 //      position (twist = two 156-wide parallel phases per 312 words).
 //   2. polar_count: accept flags of every attempt (pair of draws), per-tile
@@ -25,10 +25,28 @@
 //      consumed draw + index, libstdc++'s lazy convention) and the cache.
 // The host Rng state is passed in and returned advanced by exactly the draws
 // consumed, so a host rsvd::Rng continues bit-identically.
+//
+// Exact mode (default; RSVD_OMEGA_EXACT=0 turns it off): the device log is
+// correctly rounded, glibc's is not, so the two differ on ~0.08 % of polar
+// inputs -- always ones whose exact log lies within ~0.02 ulp of a rounding
+// midpoint (ddlog.cuh log_near_midpoint; ~1.7 % of inputs fall inside the
+// window).  polar_write appends every such accepted pair (stream index, r2, x,
+// y) to a pinned, device-mapped list; a host node (cudaLaunchHostFunc, so the
+// call stays graph-capturable) evaluates libstdc++'s multiplier
+// sqrt(-2 * std::log(r2) / r2) with the HOST's own glibc log on a small thread
+// pool; polar_patch rewrites those normals (and the cached variate).  The
+// result is the reference's stream bit for bit on the host that runs it,
+// whichever glibc ifunc (FMA or SSE2) that host selects.
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "ddlog.cuh"
@@ -76,8 +94,7 @@ __device__ __forceinline__ Pair polar_pair(uint64_t w1, uint64_t w2) {
   p.ok = !(p.r2 > 1.0 || p.r2 == 0.0);
   return p;
 }
-__device__ __forceinline__ double polar_mult(double r2, const ddlog::Entry* table) {
-  const double lg = ddlog::log_cr(r2, table);
+__device__ __forceinline__ double polar_mult_from_log(double r2, double lg) {
   return __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, lg), r2));
 }
 
@@ -278,6 +295,21 @@ __global__ void scan_counts_kernel(const int* __restrict__ cnt, int64_t ntiles,
   if (threadIdx.x == 0) *total = carry;
 }
 
+// Exact-mode patch list (pinned, device-mapped): written by polar_write,
+// completed by the host node, applied by polar_patch.
+struct PatchEntry {
+  int64_t e0;  // stream index of the pair's first normal
+  double r2, x, y;
+};
+struct PatchOut {
+  double vy, vx;
+};
+struct PatchList {
+  unsigned long long* count;  // device counter (workspace)
+  PatchEntry* ent;            // mapped host memory, cap entries
+  int64_t cap;
+};
+
 struct GaussOut {
   double* out;
   int64_t n, ld;      // rows of the output, leading dimension
@@ -292,7 +324,8 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
                                    int64_t attempts, const int64_t* __restrict__ tile_off,
                                    const int* __restrict__ tile_count, GaussOut g,
                                    int64_t* __restrict__ done_attempt,
-                                   double* __restrict__ cache_val) {
+                                   double* __restrict__ cache_val, PatchList pl,
+                                   int* __restrict__ flags) {
   RSVD_PDL_ENTRY();
   const int64_t p0 = int64_t(*p0p);
   const int64_t base = int64_t(blockIdx.x) * kTile;
@@ -332,22 +365,50 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
     int before = 0;
     for (int w = 0; w < warp; ++w) before += wcnt[w];
     const int64_t rank = run + before + __popc(bal & ((1u << lane) - 1u));
+    bool near = false;
+    const int64_t e0 = g.first + 2 * rank;
     if (p.ok && rank < g.pairs) {
-      const double mult = polar_mult(p.r2, tab);
+      const ddlog::dd ls = ddlog::log_dd(p.r2, tab);
+      const double lg = ls.hi + ls.lo;
+      const double mult = polar_mult_from_log(p.r2, lg);
       const double vy = __dadd_rn(__dmul_rn(p.y, mult), 0.0);
       const double vx = __dadd_rn(__dmul_rn(p.x, mult), 0.0);
-      const int64_t e0 = g.first + 2 * rank;
+      bool used = e0 + 1 >= g.total;  // its second normal becomes the cached variate
       {
         const int64_t r = e0 % g.n, c = e0 / g.n;
-        if (r >= g.row_lo && r < g.row_hi) g.out[c * g.ld + (r - g.row_lo)] = vy;
+        if (r >= g.row_lo && r < g.row_hi) {
+          g.out[c * g.ld + (r - g.row_lo)] = vy;
+          used = true;
+        }
       }
       if (e0 + 1 < g.total) {
         const int64_t r = (e0 + 1) % g.n, c = (e0 + 1) / g.n;
-        if (r >= g.row_lo && r < g.row_hi) g.out[c * g.ld + (r - g.row_lo)] = vx;
+        if (r >= g.row_lo && r < g.row_hi) {
+          g.out[c * g.ld + (r - g.row_lo)] = vx;
+          used = true;
+        }
       }
       if (rank == g.pairs - 1) {
         *done_attempt = j;
         *cache_val = (e0 + 1 < g.total) ? 0.0 : vx;
+      }
+      near = pl.ent != nullptr && used && ddlog::log_near_midpoint(ls, lg);
+    }
+    {
+      // warp-aggregated append of the near-midpoint pairs
+      const unsigned nb = __ballot_sync(0xffffffffu, near);
+      if (nb) {
+        unsigned long long base = 0;
+        if (lane == __ffs(nb) - 1) base = atomicAdd(pl.count, static_cast<unsigned long long>(__popc(nb)));
+        base = __shfl_sync(0xffffffffu, base, __ffs(nb) - 1);
+        if (near) {
+          const int64_t idx = int64_t(base) + __popc(nb & ((1u << lane) - 1u));
+          if (idx < pl.cap) {
+            pl.ent[idx] = PatchEntry{e0, p.r2, p.x, p.y};
+          } else {
+            atomicOr(flags, kFlagRngPatchOverflow);
+          }
+        }
       }
     }
     __syncthreads();
@@ -357,6 +418,30 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
       run += s;
     }
     __syncthreads();
+  }
+}
+
+// 3b. exact mode: the host-evaluated normals of the near-midpoint pairs.
+__global__ void polar_patch_kernel(const unsigned long long* __restrict__ count,
+                                   const PatchEntry* __restrict__ ent,
+                                   const PatchOut* __restrict__ po, int64_t cap, GaussOut g,
+                                   DevState* st) {
+  RSVD_PDL_ENTRY();
+  const int64_t n = min(int64_t(*count), cap);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e0 = ent[i].e0;
+    const PatchOut v = po[i];
+    {
+      const int64_t r = e0 % g.n, c = e0 / g.n;
+      if (r >= g.row_lo && r < g.row_hi) g.out[c * g.ld + (r - g.row_lo)] = v.vy;
+    }
+    if (e0 + 1 < g.total) {
+      const int64_t r = (e0 + 1) % g.n, c = (e0 + 1) / g.n;
+      if (r >= g.row_lo && r < g.row_hi) g.out[c * g.ld + (r - g.row_lo)] = v.vx;
+    } else {
+      st->cached = v.vx;  // the completing pair's second normal is the cached variate
+    }
   }
 }
 
@@ -388,6 +473,150 @@ __global__ void rng_finish_kernel(const uint64_t* __restrict__ words,
     st->has_cached = cache_out ? 1 : 0;
     st->cached = cache_out ? *cache_val : 0.0;
   }
+}
+
+// ------------------------------------------------ exact mode, host side
+// A small process-wide pool for the host node's log evaluations (a CUDA host
+// function must not call CUDA; plain threads are fine).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  // f(lo, hi) over [0, n) in up to size()+1 chunks; the caller runs one.
+  void run(int64_t n, const std::function<void(int64_t, int64_t)>& f) {
+    const int nw = int(workers_.size());
+    static const int64_t kMinChunk = [] {
+      const char* e = std::getenv("RSVD_HOST_MIN_CHUNK");
+      return int64_t(e ? std::max(1, std::atoi(e)) : 512);
+    }();
+    const int parts = int(std::min<int64_t>(nw + 1, (n + kMinChunk - 1) / kMinChunk));
+    if (parts <= 1) {
+      if (n > 0) f(0, n);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    fn_ = &f;
+    n_ = n;
+    parts_ = parts;
+    next_ = 1;
+    pending_ = parts - 1;
+    ++epoch_;
+    cv_.notify_all();
+    lk.unlock();
+    f(0, n / parts);
+    lk.lock();
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    int nw = int(std::min(16u, hw)) - 1;
+    if (const char* e = std::getenv("RSVD_HOST_THREADS")) nw = std::max(0, std::atoi(e) - 1);
+    for (int i = 0; i < nw; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(m_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || (epoch_ != seen && next_ < parts_); });
+      if (stop_) return;
+      seen = epoch_;
+      while (next_ < parts_) {
+        const int k = next_++;
+        const int64_t lo = n_ * k / parts_, hi = n_ * (k + 1) / parts_;
+        const auto* f = fn_;
+        lk.unlock();
+        (*f)(lo, hi);
+        lk.lock();
+        if (--pending_ == 0) done_cv_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
+  int64_t n_ = 0;
+  int parts_ = 0, next_ = 0, pending_ = 0;
+  uint64_t epoch_ = 0;
+  bool stop_ = false;
+};
+
+// Immutable per-layout job (captured graphs keep its address).
+struct PatchJob {
+  const unsigned long long* count;  // pinned copy of the device counter
+  const PatchEntry* ent;
+  PatchOut* out;
+  int64_t cap;
+};
+
+// libstdc++ polar multiplier with the host's log (random.tcc:1837:
+// __mult = std::sqrt(-2 * std::log(__r2) / __r2); normal = (y * mult) * 1 + 0).
+void CUDART_CB patch_host_fn(void* p) {
+  const PatchJob* j = static_cast<const PatchJob*>(p);
+  const int64_t n = std::min<int64_t>(int64_t(*j->count), j->cap);
+  HostPool::get().run(n, [j](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      const PatchEntry& e = j->ent[i];
+      const double mult = std::sqrt(-2 * std::log(e.r2) / e.r2);
+      j->out[i].vy = e.y * mult * 1.0 + 0.0;
+      j->out[i].vx = e.x * mult * 1.0 + 0.0;
+    }
+  });
+}
+
+bool exact_mode_env() {
+  static const bool on = [] {
+    const char* e = std::getenv("RSVD_OMEGA_EXACT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Pinned mapped bytes from the handle's patch chunks (see common.cuh).
+char* patch_alloc(Handle& h, size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  while (h.patch_chunk < h.patch_chunks.size()) {
+    auto& c = h.patch_chunks[h.patch_chunk];
+    if (h.patch_off + bytes <= c.second) {
+      char* p = c.first + h.patch_off;
+      h.patch_off += bytes;
+      return p;
+    }
+    ++h.patch_chunk;
+    h.patch_off = 0;
+  }
+  const size_t sz = std::max<size_t>(bytes, size_t(1) << 20);
+  void* p = nullptr;
+  RSVD_CUDA(cudaHostAlloc(&p, sz, cudaHostAllocMapped | cudaHostAllocPortable));
+  h.patch_chunks.push_back({static_cast<char*>(p), sz});
+  h.patch_chunk = h.patch_chunks.size() - 1;
+  h.patch_off = bytes;
+  return static_cast<char*>(p);
+}
+
+const PatchJob* patch_job(Handle& h, const unsigned long long* cnt, const PatchEntry* ent,
+                          PatchOut* out, int64_t cap) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<PatchJob>> jobs;  // process lifetime, deduplicated
+  std::lock_guard<std::mutex> lk(mu);
+  (void)h;
+  for (auto& j : jobs)
+    if (j->count == cnt && j->ent == ent && j->out == out && j->cap == cap) return j.get();
+  jobs.emplace_back(new PatchJob{cnt, ent, out, cap});
+  return jobs.back().get();
 }
 
 std::once_flag g_table_once;
@@ -497,12 +726,7 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
       const int parts = int(std::max<int64_t>(1, std::min<int64_t>(32, (2 * h.sm_count) / (nseg - 1))));
       const int wpp = (kPolyWords + parts - 1) / parts;
       const size_t jsmem = size_t(64 * wpp + kN) * 8;
-      static size_t jcur = 0;
-      if (jsmem > jcur) {
-        RSVD_CUDA(cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(jsmem)));
-        jcur = jsmem;
-      }
+      smem_attr(mt_jump_kernel, jsmem);
       RSVD_CUDA(cudaMemsetAsync(windows, 0, size_t(nseg) * kN * 8, h.stream));
       launch_k(h, mt_jump_kernel, dim3(unsigned(nseg - 1), unsigned(parts)), 320, jsmem, 
           words, dpolys, wpp, reinterpret_cast<unsigned long long*>(windows));
@@ -530,13 +754,41 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
       RSVD_LAUNCHED(h);
     }
     GaussOut g{out.p, n, out.ld, total, first, pairs, row_lo, row_hi};
+    // exact mode: room for 4 % of the pairs (the window flags ~1.7 %; the
+    // count is binomial, so this is > 40 standard deviations for C2's
+    // 102400 pairs) -- an overflow raises an error, never a silent mismatch
+    PatchList pl{nullptr, nullptr, 0};
+    PatchOut* pout = nullptr;
+    unsigned long long* hcount = nullptr;
+    if (exact_mode_env()) {
+      const int64_t stored = (row_hi - row_lo) * l;
+      pl.cap = std::min<int64_t>(pairs, (std::min(pairs, stored + 1) * 4) / 100 + 1024);
+      char* buf = patch_alloc(h, 64 + size_t(pl.cap) * (sizeof(PatchEntry) + sizeof(PatchOut)));
+      hcount = reinterpret_cast<unsigned long long*>(buf);
+      pl.ent = reinterpret_cast<PatchEntry*>(buf + 64);
+      pout = reinterpret_cast<PatchOut*>(buf + 64 + size_t(pl.cap) * sizeof(PatchEntry));
+      pl.count = reinterpret_cast<unsigned long long*>(h.ws.alloc_bytes(64));
+      RSVD_CUDA(cudaMemsetAsync(pl.count, 0, 8, h.stream));
+    }
     launch_k(h, polar_write_kernel, unsigned(ntiles), 256, 0, words, &dst->pos, attempts,
              self_scan ? static_cast<const int64_t*>(nullptr) : static_cast<const int64_t*>(off),
-             static_cast<const int*>(cnt), g, done, cache);
+             static_cast<const int*>(cnt), g, done, cache, pl, h.d_flags);
     RSVD_LAUNCHED(h);
     launch_k(h, rng_finish_kernel, 1, 320, 0, words, done, cache, pairs, cache_out, dst,
                                                h.d_flags);
     RSVD_LAUNCHED(h);
+    if (pl.ent) {
+      RSVD_CUDA(cudaMemcpyAsync(hcount, pl.count, 8, cudaMemcpyDeviceToHost, h.stream));
+      const PatchJob* job = patch_job(h, hcount, pl.ent, pout, pl.cap);
+      RSVD_CUDA(cudaLaunchHostFunc(h.stream, patch_host_fn, const_cast<PatchJob*>(job)));
+      if (h.trace) trace_mark(h, "rng.cu:exact-host-log");
+      const int blocks = int(std::min<int64_t>(ceil_div(pl.cap, 256), 2 * h.sm_count));
+      launch_k(h, polar_patch_kernel, unsigned(blocks), 256, 0,
+               static_cast<const unsigned long long*>(pl.count),
+               static_cast<const PatchEntry*>(pl.ent), static_cast<const PatchOut*>(pout), pl.cap,
+               g, dst);
+      RSVD_LAUNCHED(h);
+    }
   } else {
     launch_k(h, rng_finish_kernel, 1, 32, 0, nullptr, nullptr, nullptr, 0, 0, dst, h.d_flags);
     RSVD_LAUNCHED(h);
@@ -548,4 +800,17 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
 
 extern "C" double rsvd_debug_log_cr(double x) {
   return rsvdb::ddlog::log_cr(x, rsvdb::host_log_table());
+}
+
+// Exact-mode flag test over an array (host evaluation of the device code):
+// cr[i] = correctly rounded log(x[i]), flag[i] = 1 where the host log must be
+// used (ddlog.cuh log_near_midpoint).
+extern "C" void rsvd_debug_log_window(const double* x, int64_t n, double* cr, uint8_t* flag) {
+  const rsvdb::ddlog::Entry* t = rsvdb::host_log_table();
+  for (int64_t i = 0; i < n; ++i) {
+    const rsvdb::ddlog::dd s = rsvdb::ddlog::log_dd(x[i], t);
+    const double v = s.hi + s.lo;
+    cr[i] = v;
+    flag[i] = rsvdb::ddlog::log_near_midpoint(s, v) ? 1 : 0;
+  }
 }

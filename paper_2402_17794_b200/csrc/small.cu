@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(kCholThreads) chol_inv_small_kernel(
     double* __restrict__ Rinv, int64_t ldri, int* shift_used, int* flags) {
   RSVD_PDL_ENTRY();
   constexpr int LD = 33;
-  __shared__ double G0[32 * LD], piv[2 * 136], Rs[32 * LD], Ri[32 * LD];
+  __shared__ double G0[32 * LD], piv[kCholPivScratch], Rs[32 * LD], Ri[32 * LD];
   for (int e = threadIdx.x; e < l * l; e += kCholThreads)
     G0[(e % l) + LD * (e / l)] = G[int64_t(e / l) * ldg + (e % l)];
   __syncthreads();
@@ -1091,12 +1091,8 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr_fused_kernel(
 // =================================================================== host
 // Opt a kernel into `bytes` of dynamic shared memory (idempotent, grows only).
 template <class K>
-static void ensure_smem(K kernel, size_t bytes, size_t& current) {
-  // (static shared memory counts toward the 48 KB default too: always opt in)
-  if (bytes > current) {
-    RSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-    current = bytes;
-  }
+static void ensure_smem(K kernel, size_t bytes) {
+  smem_attr(kernel, bytes);
 }
 
 void check_flags(Handle& h, const char* what) {
@@ -1112,6 +1108,7 @@ void check_flags(Handle& h, const char* what) {
     if (f & kFlagCholBreakdown) throw_numeric(m + "Cholesky breakdown");
     if (f & kFlagPowerCap) throw_numeric(m + "power iteration hit the 5000-step cap");
     if (f & kFlagRngExhausted) throw Error(RSVD_ERR_INTERNAL, m + "rng attempt budget exhausted");
+    if (f & kFlagRngPatchOverflow) throw Error(RSVD_ERR_INTERNAL, m + "rng exact-log patch list overflow");
     throw Error(RSVD_ERR_INTERNAL, m + "device flag set");
   }
 }
@@ -1178,8 +1175,7 @@ DMat tsqr_factor(Handle& h, const DMat& X, std::vector<TsqrLevel>& lv) {
   const int l = int(X.cols);
   const int b = tsqr_block_rows(l);
   const size_t smem_f = (size_t(b) * l + 4) * 8;
-  static size_t cur_f = 0;
-  ensure_smem(hh_factor_kernel, smem_f, cur_f);
+  ensure_smem(hh_factor_kernel, smem_f);
   DMat cur = X;
   while (true) {
     TsqrLevel L;
@@ -1203,8 +1199,7 @@ void tsqr_form(Handle& h, const std::vector<TsqrLevel>& lv, int l, const double*
                int64_t ld_top, DMat Q) {
   const int b = tsqr_block_rows(l);
   const size_t smem_a = size_t(2) * b * l * 8;
-  static size_t cur_a = 0;
-  ensure_smem(hh_apply_kernel, smem_a, cur_a);
+  ensure_smem(hh_apply_kernel, smem_a);
   const double* parent = c_top;
   int64_t ldp = ld_top;
   for (int t = int(lv.size()) - 1; t >= 0; --t) {
@@ -1272,12 +1267,7 @@ static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
   const size_t smem = (size_t(rp) * 33 + 12 * 32 * 33) * 8;
   if (rp > 512 || smem > 220 * 1024) return false;
   G = ceil_div(m, rp);
-  static size_t cur = 0;
-  if (smem > cur) {
-    RSVD_CUDA(cudaFuncSetAttribute(cholqr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
-    cur = smem;
-  }
+  smem_attr(cholqr_fused_kernel, smem);
   double* part = h.ws.alloc(2 * G * 1024);
   const double coef = 11.0 * (double(m) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
   // the kernel stops as soon as Q^T Q = I to 4 l u; numerically rank-deficient
@@ -1325,8 +1315,7 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   double* gA = in_smem ? nullptr : h.ws.alloc(int64_t(l) * l);
   int* shift_used = reinterpret_cast<int*>(h.ws.alloc_bytes(16));
   RSVD_CUDA(cudaMemsetAsync(shift_used, 0, 16, h.stream));
-  static size_t cur_c = 0;
-  ensure_smem(chol_inv_kernel, in_smem ? size_t(l) * l * 8 : 0, cur_c);
+  ensure_smem(chol_inv_kernel, in_smem ? size_t(l) * l * 8 : 0);
   int64_t m_global = X.rows, row_off = 0;
   if (dist) shard_rows(h, X.rows, &m_global, &row_off);
   const double coef = 11.0 * (double(m_global) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
@@ -1430,8 +1419,7 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
   const size_t dyn = in_smem ? size_t(2) * l * l * 8 : 0;
   const int pairs = (l + 1) / 2;
   if (l <= 64) {
-    static size_t cur_j8 = 0;
-    ensure_smem(jacobi_svd_kernel<8>, dyn, cur_j8);
+    ensure_smem(jacobi_svd_kernel<8>, dyn);
     // l <= 32: one warp per column pair (the kernel's register path)
     const int thr = (l <= 32) ? 32 * pairs : std::max(32, int(round_up(8 * pairs, 32)));
     static const bool probe_on = std::getenv("RSVD_PROBE_FQ") != nullptr;
@@ -1457,8 +1445,7 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
       std::fprintf(stderr, "\n");
     }
   } else {
-    static size_t cur_j = 0;
-    ensure_smem(jacobi_svd_kernel<32>, dyn, cur_j);
+    ensure_smem(jacobi_svd_kernel<32>, dyn);
     // one warp per column pair of a round (no idle warps in the per-round barrier)
     const int thr = 32 * std::max(1, std::min(32, pairs));
     launch_k(h, jacobi_svd_kernel<32>, 1, thr, dyn, Rm.p, Rm.ld, l, J.p, J.ld, W.p, W.ld, sigma,
@@ -1482,8 +1469,7 @@ void jacobi_evd_sym(Handle& h, const DMat& C, DMat U, double* lambda) {
     gA = h.ws.alloc(int64_t(l) * l);
     gV = h.ws.alloc(int64_t(l) * l);
   }
-  static size_t cur_e = 0;
-  ensure_smem(jacobi_evd_kernel, in_smem ? size_t(2) * l * l * 8 : 0, cur_e);
+  ensure_smem(jacobi_evd_kernel, in_smem ? size_t(2) * l * l * 8 : 0);
   launch_k(h, jacobi_evd_kernel, 1, 1024, in_smem ? size_t(2) * l * l * 8 : 0, 
       C.p, C.ld, l, U.p, U.ld, lambda, gA, gV, in_smem ? 1 : 0, nullptr, h.d_flags);
   RSVD_LAUNCHED(h);

@@ -71,6 +71,7 @@ enum FlagBits : int {
   kFlagAsymmetric = 8,
   kFlagCholBreakdown = 16,
   kFlagPowerCap = 32,
+  kFlagRngPatchOverflow = 64,
 };
 // Raises NumericError if any flag is set (synchronizes the stream).
 void check_flags(Handle& h, const char* what);

@@ -82,6 +82,21 @@ def test_device_log_agreement_with_glibc_is_measured(orc):
     assert mism / len(r2s) < 2e-3
 
 
+def test_exact_mode_window_covers_every_glibc_mismatch(orc):
+    """Exact Omega stream (rng.cu): every polar input whose glibc log differs
+    from the correctly rounded value must fall inside the device's flag window
+    (ddlog.cuh log_near_midpoint), so the host log patches it.  2e6 reference
+    polar inputs here; tools/logwindow.cpp runs the same check over 1e9 per
+    glibc ifunc variant (profiles/r02_logwindow.txt)."""
+    import paper_2402_17794_b200 as eng
+    r2, lg = orc.Rng(20260).polar_r2_log(2_000_000)
+    cr, flag = eng.debug_log_window(r2)
+    mism = cr != lg
+    assert mism.sum() > 500  # glibc is not correctly rounded (~0.08 %)
+    assert not (mism & ~flag).any(), r2[mism & ~flag][:5]
+    assert flag.mean() < 0.025  # the window stays narrow (~1.7 % flagged)
+
+
 def test_library_loads_before_torch_without_breaking_it():
     """The engine links PyTorch's NCCL (same SONAME as the system copy): loading
     it first must not break a later `import torch` (the build() -> smoke()

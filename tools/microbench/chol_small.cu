@@ -7,7 +7,7 @@
 
 __global__ void run(const double* G, int l, long long* pr, double* out) {
   constexpr int LD = 33;
-  __shared__ double G0[32 * LD], piv[2 * 72], Rs[32 * LD], Ri[32 * LD];
+  __shared__ double G0[32 * LD], piv[rsvdb::kCholPivScratch], Rs[32 * LD], Ri[32 * LD];
   for (int e = threadIdx.x; e < 32 * LD; e += 256) G0[e] = 0.0;
   __syncthreads();
   for (int e = threadIdx.x; e < l * l; e += 256) G0[(e % l) + LD * (e / l)] = G[e];
@@ -31,8 +31,9 @@ int main() {
     long long h[256];
     cudaMemcpy(h, dp, sizeof h, cudaMemcpyDeviceToHost);
     for (int r = 0; r < 4; ++r) printf("[%lld %lld] ", h[64 * r + 1] - h[64 * r], h[64 * r + 2] - h[64 * r + 1]);
-    printf("\n steps:");
-    for (int j = 0; j < l; ++j) printf(" %lld", h[64 + 8 + j] - (j ? h[64 + 8 + j - 1] : h[64]));
+    // the probe stamps once per barrier (two pivots): print per barrier
+    printf("\n per 2-pivot barrier:");
+    for (int j = 0; j < l; j += 2) printf(" %lld", h[64 + 8 + j] - (j ? h[64 + 8 + j - 2] : h[64]));
     printf("  err=%s\n", cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
