@@ -1,15 +1,18 @@
 #!/usr/bin/env python
 """Headline benchmark: randomized-SVD factorizations on B200.
 
-Workload (BASELINE.json configs[1] = C2, the config the metric is quoted on):
-Algorithm 3 (power iteration, no re-orthonormalization), A = U diag(sigma) V^T
-8192 x 8192 fp64 with Haar U, V; sigma_j = 1 (j <= 20), 1e-2 (j-20)^-1
-(j > 20); k = 20, p = 5, q = 2; Omega 8192 x 25 from Rng(seed).  One step =
-one full factorization through the public API (rsvd(A, cfg), reference
-factor.hpp:21-24): Omega generation, 6 streaming passes over A, TSQR,
-the small SVD, and the lift.
+Workload (default C5 = BASELINE.json configs[4], the largest configuration that
+fits one GPU: 68.7 GB of A in 180 GB of HBM): Algorithm 6, the single-pass
+general SVD (reference spsvd_general, singlepass.hpp:109-137), A 262144 x
+32768 fp64 = U_r diag(sigma) V_r^T + 1e-6 G with Haar U_r, V_r of rank 1000,
+sigma_j = exp(-j/200); k = 500, p = 50; Omega_c 32768 x 550 then Psi 262144 x
+550 from one Rng(seed).  One step = one full factorization through the public
+API: the exact Omega/Psi streams, ONE fused pass over A (Y_c = A Omega_c and
+W = A^T Psi), CholeskyQR of Y_c and W, the four l x l inner products, the
+Kronecker joint core solve, its SVD and the two lifts.  --config C1..C4 select
+the other BASELINE configurations (parity-test cases, not the headline).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
 
 Multi-GPU (torchrun, one rank per GPU): A is row-sharded; n x l and l x l
 partials are NCCL-allreduced; every rank's time is measured with CUDA events
@@ -218,6 +221,35 @@ def cpu_reference(cfg, steps, warmup, threads, a_host=None):
     return dt
 
 
+def host_info():
+    """The host the CPU legs ran on: the Omega stream's bits depend on glibc's
+    log ifunc (FMA vs SSE2), so the CPU model, flags, glibc and the compiler
+    of the oracle's <random> instantiation are part of the baseline."""
+    import platform
+    info = {"cpu_model": None, "flags": None, "glibc": None, "gcc": None, "glibc_log_ifunc": None}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name") and not info["cpu_model"]:
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+            if line.startswith("flags") and not info["flags"]:
+                fl = set(line.split(":", 1)[1].split())
+                info["flags"] = " ".join(f for f in ("sse4_2", "avx", "avx2", "fma", "avx512f", "amx_tile")
+                                         if f in fl)
+                info["glibc_log_ifunc"] = "FMA" if {"fma", "avx2"} <= fl else "SSE2"
+    except OSError:
+        pass
+    try:
+        info["glibc"] = " ".join(platform.libc_ver())
+    except Exception:
+        pass
+    try:
+        import oracle
+        info["gcc"] = oracle.compiler()
+    except Exception:
+        pass
+    return info
+
+
 def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -236,7 +268,8 @@ def run_reference_arm(args, cfg):
         "cpu_baseline": {"value": value, "unit": "factorizations/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{steps} full {args.config} factorizations, oracle/rsvd_oracle.cpp "
-                                   f"with {threads} OpenBLAS threads"},
+                                   f"with {threads} OpenBLAS threads",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "factorizations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -250,7 +283,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -425,23 +458,30 @@ def main():
     if dp["bound"] == "tensor":
         roof = {"bound": "tensor", "achieved": dp["tflops"], "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": dp["tflops"] / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "peak_source": FP64_PEAK_SOURCE, "kernel": f"pass_kernel ({dom})"}
+                "peak_source": FP64_PEAK_SOURCE,
+                "kernel": "fused_pass_kernel (Y_c = A Omega_c + W = A^T Psi, 4mnl flops)" if dom == "fused"
+                          else f"pass_kernel ({dom})"}
     else:
         roof = {"bound": "hbm", "achieved": dp["gbs"], "peak": hbm, "unit": "GB/s",
                 "frac": dp["gbs"] / hbm, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernel": f"pass_kernel ({dom})"}
 
-    # ---- CPU baseline (rank 0, N = 1 only): the oracle on the host cores
+    # ---- CPU baseline (rank 0, N = 1 only): the oracle on the host cores,
+    # on the pinned host copy of A the e2e leg already holds (C5: one 68.7 GB
+    # host copy, not two)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        a_np = np.asfortranarray(a_full.cpu().numpy())
         threads = os.cpu_count() or 1
-        dt = cpu_reference(cfg, 2, 1, threads, a_np)
-        dt1 = cpu_reference(cfg, 1, 0, 1, a_np) if args.config in ("C1", "C2") else None
+        big = cfg["m"] * cfg["n"] * 8 > (8 << 30)
+        # bounded sample: one factorization for the multi-GB configs (C3-C5:
+        # ~10-40 s each on 16 cores), two (after one warm-up) below
+        nrep, nwarm = (1, 0) if big else (2, 1)
+        dt = cpu_reference(cfg, nrep, nwarm, threads, a_host)
+        dt1 = cpu_reference(cfg, 1, 0, 1, a_host) if args.config in ("C1", "C2") else None
         cpu = {"value": 1.0 / dt, "unit": "factorizations/s", "cores": threads, "kind": "port",
-               "sample": f"2 full {args.config} factorizations, oracle/rsvd_oracle.cpp "
+               "sample": f"{nrep} full {args.config} factorization(s), oracle/rsvd_oracle.cpp "
                          f"(libstdc++ mt19937_64 + OpenBLAS {threads} threads)",
-               "value_1thread": (1.0 / dt1) if dt1 else None}
+               "value_1thread": (1.0 / dt1) if dt1 else None, "host": host_info()}
 
     if rank == 0:
         line = {
@@ -458,7 +498,10 @@ def main():
                               "inputs larger than L2 (|A| = %.0f MB)") % (m * n * 8 / 1e6)},
             "e2e": {"value": 1000.0 / e2e_ms, "unit": "factorizations/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms, "api": "rsvd_rsvd_host (pinned host A)"},
+                    "ms_per_step": e2e_ms,
+                    "api": {5: "rsvd_spevd_host", 6: "rsvd_spsvd_host"}.get(cfg["alg"], "rsvd_rsvd_host")
+                           + " (pinned host A" + (", streamed in row panels into the pass)"
+                                                  if cfg["alg"] >= 5 else ")")},
             "roofline": roof,
             "passes": passes,
             "profiled_run_ms_per_step": ms_prof / args.steps,

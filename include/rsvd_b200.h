@@ -237,6 +237,15 @@ rsvd_status rsvd_apply_adjoint_dev(rsvd_handle* h, int64_t m, int64_t n, const d
                                    int64_t lda, int64_t l, const double* y, int64_t ldy,
                                    double* z, int64_t ldz);
 
+/* Alg 6's fused pass alone (Y = A Omega_c, W = A^T Psi from one traversal of
+ * A; A m x n, Omega_c n x l, Psi m x l): for unit parity tests.
+ * panel_rows > 0 issues it in row panels (the streamed launch sequence);
+ * macroblock > 0 overrides the macroblock edge (multiple of 64). */
+rsvd_status rsvd_debug_dual_pass_dev(rsvd_handle* h, int64_t m, int64_t n, int64_t l,
+                                     const double* a, int64_t lda, const double* oc, int64_t ldo,
+                                     const double* psi, int64_t ldp, double* y, int64_t ldy,
+                                     double* w, int64_t ldw, int64_t panel_rows, int macroblock);
+
 /* ------------------------------------------- rangefinder.hpp (L2) */
 /* range_basis(A, cfg, rng) (reference rangefinder.hpp:97-105): Q m x (k+p). */
 rsvd_status rsvd_range_basis_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,
@@ -264,8 +273,10 @@ rsvd_status rsvd_spevd_host(rsvd_handle* h, int64_t n, const double* a, int64_t 
                             int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                             double* lambda);
 /* spsvd_general(A, k, p, rng) (reference singlepass.hpp:109-137): Y_c = A
- * Omega_c and W = A^T Psi (one apply, one adjoint; two streaming passes, see
- * DESIGN.md section 6).  U m x k, sigma k, V n x k. */
+ * Omega_c and W = A^T Psi formed in ONE traversal of A (counted as one
+ * apply, one adjoint, one physical pass).  U m x k, sigma k, V n x k.  The
+ * _host variants (this and spevd) stream A up in row panels and compute on
+ * each panel as it lands. */
 rsvd_status rsvd_spsvd_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a, int64_t lda,
                            int64_t k, int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                            double* sigma, double* v, int64_t ldv);

@@ -73,6 +73,7 @@ def lib():
         L.orc_rng_get_state.argtypes = [P, ctypes.POINTER(RngState)]
         L.orc_rng_set_state.argtypes = [P, ctypes.POINTER(RngState)]
         L.orc_set_threads.argtypes = [I]
+        L.orc_compiler.restype = ctypes.c_char_p
         L.orc_gaussian.argtypes = [I64, I64, P, P]
         L.orc_gemm.argtypes = [I64, I64, I64, P, I, P, I, P]
         L.orc_orthonormalize.argtypes = [I64, I64, P, P]
@@ -104,6 +105,10 @@ def _f(a):
 
 def _p(a):
     return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def compiler() -> str:
+    return lib().orc_compiler().decode()
 
 
 def set_threads(n: int) -> None:

@@ -672,6 +672,8 @@ extern "C" {
 
 const char* orc_last_error() { return g_last_error.c_str(); }
 void orc_set_threads(int n) { scipy_openblas_set_num_threads(n); }
+// The compiler that instantiated the libstdc++ <random> templates of the Omega stream.
+const char* orc_compiler() { return "g++ " __VERSION__; }
 int orc_get_threads() { return scipy_openblas_get_num_threads(); }
 
 void* orc_rng_new(uint64_t seed) { return new Rng(seed); }

@@ -171,6 +171,8 @@ def _load():
         L.rsvd_version.restype = ctypes.c_char_p
         L.rsvd_debug_log_cr.argtypes = [D]
         L.rsvd_debug_log_cr.restype = D
+        L.rsvd_debug_dual_pass_dev.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, I64, P, I64, P, I64, I64, I]
+        L.rsvd_debug_dual_pass_dev.restype = ctypes.c_int
         L.rsvd_debug_log_window.argtypes = [ctypes.c_void_p, I64, ctypes.c_void_p, ctypes.c_void_p]
         L.rsvd_debug_log_window.restype = None
         _lib = L
@@ -240,7 +242,7 @@ class Engine:
 
     def profile_read(self) -> dict:
         out = {}
-        for kind, name in ((0, "apply"), (1, "adjoint"), (2, "other")):
+        for kind, name in ((0, "apply"), (1, "adjoint"), (2, "other"), (3, "fused")):
             n, ms, fl, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
             _check(_load().rsvd_profile_read(self._h, kind, ctypes.byref(n), ctypes.byref(ms),
                                              ctypes.byref(fl), ctypes.byref(by)))
@@ -634,6 +636,7 @@ class CountingOperator:
         self._a = a
         self.apply_count_ = 0
         self.adjoint_count_ = 0
+        self.physical_passes_ = 0
 
     def matrix(self):
         return self._a
@@ -649,6 +652,11 @@ class CountingOperator:
 
     def adjoint_count(self) -> int:
         return self.adjoint_count_
+
+    def physical_passes(self) -> int:
+        """Streaming traversals of A (engine extension): Alg 6's fused pass
+        counts one apply, one adjoint and ONE physical pass."""
+        return self.physical_passes_
 
     def apply(self, x):
         self.apply_count_ += 1
@@ -670,6 +678,7 @@ def _counted(a, fn):
     if op is not None:
         op.apply_count_ += after["apply"] - before["apply"]
         op.adjoint_count_ += after["adjoint"] - before["adjoint"]
+        op.physical_passes_ += after["physical_passes"] - before["physical_passes"]
     return res
 
 
@@ -779,6 +788,24 @@ def spsvd_host(a: np.ndarray, k: int, p: int, rng: Rng):
 def debug_log_cr(x: float) -> float:
     """Host evaluation of the device polar-sampler log (ddlog.cuh), for tests."""
     return _load().rsvd_debug_log_cr(float(x))
+
+
+def debug_dual_pass(a, oc, psi, panel_rows: int = 0, macroblock: int = 0):
+    """The fused Alg-6 pass alone (fused.cu): returns (A @ oc, A.T @ psi) from
+    one traversal of A.  panel_rows > 0 issues A in row panels of that many
+    rows (the streamed host path's launch sequence); macroblock > 0 overrides
+    the macroblock edge.  Device tensors in, device tensors out."""
+    import torch
+    e = default_engine()
+    m, n = a.shape
+    l = oc.shape[1]
+    y = torch.empty((l, m), dtype=torch.float64, device="cuda").t()
+    w = torch.empty((l, n), dtype=torch.float64, device="cuda").t()
+    ld = lambda t: int(t.stride(1)) if t.shape[1] > 1 else max(int(t.shape[0]), 1)  # noqa: E731
+    _check(_load().rsvd_debug_dual_pass_dev(e.handle, m, n, l, a.data_ptr(), ld(a), oc.data_ptr(), ld(oc),
+                                             psi.data_ptr(), ld(psi), y.data_ptr(), m, w.data_ptr(), n,
+                                             int(panel_rows), int(macroblock)))
+    return y, w
 
 
 def debug_log_window(x):

@@ -695,7 +695,7 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
     double hm[kBJMaxSweeps];
     RSVD_CUDA(cudaMemcpyAsync(hc, work[0].changed, sizeof hc, cudaMemcpyDeviceToHost, h.stream));
     RSVD_CUDA(cudaMemcpyAsync(hm, work[0].smax, sizeof hm, cudaMemcpyDeviceToHost, h.stream));
-    RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    stream_sync(h);
     std::fprintf(stderr, "bjacobi max rel g per sweep:");
     for (int i = 0; i < kBJMaxSweeps && hm[i] > 0.0; ++i) std::fprintf(stderr, " %.1e", std::sqrt(hm[i]));
     std::fprintf(stderr, "\n");

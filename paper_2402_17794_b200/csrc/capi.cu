@@ -13,6 +13,7 @@
 #include "trials.cuh"
 #include "dist.cuh"
 #include "engine.cuh"
+#include "fused.cuh"
 #include "pass.cuh"
 #include "rng.cuh"
 #include "small.cuh"
@@ -71,6 +72,7 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
     cudaGetLastError();  // clear a non-sticky runtime error so the next call starts clean
     if (hd) {
       hd->h.rng_user_out = nullptr;
+      rsvdb::patch_cancel(hd->h);
       cudaStreamSynchronize(hd->h.stream);
       if (hd->h.copy_stream) cudaStreamSynchronize(hd->h.copy_stream);
       cudaMemsetAsync(hd->h.d_flags, 0, sizeof(int), hd->h.stream);
@@ -78,6 +80,10 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
     return e.code;
   } catch (const std::exception& e) {
     g_err = e.what();
+    if (hd) {
+      rsvdb::patch_cancel(hd->h);
+      cudaStreamSynchronize(hd->h.stream);
+    }
     return RSVD_ERR_INTERNAL;
   }
 }
@@ -165,6 +171,11 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     rsvdb::Handle::GraphEntry& e = h.graph_cache[h.prof ? key + "|prof" : key];
     if (e.exec && e.gen == gen_now()) {
       if (rng) std::memcpy(h.h_rng_in, rng, sizeof(rsvd_rng_state));
+      for (rsvdb::PatchHdr* ph : e.patch) {  // re-arm the exact-mode lists
+        ph->ready = 0;
+        ph->done = 0;
+      }
+      h.patch_pending = e.patch;
       RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
       stage_copy_out(h, e.stage, outs);
       add(h.counters, e.delta, 1);
@@ -185,6 +196,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     if (++e.seen >= 2 && !e.bad) {
       h.ws.reset();
       h.patch_chunk = h.patch_off = 0;
+      h.patch_pending.clear();
       h.rng_user_out = nullptr;
       const rsvd_counters before = h.counters;
       const uint64_t g0 = gen_now();
@@ -217,6 +229,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
           for (auto& r : h.prof_pending) r.graph = true;  // the graph keeps these events
           e.prof = h.prof_pending;
           e.stage = h.stage;
+          e.patch = h.patch_pending;  // armed at capture, serviced by finish_call
           RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
           stage_copy_out(h, e.stage, outs);
           h.rng_user_out = rng;
@@ -226,6 +239,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
         cudaGetLastError();
       }
       if (graph) cudaGraphDestroy(graph);
+      h.patch_pending.clear();  // nothing of the failed capture ran
       h.counters = before;
       for (auto& r : h.prof_pending) {  // events of the failed capture back to the pool
         h.prof_pool.push_back(r.a);
@@ -238,6 +252,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     g_err = err.what();
     cudaGetLastError();
     h.rng_user_out = nullptr;
+    rsvdb::patch_cancel(h);
     cudaStreamSynchronize(h.stream);
     cudaMemsetAsync(h.d_flags, 0, sizeof(int), h.stream);
     return err.code;
@@ -319,6 +334,35 @@ struct HostIO {
     }
     return d;
   }
+  // A's upload in row panels on the copy stream, one event per panel, so the
+  // single-pass algorithms compute on panel i while panel i+1 is in flight
+  // (the panels' starts are multiples of the fused pass's macroblock edge).
+  rsvdb::DMat up_panels(const double* a, int64_t r, int64_t c, int64_t ld,
+                        std::vector<rsvdb::Problem::Panel>* panels) {
+    rsvdb::DMat d = h.ws.mat(r, c);
+    panels->clear();
+    if (r * c == 0) return d;
+    const int64_t mb = rsvdb::fused_macroblock(h);
+    // ~24 panels (the last panel's compute is the exposed tail), >= 64 MB each
+    int64_t rows = std::max<int64_t>(rsvdb::ceil_div(r, 24), (int64_t(64) << 20) / (8 * c));
+    rows = std::max<int64_t>(mb, rsvdb::ceil_div(rows, mb) * mb);
+    const int64_t np = rsvdb::ceil_div(r, rows);
+    while (int64_t(h.panel_ev.size()) < np) {
+      cudaEvent_t e;
+      RSVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h.panel_ev.push_back(e);
+    }
+    RSVD_CUDA(cudaEventRecord(h.order_ev, h.stream));  // after this call's earlier work
+    RSVD_CUDA(cudaStreamWaitEvent(h.copy_stream, h.order_ev, 0));
+    for (int64_t i = 0; i < np; ++i) {
+      const int64_t r0 = i * rows, r1 = std::min(r, r0 + rows);
+      RSVD_CUDA(cudaMemcpy2DAsync(d.p + r0, d.ld * 8, a + r0, ld * 8, (r1 - r0) * 8, c,
+                                  cudaMemcpyHostToDevice, h.copy_stream));
+      RSVD_CUDA(cudaEventRecord(h.panel_ev[i], h.copy_stream));
+      panels->push_back({r0, r1, h.panel_ev[i]});
+    }
+    return d;
+  }
   void down(const rsvdb::DMat& d, double* a, int64_t ld) {
     if (d.rows * d.cols > 0)
       RSVD_CUDA(cudaMemcpy2DAsync(a, ld * 8, d.p, d.ld * 8, d.rows * 8, d.cols,
@@ -367,6 +411,7 @@ void rsvd_destroy(rsvd_handle* hd) {
   if (!hd) return;
   rsvdb::Handle& h = hd->h;
   cudaSetDevice(h.device);
+  rsvdb::patch_cancel(h);
   cudaStreamSynchronize(h.stream);
   rsvdb::comm_destroy(h);
   if (h.d_counters) cudaFree(h.d_counters);
@@ -392,6 +437,7 @@ void rsvd_destroy(rsvd_handle* hd) {
     cudaStreamDestroy(h.copy_stream);
   }
   if (h.copy_ev) cudaEventDestroy(h.copy_ev);
+  for (cudaEvent_t e : h.panel_ev) cudaEventDestroy(e);
   if (h.order_ev) cudaEventDestroy(h.order_ev);
   if (h.own_stream) cudaStreamDestroy(h.own_stream);
   delete hd;
@@ -424,7 +470,7 @@ rsvd_status rsvd_profile_enable(rsvd_handle* hd, int on) {
   if (!hd) return RSVD_ERR_PARAMETER;
   rsvdb::Handle& h = hd->h;
   h.prof = on != 0;
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     h.prof_ms[k] = h.prof_flops[k] = h.prof_bytes[k] = 0;
     h.prof_count[k] = 0;
   }
@@ -433,7 +479,7 @@ rsvd_status rsvd_profile_enable(rsvd_handle* hd, int on) {
 
 rsvd_status rsvd_profile_read(rsvd_handle* hd, int kind, int64_t* launches, double* ms,
                               double* flops, double* bytes) {
-  if (!hd || kind < 0 || kind > 2) return RSVD_ERR_PARAMETER;
+  if (!hd || kind < 0 || kind > 3) return RSVD_ERR_PARAMETER;
   rsvdb::Handle& h = hd->h;
   if (launches) *launches = h.prof_count[kind];
   if (ms) *ms = h.prof_ms[kind];
@@ -616,10 +662,10 @@ rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t
                             double* lambda) {
   return guard(hd, "spevd_hermitian", [&](rsvdb::Handle& h) {
     HostIO io{h};
-    cudaEvent_t a_up = nullptr;
-    rsvdb::DMat A = io.up_overlapped(a, n, n, lda, &a_up);
+    std::vector<rsvdb::Problem::Panel> panels;
+    rsvdb::DMat A = io.up_panels(a, n, n, lda, &panels);
     rsvdb::Problem P = rsvdb::make_problem(h, A.p, n, n, A.ld);
-    P.ready = a_up;
+    P.panels = panels;
     const int64_t kk = std::max<int64_t>(k, 0);
     rsvdb::DMat U = h.ws.mat(n, kk);
     double* lam = h.ws.alloc(std::max<int64_t>(kk, 1));
@@ -650,10 +696,10 @@ rsvd_status rsvd_spsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double*
                             double* sigma, double* v, int64_t ldv) {
   return guard(hd, "spsvd_general", [&](rsvdb::Handle& h) {
     HostIO io{h};
-    cudaEvent_t a_up = nullptr;
-    rsvdb::DMat A = io.up_overlapped(a, m, n, lda, &a_up);
+    std::vector<rsvdb::Problem::Panel> panels;
+    rsvdb::DMat A = io.up_panels(a, m, n, lda, &panels);
     rsvdb::Problem P = rsvdb::make_problem(h, A.p, m, n, A.ld);
-    P.ready = a_up;
+    P.panels = panels;
     const int64_t kk = std::max<int64_t>(k, 0);
     rsvdb::DMat U = h.ws.mat(m, kk), V = h.ws.mat(n, kk);
     double* s = h.ws.alloc(std::max<int64_t>(kk, 1));
@@ -663,6 +709,30 @@ rsvd_status rsvd_spsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double*
     io.down(U, u, ldu);
     io.down_vec(s, sigma, kk);
     io.down(V, v, ldv);
+  });
+}
+
+rsvd_status rsvd_debug_dual_pass_dev(rsvd_handle* hd, int64_t m, int64_t n, int64_t l,
+                                     const double* a, int64_t lda, const double* oc, int64_t ldo,
+                                     const double* psi, int64_t ldp, double* y, int64_t ldy,
+                                     double* w, int64_t ldw, int64_t panel_rows, int macroblock) {
+  return guard(hd, "dual_pass", [&](rsvdb::Handle& h) {
+    struct Mb {  // restored on exceptions too
+      rsvdb::Handle& h;
+      int old;
+      ~Mb() { h.fused_mb = old; }
+    } mb_scope{h, h.fused_mb};
+    if (macroblock > 0) h.fused_mb = macroblock;
+    rsvdb::Problem P;
+    P.A = dm(a, m, n, lda);
+    P.dist = h.dist();
+    P.m_global = m;
+    if (panel_rows > 0) {
+      const int64_t mb = rsvdb::fused_macroblock(h);
+      const int64_t rows = std::max<int64_t>(mb, rsvdb::ceil_div(panel_rows, mb) * mb);
+      for (int64_t r0 = 0; r0 < m; r0 += rows) P.panels.push_back({r0, std::min(m, r0 + rows), nullptr});
+    }
+    rsvdb::op_dual(h, P, dm(oc, n, l, ldo), dm(psi, m, l, ldp), dm(y, m, l, ldy), dm(w, n, l, ldw));
   });
 }
 

@@ -99,6 +99,14 @@ class Arena {
 
 struct Comm;  // NCCL communicator wrapper (dist.cu)
 
+// Header of an exact-mode patch list (rng.cu), in pinned mapped memory.
+struct PatchHdr {
+  uint32_t ready;  // device -> host: count is final
+  uint32_t done;   // host -> device: 1 = normals written, 2 = cancelled
+  uint64_t count;
+  int64_t cap;
+};
+
 struct Handle {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -111,6 +119,10 @@ struct Handle {
   // generated on `stream`; the first use of A waits on copy_ev (Problem::ready)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t copy_ev = nullptr, order_ev = nullptr;
+  // one event per row panel of a streamed upload (single-pass host entry points)
+  std::vector<cudaEvent_t> panel_ev;
+  // fused Alg-6 pass macroblock edge override (0 = RSVD_FUSED_MB / default)
+  int fused_mb = 0;
   Arena ws;
   int* d_counters = nullptr;   // split-K tile semaphores (kept zeroed)
   int64_t n_counters = 0;
@@ -129,14 +141,14 @@ struct Handle {
   bool prof = false;
   struct ProfRec {
     cudaEvent_t a, b;
-    int kind;  // 0 = NN (Y = A X), 1 = TN (Z = A^T Y)
+    int kind;  // 0 = NN (Y = A X), 1 = TN (Z = A^T Y), 2 = other, 3 = fused Alg-6 pass
     double flops, bytes;
     bool graph = false;  // events owned by a captured graph (not pooled)
   };
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> prof_pool;
-  double prof_ms[3] = {0, 0, 0}, prof_flops[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
-  int64_t prof_count[3] = {0, 0, 0};
+  double prof_ms[4] = {0, 0, 0, 0}, prof_flops[4] = {0, 0, 0, 0}, prof_bytes[4] = {0, 0, 0, 0};
+  int64_t prof_count[4] = {0, 0, 0, 0};
   // Launch-site trace (rsvd_trace_enable): an event after every launch; the
   // time between consecutive events (kernel + any idle gap before it) is
   // charged to the launch site at the call's final synchronization.
@@ -159,6 +171,7 @@ struct Handle {
   // handle (captured graphs keep pointers into them).
   std::vector<std::pair<char*, size_t>> patch_chunks;
   size_t patch_chunk = 0, patch_off = 0;
+  std::vector<PatchHdr*> patch_pending;  // lists of this call, queue order
   // pinned staging for the per-trial seeded states of batched trials (trials.cu)
   rsvd_rng_state* h_rng_batch = nullptr;
   int64_t h_rng_batch_cap = 0;
@@ -183,6 +196,7 @@ struct Handle {
     int seen = 0;
     bool bad = false;  // not capturable (host synchronization inside the call)
     std::vector<DMat> stage;  // output staging the graph writes (copied out per call)
+    std::vector<PatchHdr*> patch;  // exact-mode lists the graph waits on (re-armed per launch)
   };
   // output staging of the current graph-cached call (see capi.cu guard_graph)
   std::vector<DMat> stage;
@@ -240,6 +254,13 @@ void finish_call(Handle& h, const char* what);
 void trace_mark(Handle& h, const char* site);
 void trace_begin(Handle& h);
 void trace_collect(Handle& h);
+
+// Answer / cancel this call's exact-mode lists (rng.cu); stream_sync services
+// them and then synchronizes h.stream -- every mid-call host wait goes
+// through it (a plain synchronize would wait on a kernel that waits on us).
+void patch_service(Handle& h);
+void patch_cancel(Handle& h);
+void stream_sync(Handle& h);
 
 // Opt `kernel` into `bytes` of dynamic shared memory on the CURRENT device.
 // The attribute belongs to the device context, so it is tracked per

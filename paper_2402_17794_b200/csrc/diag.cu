@@ -323,7 +323,7 @@ __global__ void sum_kernel(const double* __restrict__ part, int G, double* out) 
 double read_scalar(Handle& h, const double* d) {
   double v = 0.0;
   RSVD_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, h.stream));
-  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  stream_sync(h);
   return v;
 }
 
@@ -446,7 +446,7 @@ double spectral_norm_impl(Handle& h, const DMat& M, int64_t* iterations) {
   check_flags(h, "spectral_norm");  // the 5000-step cap (core.hpp:220)
   double out[2];
   RSVD_CUDA(cudaMemcpyAsync(out, p.out, sizeof out, cudaMemcpyDeviceToHost, h.stream));
-  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  stream_sync(h);
   if (iterations) *iterations = int64_t(out[1]);
   return out[0];
 }

@@ -102,7 +102,7 @@ void shard_rows(Handle& h, int64_t m_local, int64_t* m_global, int64_t* row_offs
   std::vector<double> all(size_t(h.nranks));
   RSVD_CUDA(cudaMemcpyAsync(all.data(), d + 1, 8 * size_t(h.nranks), cudaMemcpyDeviceToHost,
                             h.stream));
-  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  stream_sync(h);
   int64_t tot = 0, off = 0;
   for (int r = 0; r < h.nranks; ++r) {
     if (r == h.rank) off = tot;

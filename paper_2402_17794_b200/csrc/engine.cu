@@ -18,6 +18,7 @@
 #include "dist.cuh"
 #include "engine.cuh"
 #include "pass.cuh"
+#include "fused.cuh"
 #include "rng.cuh"
 #include "small.cuh"
 
@@ -94,7 +95,7 @@ void* Arena::alloc_bytes(size_t bytes) {
 int* tile_counters(Handle& h, int64_t n) {
   if (n > h.n_counters) {
     if (h.d_counters) {
-      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      stream_sync(h);
       RSVD_CUDA(cudaFree(h.d_counters));
     }
     const int64_t cap = std::max<int64_t>(n, 4096);
@@ -152,6 +153,7 @@ void trace_collect(Handle& h) {
 void finish_call(Handle& h, const char* what) {
   rsvd_rng_state* user = h.rng_user_out;
   h.rng_user_out = nullptr;
+  patch_service(h);  // exact-mode Omega lists the queued kernels wait on
   if (h.copy_stream) RSVD_CUDA(cudaStreamSynchronize(h.copy_stream));  // an upload nothing waited on
   check_flags(h, what);  // synchronizes
   if (user) std::memcpy(user, h.h_rng, sizeof(rsvd_rng_state));
@@ -326,9 +328,22 @@ void check_symmetric(Handle& h, const DMat& C, bool dist_unused) {
 // ------------------------------------------------------------ operators
 static void a_ready(Handle& h, const Problem& P) {
   if (P.ready) RSVD_CUDA(cudaStreamWaitEvent(h.stream, P.ready, 0));
+  for (const Problem::Panel& pn : P.panels)
+    if (pn.ready) RSVD_CUDA(cudaStreamWaitEvent(h.stream, pn.ready, 0));
 }
 
 void op_apply(Handle& h, const Problem& P, const DMat& X, DMat Y) {
+  if (!P.panels.empty()) {
+    // streamed upload: each row panel's rows of Y as soon as the panel lands
+    for (const Problem::Panel& pn : P.panels) {
+      if (pn.ready) RSVD_CUDA(cudaStreamWaitEvent(h.stream, pn.ready, 0));
+      gemm_nn(h, DMat(P.A.p + pn.row0, pn.row1 - pn.row0, P.A.cols, P.A.ld), X,
+              DMat(Y.p + pn.row0, pn.row1 - pn.row0, Y.cols, Y.ld));
+    }
+    h.counters.apply++;
+    h.counters.physical_passes++;
+    return;
+  }
   a_ready(h, P);
   gemm_nn(h, P.A, X, Y);
   h.counters.apply++;
@@ -339,6 +354,34 @@ void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z) {
   a_ready(h, P);
   gemm_tn(h, P.A, Y, Z);
   if (P.dist) allreduce_mat(h, Z);
+  h.counters.adjoint++;
+  h.counters.physical_passes++;
+}
+
+// Alg 6's two sketches from one traversal of A (fused.cu): counts one apply,
+// one adjoint and ONE physical pass (the CountingOperator contract,
+// singlepass.hpp:15-40, plus the single-pass property of Alg 6).  A host
+// entry point that streams A in row panels runs one launch per panel as it
+// lands (P.panels); otherwise one launch covers A.
+void op_dual(Handle& h, const Problem& P, const DMat& Oc, const DMat& Psi, DMat Yc, DMat W) {
+  const DMat Ov = tma_view(h, Oc), Pv = tma_view(h, Psi);
+  DMat A = P.A;
+  if (!tma_ok(A)) {
+    a_ready(h, P);
+    A = tma_view(h, P.A);
+  }
+  int* sem = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(fused_semaphores(A.rows, A.cols, Oc.cols)) * 4));
+  if (P.panels.empty() || A.p != P.A.p) {
+    a_ready(h, P);
+    fused_dual_pass(h, A, Ov, Pv, Yc, W, 0, A.rows, sem, true);
+  } else {
+    for (size_t i = 0; i < P.panels.size(); ++i) {
+      if (P.panels[i].ready) RSVD_CUDA(cudaStreamWaitEvent(h.stream, P.panels[i].ready, 0));
+      fused_dual_pass(h, A, Ov, Pv, Yc, W, P.panels[i].row0, P.panels[i].row1, sem, i == 0);
+    }
+  }
+  if (P.dist) allreduce_mat(h, W);
+  h.counters.apply++;
   h.counters.adjoint++;
   h.counters.physical_passes++;
 }
@@ -522,15 +565,18 @@ void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
                 DMat U, double* lambda) {
   const int64_t n = P.A.cols, ml = P.A.rows;
   if (P.m_global != n) throw_dim("spevd_hermitian: matrix is not square");
-  if (check_sym && !P.dist) {
-    // reference singlepass.hpp:49-53: uncounted precondition read of A
-    a_ready(h, P);
-    check_symmetric(h, P.A, false);
-    check_flags(h, "spevd_hermitian");
-  }
   if (k < 1) throw_param("spevd_hermitian: k must be >= 1");
   if (p < 0) throw_param("spevd_hermitian: p must be >= 0");
   if (k + p > n) throw_dim("spevd_hermitian: k+p exceeds n");
+  // Reference singlepass.hpp:49-53: an uncounted precondition read of A.  It
+  // raises a sticky device flag that the call's final check turns into the
+  // reference's NumericError (no mid-call host wait, so the call stays
+  // graph-replayable); a streamed upload checks once every panel has landed.
+  const bool sym_first = check_sym && !P.dist && P.panels.empty();
+  if (sym_first) {
+    a_ready(h, P);
+    check_symmetric(h, P.A, false);
+  }
   const int64_t l = k + p;
   DMat Omega = h.ws.mat(n, l);
   gaussian_dev(h, n, l, rng, Omega);
@@ -542,6 +588,10 @@ void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
     } cfg_scope{h};
     h.pass_cfg_big = 1;
     op_apply(h, P, Omega, Y);  // the single pass over A
+  }
+  if (check_sym && !P.dist && !sym_first) {
+    a_ready(h, P);
+    check_symmetric(h, P.A, false);
   }
   DMat Q = h.ws.mat(ml, l);
   orthonormalize(h, Y, Q, nullptr, P.dist);
@@ -577,8 +627,7 @@ void spsvd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
   DMat Psi = h.ws.mat(ml, l);
   gaussian_dev(h, m, l, rng, Psi, P.row_off, P.row_off + ml);  // Omega_r (local rows)
   DMat Yc = h.ws.mat(ml, l), W = h.ws.mat(n, l);
-  op_apply(h, P, Oc, Yc);     // Y_c = A Omega_c
-  op_adjoint(h, P, Psi, W);   // Y_r = A^T Omega_r
+  op_dual(h, P, Oc, Psi, Yc, W);  // Y_c = A Omega_c and Y_r = A^T Omega_r, ONE pass over A
   DMat Qc = h.ws.mat(ml, l), Qr = h.ws.mat(n, l);
   orthonormalize(h, Yc, Qc, nullptr, P.dist);
   orthonormalize(h, W, Qr, nullptr, false);

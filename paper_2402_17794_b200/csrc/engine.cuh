@@ -1,5 +1,7 @@
 // Pipelines (engine.cu).
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 #include "rng.cuh"
 
@@ -11,11 +13,19 @@ struct Problem {
   int64_t row_off = 0;
   bool dist = false;
   cudaEvent_t ready = nullptr;  // A's upload (host entry points): waited on before first use
+  // Row panels of a streamed upload (host entry points of the single-pass
+  // algorithms): rows [row0, row1) are resident once `ready` fires.
+  struct Panel {
+    int64_t row0, row1;
+    cudaEvent_t ready;
+  };
+  std::vector<Panel> panels;
 };
 
 Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda);
 void op_apply(Handle& h, const Problem& P, const DMat& X, DMat Y);
 void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z);
+void op_dual(Handle& h, const Problem& P, const DMat& Oc, const DMat& Psi, DMat Yc, DMat W);
 void check_symmetric(Handle& h, const DMat& C, bool dist);
 
 // thin SVD without the sign rule (engine.cu)

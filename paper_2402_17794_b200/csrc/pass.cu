@@ -571,6 +571,45 @@ CUtensorMap make_map(const double* p, int64_t rows, int64_t cols, int64_t ld, in
   return m;
 }
 
+ProfScope::ProfScope(Handle& hh, int kind, double flops, double bytes) : h(hh) {
+  if (!h.prof) return;
+  on = true;
+  for (int i = 0; i < 2; ++i) {
+    cudaEvent_t e;
+    if (h.prof_pool.empty()) {
+      RSVD_CUDA(cudaEventCreate(&e));
+    } else {
+      e = h.prof_pool.back();
+      h.prof_pool.pop_back();
+    }
+    (i == 0 ? rec.a : rec.b) = e;
+  }
+  rec.kind = kind;
+  rec.flops = flops;
+  rec.bytes = bytes;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  RSVD_CUDA(cudaStreamIsCapturing(h.stream, &cap));
+  // under capture the event must be an external event-record node to be timeable
+  flags = (cap == cudaStreamCaptureStatusActive) ? cudaEventRecordExternal : cudaEventRecordDefault;
+  RSVD_CUDA(cudaEventRecordWithFlags(rec.a, h.stream, flags));
+}
+
+void ProfScope::end() {
+  if (!on) return;
+  on = false;
+  RSVD_CUDA(cudaEventRecordWithFlags(rec.b, h.stream, flags));
+  h.prof_pending.push_back(rec);
+}
+
+// Copy into an aligned, even-ld workspace when TMA cannot address x directly.
+DMat tma_view(Handle& h, const DMat& x) {
+  if (tma_ok(x)) return x;
+  DMat y = h.ws.mat(x.rows, x.cols);
+  RSVD_CUDA(cudaMemcpy2DAsync(y.p, y.ld * 8, x.p, x.ld * 8, x.rows * 8, x.cols,
+                              cudaMemcpyDeviceToDevice, h.stream));
+  return y;
+}
+
 bool tma_ok(const DMat& x) {
   return (reinterpret_cast<uintptr_t>(x.p) % 16 == 0) && (x.ld % 2 == 0) && x.ld >= x.rows;
 }
@@ -584,7 +623,7 @@ void probe_report(Handle& h, const unsigned long long* dprobe, int64_t nct, int6
                   int64_t K, int stream_k) {
   std::vector<unsigned long long> v(size_t(nct) * 16);
   RSVD_CUDA(cudaMemcpyAsync(v.data(), dprobe, v.size() * 8, cudaMemcpyDeviceToHost, h.stream));
-  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  stream_sync(h);
   unsigned long long t0 = ~0ull, t1 = 0;
   for (int64_t c = 0; c < nct; ++c) {
     t0 = std::min(t0, v[size_t(c) * 16]);
@@ -724,31 +763,11 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
   CUtensorMap ta = kNN ? make_map(P.p, P.rows, P.cols, P.ld, 16, BK)
                        : make_map(P.p, P.rows, P.cols, P.ld, 16, Cfg::BM);
   CUtensorMap tb = make_map(R.p, R.rows, R.cols, R.ld, 16, BN);
-  Handle::ProfRec rec{};
-  unsigned rec_flags = cudaEventRecordDefault;
-  if (h.prof) {
-    for (int i = 0; i < 2; ++i) {
-      cudaEvent_t e;
-      if (h.prof_pool.empty()) {
-        RSVD_CUDA(cudaEventCreate(&e));
-      } else {
-        e = h.prof_pool.back();
-        h.prof_pool.pop_back();
-      }
-      (i == 0 ? rec.a : rec.b) = e;
-    }
-    // kinds: 0 = apply pass over A (A X), 1 = adjoint pass (A^T Y), 2 = other
-    // skinny products (the lift Q U_B): the streamed operand is A exactly when
-    // both of its dimensions dwarf the skinny one
-    rec.kind = (std::min(M, K) > 2 * N) ? (kNN ? 0 : 1) : 2;
-    rec.flops = 2.0 * double(M) * double(N) * double(K);
-    rec.bytes = 8.0 * (double(M) * K + double(K) * N + double(M) * N);
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    RSVD_CUDA(cudaStreamIsCapturing(h.stream, &cap));
-    // under capture the event must be an external event-record node to be timeable
-    rec_flags = (cap == cudaStreamCaptureStatusActive) ? cudaEventRecordExternal : cudaEventRecordDefault;
-    RSVD_CUDA(cudaEventRecordWithFlags(rec.a, h.stream, rec_flags));
-  }
+  // kinds: 0 = apply pass over A (A X), 1 = adjoint pass (A^T Y), 2 = other
+  // skinny products (the lift Q U_B): the streamed operand is A exactly when
+  // both of its dimensions dwarf the skinny one
+  ProfScope prof(h, (std::min(M, K) > 2 * N) ? (kNN ? 0 : 1) : 2, 2.0 * double(M) * double(N) * double(K),
+                 8.0 * (double(M) * K + double(K) * N + double(M) * N));
   static const bool probe_pass = std::getenv("RSVD_PROBE_PASS") != nullptr;
   const int64_t nct = int64_t(grid.x) * grid.y * grid.z;
   if (probe_pass) {
@@ -768,20 +787,9 @@ void launch(Handle& h, const DMat& P, const DMat& R, DMat C, int64_t M, int64_t 
     RSVD_LAUNCHED(h);
   }
   if (probe_pass) probe_report(h, pp.probe, nct, M, N, K, pp.stream_k);
-  if (h.prof) {
-    RSVD_CUDA(cudaEventRecordWithFlags(rec.b, h.stream, rec_flags));
-    h.prof_pending.push_back(rec);
-  }
+  prof.end();
 }
 
-// Copy into an aligned, even-ld workspace when TMA cannot address x directly.
-DMat tma_view(Handle& h, const DMat& x) {
-  if (tma_ok(x)) return x;
-  DMat y = h.ws.mat(x.rows, x.cols);
-  RSVD_CUDA(cudaMemcpy2DAsync(y.p, y.ld * 8, x.p, x.ld * 8, x.rows * 8, x.cols,
-                              cudaMemcpyDeviceToDevice, h.stream));
-  return y;
-}
 
 // Kernel-variant override for tuning experiments (tools/pass_sweep.py); 0 = default.
 // Measured on C2 (l = 25), all within 0-9 % slower than the default: BM 256

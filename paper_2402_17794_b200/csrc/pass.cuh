@@ -15,4 +15,18 @@ void gemm_tn(Handle& h, const DMat& P, const DMat& R, DMat C, int force_splits =
 CUtensorMap make_map(const double* p, int64_t rows, int64_t cols, int64_t ld, int box_inner,
                      int box_outer);
 bool tma_ok(const DMat& x);
+// x itself when tma_ok, else a copy in an aligned even-ld workspace.
+DMat tma_view(Handle& h, const DMat& x);
+// Live per-launch timing of a streaming pass (rsvd_profile_enable): CUDA
+// events on h.stream around the launch, folded into per-kind totals at the
+// call's final synchronization.  Kinds: 0 apply, 1 adjoint, 2 other skinny
+// products, 3 the fused Alg-6 pass.
+struct ProfScope {
+  ProfScope(Handle& h, int kind, double flops, double bytes);
+  void end();
+  Handle& h;
+  Handle::ProfRec rec{};
+  unsigned flags = 0;
+  bool on = false;
+};
 }  // namespace rsvdb

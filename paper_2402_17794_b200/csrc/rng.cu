@@ -31,13 +31,21 @@
 // inputs -- always ones whose exact log lies within ~0.02 ulp of a rounding
 // midpoint (ddlog.cuh log_near_midpoint; ~1.7 % of inputs fall inside the
 // window).  polar_write appends every such accepted pair (stream index, r2, x,
-// y) to a pinned, device-mapped list; a host node (cudaLaunchHostFunc, so the
-// call stays graph-capturable) evaluates libstdc++'s multiplier
-// sqrt(-2 * std::log(r2) / r2) with the HOST's own glibc log on a small thread
-// pool; polar_patch rewrites those normals (and the cached variate).  The
-// result is the reference's stream bit for bit on the host that runs it,
-// whichever glibc ifunc (FMA or SSE2) that host selects.
+// y) to a pinned, device-mapped list; patch_signal publishes its length in
+// the list's header; the calling host thread -- which has already queued the
+// whole call and is about to wait for it anyway -- spins on that header,
+// evaluates libstdc++'s multiplier sqrt(-2 * std::log(r2) / r2) with the
+// HOST's own glibc log (a spinning worker pool for long lists) and releases
+// the header; polar_patch, spinning on the release, rewrites those normals
+// (and the cached variate).  No host node and no mid-call synchronization:
+// the GPU waits ~the host's compute time, and the call stays graph-replayable
+// (a replay re-arms the same headers and answers them after the launch; an
+// eager call answers each list as soon as it is queued).  The result is the reference's stream
+// bit for bit on the host that runs it, whichever glibc ifunc (FMA or SSE2)
+// that host selects.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstdlib>
@@ -296,7 +304,7 @@ __global__ void scan_counts_kernel(const int* __restrict__ cnt, int64_t ntiles,
 }
 
 // Exact-mode patch list (pinned, device-mapped): written by polar_write,
-// completed by the host node, applied by polar_patch.
+// completed by the host (patch_service), applied by polar_patch.
 struct PatchEntry {
   int64_t e0;  // stream index of the pair's first normal
   double r2, x, y;
@@ -405,6 +413,7 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
           const int64_t idx = int64_t(base) + __popc(nb & ((1u << lane) - 1u));
           if (idx < pl.cap) {
             pl.ent[idx] = PatchEntry{e0, p.r2, p.x, p.y};
+            __threadfence_system();  // visible to the host before patch_signal's header store
           } else {
             atomicOr(flags, kFlagRngPatchOverflow);
           }
@@ -421,13 +430,54 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
   }
 }
 
-// 3b. exact mode: the host-evaluated normals of the near-midpoint pairs.
-__global__ void polar_patch_kernel(const unsigned long long* __restrict__ count,
-                                   const PatchEntry* __restrict__ ent,
-                                   const PatchOut* __restrict__ po, int64_t cap, GaussOut g,
-                                   DevState* st) {
+// 3b. exact mode: publish the list length to the host (after polar_write).
+__global__ void patch_signal_kernel(const unsigned long long* __restrict__ count, PatchHdr* hdr) {
   RSVD_PDL_ENTRY();
-  const int64_t n = min(int64_t(*count), cap);
+  hdr->count = *count;
+  __threadfence_system();
+  asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(&hdr->ready), "r"(1u) : "memory");
+}
+
+// 3c. exact mode: wait for the host's normals, write them (and the cache).
+// CTA 0 polls the host-written header (one PCIe read per ~1 us); the other
+// CTAs poll a device-memory gate it opens.  Grid <= SMs, so all CTAs are
+// co-resident.  A host that never answers (it died) makes the kernel trap
+// after ~60 s rather than hang the GPU.
+__global__ void __launch_bounds__(256) polar_patch_kernel(
+    const PatchHdr* hdr, unsigned* __restrict__ gate, const PatchEntry* __restrict__ ent,
+    const PatchOut* __restrict__ po, int64_t cap, GaussOut g, DevState* st) {
+  RSVD_PDL_ENTRY();
+  __shared__ unsigned verdict;
+  if (threadIdx.x == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned d = 0;
+    if (blockIdx.x == 0) {
+      for (;;) {
+        asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(d) : "l"(&hdr->done) : "memory");
+        if (d) break;
+        __nanosleep(1000);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 60ull * 1000000000ull) __trap();
+      }
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gate), "r"(d) : "memory");
+    } else {
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(gate) : "memory");
+        if (d) break;
+        __nanosleep(500);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 60ull * 1000000000ull) __trap();
+      }
+    }
+    verdict = d;
+  }
+  __syncthreads();
+  if (verdict != 1) return;  // cancelled (the call failed on the host)
+  const int64_t n = min(int64_t(hdr->count), cap);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t e0 = ent[i].e0;
@@ -476,8 +526,8 @@ __global__ void rng_finish_kernel(const uint64_t* __restrict__ words,
 }
 
 // ------------------------------------------------ exact mode, host side
-// A small process-wide pool for the host node's log evaluations (a CUDA host
-// function must not call CUDA; plain threads are fine).
+// Worker pool for long patch lists.  Workers spin (pause loop) for a while
+// after each job so back-to-back calls dispatch in ~0.1 us, then sleep.
 class HostPool {
  public:
   static HostPool& get() {
@@ -486,96 +536,86 @@ class HostPool {
   }
   // f(lo, hi) over [0, n) in up to size()+1 chunks; the caller runs one.
   void run(int64_t n, const std::function<void(int64_t, int64_t)>& f) {
-    const int nw = int(workers_.size());
     static const int64_t kMinChunk = [] {
       const char* e = std::getenv("RSVD_HOST_MIN_CHUNK");
-      return int64_t(e ? std::max(1, std::atoi(e)) : 512);
+      return int64_t(e ? std::max(1, std::atoi(e)) : 256);
     }();
+    const int nw = int(workers_.size());
     const int parts = int(std::min<int64_t>(nw + 1, (n + kMinChunk - 1) / kMinChunk));
     if (parts <= 1) {
       if (n > 0) f(0, n);
       return;
     }
-    std::unique_lock<std::mutex> lk(m_);
     fn_ = &f;
     n_ = n;
     parts_ = parts;
-    next_ = 1;
-    pending_ = parts - 1;
-    ++epoch_;
-    cv_.notify_all();
-    lk.unlock();
+    pending_.store(parts - 1, std::memory_order_relaxed);
+    next_.store(1, std::memory_order_relaxed);
+    epoch_.fetch_add(1, std::memory_order_release);
+    if (sleepers_.load(std::memory_order_acquire) > 0) {
+      std::lock_guard<std::mutex> lk(m_);
+      cv_.notify_all();
+    }
     f(0, n / parts);
-    lk.lock();
-    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    while (pending_.load(std::memory_order_acquire) > 0) spin_pause();
     fn_ = nullptr;
   }
 
  private:
+  static void spin_pause() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
   HostPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    int nw = int(std::min(16u, hw)) - 1;
+    int nw = int(std::min(8u, hw)) - 1;
     if (const char* e = std::getenv("RSVD_HOST_THREADS")) nw = std::max(0, std::atoi(e) - 1);
     for (int i = 0; i < nw; ++i) workers_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
+    stop_.store(true);
     {
       std::lock_guard<std::mutex> lk(m_);
-      stop_ = true;
+      cv_.notify_all();
     }
-    cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
   void loop() {
-    uint64_t seen = 0;
-    std::unique_lock<std::mutex> lk(m_);
+    uint64_t seen = epoch_.load();
     for (;;) {
-      cv_.wait(lk, [&] { return stop_ || (epoch_ != seen && next_ < parts_); });
-      if (stop_) return;
-      seen = epoch_;
-      while (next_ < parts_) {
-        const int k = next_++;
+      // spin ~2 ms for the next job, then sleep
+      const auto t0 = std::chrono::steady_clock::now();
+      while (epoch_.load(std::memory_order_acquire) == seen && !stop_.load()) {
+        spin_pause();
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+          std::unique_lock<std::mutex> lk(m_);
+          sleepers_.fetch_add(1);
+          cv_.wait(lk, [&] { return epoch_.load() != seen || stop_.load(); });
+          sleepers_.fetch_sub(1);
+        }
+      }
+      if (stop_.load()) return;
+      seen = epoch_.load(std::memory_order_acquire);
+      for (;;) {
+        const int k = next_.fetch_add(1);
+        if (k >= parts_) break;
         const int64_t lo = n_ * k / parts_, hi = n_ * (k + 1) / parts_;
-        const auto* f = fn_;
-        lk.unlock();
-        (*f)(lo, hi);
-        lk.lock();
-        if (--pending_ == 0) done_cv_.notify_all();
+        (*fn_)(lo, hi);
+        pending_.fetch_sub(1, std::memory_order_release);
       }
     }
   }
   std::vector<std::thread> workers_;
   std::mutex m_;
-  std::condition_variable cv_, done_cv_;
+  std::condition_variable cv_;
   const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
   int64_t n_ = 0;
-  int parts_ = 0, next_ = 0, pending_ = 0;
-  uint64_t epoch_ = 0;
-  bool stop_ = false;
+  int parts_ = 0;
+  std::atomic<int> next_{0}, pending_{0}, sleepers_{0};
+  std::atomic<uint64_t> epoch_{0};
+  std::atomic<bool> stop_{false};
 };
-
-// Immutable per-layout job (captured graphs keep its address).
-struct PatchJob {
-  const unsigned long long* count;  // pinned copy of the device counter
-  const PatchEntry* ent;
-  PatchOut* out;
-  int64_t cap;
-};
-
-// libstdc++ polar multiplier with the host's log (random.tcc:1837:
-// __mult = std::sqrt(-2 * std::log(__r2) / __r2); normal = (y * mult) * 1 + 0).
-void CUDART_CB patch_host_fn(void* p) {
-  const PatchJob* j = static_cast<const PatchJob*>(p);
-  const int64_t n = std::min<int64_t>(int64_t(*j->count), j->cap);
-  HostPool::get().run(n, [j](int64_t lo, int64_t hi) {
-    for (int64_t i = lo; i < hi; ++i) {
-      const PatchEntry& e = j->ent[i];
-      const double mult = std::sqrt(-2 * std::log(e.r2) / e.r2);
-      j->out[i].vy = e.y * mult * 1.0 + 0.0;
-      j->out[i].vx = e.x * mult * 1.0 + 0.0;
-    }
-  });
-}
 
 bool exact_mode_env() {
   static const bool on = [] {
@@ -607,18 +647,6 @@ char* patch_alloc(Handle& h, size_t bytes) {
   return static_cast<char*>(p);
 }
 
-const PatchJob* patch_job(Handle& h, const unsigned long long* cnt, const PatchEntry* ent,
-                          PatchOut* out, int64_t cap) {
-  static std::mutex mu;
-  static std::vector<std::unique_ptr<PatchJob>> jobs;  // process lifetime, deduplicated
-  std::lock_guard<std::mutex> lk(mu);
-  (void)h;
-  for (auto& j : jobs)
-    if (j->count == cnt && j->ent == ent && j->out == out && j->cap == cap) return j.get();
-  jobs.emplace_back(new PatchJob{cnt, ent, out, cap});
-  return jobs.back().get();
-}
-
 std::once_flag g_table_once;
 ddlog::Entry g_host_table[ddlog::kTableSize];
 
@@ -629,6 +657,62 @@ const ddlog::Entry* host_log_table() {
   return g_host_table;
 }
 
+// Answer the exact-mode lists of this call, in queue order (see "Exact mode").
+// Called by the host thread before it waits for the stream.
+void patch_service(Handle& h) {
+  if (h.patch_pending.empty()) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  RSVD_CUDA(cudaStreamIsCapturing(h.stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return;  // nothing runs before the graph launches
+  for (PatchHdr* hdr : h.patch_pending) {
+    int polls = 0;
+    while (reinterpret_cast<volatile PatchHdr*>(hdr)->ready == 0) {
+      if (++polls % 4096 == 0) {
+        // the GPU may have failed before reaching the list: do not spin forever
+        const cudaError_t q = cudaStreamQuery(h.stream);
+        if (q != cudaErrorNotReady) {
+          patch_cancel(h);
+          if (q != cudaSuccess) RSVD_CUDA(q);
+          throw Error(RSVD_ERR_INTERNAL, "exact-mode patch list never published");
+        }
+      }
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const int64_t n = std::min<int64_t>(int64_t(hdr->count), hdr->cap);
+    const PatchEntry* ent = reinterpret_cast<const PatchEntry*>(reinterpret_cast<char*>(hdr) + 64);
+    PatchOut* out = reinterpret_cast<PatchOut*>(reinterpret_cast<char*>(hdr) + 64 +
+                                                size_t(hdr->cap) * sizeof(PatchEntry));
+    // libstdc++ polar multiplier with the host's log (random.tcc:1837:
+    // __mult = std::sqrt(-2 * std::log(__r2) / __r2); normal = (y * mult) * 1 + 0)
+    HostPool::get().run(n, [ent, out](int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i) {
+        const PatchEntry e = ent[i];
+        const double mult = std::sqrt(-2 * std::log(e.r2) / e.r2);
+        out[i].vy = e.y * mult * 1.0 + 0.0;
+        out[i].vx = e.x * mult * 1.0 + 0.0;
+      }
+    });
+    std::atomic_thread_fence(std::memory_order_release);
+    reinterpret_cast<volatile PatchHdr*>(hdr)->done = 1;
+  }
+  h.patch_pending.clear();
+}
+
+// Release every pending list without patching (the call failed on the host):
+// the waiting patch kernels exit.
+void patch_cancel(Handle& h) {
+  for (PatchHdr* hdr : h.patch_pending) reinterpret_cast<volatile PatchHdr*>(hdr)->done = 2;
+  h.patch_pending.clear();
+}
+
+void stream_sync(Handle& h) {
+  patch_service(h);
+  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+}
+
 // Jump polynomials on the device, cached per handle (grown on demand).
 static const uint64_t* device_jump_polys(Handle& h, uint64_t L, int count) {
   if (count <= 0) return nullptr;
@@ -636,7 +720,7 @@ static const uint64_t* device_jump_polys(Handle& h, uint64_t L, int count) {
     if (h.jump_L == L) count = std::max(count, 2 * h.jump_count);  // grow geometrically
     const uint64_t* hp = mtjump::jump_polys(L, count);
     if (h.d_jump) {
-      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      stream_sync(h);
       RSVD_CUDA(cudaFree(h.d_jump));
     }
     RSVD_CUDA(cudaMalloc(&h.d_jump, size_t(count) * kPolyWords * 8));
@@ -759,16 +843,19 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
     // 102400 pairs) -- an overflow raises an error, never a silent mismatch
     PatchList pl{nullptr, nullptr, 0};
     PatchOut* pout = nullptr;
-    unsigned long long* hcount = nullptr;
+    PatchHdr* hdr = nullptr;
     if (exact_mode_env()) {
       const int64_t stored = (row_hi - row_lo) * l;
       pl.cap = std::min<int64_t>(pairs, (std::min(pairs, stored + 1) * 4) / 100 + 1024);
       char* buf = patch_alloc(h, 64 + size_t(pl.cap) * (sizeof(PatchEntry) + sizeof(PatchOut)));
-      hcount = reinterpret_cast<unsigned long long*>(buf);
+      hdr = reinterpret_cast<PatchHdr*>(buf);
+      hdr->ready = 0;
+      hdr->done = 0;
+      hdr->cap = pl.cap;
       pl.ent = reinterpret_cast<PatchEntry*>(buf + 64);
       pout = reinterpret_cast<PatchOut*>(buf + 64 + size_t(pl.cap) * sizeof(PatchEntry));
       pl.count = reinterpret_cast<unsigned long long*>(h.ws.alloc_bytes(64));
-      RSVD_CUDA(cudaMemsetAsync(pl.count, 0, 8, h.stream));
+      RSVD_CUDA(cudaMemsetAsync(pl.count, 0, 16, h.stream));  // count + gate
     }
     launch_k(h, polar_write_kernel, unsigned(ntiles), 256, 0, words, &dst->pos, attempts,
              self_scan ? static_cast<const int64_t*>(nullptr) : static_cast<const int64_t*>(off),
@@ -777,17 +864,22 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
     launch_k(h, rng_finish_kernel, 1, 320, 0, words, done, cache, pairs, cache_out, dst,
                                                h.d_flags);
     RSVD_LAUNCHED(h);
-    if (pl.ent) {
-      RSVD_CUDA(cudaMemcpyAsync(hcount, pl.count, 8, cudaMemcpyDeviceToHost, h.stream));
-      const PatchJob* job = patch_job(h, hcount, pl.ent, pout, pl.cap);
-      RSVD_CUDA(cudaLaunchHostFunc(h.stream, patch_host_fn, const_cast<PatchJob*>(job)));
-      if (h.trace) trace_mark(h, "rng.cu:exact-host-log");
-      const int blocks = int(std::min<int64_t>(ceil_div(pl.cap, 256), 2 * h.sm_count));
-      launch_k(h, polar_patch_kernel, unsigned(blocks), 256, 0,
-               static_cast<const unsigned long long*>(pl.count),
-               static_cast<const PatchEntry*>(pl.ent), static_cast<const PatchOut*>(pout), pl.cap,
-               g, dst);
+    if (hdr) {
+      launch_k(h, patch_signal_kernel, 1, 32, 0, static_cast<const unsigned long long*>(pl.count), hdr);
       RSVD_LAUNCHED(h);
+      unsigned* gate = reinterpret_cast<unsigned*>(pl.count + 1);
+      const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(pl.cap, 1024), h.sm_count)));
+      launch_k(h, polar_patch_kernel, unsigned(blocks), 256, 0, static_cast<const PatchHdr*>(hdr), gate,
+               static_cast<const PatchEntry*>(pl.ent), static_cast<const PatchOut*>(pout), pl.cap, g, dst);
+      RSVD_LAUNCHED(h);
+      h.patch_pending.push_back(hdr);
+      // Eager calls answer the list right here: anything the host does later
+      // in the call may synchronize the device implicitly (cudaMalloc of a
+      // growing workspace, cudaFree), which would wait on polar_patch while
+      // polar_patch waits on the host.  Under capture nothing runs yet: the
+      // list is answered after the graph launch (finish_call), when the host
+      // does nothing else.
+      patch_service(h);
     }
   } else {
     launch_k(h, rng_finish_kernel, 1, 32, 0, nullptr, nullptr, nullptr, 0, 0, dst, h.d_flags);

@@ -1097,7 +1097,7 @@ static void ensure_smem(K kernel, size_t bytes) {
 
 void check_flags(Handle& h, const char* what) {
   RSVD_CUDA(cudaMemcpyAsync(h.h_flags, h.d_flags, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
-  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  stream_sync(h);
   const int f = *h.h_flags;
   if (f) {
     clear_flags(h);
@@ -1296,7 +1296,7 @@ static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
   if (probe) {
     long long hp[64];
     RSVD_CUDA(cudaMemcpyAsync(hp, probe, sizeof hp, cudaMemcpyDeviceToHost, h.stream));
-    RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    stream_sync(h);
     std::fprintf(stderr, "cholqr_fused m=%lld l=%d G=%lld:", (long long)m, l, (long long)G);
     for (int i = 1; i < 44 && hp[i]; ++i) std::fprintf(stderr, " %lld", hp[i] - hp[i - 1]);
     std::fprintf(stderr, "\n  chol/inv/rtotal:");
@@ -1359,7 +1359,7 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   if (l > 64) {
     int used = 0;
     RSVD_CUDA(cudaMemcpyAsync(&used, shift_used, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
-    RSVD_CUDA(cudaStreamSynchronize(h.stream));
+    stream_sync(h);
     passes = used ? 4 : 2;
   }
   for (int i = 1; i < passes; ++i) pass(Q, Q);
@@ -1370,7 +1370,7 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   // check's Gram is the next pass's Gram.
   int used = 0;
   RSVD_CUDA(cudaMemcpyAsync(&used, shift_used, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
-  RSVD_CUDA(cudaStreamSynchronize(h.stream));
+  stream_sync(h);
   if (used) {
     const double tol = 8.0 * l * 1.1102230246251565e-16;
     for (int extra = 0; extra < 8; ++extra) {
@@ -1433,7 +1433,7 @@ void jacobi_svd_square(Handle& h, const DMat& Rm, DMat J, DMat W, double* sigma)
     if (probe_on) {
       double hd[128];
       RSVD_CUDA(cudaMemcpyAsync(hd, dbg, sizeof hd, cudaMemcpyDeviceToHost, h.stream));
-      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      stream_sync(h);
       std::fprintf(stderr, "jacobi_svd l=%d sweeps=%d max rel g per sweep:", l, int(hd[0]));
       for (int i = 1; i <= int(hd[0]) && i < 31; ++i) std::fprintf(stderr, " %.1e", hd[i]);
       std::fprintf(stderr, "\n  round phases (cycles: load, reduce, rotation, store, barrier; round total):");

@@ -49,13 +49,13 @@ DMat block(const DMat& X, int64_t t, int64_t l) { return DMat(X.p + t * l * X.ld
 void gaussian_trials(Handle& h, int64_t n, int64_t l, uint64_t seed_base, int64_t T, DMat Om) {
   if (T > h.h_rng_batch_cap) {
     if (h.h_rng_batch) {
-      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      stream_sync(h);
       RSVD_CUDA(cudaFreeHost(h.h_rng_batch));
     }
     RSVD_CUDA(cudaMallocHost(&h.h_rng_batch, size_t(T) * sizeof(rsvd_rng_state)));
     h.h_rng_batch_cap = T;
   } else {
-    RSVD_CUDA(cudaStreamSynchronize(h.stream));  // the staging buffer may still be in flight
+    stream_sync(h);  // the staging buffer may still be in flight
   }
   for (int64_t t = 0; t < T; ++t) seeded_state(seed_base + uint64_t(t), h.h_rng_batch + t);
   auto* d = static_cast<rsvd_rng_state*>(h.ws.alloc_bytes(size_t(T) * sizeof(rsvd_rng_state)));
