@@ -325,6 +325,8 @@ def main():
     rows = np.array_split(np.arange(m), world)[rank]
     r0, r1 = int(rows[0]), int(rows[-1]) + 1
     a_loc = a_full[r0:r1, :].t().contiguous().t() if world > 1 else a_full
+    if dist_mode:
+        engine.set_shard(m, r0)  # shard descriptor: no per-call row-count exchange
     mode = eng.RangeMode[cfg["mode"]] if cfg["alg"] <= 4 else eng.RangeMode.basic
     sk = eng.SketchConfig(k, p, q, mode, SEED_OMEGA)
     torch.cuda.synchronize()

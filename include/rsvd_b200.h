@@ -92,6 +92,19 @@ const char* rsvd_version(void);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores
  * the handle's own non-blocking stream, on which every call first waits for
  * the work already queued on the legacy default stream (the caller's inputs). */
+/* Virtual communicator: nranks ranks of the row-sharded engine in ONE process
+ * on ONE device (one host thread per rank, one handle per rank, one shared
+ * stream; fixed-order device reductions stand in for NCCL).  Runs the
+ * multi-GPU code path -- shard offsets, Psi row selection, distributed
+ * CholeskyQR / TSQR, every exchange -- for tests without P GPUs. */
+typedef struct rsvd_vcomm rsvd_vcomm;
+rsvd_status rsvd_vcomm_create(rsvd_vcomm** vc, int nranks);
+void rsvd_vcomm_destroy(rsvd_vcomm* vc);
+rsvd_status rsvd_create_virtual(rsvd_handle** h, int device, int rank, rsvd_vcomm* vc);
+/* Shard descriptor of a distributed handle: the global row count and this
+ * rank's first row (so a call needs no row-count exchange; 0, 0 = exchange). */
+rsvd_status rsvd_set_shard(rsvd_handle* h, int64_t m_global, int64_t row_offset);
+
 rsvd_status rsvd_set_stream(rsvd_handle* h, void* cuda_stream);
 rsvd_status rsvd_synchronize(rsvd_handle* h);
 rsvd_status rsvd_get_counters(rsvd_handle* h, rsvd_counters* out);
@@ -269,6 +282,13 @@ rsvd_status rsvd_rsvd_host(rsvd_handle* h, int64_t m, int64_t n, const double* a
 rsvd_status rsvd_spevd_dev(rsvd_handle* h, int64_t n, const double* a, int64_t lda, int64_t k,
                            int64_t p, rsvd_rng_state* rng, int check_symmetry, double* u,
                            int64_t ldu, double* lambda);
+/* The same on a row shard of a distributed handle: this rank holds rows
+ * [row_offset, row_offset + m_local) of the n x n matrix (m_local == n on a
+ * single-GPU handle); U m_local x k.  The asymmetry precondition compares the
+ * shards' transposed blocks rank to rank (an uncounted validation pass). */
+rsvd_status rsvd_spevd_shard_dev(rsvd_handle* h, int64_t m_local, int64_t n, const double* a,
+                                 int64_t lda, int64_t k, int64_t p, rsvd_rng_state* rng,
+                                 int check_symmetry, double* u, int64_t ldu, double* lambda);
 rsvd_status rsvd_spevd_host(rsvd_handle* h, int64_t n, const double* a, int64_t lda, int64_t k,
                             int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                             double* lambda);

@@ -40,7 +40,7 @@ __all__ = [
     "solve_joint_core", "RangeMode", "SketchConfig", "fixed_rank_range", "power_range",
     "subspace_iter_range", "range_basis", "SvdApprox", "EvdApprox", "rsvd", "truncate",
     "CountingOperator", "spevd_hermitian", "spsvd_general", "apply", "apply_adjoint", "Engine",
-    "default_engine", "lib_path", "build", "using_engine", "rsvd_host", "singular_values",
+    "default_engine", "VirtualComm", "lib_path", "build", "using_engine", "rsvd_host", "singular_values",
     "spectral_norm", "computed_range_error", "canonical_sines", "subspace_quality", "AngleReport",
     "reconstruction_error", "range_basis_trials", "rsvd_trials", "range_error_trials",
 ]
@@ -119,6 +119,9 @@ def _load():
             "rsvd_create": [ctypes.POINTER(P), I],
             "rsvd_nccl_unique_id": [P],
             "rsvd_create_dist": [ctypes.POINTER(P), I, I, I, P],
+            "rsvd_vcomm_create": [ctypes.POINTER(P), I],
+            "rsvd_create_virtual": [ctypes.POINTER(P), I, I, P],
+            "rsvd_set_shard": [P, I64, I64],
             "rsvd_set_stream": [P, P],
             "rsvd_synchronize": [P],
             "rsvd_get_counters": [P, ctypes.POINTER(Counters)],
@@ -141,6 +144,7 @@ def _load():
             "rsvd_rsvd_dev": [P, I64, I64, P, I64, I64, I64, I, I, PS, P, I64, P, P, I64],
             "rsvd_rsvd_host": [P, I64, I64, P, I64, I64, I64, I, I, PS, P, I64, P, P, I64],
             "rsvd_spevd_dev": [P, I64, P, I64, I64, I64, PS, I, P, I64, P],
+            "rsvd_spevd_shard_dev": [P, I64, I64, P, I64, I64, I64, PS, I, P, I64, P],
             "rsvd_spevd_host": [P, I64, P, I64, I64, I64, PS, P, I64, P],
             "rsvd_spsvd_dev": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
             "rsvd_spsvd_host": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
@@ -167,6 +171,8 @@ def _load():
             f.restype = ctypes.c_int
         L.rsvd_destroy.argtypes = [P]
         L.rsvd_destroy.restype = None
+        L.rsvd_vcomm_destroy.argtypes = [P]
+        L.rsvd_vcomm_destroy.restype = None
         L.rsvd_last_error.restype = ctypes.c_char_p
         L.rsvd_version.restype = ctypes.c_char_p
         L.rsvd_debug_log_cr.argtypes = [D]
@@ -186,22 +192,85 @@ def _check(rc: int) -> None:
 
 
 # ---------------------------------------------------------------- engine
+class VirtualComm:
+    """nranks ranks of the row-sharded engine in this process on one device
+    (rsvd_vcomm_create): one Engine per rank, each driven by its own thread;
+    fixed-order device reductions stand in for NCCL.  For tests of the
+    multi-GPU code path without several GPUs."""
+
+    def __init__(self, nranks: int, device: int = 0):
+        self.nranks = nranks
+        self.ptr = ctypes.c_void_p()
+        _check(_load().rsvd_vcomm_create(ctypes.byref(self.ptr), nranks))
+        self.engines = [Engine(device, r, nranks, vcomm=self) for r in range(nranks)]
+
+    def run(self, fn):
+        """fn(rank, engine) on one thread per rank (the module-level API
+        routed through that rank's engine); returns the per-rank results."""
+        import threading
+        out = [None] * self.nranks
+        err = [None] * self.nranks
+
+        def body(r):
+            try:
+                with using_engine(self.engines[r]):
+                    out[r] = fn(r, self.engines[r])
+            except BaseException as ex:  # noqa: BLE001
+                err[r] = ex
+        th = [threading.Thread(target=body, args=(r,)) for r in range(self.nranks)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        # the root cause first: a failing rank releases its peers with
+        # "a peer rank failed"
+        errs = [e for e in err if e is not None]
+        errs.sort(key=lambda e: "peer rank failed" in str(e))
+        if errs:
+            raise errs[0]
+        return out
+
+    def close(self):
+        for e in self.engines:
+            e.close()
+        self.engines = []
+        if self.ptr.value:
+            _load().rsvd_vcomm_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Engine:
     """Owns one rsvd_handle (one GPU; a row shard when created distributed)."""
 
     def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, vcomm: Optional["VirtualComm"] = None):
         L = _load()
         self._h = ctypes.c_void_p()
         self.device = device
+        self.virtual = vcomm is not None
+        self._vcomm = vcomm  # keeps the communicator alive
         # nranks == 1 with an id: a one-rank NCCL communicator, i.e. the
         # row-sharded code path (every exchange included) on one GPU
-        if nranks > 1 or nccl_id is not None:
+        if vcomm is not None:
+            _check(L.rsvd_create_virtual(ctypes.byref(self._h), device, rank, vcomm.ptr))
+            nranks = vcomm.nranks
+        elif nranks > 1 or nccl_id is not None:
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             _check(L.rsvd_create_dist(ctypes.byref(self._h), device, rank, nranks, buf))
         else:
             _check(L.rsvd_create(ctypes.byref(self._h), device))
         self.rank, self.nranks = rank, nranks
+
+    def set_shard(self, m_global: int, row_offset: int) -> None:
+        """Shard descriptor: global rows and this rank's first row (no per-call
+        row-count exchange)."""
+        _check(_load().rsvd_set_shard(self._h, int(m_global), int(row_offset)))
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -686,12 +755,15 @@ def spevd_hermitian(a, k: int, p: int, rng: Rng) -> EvdApprox:
     """Single-pass symmetric EVD, Alg 5 (singlepass.hpp:45-78)."""
     def run(d, e):
         import torch
-        if d.rows != d.cols:
+        # a distributed engine takes this rank's (m_local x n) row shard;
+        # squareness is then m_global == n (checked by the engine)
+        if d.rows != d.cols and e.nranks == 1 and not e.virtual:
             raise DimensionError("spevd_hermitian: matrix is not square")
         u = _empty(d.rows, max(k, 0), d.host)
         lam = torch.empty(max(k, 1), dtype=torch.float64, device="cuda")
-        _check(_load().rsvd_spevd_dev(e.handle, d.rows, d.ptr, d.ld, k, p, ctypes.byref(rng.state),
-                                      1, u.data_ptr(), max(d.rows, 1), lam.data_ptr()))
+        _check(_load().rsvd_spevd_shard_dev(e.handle, d.rows, d.cols, d.ptr, d.ld, k, p,
+                                            ctypes.byref(rng.state), 1, u.data_ptr(), max(d.rows, 1),
+                                            lam.data_ptr()))
         return EvdApprox(_out(u, d.host), _vec_out(lam[:max(k, 0)], d.host))
     return _counted(a, run)
 

@@ -3,14 +3,20 @@
 // sweep each cost a full block barrier over one SM.
 //
 //   M J = W diag(sigma):  columns of M are grouped in blocks of kBJ; a sweep is
-//   a round-robin over block pairs (nb/2 pairs per round, one CTA each, all in
-//   parallel).  A CTA loads its two blocks (l x 2kBJ) into shared memory, runs
-//   one inner sweep of one-sided Jacobi on those columns while accumulating
-//   the 2kBJ x 2kBJ rotation V, writes the columns back and applies V to the
-//   same two block-columns of J.  Rounds are separated by a grid-wide barrier
-//   (cooperative launch); a sweep with no rotation above the threshold ends
-//   the iteration.  Deterministic: the pair schedule and every reduction are
-//   fixed, no atomics on data.
+//   a round-robin over block pairs (nb/2 pairs per round, all in parallel).
+//   A block pair is visited by a CLUSTER of CS CTAs (CS = 1..8, chosen so the
+//   visits of a round fill the SMs): CTA r of the cluster owns rows
+//   [r*rp, (r+1)*rp) of the pair's two block-columns (l x 2kBJ), loads them
+//   into shared memory, forms its partial 2kBJ x 2kBJ Gram with DMMA; the
+//   partials are summed over distributed shared memory in rank order (every
+//   CTA gets the same Gram), every CTA runs the same inner two-sided sweep on
+//   it accumulating the rotation V, and applies V to its own rows of the
+//   block-columns of M and J.  The l-long work of a visit is split CS ways;
+//   only the 32 x 32 inner sweep is replicated.  Rounds are separated by a
+//   grid-wide barrier (cooperative launch); a sweep with no rotation above
+//   the threshold ends the iteration.  Deterministic: the pair schedule and
+//   every reduction are fixed, no atomics on data.  The panel held per CTA is
+//   rp x 2kBJ, so l is bounded only by 8 x (shared memory / 256 B).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -80,7 +86,7 @@ struct BJBatch {
 };
 
 __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int l, int ldp,
-                                                            int nb, int inner_max,
+                                                            int rows_per, int nb, int inner_max,
                                                             double graded_ratio,
                                                             long long* __restrict__ probe) {
   RSVD_PDL_ENTRY();
@@ -93,10 +99,16 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
     }
   };
   cg::grid_group grid = cg::this_grid();
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = int(cluster.num_blocks()), crank = int(cluster.block_rank());
+  const int cid = int(blockIdx.x) / cs, ncl = int(gridDim.x) / cs;
+  const int r_lo = crank * rows_per, r_hi = min(l, r_lo + rows_per), nr = max(0, r_hi - r_lo);
   extern __shared__ double sm[];
-  double* Xb = sm;                           // kBJW columns x ldp rows (rows >= l are zero)
-  double* G = Xb + size_t(kBJW) * ldp;       // kBJW x kBJW, ld kGL
+  double* Xb = sm;                           // kBJW columns x ldp local rows (rows >= nr are zero)
+  double* G = Xb + size_t(kBJW) * ldp;       // kBJW x kBJW, ld kGL (the cluster's sum)
   double* V = G + kBJW * kGL;                // kBJW x kBJW, ld kVL (column-major: V[c * kVL + r])
+  double* Gp = V + kBJW * kVL;               // this CTA's partial Gram, ld kGL
+  double* Dp = Gp + kBJW * kGL;              // graded route: partial (a, b, g) of 16 pairs
   __shared__ int colmap[kBJW];
   __shared__ double rc[kBJW / 2], rs[kBJW / 2];
   __shared__ int rp[kBJW / 2], rq[kBJW / 2];
@@ -111,7 +123,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
   bool done0 = false, done1 = batch.nprob < 2;  // identical in every thread
   for (int sweep = 0; sweep < kBJMaxSweeps; ++sweep) {
     for (int round = 0; round < nbp - 1; ++round) {
-      for (int item = blockIdx.x; item < batch.nprob * npairs; item += gridDim.x) {
+      for (int item = cid; item < batch.nprob * npairs; item += ncl) {
         const int prob = item / npairs, pr = item % npairs;
         if (prob == 0 ? done0 : done1) continue;
         double* __restrict__ X = batch.p[prob].X;
@@ -130,10 +142,10 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
         // warp w: columns w and w + 16, lanes along rows, 4 loads in flight
         for (int c = warp; c < kBJW; c += 16) {
           const int gc = colmap[c];
-          const double* src = X + int64_t(gc < 0 ? 0 : gc) * l;
+          const double* src = X + int64_t(gc < 0 ? 0 : gc) * l + r_lo;
           double* dst = Xb + c * ldp;
 #pragma unroll 4
-          for (int r = lane; r < ldp; r += 32) dst[r] = (gc >= 0 && r < l) ? src[r] : 0.0;
+          for (int r = lane; r < ldp; r += 32) dst[r] = (gc >= 0 && r < nr) ? src[r] : 0.0;
         }
         for (int e = tid; e < kBJW * kVL; e += blockDim.x) V[e] = ((e % kVL) == (e / kVL)) ? 1.0 : 0.0;
         __syncthreads();
@@ -154,8 +166,17 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
           for (int u = 0; u < 3; ++u)
             if (k0 + 4 * u < ldp) dmma884(g[u][0], g[u][1], pa[k0 + 4 * u], pb[k0 + 4 * u]);
           const int gi = ti * 8 + r8, gj = tj * 8 + 2 * c4;
-          G[gi + kGL * gj] = (g[0][0] + g[1][0]) + (g[2][0] + g[3][0]);
-          G[gi + kGL * (gj + 1)] = (g[0][1] + g[1][1]) + (g[2][1] + g[3][1]);
+          Gp[gi + kGL * gj] = (g[0][0] + g[1][0]) + (g[2][0] + g[3][0]);
+          Gp[gi + kGL * (gj + 1)] = (g[0][1] + g[1][1]) + (g[2][1] + g[3][1]);
+        }
+        // the cluster's Gram: partials summed in rank order over distributed
+        // shared memory (bitwise the same G in every CTA of the cluster)
+        cluster.sync();
+        for (int e = tid; e < kBJW * kBJW; e += blockDim.x) {
+          const int o = (e % kBJW) + kGL * (e / kBJW);
+          double v = 0.0;
+          for (int r = 0; r < cs; ++r) v += cluster.map_shared_rank(Gp, r)[o];
+          G[o] = v;
         }
         __syncthreads();
         mark(1);
@@ -195,7 +216,34 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
             if (tid == 0) any_inner = 0;
             __syncthreads();
             for (int r2 = 0; r2 < wp - 1; ++r2) {
-              if (warp < np2) {  // warp = pair: dot products, rotation, update
+              // partial dot products of this CTA's rows, summed over the
+              // cluster in rank order (distributed shared memory)
+              if (warp < np2) {
+                int pa, pb;
+                circle(warp, r2, wp, pa, pb);
+                const int p0 = min(pa, pb), q0 = max(pa, pb);
+                double al = 0.0, be = 0.0, ga = 0.0;
+                if (q0 < w) {
+                  const double* xp = Xb + p0 * ldp;
+                  const double* xq = Xb + q0 * ldp;
+                  for (int r = lane; r < ldp; r += 32) {
+                    const double a = xp[r], b = xq[r];
+                    al = fma(a, a, al);
+                    be = fma(b, b, be);
+                    ga = fma(a, b, ga);
+                  }
+                }
+                al = wsum(al);
+                be = wsum(be);
+                ga = wsum(ga);
+                if (lane == 0) {
+                  Dp[3 * warp] = al;
+                  Dp[3 * warp + 1] = be;
+                  Dp[3 * warp + 2] = ga;
+                }
+              }
+              cluster.sync();
+              if (warp < np2) {  // warp = pair: rotation, update of the local rows
                 int pa, pb;
                 circle(warp, r2, wp, pa, pb);
                 const int p0 = min(pa, pb), q0 = max(pa, pb);
@@ -203,15 +251,12 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
                   double* xp = Xb + p0 * ldp;
                   double* xq = Xb + q0 * ldp;
                   double al = 0.0, be = 0.0, ga = 0.0;
-                  for (int r = lane; r < ldp; r += 32) {
-                    const double a = xp[r], b = xq[r];
-                    al = fma(a, a, al);
-                    be = fma(b, b, be);
-                    ga = fma(a, b, ga);
+                  for (int r = 0; r < cs; ++r) {
+                    const double* d = cluster.map_shared_rank(Dp, r);
+                    al += d[3 * warp];
+                    be += d[3 * warp + 1];
+                    ga += d[3 * warp + 2];
                   }
-                  al = wsum(al);
-                  be = wsum(be);
-                  ga = wsum(ga);
                   if (ga * ga > tol2 * (al * be) && ga != 0.0) {
                     const double d = be - al, g2 = 2.0 * ga;
                     const double ir = rsqrt(fma(d, d, g2 * g2));
@@ -230,7 +275,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
                   }
                 }
               }
-              __syncthreads();
+              cluster.sync();  // every CTA read the partials before they are rewritten
             }
             const int rot = any_inner;
             if (tid == 0) {
@@ -244,9 +289,17 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
         // ---- cyclic two-sided Jacobi on G (w active columns), accumulating V.
         // Per round: the wp/2 rotations (one thread each), then G <- R^T G R as
         // independent 2 x 2 blocks (pair i rows x pair j columns) and V <- V R:
-        // two barriers per round.  (A warp-per-pair variant with rows in
-        // registers and shuffled column rotations measured 2x slower.)
-        for (int it = 0; !graded && it < inner_max; ++it) {
+        // two barriers per round.  Measured alternatives: a warp-per-pair
+        // variant with rows in registers and shuffled column rotations (2x
+        // slower); every thread computing its own rotations with G double
+        // buffered, one barrier per round (~1300 vs ~1060 cycles per round:
+        // the two dependent DP reciprocal square roots of a rotation dominate).
+        double vmax_visit = 0.0;
+        for (int wi = 0; wi < int(blockDim.x >> 5); ++wi) vmax_visit = fmax(vmax_visit, vmaxw[wi]);
+        // a visit whose fresh Gram is diagonal to the rotation threshold makes
+        // no rotation: skip its inner sweep (the clean visits of the last sweeps)
+        const bool clean = !graded && !(vmax_visit > tol2);
+        for (int it = 0; !graded && !clean && it < inner_max; ++it) {
           if (tid == 0) any_inner = 0;
           for (int r2 = 0; r2 < wp - 1; ++r2) {
             if (tid < np2) {
@@ -322,20 +375,20 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
           for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) vb[nt][ks] = V[(nt * 8 + r8) * kVL + ks * 4 + c4];
-          const int ntiles = (l + 7) / 8;
+          const int ntiles = (nr + 7) / 8;
 #pragma unroll 2
           for (int mt = warp; mt < 2 * ntiles; mt += 16) {
             const bool isJ = mt >= ntiles;
-            const int m0 = (isJ ? mt - ntiles : mt) * 8;
+            const int m0 = (isJ ? mt - ntiles : mt) * 8;  // local row tile
             if (graded && !isJ) {  // one-sided route: Xb holds the rotated columns
               const int row = m0 + r8;
-              if (row < l)
+              if (row < nr)
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
                   for (int e = 0; e < 2; ++e) {
                     const int cc = nt * 8 + 2 * c4 + e, gc = colmap[cc];
-                    if (gc >= 0) X[int64_t(gc) * l + row] = Xb[cc * ldp + row];
+                    if (gc >= 0) X[int64_t(gc) * l + r_lo + row] = Xb[cc * ldp + row];
                   }
               continue;
             }
@@ -347,7 +400,7 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
                 af[ks] = Xb[k * ldp + row];
               } else {
                 const int gc = colmap[k];
-                af[ks] = (gc >= 0 && row < l) ? Jm[int64_t(gc) * l + row] : 0.0;
+                af[ks] = (gc >= 0 && row < nr) ? Jm[int64_t(gc) * l + r_lo + row] : 0.0;
               }
             }
             double acc[4][2];
@@ -359,25 +412,21 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
             }
             double* dst = isJ ? Jm : X;
             const int row = m0 + r8;
-            if (row < l) {
+            if (row < nr) {
 #pragma unroll
               for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                   const int gc = colmap[nt * 8 + 2 * c4 + e];
-                  if (gc >= 0) dst[int64_t(gc) * l + row] = acc[nt][e];
+                  if (gc >= 0) dst[int64_t(gc) * l + r_lo + row] = acc[nt][e];
                 }
             }
           }
         }
-        if (tid == 0 && any_first) atomicOr(&changed[sweep], 1);
+        if (tid == 0 && crank == 0 && any_first) atomicOr(&changed[sweep], 1);
         // graded panels' Gram entries carry absolute rounding: no early stop
-        if (tid == 0) {
-          double vm = 1.0;
-          if (!graded) {
-            vm = 0.0;
-            for (int wi = 0; wi < int(blockDim.x >> 5); ++wi) vm = fmax(vm, vmaxw[wi]);
-          }
+        if (tid == 0 && crank == 0) {
+          const double vm = graded ? 1.0 : vmax_visit;
           atomicMax(&batch.p[prob].smax[sweep], static_cast<unsigned long long>(__double_as_longlong(vm)));
         }
         __syncthreads();
@@ -652,10 +701,55 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
   const int nb = (l + kBJ - 1) / kBJ;
   // panel rows padded to ldp = l rounded up to 8 with ldp % 16 in {4, 12}... use the
   // smallest ldp >= l, ldp % 4 == 0, (ldp / 4) odd: conflict-free DMMA fragment loads
-  int ldp = (l + 3) / 4 * 4;
-  if ((ldp / 4) % 2 == 0) ldp += 4;
-  const size_t smem = (size_t(ldp) * kBJW + kBJW * kGL + kBJW * kVL) * 8;
-  if (smem > 227 * 1024) throw_dim("block_jacobi_svd: l too large for one block pair in shared memory");
+  const int nbp = nb + (nb & 1);
+  const int items = nprob * (nbp / 2);
+  // cluster size: split each visit's rows CS ways while the round's visits
+  // still fit the SMs (RSVD_BJ_CLUSTER overrides; 1 = the unsplit visit)
+  const int cs_env = std::getenv("RSVD_BJ_CLUSTER") ? std::atoi(std::getenv("RSVD_BJ_CLUSTER")) : 0;
+  int cs = 1;
+  if (cs_env > 0) {
+    cs = std::min(8, cs_env);
+  } else {
+    while (cs < 8 && items * (2 * cs) <= h.sm_count && ceil_div(l, 2 * cs) >= 16) cs *= 2;
+  }
+  auto panel_ld = [](int rows) {
+    int ld = (rows + 3) / 4 * 4;
+    if ((ld / 4) % 2 == 0) ld += 4;
+    return ld;
+  };
+  auto smem_of = [&](int c) {
+    const int rpc = int(ceil_div(l, c));
+    return (size_t(panel_ld(rpc)) * kBJW + 2 * kBJW * kGL + kBJW * kVL + 64) * 8;
+  };
+  while (cs < 8 && smem_of(cs) > 220 * 1024) cs *= 2;  // large l: more CTAs per visit
+  // co-residency (cooperative launch): at most the device's active clusters
+  auto max_clusters = [&](int c) {
+    smem_attr(bjacobi_kernel, smem_of(c));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(c * std::max(1, h.sm_count / c)));
+    cfg.blockDim = dim3(kBJThreads);
+    cfg.dynamicSmemBytes = smem_of(c);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(c);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    RSVD_CUDA(cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(bjacobi_kernel), &cfg));
+    return n;
+  };
+  int ncl_max = max_clusters(cs);
+  while (cs > 1 && ncl_max < std::min(items, h.sm_count / cs) && smem_of(cs / 2) <= 220 * 1024) {
+    cs /= 2;  // fewer, larger clusters did not all fit: trade split for co-residency
+    ncl_max = max_clusters(cs);
+  }
+  if (ncl_max < 1) throw_dim("block_jacobi_svd: no co-resident cluster fits");
+  const size_t smem = smem_of(cs);
+  if (smem > 227 * 1024) throw_dim("block_jacobi_svd: l too large for a block pair on 8 SMs");
+  const int rp = int(ceil_div(l, cs));
+  const int ldp = panel_ld(rp);
   smem_attr(bjacobi_kernel, smem);
   BJBatch batch{};
   batch.nprob = nprob;
@@ -663,13 +757,12 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
     const BJWork& w = work[q < nprob ? q : 0];
     batch.p[q] = BJProblem{w.X, w.Jm, w.changed, w.smax};
   }
-  int nbv = nb, lv = l, ldpv = ldp;
+  int nbv = nb, lv = l, ldpv = ldp, rpv = rp;
   // one inner sweep per visit: more inner sweeps do not reduce the outer sweep
   // count measurably (C3-C5 shapes)
   static const int inner_env = std::getenv("RSVD_BJ_INNER") ? std::atoi(std::getenv("RSVD_BJ_INNER")) : 1;
   int inner = inner_env;
-  const int nbp = nb + (nb & 1);
-  int grid = std::max(1, std::min(nprob * (nbp / 2), h.sm_count));
+  int grid = cs * std::max(1, std::min(std::min(items, h.sm_count / cs), ncl_max));
   static const double graded_env =
       std::getenv("RSVD_BJ_GRADED") ? std::atof(std::getenv("RSVD_BJ_GRADED")) : 1e-12;
   double graded_ratio = graded_env;
@@ -679,15 +772,30 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
     probe = reinterpret_cast<long long*>(h.ws.alloc_bytes(8 * 8));
     RSVD_CUDA(cudaMemsetAsync(probe, 0, 64, h.stream));
   }
-  void* args[] = {&batch, &lv, &ldpv, &nbv, &inner, &graded_ratio, &probe};
+  void* args[] = {&batch, &lv, &ldpv, &rpv, &nbv, &inner, &graded_ratio, &probe};
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   if (probe_on) {
     cudaEventCreate(&pe0);
     cudaEventCreate(&pe1);
     cudaEventRecord(pe0, h.stream);
   }
-  RSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bjacobi_kernel), dim3(grid),
-                                        dim3(kBJThreads), args, smem, h.stream));
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBJThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h.stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = unsigned(cs);
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    RSVD_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(bjacobi_kernel), args));
+  }
   RSVD_LAUNCHED(h);
   if (probe_on) {
     cudaEventRecord(pe1, h.stream);
@@ -706,9 +814,9 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
     long long hp[6];
     RSVD_CUDA(cudaMemcpy(hp, probe, sizeof hp, cudaMemcpyDeviceToHost));
     std::fprintf(stderr,
-                 "bjacobi l=%d nb=%d nprob=%d grid=%d sweeps=%d (+1 clean) %.3f ms  cycles load %lld "
+                 "bjacobi l=%d nb=%d nprob=%d grid=%d cluster=%d sweeps=%d (+1 clean) %.3f ms  cycles load %lld "
                  "gram %lld inner %lld update %lld gridsync %lld\n",
-                 l, nb, nprob, grid, sw, ms, hp[0], hp[1], hp[2], hp[3], hp[4]);
+                 l, nb, nprob, grid, cs, sw, ms, hp[0], hp[1], hp[2], hp[3], hp[4]);
     cudaEventDestroy(pe0);
     cudaEventDestroy(pe1);
   }

@@ -64,7 +64,15 @@ rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
     join_caller_stream(h);
     h.rng_user_out = nullptr;
     rsvdb::trace_begin(h);
-    f(h);
+    try {
+      f(h);
+    } catch (...) {
+      // a rank failing inside the pipeline releases peers blocked in a
+      // virtual collective; errors of the final check (finish_call) are raised
+      // by every rank alike and leave the communicator usable
+      rsvdb::vcomm_fail(h);
+      throw;
+    }
     rsvdb::finish_call(h, what);
     return RSVD_OK;
   } catch (const rsvdb::Error& e) {
@@ -394,6 +402,52 @@ rsvd_status rsvd_nccl_unique_id(void* out128) {
   }
 }
 
+struct rsvd_vcomm {
+  rsvdb::VComm* v;
+};
+
+rsvd_status rsvd_vcomm_create(rsvd_vcomm** out, int nranks) {
+  try {
+    if (!out) throw rsvdb::Error(RSVD_ERR_PARAMETER, "null output");
+    *out = new rsvd_vcomm{rsvdb::vcomm_create(nranks)};
+    return RSVD_OK;
+  } catch (const rsvdb::Error& e) {
+    g_err = e.what();
+    return e.code;
+  }
+}
+
+void rsvd_vcomm_destroy(rsvd_vcomm* vc) {
+  if (!vc) return;
+  rsvdb::vcomm_destroy(vc->v);
+  delete vc;
+}
+
+rsvd_status rsvd_create_virtual(rsvd_handle** h, int device, int rank, rsvd_vcomm* vc) {
+  if (!vc) {
+    g_err = "rsvd_create_virtual: null communicator";
+    return RSVD_ERR_PARAMETER;
+  }
+  const rsvd_status st = create_impl(h, device, 0, 1, nullptr);
+  if (st != RSVD_OK) return st;
+  try {
+    rsvdb::vcomm_attach((*h)->h, vc->v, rank);
+    return RSVD_OK;
+  } catch (const rsvdb::Error& e) {
+    g_err = e.what();
+    rsvd_destroy(*h);
+    *h = nullptr;
+    return e.code;
+  }
+}
+
+rsvd_status rsvd_set_shard(rsvd_handle* hd, int64_t m_global, int64_t row_offset) {
+  if (!hd || m_global < 0 || row_offset < 0) return RSVD_ERR_PARAMETER;
+  hd->h.shard_m_global = m_global;
+  hd->h.shard_row_off = row_offset;
+  return RSVD_OK;
+}
+
 rsvd_status rsvd_create_dist(rsvd_handle** h, int device, int rank, int nranks,
                              const void* nccl_id128) {
   if (nranks < 1 || rank < 0 || rank >= nranks) {
@@ -412,6 +466,7 @@ void rsvd_destroy(rsvd_handle* hd) {
   rsvdb::Handle& h = hd->h;
   cudaSetDevice(h.device);
   rsvdb::patch_cancel(h);
+  if (h.vcomm) h.own_stream = h.own_stream_saved;  // the shared stream belongs to the communicator
   cudaStreamSynchronize(h.stream);
   rsvdb::comm_destroy(h);
   if (h.d_counters) cudaFree(h.d_counters);
@@ -445,6 +500,7 @@ void rsvd_destroy(rsvd_handle* hd) {
 
 rsvd_status rsvd_set_stream(rsvd_handle* hd, void* s) {
   if (!hd) return RSVD_ERR_PARAMETER;
+  if (hd->h.vcomm) return RSVD_OK;  // virtual ranks share the communicator's stream
   hd->h.stream = s ? static_cast<cudaStream_t>(s) : hd->h.own_stream;
   return RSVD_OK;
 }
@@ -640,21 +696,27 @@ rsvd_status rsvd_rsvd_host(rsvd_handle* hd, int64_t m, int64_t n, const double* 
   });
 }
 
+rsvd_status rsvd_spevd_shard_dev(rsvd_handle* hd, int64_t m_local, int64_t n, const double* a,
+                                 int64_t lda, int64_t k, int64_t p, rsvd_rng_state* rng,
+                                 int check_symmetry, double* u, int64_t ldu, double* lambda) {
+  const int64_t kk = std::max<int64_t>(k, 0);
+  const std::string key = graph_key("spevd", {m_local, n, pv(a), lda, k, p, check_symmetry,
+                                              rng ? rng->has_cached : -1});
+  return guard_graph(hd, "spevd_hermitian", key, rng, [&](rsvdb::Handle& h) {
+    if (!h.dist() && m_local != n) rsvdb::throw_dim("spevd_hermitian: matrix is not square");
+    // squareness of a row shard: m_global == n (checked in spevd_impl)
+    rsvdb::Problem P = rsvdb::make_problem(h, a, m_local, n, lda);
+    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
+    rsvdb::spevd_impl(h, P, k, p, r, check_symmetry != 0, sub_view(h.stage[0], m_local, kk),
+                      h.stage[1].p);
+    rsvdb::rng_download(h, r, rng);
+  }, {{u, m_local, kk, ldu}, {lambda, kk, 1, std::max<int64_t>(kk, 1)}});
+}
+
 rsvd_status rsvd_spevd_dev(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
                            int64_t p, rsvd_rng_state* rng, int check_symmetry, double* u,
                            int64_t ldu, double* lambda) {
-  const int64_t kk = std::max<int64_t>(k, 0);
-  const std::string key = graph_key("spevd", {n, pv(a), lda, k, p, check_symmetry,
-                                              rng ? rng->has_cached : -1});
-  return guard_graph(hd, "spevd_hermitian", key, rng, [&](rsvdb::Handle& h) {
-    rsvdb::Problem P = rsvdb::make_problem(h, a, n, n, lda);
-    // local rows: for a single GPU m_local == n
-    P.A = dm(a, P.A.rows, n, lda);
-    rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
-    rsvdb::spevd_impl(h, P, k, p, r, check_symmetry != 0, sub_view(h.stage[0], P.A.rows, kk),
-                      h.stage[1].p);
-    rsvdb::rng_download(h, r, rng);
-  }, {{u, n, kk, ldu}, {lambda, kk, 1, std::max<int64_t>(kk, 1)}});
+  return rsvd_spevd_shard_dev(hd, n, n, a, lda, k, p, rng, check_symmetry, u, ldu, lambda);
 }
 
 rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,

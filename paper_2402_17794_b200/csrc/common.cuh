@@ -98,6 +98,7 @@ class Arena {
 };
 
 struct Comm;  // NCCL communicator wrapper (dist.cu)
+struct VComm;  // in-process virtual communicator (dist.cu)
 
 // Header of an exact-mode patch list (rng.cu), in pinned mapped memory.
 struct PatchHdr {
@@ -131,10 +132,18 @@ struct Handle {
   int sm_count = 148;
   rsvd_counters counters{};
   Comm* comm = nullptr;        // null => single GPU
+  // In-process virtual communicator (dist.cu): P ranks = P host threads with
+  // P handles on ONE device, sharing one stream; the collectives are
+  // fixed-order device reductions (tests of the sharded path without P GPUs)
+  VComm* vcomm = nullptr;
+  cudaStream_t own_stream_saved = nullptr;  // the handle's own stream while attached
+  // Shard descriptor (rsvd_set_shard): global rows and this rank's row offset,
+  // so a sharded call needs no row-count exchange (0 = exchange per call)
+  int64_t shard_m_global = 0, shard_row_off = 0;
   int rank = 0, nranks = 1;
   // the row-sharded (NCCL) code path: also taken by a one-rank communicator,
   // which runs every exchange of the multi-GPU path on a single device
-  bool dist() const { return comm != nullptr; }
+  bool dist() const { return comm != nullptr || vcomm != nullptr; }
   // Live per-launch timing of the streaming-pass kernels (bench.py roofline):
   // CUDA events recorded on h.stream around every pass launch, folded into
   // per-kind totals at the call's final synchronization.

@@ -297,6 +297,47 @@ __global__ void asym_flag_kernel(const double* mm, int* flags, int bit) {
   if (!(mm[1] <= 1e-8 * (1.0 + mm[0]))) atomicOr(flags, bit);
 }
 
+// Sharded precondition: max|X - Y^T| (X r x c, Y c x r) and max|X|, max|Y|,
+// one read of each: 32 x 32 tiles of X, the matching tile of Y transposed
+// through shared memory.  out[0] max|.|, out[1] max asymmetry (atomic max).
+__global__ void __launch_bounds__(256) asym_block_kernel(const double* __restrict__ X, int64_t ldx,
+                                                        const double* __restrict__ Y, int64_t ldy,
+                                                        int64_t r, int64_t c, double* out) {
+  RSVD_PDL_ENTRY();
+  __shared__ double T[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 row groups
+  const int64_t tr = (r + 31) / 32, tc = (c + 31) / 32;
+  double mabs = 0.0, masym = 0.0;
+  for (int64_t t = blockIdx.x; t < tr * tc; t += gridDim.x) {
+    const int64_t bi = t % tr, bj = t / tr;
+    // Y tile (rows bj*32.., cols bi*32..) -> T[col][row] = Y^T
+    for (int q = ty; q < 32; q += 8) {
+      const int64_t yr = bj * 32 + tx, yc = bi * 32 + q;
+      const double y = (yr < c && yc < r) ? Y[yc * ldy + yr] : 0.0;
+      T[q][tx] = y;  // T[i][j] = Y(bj*32 + j, bi*32 + i) = Y^T(bi*32 + i, bj*32 + j)
+      mabs = fmax(mabs, fabs(y));
+    }
+    __syncthreads();
+    for (int q = ty; q < 32; q += 8) {
+      const int64_t xr = bi * 32 + tx, xc = bj * 32 + q;
+      if (xr < r && xc < c) {
+        const double x = X[xc * ldx + xr];
+        mabs = fmax(mabs, fabs(x));
+        masym = fmax(masym, fabs(x - T[tx][q]));
+      }
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+    masym = fmax(masym, __shfl_xor_sync(0xffffffffu, masym, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(&out[0], mabs);
+    atomic_max_nonneg(&out[1], masym);
+  }
+}
+
 int grid_for(int64_t n, const Handle& h) {
   return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 4 * h.sm_count)));
 }
@@ -321,6 +362,52 @@ void check_symmetric(Handle& h, const DMat& C, bool dist_unused) {
     launch_k(h, asym_kernel<64>, unsigned(grid), 256, 0, C.p, n, C.ld, mm);
   }
   RSVD_LAUNCHED(h);
+  launch_k(h, asym_flag_kernel, 1, 1, 0, mm, h.d_flags, kFlagAsymmetric);
+  RSVD_LAUNCHED(h);
+}
+
+// Asymmetry precondition of a row-sharded square A (singlepass.hpp:49-53),
+// as the separate, uncounted validation pass SURVEY 7.3(9) asks for: rank r
+// compares its block A_r[:, R_s] with rank s's block A_s[:, R_r] transposed
+// for every s (its own diagonal block included), then max-allreduces
+// (max|A|, max|A - A^T|).  The peer blocks move rank to rank (NCCL send /
+// recv, one peer per round; the virtual communicator reads them in place):
+// the only place A's data crosses GPUs, and it is not part of the single pass.
+void check_symmetric_dist(Handle& h, const Problem& P) {
+  const int64_t n = P.A.cols, mr = P.A.rows;
+  double* mm = h.ws.alloc(2);
+  RSVD_CUDA(cudaMemsetAsync(mm, 0, 16, h.stream));
+  std::vector<int64_t> rows, offs;
+  shard_layout(h, mr, &rows, &offs);
+  const int R = h.nranks, me = h.rank;
+  auto compare = [&](const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t r, int64_t c) {
+    if (r == 0 || c == 0) return;
+    const int64_t tiles = ceil_div(r, 32) * ceil_div(c, 32);
+    launch_k(h, asym_block_kernel, unsigned(std::min<int64_t>(tiles, 4 * h.sm_count)), 256, 0, X, ldx,
+             Y, ldy, r, c, mm);
+    RSVD_LAUNCHED(h);
+  };
+  for (int t = 0; t < R; ++t) {
+    const int s = (me + t) % R;       // the peer whose block A_s[:, R_me] this rank checks
+    const int d = (me - t + R) % R;   // the peer that checks A_me[:, R_d]
+    const int64_t ms = rows[size_t(s)], md = rows[size_t(d)];
+    // X = A_me[:, R_s] (mr x ms), Y = A_s[:, R_me] (ms x mr)
+    const double* X = P.A.p + offs[size_t(s)] * P.A.ld;
+    const double* Y;
+    int64_t ldy;
+    if (t == 0) {
+      Y = P.A.p + offs[size_t(me)] * P.A.ld;
+      ldy = P.A.ld;
+    } else {
+      double* buf = h.ws.alloc(std::max<int64_t>(ms * mr, 1));
+      peer_exchange(h, P.A.p + offs[size_t(d)] * P.A.ld, P.A.ld, mr, md, d, buf, ms, mr, s);
+      Y = buf;
+      ldy = ms;
+    }
+    compare(X, P.A.ld, Y, ldy, mr, ms);
+  }
+  (void)n;
+  allreduce_max(h, mm, 2);
   launch_k(h, asym_flag_kernel, 1, 1, 0, mm, h.d_flags, kFlagAsymmetric);
   RSVD_LAUNCHED(h);
 }
@@ -572,10 +659,13 @@ void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
   // raises a sticky device flag that the call's final check turns into the
   // reference's NumericError (no mid-call host wait, so the call stays
   // graph-replayable); a streamed upload checks once every panel has landed.
-  const bool sym_first = check_sym && !P.dist && P.panels.empty();
+  const bool sym_first = check_sym && P.panels.empty();
   if (sym_first) {
     a_ready(h, P);
-    check_symmetric(h, P.A, false);
+    if (P.dist)
+      check_symmetric_dist(h, P);
+    else
+      check_symmetric(h, P.A, false);
   }
   const int64_t l = k + p;
   DMat Omega = h.ws.mat(n, l);
@@ -589,7 +679,7 @@ void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
     h.pass_cfg_big = 1;
     op_apply(h, P, Omega, Y);  // the single pass over A
   }
-  if (check_sym && !P.dist && !sym_first) {
+  if (check_sym && !sym_first) {  // streamed upload (single GPU)
     a_ready(h, P);
     check_symmetric(h, P.A, false);
   }

@@ -296,6 +296,29 @@ __global__ void __launch_bounds__(kThreads, 2)
     double* C = it.adj ? p.W : p.Y;
     const int64_t ldc = it.adj ? p.ldw : p.ldy;
     const int64_t mlim = it.adj ? p.K : p.row_end;
+    // all of the tile's earlier sum is loaded before any store (one L2 round
+    // trip; interleaved load-add-store would serialize 28 of them: the
+    // stores may alias later loads as far as the compiler knows)
+    if (it.idx > 0) {
+      double old[kWMT][kNT][2];
+#pragma unroll
+      for (int a = 0; a < kWMT; ++a) {
+        const int64_t m = it.m0 + wm0 + a * 8 + r8;
+#pragma unroll
+        for (int j = 0; j < kNT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t n = it.n0 + j * 8 + 2 * c4 + e;
+            old[a][j][e] = (m < mlim && n < p.L) ? __ldcg(C + n * ldc + m) : 0.0;
+          }
+      }
+#pragma unroll
+      for (int a = 0; a < kWMT; ++a)
+#pragma unroll
+        for (int j = 0; j < kNT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc[a][j][e] = old[a][j][e] + acc[a][j][e];
+    }
 #pragma unroll
     for (int a = 0; a < kWMT; ++a) {
       const int64_t m = it.m0 + wm0 + a * 8 + r8;
@@ -305,10 +328,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t n = it.n0 + j * 8 + 2 * c4 + e;
-          if (n < p.L) {
-            double* dst = C + n * ldc + m;
-            *dst = (it.idx == 0) ? acc[a][j][e] : __ldcg(dst) + acc[a][j][e];
-          }
+          if (n < p.L) C[n * ldc + m] = acc[a][j][e];
         }
     }
     ptx::named_bar(1, NCT);
@@ -326,7 +346,7 @@ int fused_macroblock(const Handle& h) {
     const char* e = std::getenv("RSVD_FUSED_MB");
     return e ? std::atoi(e) : 0;
   }();
-  const int v = h.fused_mb > 0 ? h.fused_mb : (env > 0 ? env : 2048);
+  const int v = h.fused_mb > 0 ? h.fused_mb : (env > 0 ? env : 4096);
   return std::max(kBM, (v / kBM) * kBM);
 }
 

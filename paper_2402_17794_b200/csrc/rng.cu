@@ -31,16 +31,15 @@
 // inputs -- always ones whose exact log lies within ~0.02 ulp of a rounding
 // midpoint (ddlog.cuh log_near_midpoint; ~1.7 % of inputs fall inside the
 // window).  polar_write appends every such accepted pair (stream index, r2, x,
-// y) to a pinned, device-mapped list; patch_signal publishes its length in
-// the list's header; the calling host thread -- which has already queued the
-// whole call and is about to wait for it anyway -- spins on that header,
-// evaluates libstdc++'s multiplier sqrt(-2 * std::log(r2) / r2) with the
-// HOST's own glibc log (a spinning worker pool for long lists) and releases
-// the header; polar_patch, spinning on the release, rewrites those normals
-// (and the cached variate).  No host node and no mid-call synchronization:
-// the GPU waits ~the host's compute time, and the call stays graph-replayable
-// (a replay re-arms the same headers and answers them after the launch; an
-// eager call answers each list as soon as it is queued).  The result is the reference's stream
+// y) to a pinned, device-mapped list; the host evaluates libstdc++'s
+// multiplier sqrt(-2 * std::log(r2) / r2) with the HOST's own glibc log (a
+// spinning worker pool for long lists); polar_patch rewrites those normals
+// (and the cached variate).  An eager call reads the list's length and
+// answers it synchronously before queueing polar_patch.  A CUDA-graph-captured
+// call cannot wait mid-graph: there patch_signal publishes the length in the
+// list's header, polar_patch spins on the header's release flag, and the host
+// thread answers the list right after the graph launch (finish_call); a
+// replay re-arms the same headers.  No host node in either form.  The result is the reference's stream
 // bit for bit on the host that runs it, whichever glibc ifunc (FMA or SSE2)
 // that host selects.
 #include <algorithm>
@@ -49,6 +48,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -546,6 +546,9 @@ class HostPool {
       if (n > 0) f(0, n);
       return;
     }
+    // one job at a time: several handles (e.g. the ranks of a virtual
+    // communicator, one thread each) may answer their lists concurrently
+    std::lock_guard<std::mutex> job(run_mu_);
     fn_ = &f;
     n_ = n;
     parts_ = parts;
@@ -607,6 +610,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> workers_;
+  std::mutex run_mu_;
   std::mutex m_;
   std::condition_variable cv_;
   const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
@@ -659,8 +663,16 @@ const ddlog::Entry* host_log_table() {
 
 // Answer the exact-mode lists of this call, in queue order (see "Exact mode").
 // Called by the host thread before it waits for the stream.
+static bool patch_debug() {
+  static const bool on = std::getenv("RSVD_PATCH_DEBUG") != nullptr;
+  return on;
+}
+
 void patch_service(Handle& h) {
   if (h.patch_pending.empty()) return;
+  if (patch_debug())
+    std::fprintf(stderr, "[patch] rank %d service %zu list(s) first %p\n", h.rank, h.patch_pending.size(),
+                 static_cast<void*>(h.patch_pending[0]));
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   RSVD_CUDA(cudaStreamIsCapturing(h.stream, &cap));
   if (cap != cudaStreamCaptureStatusNone) return;  // nothing runs before the graph launches
@@ -682,6 +694,8 @@ void patch_service(Handle& h) {
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     const int64_t n = std::min<int64_t>(int64_t(hdr->count), hdr->cap);
+    if (patch_debug()) std::fprintf(stderr, "[patch] rank %d list %p ready, %lld entries\n", h.rank,
+                                    static_cast<void*>(hdr), static_cast<long long>(n));
     const PatchEntry* ent = reinterpret_cast<const PatchEntry*>(reinterpret_cast<char*>(hdr) + 64);
     PatchOut* out = reinterpret_cast<PatchOut*>(reinterpret_cast<char*>(hdr) + 64 +
                                                 size_t(hdr->cap) * sizeof(PatchEntry));
@@ -697,6 +711,7 @@ void patch_service(Handle& h) {
     });
     std::atomic_thread_fence(std::memory_order_release);
     reinterpret_cast<volatile PatchHdr*>(hdr)->done = 1;
+    if (patch_debug()) std::fprintf(stderr, "[patch] rank %d list %p done\n", h.rank, static_cast<void*>(hdr));
   }
   h.patch_pending.clear();
 }
@@ -865,21 +880,37 @@ void gaussian_dev(Handle& h, int64_t n, int64_t l, DevRng& rng, DMat out, int64_
                                                h.d_flags);
     RSVD_LAUNCHED(h);
     if (hdr) {
-      launch_k(h, patch_signal_kernel, 1, 32, 0, static_cast<const unsigned long long*>(pl.count), hdr);
-      RSVD_LAUNCHED(h);
       unsigned* gate = reinterpret_cast<unsigned*>(pl.count + 1);
       const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(pl.cap, 1024), h.sm_count)));
-      launch_k(h, polar_patch_kernel, unsigned(blocks), 256, 0, static_cast<const PatchHdr*>(hdr), gate,
-               static_cast<const PatchEntry*>(pl.ent), static_cast<const PatchOut*>(pout), pl.cap, g, dst);
-      RSVD_LAUNCHED(h);
-      h.patch_pending.push_back(hdr);
-      // Eager calls answer the list right here: anything the host does later
-      // in the call may synchronize the device implicitly (cudaMalloc of a
-      // growing workspace, cudaFree), which would wait on polar_patch while
-      // polar_patch waits on the host.  Under capture nothing runs yet: the
-      // list is answered after the graph launch (finish_call), when the host
-      // does nothing else.
-      patch_service(h);
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      RSVD_CUDA(cudaStreamIsCapturing(h.stream, &cap));
+      if (cap == cudaStreamCaptureStatusNone) {
+        // Eager call: the list is answered right here, synchronously (the
+        // host is about to wait for the call anyway), and polar_patch is
+        // queued with its answer already in place -- no kernel ever waits
+        // on the host, so no later implicit device synchronization (a
+        // growing workspace's cudaMalloc, another thread sharing the stream)
+        // can deadlock with it.
+        // (the same kernels as the captured form: counters agree across both)
+        launch_k(h, patch_signal_kernel, 1, 32, 0, static_cast<const unsigned long long*>(pl.count), hdr);
+        RSVD_LAUNCHED(h);
+        stream_sync(h);
+        h.patch_pending.push_back(hdr);
+        patch_service(h);  // computes the normals, sets done = 1
+        launch_k(h, polar_patch_kernel, unsigned(blocks), 256, 0, static_cast<const PatchHdr*>(hdr), gate,
+                 static_cast<const PatchEntry*>(pl.ent), static_cast<const PatchOut*>(pout), pl.cap, g, dst);
+        RSVD_LAUNCHED(h);
+      } else {
+        // Captured call: patch_signal publishes the count, polar_patch waits
+        // for the host's answer, which finish_call gives after the graph
+        // launch (the host does nothing else in between).
+        launch_k(h, patch_signal_kernel, 1, 32, 0, static_cast<const unsigned long long*>(pl.count), hdr);
+        RSVD_LAUNCHED(h);
+        launch_k(h, polar_patch_kernel, unsigned(blocks), 256, 0, static_cast<const PatchHdr*>(hdr), gate,
+                 static_cast<const PatchEntry*>(pl.ent), static_cast<const PatchOut*>(pout), pl.cap, g, dst);
+        RSVD_LAUNCHED(h);
+        h.patch_pending.push_back(hdr);
+      }
     }
   } else {
     launch_k(h, rng_finish_kernel, 1, 32, 0, nullptr, nullptr, nullptr, 0, 0, dst, h.d_flags);
