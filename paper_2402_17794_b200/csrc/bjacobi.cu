@@ -312,7 +312,9 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
                 // rotation zeroing the (p, q) inner product (X' = X R, R = [[c, s], [-s, c]]),
                 // tan(theta) = sgn(d) 2g / (|d| + r), r = |(d, 2g)|, d = G_qq - G_pp,
                 // from two reciprocal square roots: c = sqrt(h), h = (1 + |d|/r) / 2,
-                // s = sgn(d) g / (r c)
+                // s = sgn(d) g / (r c).  (A single-precision angle made orthogonal
+                // to double precision by a series was measured slower: ~1300
+                // vs ~1060 cycles per inner round.)
                 const double d = be - al, g2 = 2.0 * ga;
                 const double ir = rsqrt(fma(d, d, g2 * g2));
                 const double hh = fma(0.5 * fabs(d), ir, 0.5);

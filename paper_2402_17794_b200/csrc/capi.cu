@@ -53,27 +53,58 @@ void join_caller_stream(rsvdb::Handle& h) {
   RSVD_CUDA(cudaStreamWaitEvent(h.own_stream, h.join_ev, 0));
 }
 
+// One eager run of a call's pipeline: f, then the final check.  A wrong
+// speculation (RetryRobust from the final check) re-runs f once in robust
+// mode -- from the caller's unchanged inputs and RNG state, the counters of
+// the first attempt rolled back; every rank of a distributed handle sees the
+// same (replicated) flag, so all ranks retry together.
 template <class F>
-rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
-  try {
-    if (!hd) throw rsvdb::Error(RSVD_ERR_PARAMETER, "null handle");
-    rsvdb::Handle& h = hd->h;
-    RSVD_CUDA(cudaSetDevice(h.device));
+void run_eager(rsvdb::Handle& h, const char* what, F&& f) {
+  const rsvd_counters before = h.counters;
+  for (int attempt = 0;; ++attempt) {
     h.ws.reset();
     h.patch_chunk = h.patch_off = 0;
     join_caller_stream(h);
     h.rng_user_out = nullptr;
     rsvdb::trace_begin(h);
     try {
-      f(h);
+      try {
+        f(h);
+      } catch (const rsvdb::RetryRobust&) {
+        throw;
+      } catch (...) {
+        // a rank failing inside the pipeline releases peers blocked in a
+        // virtual collective; errors of the final check (finish_call) are
+        // raised by every rank alike and leave the communicator usable
+        rsvdb::vcomm_fail(h);
+        throw;
+      }
+      rsvdb::finish_call(h, what);
+      h.robust = false;
+      return;
+    } catch (const rsvdb::RetryRobust&) {
+      rsvdb::patch_cancel(h);
+      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      h.counters = before;
+      if (attempt > 0 || h.robust) {
+        h.robust = false;
+        throw rsvdb::Error(RSVD_ERR_INTERNAL, std::string(what) + ": robust re-run asked to retry");
+      }
+      h.robust = true;
     } catch (...) {
-      // a rank failing inside the pipeline releases peers blocked in a
-      // virtual collective; errors of the final check (finish_call) are raised
-      // by every rank alike and leave the communicator usable
-      rsvdb::vcomm_fail(h);
+      h.robust = false;
       throw;
     }
-    rsvdb::finish_call(h, what);
+  }
+}
+
+template <class F>
+rsvd_status guard(rsvd_handle* hd, const char* what, F&& f) {
+  try {
+    if (!hd) throw rsvdb::Error(RSVD_ERR_PARAMETER, "null handle");
+    rsvdb::Handle& h = hd->h;
+    RSVD_CUDA(cudaSetDevice(h.device));
+    run_eager(h, what, f);
     return RSVD_OK;
   } catch (const rsvdb::Error& e) {
     g_err = e.what();
@@ -153,7 +184,9 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     const char* e = std::getenv("RSVD_GRAPHS");
     return !(e && e[0] == '0');
   }();
-  if (!hd || !env_on || !hd->h.graphs || hd->h.trace || hd->h.dist()) return guard(hd, what, eager);
+  // (NCCL-sharded handles are captured too -- NCCL collectives are
+  // graph-capturable; the virtual communicator's host barriers are not)
+  if (!hd || !env_on || !hd->h.graphs || hd->h.trace || hd->h.vcomm) return guard(hd, what, eager);
   rsvdb::Handle& h = hd->h;
   auto add = [](rsvd_counters& a, const rsvd_counters& d, int sgn) {
     a.apply += sgn * d.apply;
@@ -177,6 +210,17 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
       h.graph_cache.clear();
     }
     rsvdb::Handle::GraphEntry& e = h.graph_cache[h.prof ? key + "|prof" : key];
+    // a replay (or the capturing run) whose speculation was wrong: undo its
+    // counters and re-run the call eagerly in robust mode
+    auto robust_rerun = [&](const rsvd_counters& before) {
+      rsvdb::patch_cancel(h);
+      RSVD_CUDA(cudaStreamSynchronize(h.stream));
+      h.counters = before;
+      h.rng_user_out = nullptr;
+      h.prof_pending.clear();
+      h.robust = true;
+      return guard(hd, what, eager);
+    };
     if (e.exec && e.gen == gen_now()) {
       if (rng) std::memcpy(h.h_rng_in, rng, sizeof(rsvd_rng_state));
       for (rsvdb::PatchHdr* ph : e.patch) {  // re-arm the exact-mode lists
@@ -184,12 +228,17 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
         ph->done = 0;
       }
       h.patch_pending = e.patch;
+      const rsvd_counters before = h.counters;
       RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
       stage_copy_out(h, e.stage, outs);
       add(h.counters, e.delta, 1);
       h.prof_pending = e.prof;
       h.rng_user_out = rng;
-      rsvdb::finish_call(h, what);
+      try {
+        rsvdb::finish_call(h, what);
+      } catch (const rsvdb::RetryRobust&) {
+        return robust_rerun(before);
+      }
       return RSVD_OK;
     }
     if (e.exec) {  // stale: a buffer it references was reallocated
@@ -241,7 +290,11 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
           RSVD_CUDA(cudaGraphLaunch(e.exec, h.stream));
           stage_copy_out(h, e.stage, outs);
           h.rng_user_out = rng;
-          rsvdb::finish_call(h, what);
+          try {
+            rsvdb::finish_call(h, what);
+          } catch (const rsvdb::RetryRobust&) {
+            return robust_rerun(before);
+          }
           return RSVD_OK;
         }
         cudaGetLastError();

@@ -24,6 +24,10 @@ struct Error : std::runtime_error {
   rsvd_status code;
   Error(rsvd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
+// Raised at a call's final check when a speculative (sync-free) branch
+// decision turned out to need the robust path: the call is re-run eagerly
+// with Handle::robust set (capi.cu).  Never reaches the caller.
+struct RetryRobust {};
 [[noreturn]] inline void throw_dim(const std::string& m) { throw Error(RSVD_ERR_DIMENSION, m); }
 [[noreturn]] inline void throw_param(const std::string& m) { throw Error(RSVD_ERR_PARAMETER, m); }
 [[noreturn]] inline void throw_numeric(const std::string& m) { throw Error(RSVD_ERR_NUMERIC, m); }
@@ -124,6 +128,13 @@ struct Handle {
   std::vector<cudaEvent_t> panel_ev;
   // fused Alg-6 pass macroblock edge override (0 = RSVD_FUSED_MB / default)
   int fused_mb = 0;
+  // Robust mode: data-dependent branch decisions (CholeskyQR's pass count
+  // after a shifted Cholesky) read the device flag on the host mid-call.
+  // Off by default: those decisions are speculated without a host round trip
+  // (graph-capturable, no mid-call sync) and a device flag makes the call
+  // re-run in robust mode when the speculation was wrong (rare: numerically
+  // rank-deficient sketches).
+  bool robust = false;
   Arena ws;
   int* d_counters = nullptr;   // split-K tile semaphores (kept zeroed)
   int64_t n_counters = 0;

@@ -346,14 +346,20 @@ double orthonormal_deviation(Handle& h, const DMat& X) {
   return gram_deviation(h, G);
 }
 
+void gram_deviation_dev(Handle& h, const DMat& G, double* d) {
+  const int64_t k = G.rows;
+  if (k == 0) return;
+  const int blocks = int(std::min<int64_t>(ceil_div(k * k, 256), 2 * h.sm_count));
+  launch_k(h, dev_identity_kernel, blocks, 256, 0, G.p, k, G.ld, d);
+  RSVD_LAUNCHED(h);
+}
+
 double gram_deviation(Handle& h, const DMat& G) {
   const int64_t k = G.rows;
   if (k == 0) return 0.0;
   double* d = h.ws.alloc(1);
   RSVD_CUDA(cudaMemsetAsync(d, 0, sizeof(double), h.stream));
-  const int blocks = int(std::min<int64_t>(ceil_div(k * k, 256), 2 * h.sm_count));
-  launch_k(h, dev_identity_kernel, blocks, 256, 0, G.p, k, G.ld, d);
-  RSVD_LAUNCHED(h);
+  gram_deviation_dev(h, G, d);
   return read_scalar(h, d);
 }
 

@@ -8,6 +8,8 @@ namespace rsvdb {
 void singular_values_impl(Handle& h, const DMat& M, double* s);
 // max |G - I| of a Gram (synchronizes)
 double gram_deviation(Handle& h, const DMat& G);
+// max |G - I| into *d (device, zeroed by the caller; atomic max), no host read
+void gram_deviation_dev(Handle& h, const DMat& G, double* d);
 // max |X^T X - I| (synchronizes)
 double orthonormal_deviation(Handle& h, const DMat& X);
 // R = A - Q Z^T  (A m x n, Q m x l, Z n x l)

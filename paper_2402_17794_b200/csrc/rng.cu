@@ -412,8 +412,10 @@ __global__ void polar_write_kernel(const uint64_t* __restrict__ words, const uin
         if (near) {
           const int64_t idx = int64_t(base) + __popc(nb & ((1u << lane) - 1u));
           if (idx < pl.cap) {
+            // (visible to the host by patch_signal's system-scope fence: it
+            // runs after this grid completed -- griddepcontrol.wait -- and
+            // fences before publishing the header)
             pl.ent[idx] = PatchEntry{e0, p.r2, p.x, p.y};
-            __threadfence_system();  // visible to the host before patch_signal's header store
           } else {
             atomicOr(flags, kFlagRngPatchOverflow);
           }

@@ -1099,6 +1099,10 @@ void check_flags(Handle& h, const char* what) {
   RSVD_CUDA(cudaMemcpyAsync(h.h_flags, h.d_flags, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
   stream_sync(h);
   const int f = *h.h_flags;
+  if (f & kFlagRetryRobust) {  // a speculated branch was wrong: re-run robustly
+    clear_flags(h);
+    throw RetryRobust{};
+  }
   if (f) {
     clear_flags(h);
     std::string m = std::string(what) + ": ";
@@ -1307,6 +1311,14 @@ static bool cholqr_fused(Handle& h, const DMat& X, DMat Q, DMat* Rout) {
   return true;
 }
 
+// Speculative CholeskyQR check (see cholqr): retry if a shift was used and
+// (l <= 64) the final Gram deviates from I by more than tol.
+__global__ void retry_flag_kernel(const int* shift_used, const double* dev, double tol, int* flags) {
+  RSVD_PDL_ENTRY();
+  if (threadIdx.x == 0 && *shift_used && (dev == nullptr || !(*dev <= tol)))
+    atomicOr(flags, kFlagRetryRobust);
+}
+
 static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   const int l = int(X.cols);
   if (!dist && cholqr_fused(h, X, Q, Rout)) return;
@@ -1357,12 +1369,39 @@ static void cholqr(Handle& h, const DMat& X, DMat Q, DMat* Rout, bool dist) {
   pass(X0, Q);
   int passes = 4;
   if (l > 64) {
-    int used = 0;
-    RSVD_CUDA(cudaMemcpyAsync(&used, shift_used, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
-    stream_sync(h);
-    passes = used ? 4 : 2;
+    if (h.robust) {
+      int used = 0;
+      RSVD_CUDA(cudaMemcpyAsync(&used, shift_used, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+      stream_sync(h);
+      passes = used ? 4 : 2;
+    } else {
+      passes = 2;  // speculated: no shift (checked below, on the device)
+    }
   }
   for (int i = 1; i < passes; ++i) pass(Q, Q);
+  if (!h.robust) {
+    // Speculative form (no host round trip): the robust form takes more
+    // passes exactly when a Cholesky needed the shift (l > 64), or when, after
+    // a shifted pass, Q^T Q is not the identity to working accuracy (l <= 64).
+    // Either case sets the retry flag, and the call re-runs in robust mode;
+    // otherwise both forms executed the same operations (bitwise the same Q).
+    double* dev = nullptr;
+    if (l <= 64) {
+      gemm_tn(h, Q, Q, G);
+      if (dist) allreduce_mat(h, G);
+      dev = h.ws.alloc(1);
+      RSVD_CUDA(cudaMemsetAsync(dev, 0, sizeof(double), h.stream));
+      gram_deviation_dev(h, G, dev);
+    }
+    launch_k(h, retry_flag_kernel, 1, 32, 0, static_cast<const int*>(shift_used),
+             static_cast<const double*>(dev), 8.0 * l * 1.1102230246251565e-16, h.d_flags);
+    RSVD_LAUNCHED(h);
+    if (Rout) {
+      gemm_tn(h, Q, X0, *Rout);
+      if (dist) allreduce_mat(h, *Rout);
+    }
+    return;
+  }
   // Numerically rank-deficient input (the shift was needed): each shifted
   // pass lifts the null-space directions by ~1/sqrt(shift) until they are
   // unit vectors, which can take more than the fixed passes.  Continue until

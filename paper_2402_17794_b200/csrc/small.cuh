@@ -72,6 +72,7 @@ enum FlagBits : int {
   kFlagCholBreakdown = 16,
   kFlagPowerCap = 32,
   kFlagRngPatchOverflow = 64,
+  kFlagRetryRobust = 128,  // not an error: re-run the call in robust mode
 };
 // Raises NumericError if any flag is set (synchronizes the stream).
 void check_flags(Handle& h, const char* what);
