@@ -272,6 +272,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int a = 0; a < kWMT; ++a)
 #pragma unroll
       for (int j = 0; j < kNT; ++j) acc[a][j][0] = acc[a][j][1] = 0.0;
+    // The tile's earlier sum is re-read in the epilogue: when its predecessor
+    // has already released it (the usual case: it ran ~2 waves earlier), pull
+    // its lines into L2 now, so the epilogue's read-modify-write does not pay
+    // an HBM round trip.  (A non-blocking peek; prefetches only.)
+    if (it.idx > 0 && ld_acquire(it.sem) == it.idx) {
+      double* C = it.adj ? p.W : p.Y;
+      const int64_t ldc = it.adj ? p.ldw : p.ldy;
+      const int64_t mlim = it.adj ? p.K : p.row_end;
+      // kBN columns x 4 lines of 128 B (64 rows) per column
+      for (int ln = tid; ln < kBN * 4; ln += NCT) {
+        const int64_t n = it.n0 + ln / 4, m = it.m0 + 16 * (ln % 4);
+        if (n < p.L && m < mlim)
+          asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(C + n * ldc + m));
+      }
+    }
     for (int kb = 0; kb < it.nkb; ++kb, ++i) {
       const int s = int(i % kStages);
       ptx::mbar_wait(&full[s], int(i / kStages) & 1);
@@ -284,15 +299,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
-    // ordered in-place accumulation into the output tile
-    if (tid == 0 && it.idx > 0) {
+    // ordered in-place accumulation into the output tile: every thread
+    // acquires the predecessor's release itself (usually already there), so
+    // no barrier precedes the read-modify-write
+    if (it.idx > 0) {
       const long long t0 = clock64();
       while (ld_acquire(it.sem) != it.idx) {
         __nanosleep(64);
         if (clock64() - t0 > (40LL << 30)) __trap();  // a schedule bug traps, never hangs
       }
     }
-    ptx::named_bar(1, NCT);
     double* C = it.adj ? p.W : p.Y;
     const int64_t ldc = it.adj ? p.ldw : p.ldy;
     const int64_t mlim = it.adj ? p.K : p.row_end;
@@ -331,11 +347,10 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (n < p.L) C[n * ldc + m] = acc[a][j][e];
         }
     }
+    // every consumer's stores happen-before thread 0's release (bar.sync
+    // orders them; st.release is cumulative): no separate fence
     ptx::named_bar(1, NCT);
-    if (tid == 0) {
-      __threadfence();
-      st_release(it.sem, it.idx + 1);
-    }
+    if (tid == 0) st_release(it.sem, it.idx + 1);
   }
 }
 
@@ -346,7 +361,7 @@ int fused_macroblock(const Handle& h) {
     const char* e = std::getenv("RSVD_FUSED_MB");
     return e ? std::atoi(e) : 0;
   }();
-  const int v = h.fused_mb > 0 ? h.fused_mb : (env > 0 ? env : 4096);
+  const int v = h.fused_mb > 0 ? h.fused_mb : (env > 0 ? env : 2048);
   return std::max(kBM, (v / kBM) * kBM);
 }
 

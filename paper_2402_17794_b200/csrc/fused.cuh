@@ -4,7 +4,7 @@
 #include "common.cuh"
 
 namespace rsvdb {
-// Macroblock edge (RSVD_FUSED_MB, default 4096): row panels passed to
+// Macroblock edge (RSVD_FUSED_MB, default 2048): row panels passed to
 // fused_dual_pass must start at multiples of it.
 int fused_macroblock(const Handle& h);
 // Tile semaphores fused_dual_pass needs for an M x K matrix and L columns.
