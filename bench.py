@@ -404,14 +404,17 @@ def main():
         a_pin = torch.empty((n, r1 - r0), dtype=torch.float64, pin_memory=True)
         a_pin.copy_(a_loc.t())
         a_host = a_pin.numpy().T  # Fortran-ordered (m_local x n) view
-        u_h = torch.empty((l, r1 - r0), dtype=torch.float64, pin_memory=True).numpy().T
-        v_h = torch.empty((l, n), dtype=torch.float64, pin_memory=True).numpy().T
-        s_h = torch.empty(l, dtype=torch.float64, pin_memory=True).numpy()
+        # output buffers: pinned, allocated once outside the timed region
+        # (the factors' width: k for the single-pass algorithms, k+p for rsvd)
+        w_out = k if cfg["alg"] >= 5 else l
+        u_h = torch.empty((w_out, r1 - r0), dtype=torch.float64, pin_memory=True).numpy().T
+        v_h = torch.empty((w_out, n), dtype=torch.float64, pin_memory=True).numpy().T
+        s_h = torch.empty(max(w_out, 1), dtype=torch.float64, pin_memory=True).numpy()
         def host_step():
             if cfg["alg"] == 5:
-                return eng.spevd_host(a_host, k, p, eng.Rng(SEED_OMEGA))
+                return eng.spevd_host(a_host, k, p, eng.Rng(SEED_OMEGA), out=(u_h, s_h))
             if cfg["alg"] == 6:
-                return eng.spsvd_host(a_host, k, p, eng.Rng(SEED_OMEGA))
+                return eng.spsvd_host(a_host, k, p, eng.Rng(SEED_OMEGA), out=(u_h, s_h, v_h))
             return eng.rsvd_host(a_host, sk, eng.Rng(SEED_OMEGA), out=(u_h, s_h, v_h))
         for _ in range(3):  # warm: the first calls grow and then merge the device workspace
             host_step()
@@ -427,7 +430,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         h2d = (r1 - r0) * n * 8
-        d2h = ((r1 - r0) * l + l + n * l) * 8
+        d2h = ((r1 - r0) * w_out + w_out + (0 if cfg["alg"] == 5 else n * w_out)) * 8
 
     # ---- roofline of the dominant pass kernel (live CUDA-event timing)
     hbm = hbm_peak_gbs()

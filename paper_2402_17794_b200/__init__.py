@@ -829,13 +829,15 @@ def rsvd_host(a: np.ndarray, cfg: SketchConfig, rng: Optional[Rng] = None, out=N
     return SvdApprox(u, s, v)
 
 
-def spevd_host(a: np.ndarray, k: int, p: int, rng: Rng):
-    """End-to-end host-buffer spevd_hermitian (rsvd_spevd_host)."""
+def spevd_host(a: np.ndarray, k: int, p: int, rng: Rng, out=None):
+    """End-to-end host-buffer spevd_hermitian (rsvd_spevd_host): A streamed up
+    in row panels into the pass; `out` optionally supplies preallocated
+    (U, lambda) host arrays (pinned memory makes the copy-back fast)."""
     if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
         a = np.asfortranarray(a, dtype=np.float64)
     n = a.shape[0]
     kk = max(k, 0)
-    u, lam = np.empty((n, kk), order="F"), np.empty(max(kk, 1))
+    u, lam = out if out is not None else (np.empty((n, kk), order="F"), np.empty(max(kk, 1)))
     e = _eng()
     P = lambda x: x.ctypes.data_as(ctypes.c_void_p)
     _check(_load().rsvd_spevd_host(e.handle, n, P(a), max(n, 1), k, p, ctypes.byref(rng.state),
@@ -843,13 +845,16 @@ def spevd_host(a: np.ndarray, k: int, p: int, rng: Rng):
     return EvdApprox(u, lam[:kk])
 
 
-def spsvd_host(a: np.ndarray, k: int, p: int, rng: Rng):
-    """End-to-end host-buffer spsvd_general (rsvd_spsvd_host)."""
+def spsvd_host(a: np.ndarray, k: int, p: int, rng: Rng, out=None):
+    """End-to-end host-buffer spsvd_general (rsvd_spsvd_host): A streamed up
+    in row panels into the fused pass; `out` optionally supplies preallocated
+    (U, sigma, V) host arrays (pinned memory makes the copy-back fast)."""
     if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
         a = np.asfortranarray(a, dtype=np.float64)
     m, n = a.shape
     kk = max(k, 0)
-    u, s, v = np.empty((m, kk), order="F"), np.empty(max(kk, 1)), np.empty((n, kk), order="F")
+    u, s, v = out if out is not None else (np.empty((m, kk), order="F"), np.empty(max(kk, 1)),
+                                           np.empty((n, kk), order="F"))
     e = _eng()
     P = lambda x: x.ctypes.data_as(ctypes.c_void_p)
     _check(_load().rsvd_spsvd_host(e.handle, m, n, P(a), max(m, 1), k, p, ctypes.byref(rng.state),

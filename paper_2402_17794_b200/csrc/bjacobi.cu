@@ -77,7 +77,7 @@ constexpr int kVL = 36;  // ld of V: 36 % 16 == 4 keeps DMMA B-fragment loads co
 struct BJProblem {
   double* X;
   double* Jm;
-  int* changed;  // kBJMaxSweeps + 2 ints
+  int* changed;  // kBJMaxSweeps + 3 ints: per sweep, no-convergence, zero-column count, launch shape
   unsigned long long* smax;  // per sweep: largest g^2/(a b) of the fresh Grams (bits)
 };
 struct BJBatch {
@@ -101,6 +101,12 @@ __global__ void __launch_bounds__(kBJThreads) bjacobi_kernel(BJBatch batch, int 
   cg::grid_group grid = cg::this_grid();
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = int(cluster.num_blocks()), crank = int(cluster.block_rank());
+  if (cs * rows_per < l) {
+    // launched without its cluster shape (seen under an ncu kernel replay):
+    // the visits would miss rows -- fail loudly instead of not converging
+    if (threadIdx.x == 0 && blockIdx.x == 0) batch.p[0].changed[kBJMaxSweeps + 2] = 1;
+    return;
+  }
   const int cid = int(blockIdx.x) / cs, ncl = int(gridDim.x) / cs;
   const int r_lo = crank * rows_per, r_hi = min(l, r_lo + rows_per), nr = max(0, r_hi - r_lo);
   extern __shared__ double sm[];
@@ -574,6 +580,7 @@ __global__ void bj_init_kernel(const double* __restrict__ Rm, int64_t ldr, int l
 __global__ void bj_flag_kernel(const int* changed, int* flags) {
   RSVD_PDL_ENTRY();
   if (changed[kBJMaxSweeps]) atomicOr(flags, kFlagJacobiNoConv);
+  if (changed[kBJMaxSweeps + 2]) atomicOr(flags, kFlagLaunchShape);
 }
 
 // mu >= max_i sum_j |c_ij| >= |lambda|_max (Gershgorin): C + mu I is PSD.
@@ -673,7 +680,7 @@ BJWork bj_prepare(Handle& h, const DMat& Rm) {
   w.Jm = h.ws.alloc(int64_t(l) * l);
   w.nrm = h.ws.alloc(l);
   w.order = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(l) * 4 + 16));
-  const size_t cb = size_t(kBJMaxSweeps + 2) * 4, mb = size_t(kBJMaxSweeps) * 8;
+  const size_t cb = size_t(kBJMaxSweeps + 4) * 4, mb = size_t(kBJMaxSweeps) * 8;
   w.changed = reinterpret_cast<int*>(h.ws.alloc_bytes(cb + mb));  // 256-byte aligned
   w.nzero = w.changed + kBJMaxSweeps + 1;
   w.smax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(w.changed) + cb);

@@ -1113,6 +1113,7 @@ void check_flags(Handle& h, const char* what) {
     if (f & kFlagPowerCap) throw_numeric(m + "power iteration hit the 5000-step cap");
     if (f & kFlagRngExhausted) throw Error(RSVD_ERR_INTERNAL, m + "rng attempt budget exhausted");
     if (f & kFlagRngPatchOverflow) throw Error(RSVD_ERR_INTERNAL, m + "rng exact-log patch list overflow");
+    if (f & kFlagLaunchShape) throw Error(RSVD_ERR_CUDA, m + "a cluster kernel was launched without its cluster shape");
     throw Error(RSVD_ERR_INTERNAL, m + "device flag set");
   }
 }

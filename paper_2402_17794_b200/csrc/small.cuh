@@ -73,6 +73,7 @@ enum FlagBits : int {
   kFlagPowerCap = 32,
   kFlagRngPatchOverflow = 64,
   kFlagRetryRobust = 128,  // not an error: re-run the call in robust mode
+  kFlagLaunchShape = 256,  // a cluster kernel ran without its cluster shape
 };
 // Raises NumericError if any flag is set (synchronizes the stream).
 void check_flags(Handle& h, const char* what);
