@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     // has already released it (the usual case: it ran ~2 waves earlier), pull
     // its lines into L2 now, so the epilogue's read-modify-write does not pay
     // an HBM round trip.  (A non-blocking peek; prefetches only.)
-    if (it.idx > 0 && ld_acquire(it.sem) == it.idx) {
+    const bool released = it.idx == 0 || ld_acquire(it.sem) == it.idx;  // this thread's acquire
+    if (it.idx > 0 && released) {
       double* C = it.adj ? p.W : p.Y;
       const int64_t ldc = it.adj ? p.ldw : p.ldy;
       const int64_t mlim = it.adj ? p.K : p.row_end;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ordered in-place accumulation into the output tile: every thread
     // acquires the predecessor's release itself (usually already there), so
     // no barrier precedes the read-modify-write
-    if (it.idx > 0) {
+    if (!released) {
       const long long t0 = clock64();
       while (ld_acquire(it.sem) != it.idx) {
         __nanosleep(64);

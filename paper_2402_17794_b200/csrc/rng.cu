@@ -540,7 +540,7 @@ class HostPool {
   void run(int64_t n, const std::function<void(int64_t, int64_t)>& f) {
     static const int64_t kMinChunk = [] {
       const char* e = std::getenv("RSVD_HOST_MIN_CHUNK");
-      return int64_t(e ? std::max(1, std::atoi(e)) : 256);
+      return int64_t(e ? std::max(1, std::atoi(e)) : 64);
     }();
     const int nw = int(workers_.size());
     const int parts = int(std::min<int64_t>(nw + 1, (n + kMinChunk - 1) / kMinChunk));
