@@ -73,6 +73,9 @@ typedef struct rsvd_counters {
   int64_t adjoint;
   int64_t physical_passes;
   int64_t kernel_launches;
+  /* calls re-run in robust mode because a speculated, sync-free branch
+   * decision (CholeskyQR's pass count) turned out wrong */
+  int64_t robust_reruns;
 } rsvd_counters;
 
 typedef struct rsvd_handle rsvd_handle;

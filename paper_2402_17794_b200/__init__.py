@@ -96,7 +96,8 @@ class RngState(ctypes.Structure):
 
 class Counters(ctypes.Structure):
     _fields_ = [("apply", ctypes.c_int64), ("adjoint", ctypes.c_int64),
-                ("physical_passes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+                ("physical_passes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("robust_reruns", ctypes.c_int64)]
 
 
 _lib = None
@@ -300,7 +301,7 @@ class Engine:
         c = Counters()
         _check(_load().rsvd_get_counters(self._h, ctypes.byref(c)))
         return {"apply": c.apply, "adjoint": c.adjoint, "physical_passes": c.physical_passes,
-                "kernel_launches": c.kernel_launches}
+                "kernel_launches": c.kernel_launches, "robust_reruns": c.robust_reruns}
 
     def reset_counters(self) -> None:
         _check(_load().rsvd_reset_counters(self._h))

@@ -86,6 +86,7 @@ void run_eager(rsvdb::Handle& h, const char* what, F&& f) {
       rsvdb::patch_cancel(h);
       RSVD_CUDA(cudaStreamSynchronize(h.stream));
       h.counters = before;
+      h.counters.robust_reruns++;
       if (attempt > 0 || h.robust) {
         h.robust = false;
         throw rsvdb::Error(RSVD_ERR_INTERNAL, std::string(what) + ": robust re-run asked to retry");
@@ -193,6 +194,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
     a.adjoint += sgn * d.adjoint;
     a.physical_passes += sgn * d.physical_passes;
     a.kernel_launches += sgn * d.kernel_launches;
+    a.robust_reruns += sgn * d.robust_reruns;
   };
   try {
     RSVD_CUDA(cudaSetDevice(h.device));
@@ -216,6 +218,7 @@ rsvd_status guard_graph(rsvd_handle* hd, const char* what, const std::string& ke
       rsvdb::patch_cancel(h);
       RSVD_CUDA(cudaStreamSynchronize(h.stream));
       h.counters = before;
+      h.counters.robust_reruns++;
       h.rng_user_out = nullptr;
       h.prof_pending.clear();
       h.robust = true;

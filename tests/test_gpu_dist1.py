@@ -79,3 +79,28 @@ def test_sharded_path_is_deterministic(eng, dist1):
         f2 = eng.rsvd(a, cfg)
     assert np.array_equal(_np(f1.sigma), _np(f2.sigma))
     assert np.array_equal(_np(f1.U), _np(f2.U))
+
+
+def test_sharded_calls_are_graph_captured_and_replayed(eng, dist1):
+    """With a shard descriptor the sharded call has no host round trip, so
+    repeated calls are captured into a CUDA graph (NCCL collectives
+    included) and replayed: every call gives bitwise the first (eager) call's
+    factors and the same counter deltas."""
+    a = _t(haar_test_matrix(2000, 500, np.exp(-np.arange(500) / 40.0), 33))
+    cfg = eng.SketchConfig(20, 5, 2, eng.RangeMode.power, 3)
+    dist1.set_shard(2000, 0)
+    try:
+        outs, deltas = [], []
+        with eng.using_engine(dist1):
+            for _ in range(4):
+                c0 = dist1.counters()
+                f = eng.rsvd(a, cfg)
+                c1 = dist1.counters()
+                outs.append((_np(f.U), _np(f.sigma), _np(f.V)))
+                deltas.append({k: c1[k] - c0[k] for k in c1})
+        for o, d in zip(outs[1:], deltas[1:]):
+            for x, y in zip(o, outs[0]):
+                assert np.array_equal(x, y)
+            assert d == deltas[0]
+    finally:
+        dist1.set_shard(0, 0)
