@@ -221,6 +221,18 @@ def cpu_reference(cfg, steps, warmup, threads, a_host=None):
     return dt
 
 
+def workload_config(name, cfg, world):
+    """The `config` object of both arms (same keys and values for the same
+    workload, so the driver can match the reference arm to ours)."""
+    m, n = cfg["m"], cfg["n"]
+    return {"workload": f"{name}: {cfg['name']}", "m": m, "n": n, "k": cfg["k"], "p": cfg["p"],
+            "q": cfg["q"], "seeds": {"U": SEED_U, "V": SEED_V, "omega": SEED_OMEGA},
+            "parallelism": f"row-shard x{world}",
+            "l2": (("L2 flushed between timed steps (512 MB read outside the step events; |A| = %.0f MB)")
+                   if -(-m // world) * n * 8 < L2_FLUSH_BELOW else "inputs larger than L2 (|A| = %.0f MB)")
+                  % (m * n * 8 / 1e6)}
+
+
 def host_info():
     """The host the CPU legs ran on: the Omega stream's bits depend on glibc's
     log ifunc (FMA vs SSE2), so the CPU model, flags, glibc and the compiler
@@ -262,9 +274,8 @@ def run_reference_arm(args, cfg):
         "impl": "reference", "metric": f"rsvd factorizations/s ({cfg['name']})", "value": value,
         "unit": "factorizations/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Haar U, V; BASELINE spectrum)",
-        "config": {"workload": f"{args.config}: {cfg['name']}", "m": cfg["m"], "n": cfg["n"],
-                   "k": cfg["k"], "p": cfg["p"], "q": cfg["q"], "seed": SEED_OMEGA},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Haar U, V from QR of seeded N(0,1); BASELINE spectrum)",
+        "config": workload_config(args.config, cfg, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": {"value": value, "unit": "factorizations/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{steps} full {args.config} factorizations, oracle/rsvd_oracle.cpp "
@@ -495,12 +506,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Haar U, V from QR of seeded N(0,1); BASELINE spectrum)",
-            "config": {"workload": f"{args.config}: {cfg['name']}", "m": m, "n": n, "k": k,
-                       "p": p, "q": q, "seeds": {"U": SEED_U, "V": SEED_V, "omega": SEED_OMEGA},
-                       "parallelism": f"row-shard x{world}",
-                       "l2": (("L2 flushed between timed steps (512 MB read outside the step events; "
-                               "|A| = %.0f MB)") if a_loc.numel() * 8 < L2_FLUSH_BELOW else
-                              "inputs larger than L2 (|A| = %.0f MB)") % (m * n * 8 / 1e6)},
+            "config": workload_config(args.config, cfg, world),
             "e2e": {"value": 1000.0 / e2e_ms, "unit": "factorizations/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms,
