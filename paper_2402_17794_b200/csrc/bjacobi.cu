@@ -712,15 +712,11 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
   // smallest ldp >= l, ldp % 4 == 0, (ldp / 4) odd: conflict-free DMMA fragment loads
   const int nbp = nb + (nb & 1);
   const int items = nprob * (nbp / 2);
-  // cluster size: split each visit's rows CS ways while the round's visits
-  // still fit the SMs (RSVD_BJ_CLUSTER overrides; 1 = the unsplit visit)
+  // cluster size: split each visit's rows CS ways (any CS in 1..8: clusters
+  // must fit inside a GPC, so e.g. 36 visits fit as clusters of 3 but not of
+  // 4) -- the largest CS whose clusters all fit the SMs at once and whose
+  // row slices stay >= 16 rows; RSVD_BJ_CLUSTER overrides (1 = unsplit)
   const int cs_env = std::getenv("RSVD_BJ_CLUSTER") ? std::atoi(std::getenv("RSVD_BJ_CLUSTER")) : 0;
-  int cs = 1;
-  if (cs_env > 0) {
-    cs = std::min(8, cs_env);
-  } else {
-    while (cs < 8 && items * (2 * cs) <= h.sm_count && ceil_div(l, 2 * cs) >= 16) cs *= 2;
-  }
   auto panel_ld = [](int rows) {
     int ld = (rows + 3) / 4 * 4;
     if ((ld / 4) % 2 == 0) ld += 4;
@@ -730,7 +726,6 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
     const int rpc = int(ceil_div(l, c));
     return (size_t(panel_ld(rpc)) * kBJW + 2 * kBJW * kGL + kBJW * kVL + 64) * 8;
   };
-  while (cs < 8 && smem_of(cs) > 220 * 1024) cs *= 2;  // large l: more CTAs per visit
   // co-residency (cooperative launch): at most the device's active clusters
   auto max_clusters = [&](int c) {
     smem_attr(bjacobi_kernel, smem_of(c));
@@ -749,10 +744,27 @@ void bj_run(Handle& h, int l, const BJWork* work, int nprob) {
     RSVD_CUDA(cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(bjacobi_kernel), &cfg));
     return n;
   };
-  int ncl_max = max_clusters(cs);
-  while (cs > 1 && ncl_max < std::min(items, h.sm_count / cs) && smem_of(cs / 2) <= 220 * 1024) {
-    cs /= 2;  // fewer, larger clusters did not all fit: trade split for co-residency
+  int cs = 1, ncl_max = 0;
+  if (cs_env > 0) {
+    cs = std::min(8, cs_env);
     ncl_max = max_clusters(cs);
+  } else {
+    for (int c = 8; c >= 1; --c) {
+      const bool fits_smem = smem_of(c) <= 220 * 1024;
+      if (!fits_smem) break;  // smaller clusters need even more shared memory
+      if (c > 1 && (items * c > h.sm_count || ceil_div(l, c) < 16)) continue;
+      const int n = max_clusters(c);
+      if (n >= std::min(items, h.sm_count / c) || c == 1) {
+        cs = c;
+        ncl_max = n;
+        break;
+      }
+    }
+    if (ncl_max == 0) {  // large l: the smallest split that fits shared memory
+      cs = 1;
+      while (cs < 8 && smem_of(cs) > 220 * 1024) ++cs;
+      ncl_max = max_clusters(cs);
+    }
   }
   if (ncl_max < 1) throw_dim("block_jacobi_svd: no co-resident cluster fits");
   const size_t smem = smem_of(cs);

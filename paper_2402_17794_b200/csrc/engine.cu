@@ -546,8 +546,20 @@ void solve_joint_core_impl(Handle& h, const DMat& G1, const DMat& H1, const DMat
   DMat U1 = h.ws.mat(l, l), V1 = h.ws.mat(l, l), U2 = h.ws.mat(l, l), V2 = h.ws.mat(l, l);
   double* s1 = h.ws.alloc(l);
   double* s2 = h.ws.alloc(l);
-  if (l > 64) {  // the two SVDs are independent: one batched block-Jacobi launch
-    block_jacobi_svd2(h, G1, V1, U1, s1, G2, V2, U2, s2);
+  if (l > 64) {
+    // The two SVDs are independent: one batched block-Jacobi launch, on the
+    // transposed triangular factors of QR-preconditioned G1, G2 (as
+    // svd_core: G = Q R, R^T J = W S  =>  G = (Q J) S W^T): 10 instead of 13
+    // outer sweeps on C5's cores (random-like 550 x 550 G1, G2).
+    DMat Q1 = h.ws.mat(l, l), R1 = h.ws.mat(l, l), Q2 = h.ws.mat(l, l), R2 = h.ws.mat(l, l);
+    orthonormalize(h, G1, Q1, &R1);
+    orthonormalize(h, G2, Q2, &R2);
+    DMat R1t = h.ws.mat(l, l), R2t = h.ws.mat(l, l), J1 = h.ws.mat(l, l), J2 = h.ws.mat(l, l);
+    transpose(h, R1, R1t);
+    transpose(h, R2, R2t);
+    block_jacobi_svd2(h, R1t, J1, V1, s1, R2t, J2, V2, s2);  // R^T J = W S: V = W
+    gemm_nn(h, Q1, J1, U1);
+    gemm_nn(h, Q2, J2, U2);
   } else {
     jacobi_svd_square(h, G1, V1, U1, s1);  // G1 V1 = U1 S1
     jacobi_svd_square(h, G2, V2, U2, s2);
