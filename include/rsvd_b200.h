@@ -292,6 +292,9 @@ rsvd_status rsvd_spevd_dev(rsvd_handle* h, int64_t n, const double* a, int64_t l
 rsvd_status rsvd_spevd_shard_dev(rsvd_handle* h, int64_t m_local, int64_t n, const double* a,
                                  int64_t lda, int64_t k, int64_t p, rsvd_rng_state* rng,
                                  int check_symmetry, double* u, int64_t ldu, double* lambda);
+rsvd_status rsvd_spevd_shard_host(rsvd_handle* h, int64_t m_local, int64_t n, const double* a,
+                                  int64_t lda, int64_t k, int64_t p, rsvd_rng_state* rng, double* u,
+                                  int64_t ldu, double* lambda);
 rsvd_status rsvd_spevd_host(rsvd_handle* h, int64_t n, const double* a, int64_t lda, int64_t k,
                             int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
                             double* lambda);

@@ -146,6 +146,7 @@ def _load():
             "rsvd_rsvd_host": [P, I64, I64, P, I64, I64, I64, I, I, PS, P, I64, P, P, I64],
             "rsvd_spevd_dev": [P, I64, P, I64, I64, I64, PS, I, P, I64, P],
             "rsvd_spevd_shard_dev": [P, I64, I64, P, I64, I64, I64, PS, I, P, I64, P],
+            "rsvd_spevd_shard_host": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P],
             "rsvd_spevd_host": [P, I64, P, I64, I64, I64, PS, P, I64, P],
             "rsvd_spsvd_dev": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
             "rsvd_spsvd_host": [P, I64, I64, P, I64, I64, I64, PS, P, I64, P, P, I64],
@@ -836,13 +837,15 @@ def spevd_host(a: np.ndarray, k: int, p: int, rng: Rng, out=None):
     (U, lambda) host arrays (pinned memory makes the copy-back fast)."""
     if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous):
         a = np.asfortranarray(a, dtype=np.float64)
-    n = a.shape[0]
+    m_local, n = a.shape  # a row shard (m_local x n) on a distributed engine
     kk = max(k, 0)
-    u, lam = out if out is not None else (np.empty((n, kk), order="F"), np.empty(max(kk, 1)))
+    u, lam = out if out is not None else (np.empty((m_local, kk), order="F"), np.empty(max(kk, 1)))
     e = _eng()
+    if m_local != n and e.nranks == 1 and not e.virtual:
+        raise DimensionError("spevd_hermitian: matrix is not square")
     P = lambda x: x.ctypes.data_as(ctypes.c_void_p)
-    _check(_load().rsvd_spevd_host(e.handle, n, P(a), max(n, 1), k, p, ctypes.byref(rng.state),
-                                   P(u), max(n, 1), P(lam)))
+    _check(_load().rsvd_spevd_shard_host(e.handle, m_local, n, P(a), max(m_local, 1), k, p,
+                                         ctypes.byref(rng.state), P(u), max(m_local, 1), P(lam)))
     return EvdApprox(u, lam[:kk])
 
 

@@ -775,17 +775,18 @@ rsvd_status rsvd_spevd_dev(rsvd_handle* hd, int64_t n, const double* a, int64_t 
   return rsvd_spevd_shard_dev(hd, n, n, a, lda, k, p, rng, check_symmetry, u, ldu, lambda);
 }
 
-rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
-                            int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
-                            double* lambda) {
+rsvd_status rsvd_spevd_shard_host(rsvd_handle* hd, int64_t m_local, int64_t n, const double* a,
+                                  int64_t lda, int64_t k, int64_t p, rsvd_rng_state* rng, double* u,
+                                  int64_t ldu, double* lambda) {
   return guard(hd, "spevd_hermitian", [&](rsvdb::Handle& h) {
+    if (!h.dist() && m_local != n) rsvdb::throw_dim("spevd_hermitian: matrix is not square");
     HostIO io{h};
     std::vector<rsvdb::Problem::Panel> panels;
-    rsvdb::DMat A = io.up_panels(a, n, n, lda, &panels);
-    rsvdb::Problem P = rsvdb::make_problem(h, A.p, n, n, A.ld);
+    rsvdb::DMat A = io.up_panels(a, m_local, n, lda, &panels);
+    rsvdb::Problem P = rsvdb::make_problem(h, A.p, m_local, n, A.ld);
     P.panels = panels;
     const int64_t kk = std::max<int64_t>(k, 0);
-    rsvdb::DMat U = h.ws.mat(n, kk);
+    rsvdb::DMat U = h.ws.mat(m_local, kk);
     double* lam = h.ws.alloc(std::max<int64_t>(kk, 1));
     rsvdb::DevRng r = rsvdb::rng_upload(h, rng);
     rsvdb::spevd_impl(h, P, k, p, r, true, U, lam);
@@ -793,6 +794,12 @@ rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t
     io.down(U, u, ldu);
     io.down_vec(lam, lambda, kk);
   });
+}
+
+rsvd_status rsvd_spevd_host(rsvd_handle* hd, int64_t n, const double* a, int64_t lda, int64_t k,
+                            int64_t p, rsvd_rng_state* rng, double* u, int64_t ldu,
+                            double* lambda) {
+  return rsvd_spevd_shard_host(hd, n, n, a, lda, k, p, rng, u, ldu, lambda);
 }
 
 rsvd_status rsvd_spsvd_dev(rsvd_handle* hd, int64_t m, int64_t n, const double* a, int64_t lda,

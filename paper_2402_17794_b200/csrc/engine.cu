@@ -691,9 +691,12 @@ void spevd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, DevRng& rng, 
     h.pass_cfg_big = 1;
     op_apply(h, P, Omega, Y);  // the single pass over A
   }
-  if (check_sym && !sym_first) {  // streamed upload (single GPU)
+  if (check_sym && !sym_first) {  // streamed upload: once every panel has landed
     a_ready(h, P);
-    check_symmetric(h, P.A, false);
+    if (P.dist)
+      check_symmetric_dist(h, P);
+    else
+      check_symmetric(h, P.A, false);
   }
   DMat Q = h.ws.mat(ml, l);
   orthonormalize(h, Y, Q, nullptr, P.dist);

@@ -171,3 +171,31 @@ def test_sharded_counts_match_single_gpu(eng, vcomms):
     for c1, c2 in vcomms(2).run(run):
         assert (c1["apply"], c1["adjoint"], c1["physical_passes"]) == (1, 1, 1)
         assert (c2["apply"], c2["adjoint"], c2["physical_passes"]) == (3, 3, 6)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_host_entry_points(eng, orc, vcomms, nranks):
+    """The host-buffer single-pass calls on row shards (what bench.py's e2e
+    leg runs under torchrun): each rank streams its shard up in row panels."""
+    a = _sym(600, 12)
+    k, p = 20, 8
+    idx = np.array_split(np.arange(a.shape[0]), nranks)
+
+    def run(r, e):
+        f = eng.spevd_host(np.asfortranarray(a[idx[r], :]), k, p, eng.Rng(1))
+        return np.asarray(f.U), np.asarray(f.lam), None
+    u, lam, _ = _assemble(vcomms(nranks).run(run))
+    uo, lo = orc.spevd_hermitian(a, k, p, orc.Rng(1))
+    assert np.max(np.abs(lam - lo) / np.abs(lo)) < SIG_TOL
+    assert sin_max(u, uo) < ANG_TOL
+    b = haar_matrix(1200, 500, np.exp(-np.arange(150) / 25.0), 13)
+    idx = np.array_split(np.arange(b.shape[0]), nranks)
+
+    def run2(r, e):
+        f = eng.spsvd_host(np.asfortranarray(b[idx[r], :]), k, p, eng.Rng(2))
+        return np.asarray(f.U), np.asarray(f.sigma), np.asarray(f.V)
+    u, s, v = _assemble(vcomms(nranks).run(run2))
+    uo, so, vo = orc.spsvd_general(b, k, p, orc.Rng(2))
+    assert np.max(np.abs(s[:k] - so[:k]) / so[:k]) < SIG_TOL
+    assert sin_max(u[:, :k], uo[:, :k]) < ANG_TOL
+    assert sin_max(v[:, :k], vo[:, :k]) < ANG_TOL
