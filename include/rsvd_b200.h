@@ -262,6 +262,18 @@ rsvd_status rsvd_debug_dual_pass_dev(rsvd_handle* h, int64_t m, int64_t n, int64
                                      const double* psi, int64_t ldp, double* y, int64_t ldy,
                                      double* w, int64_t ldw, int64_t panel_rows, int macroblock);
 
+/* Alg 6's dual product on the INT8 tensor cores (tcgen05 kind::i8, Ozaki
+ * splitting into `slices` exact 7-bit slices per operand; csrc/ozaki.cu):
+ * -1 = follow the RSVD_OZAKI environment variable (default), 0 = off (the
+ * FP64 DMMA pass), 3..8 = slices.  8 slices are below fp64's own rounding of
+ * the product; 7 are 2^-49 of the row/column maxima. */
+rsvd_status rsvd_set_ozaki_slices(rsvd_handle* h, int slices);
+/* C = A X (trans = 0: A m x n, X n x l, C m x l) or C = A^T X (trans = 1: X
+ * m x l, C n x l) by the sliced INT8 product alone: for unit parity tests. */
+rsvd_status rsvd_debug_ozaki_gemm_dev(rsvd_handle* h, int trans, int64_t m, int64_t n,
+                                      const double* a, int64_t lda, int64_t l, const double* x,
+                                      int64_t ldx, double* c, int64_t ldc, int slices);
+
 /* ------------------------------------------- rangefinder.hpp (L2) */
 /* range_basis(A, cfg, rng) (reference rangefinder.hpp:97-105): Q m x (k+p). */
 rsvd_status rsvd_range_basis_dev(rsvd_handle* h, int64_t m, int64_t n, const double* a,

@@ -181,6 +181,10 @@ def _load():
         L.rsvd_debug_log_cr.restype = D
         L.rsvd_debug_dual_pass_dev.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, I64, P, I64, P, I64, I64, I]
         L.rsvd_debug_dual_pass_dev.restype = ctypes.c_int
+        L.rsvd_set_ozaki_slices.argtypes = [P, I]
+        L.rsvd_set_ozaki_slices.restype = ctypes.c_int
+        L.rsvd_debug_ozaki_gemm_dev.argtypes = [P, I, I64, I64, P, I64, I64, P, I64, P, I64, I]
+        L.rsvd_debug_ozaki_gemm_dev.restype = ctypes.c_int
         L.rsvd_debug_log_window.argtypes = [ctypes.c_void_p, I64, ctypes.c_void_p, ctypes.c_void_p]
         L.rsvd_debug_log_window.restype = None
         _lib = L
@@ -887,6 +891,29 @@ def debug_dual_pass(a, oc, psi, panel_rows: int = 0, macroblock: int = 0):
                                              psi.data_ptr(), ld(psi), y.data_ptr(), m, w.data_ptr(), n,
                                              int(panel_rows), int(macroblock)))
     return y, w
+
+
+def set_ozaki_slices(slices: int, engine=None) -> None:
+    """Run Alg 6's dual product on the INT8 tensor cores with `slices` exact
+    7-bit slices per operand (csrc/ozaki.cu): 0 = off (FP64 DMMA pass), 3..8 =
+    slices, -1 = follow the RSVD_OZAKI environment variable."""
+    e = engine or default_engine()
+    _check(_load().rsvd_set_ozaki_slices(e.handle, int(slices)))
+
+
+def debug_ozaki_gemm(a, x, trans: bool = False, slices: int = 8):
+    """A @ x (or A.T @ x) by the sliced INT8 tensor-core product alone.
+    Column-major device tensors in, device tensor out."""
+    import torch
+    e = default_engine()
+    m, n = a.shape
+    l = x.shape[1]
+    rows = n if trans else m
+    c = torch.empty((l, rows), dtype=torch.float64, device="cuda").t()
+    ld = lambda t: int(t.stride(1)) if t.shape[1] > 1 else max(int(t.shape[0]), 1)  # noqa: E731
+    _check(_load().rsvd_debug_ozaki_gemm_dev(e.handle, int(bool(trans)), m, n, a.data_ptr(), ld(a), l,
+                                              x.data_ptr(), ld(x), c.data_ptr(), rows, int(slices)))
+    return c
 
 
 def debug_log_window(x):

@@ -14,6 +14,7 @@
 #include "dist.cuh"
 #include "engine.cuh"
 #include "fused.cuh"
+#include "ozaki.cuh"
 #include "pass.cuh"
 #include "rng.cuh"
 #include "small.cuh"
@@ -858,6 +859,26 @@ rsvd_status rsvd_debug_dual_pass_dev(rsvd_handle* hd, int64_t m, int64_t n, int6
       for (int64_t r0 = 0; r0 < m; r0 += rows) P.panels.push_back({r0, std::min(m, r0 + rows), nullptr});
     }
     rsvdb::op_dual(h, P, dm(oc, n, l, ldo), dm(psi, m, l, ldp), dm(y, m, l, ldy), dm(w, n, l, ldw));
+  });
+}
+
+rsvd_status rsvd_set_ozaki_slices(rsvd_handle* hd, int slices) {
+  return guard(hd, "set_ozaki_slices", [&](rsvdb::Handle& h) {
+    if (slices != -1 && slices != 0 && (slices < 3 || slices > 8))
+      rsvdb::throw_param("set_ozaki_slices: slices must be -1 (environment), 0 (off) or 3..8");
+    h.ozaki_slices = slices;
+    h.generation++;  // captured graphs hold the other pass
+  });
+}
+
+rsvd_status rsvd_debug_ozaki_gemm_dev(rsvd_handle* hd, int trans, int64_t m, int64_t n,
+                                      const double* a, int64_t lda, int64_t l, const double* x,
+                                      int64_t ldx, double* c, int64_t ldc, int slices) {
+  return guard(hd, "ozaki_gemm", [&](rsvdb::Handle& h) {
+    if (trans)
+      rsvdb::ozaki_gemm(h, dm(a, m, n, lda), dm(x, m, l, ldx), dm(c, n, l, ldc), true, slices);
+    else
+      rsvdb::ozaki_gemm(h, dm(a, m, n, lda), dm(x, n, l, ldx), dm(c, m, l, ldc), false, slices);
   });
 }
 

@@ -128,6 +128,9 @@ struct Handle {
   std::vector<cudaEvent_t> panel_ev;
   // fused Alg-6 pass macroblock edge override (0 = RSVD_FUSED_MB / default)
   int fused_mb = 0;
+  // Ozaki slices of the INT8 tensor-core passes (ozaki.cu): -1 = RSVD_OZAKI
+  // environment variable, 0 = off (DMMA passes), 3..8 = slices per operand
+  int ozaki_slices = -1;
   // Robust mode: data-dependent branch decisions (CholeskyQR's pass count
   // after a shifted Cholesky) read the device flag on the host mid-call.
   // Off by default: those decisions are speculated without a host round trip

@@ -19,6 +19,7 @@
 #include "engine.cuh"
 #include "pass.cuh"
 #include "fused.cuh"
+#include "ozaki.cuh"
 #include "rng.cuh"
 #include "small.cuh"
 
@@ -457,14 +458,23 @@ void op_dual(Handle& h, const Problem& P, const DMat& Oc, const DMat& Psi, DMat 
     a_ready(h, P);
     A = tma_view(h, P.A);
   }
-  int* sem = reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(fused_semaphores(A.rows, A.cols, Oc.cols)) * 4));
+  // RSVD_OZAKI / rsvd_set_ozaki_slices: the same dual product on the INT8
+  // tensor cores from exact integer slices of each row panel (ozaki.cu)
+  const int oz = ozaki_slices(h);
+  OzakiState ost;
+  int* sem = oz ? nullptr
+                : reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(fused_semaphores(A.rows, A.cols, Oc.cols)) * 4));
+  auto panel = [&](int64_t r0, int64_t r1, bool first) {
+    if (oz) ozaki_dual_pass(h, A, Ov, Pv, Yc, W, r0, r1, &ost, first, oz);
+    else fused_dual_pass(h, A, Ov, Pv, Yc, W, r0, r1, sem, first);
+  };
   if (P.panels.empty() || A.p != P.A.p) {
     a_ready(h, P);
-    fused_dual_pass(h, A, Ov, Pv, Yc, W, 0, A.rows, sem, true);
+    panel(0, A.rows, true);
   } else {
     for (size_t i = 0; i < P.panels.size(); ++i) {
       if (P.panels[i].ready) RSVD_CUDA(cudaStreamWaitEvent(h.stream, P.panels[i].ready, 0));
-      fused_dual_pass(h, A, Ov, Pv, Yc, W, P.panels[i].row0, P.panels[i].row1, sem, i == 0);
+      panel(P.panels[i].row0, P.panels[i].row1, i == 0);
     }
   }
   if (P.dist) allreduce_mat(h, W);

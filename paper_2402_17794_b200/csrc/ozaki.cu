@@ -1,0 +1,660 @@
+// FP64 streaming-pass products on the INT8 tensor cores (tcgen05.mma
+// kind::i8, int32 accumulators in TMEM) by the Ozaki splitting.
+//
+// FP64 has no tcgen05 kind on sm_100a, so the DMMA passes (pass.cu, fused.cu)
+// top out at the 37 TFLOP/s FP64 pipe.  The products of the range finder are
+// C = A X with A huge and X skinny (reference rangefinder.hpp:70-79,
+// singlepass.hpp:119-122); here each operand is written as
+//     a_ik = 2^eA[i] * sum_{s=1..S} d_s(i,k) 2^-(7s-1),   |d_s| <= 64
+// (d_s: balanced base-128 digits of the value rounded ONCE to 7S-1 fractional
+// bits below its row's largest power of two; X likewise per column), so
+//     C_ij = 2^(eA[i]+eX[j]) * sum_{c=2..S+1} 2^-(7c-2) * P_c(i,j),
+//     P_c  = sum_{s+t=c} D^A_s D^X_t          (exact int32 GEMMs)
+// The dropped terms (s+t > S+1) are below 2^-7S relative to the row/column
+// maxima: S = 8 is below fp64's own rounding of the product, S = 7 is 2^-49.
+//
+// Pipeline per row panel of A (<= 32768 rows, so int32 cannot overflow):
+//   row_exp -> slice (A read twice from HBM as fp64, slices written once)
+//   -> apply GEMM (Y rows of the panel) -> Psi' = 2^eA Psi sliced per column
+//   -> adjoint GEMM (W += A_panel^T Psi_panel) from the SAME slices of A
+// (MN-major UMMA operand for the apply, K-major for the adjoint).
+//
+// GEMM kernel: one CTA per 128 x ntile output tile; warp 0 = TMA producer
+// (3-D maps over [slice][col][row] int8), warp 1 = MMA issuer + TMEM owner,
+// warps 2-5 = epilogue (TMEM -> fp64).  A 3-stage ring of K = 32 steps; each
+// step holds every needed slice tile of both operands; the diagonals c are
+// accumulated four at a time (4 x ntile TMEM columns), high c first.
+#include "ozaki.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <mutex>
+
+#include "pass.cuh"
+#include "ptx.cuh"
+
+namespace rsvdb {
+
+namespace {
+
+constexpr int kBM = 128;           // output rows per CTA (UMMA M)
+constexpr int kKS = 32;            // contraction per ring stage = one int8 UMMA K step
+constexpr int kStages = 3;
+constexpr int kThreads = 192;      // producer warp, MMA warp, 4 epilogue warps
+constexpr int kATile = kBM * kKS;  // bytes of one A slice tile
+constexpr int kMaxS = 8;
+constexpr int kMaxK = 32768;       // (S) * K * 64 * 64 < 2^31
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(ptx::smem_u32(dst)),
+      "l"(map), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// sm_100 shared-memory matrix descriptor: start address, leading / stride byte
+// offsets (all >> 4), version 1, swizzle mode in bits 61-63 (2 = 128 B, 6 = 32 B)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(layout) << 61);
+}
+// kind::i8 instruction descriptor: s8 x s8 -> s32, M = 128
+__device__ __forceinline__ uint32_t idesc_i8(int n, int a_mn_major) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn_major) << 15) |
+         (uint32_t(n >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          ptx::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "r"(addr)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// 2^j as a double, j in [-1022, 1023]
+__host__ __device__ __forceinline__ double exp2i(int j) {
+  const unsigned long long b = (unsigned long long)(j + 1023) << 52;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+// x * 2^k for |k| up to ~2040 without an overflowing scale factor
+__device__ __forceinline__ double scale2(double x, int k) {
+  k = max(-2044, min(2046, k));  // beyond this the product under/overflows anyway
+  const int k1 = k >> 1;
+  return x * exp2i(k1) * exp2i(k - k1);
+}
+
+// ----------------------------------------------------------- exponents
+__global__ void fill_int_kernel(int* p, int n, int v) {
+  RSVD_PDL_ENTRY();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+// e[r] = max_c bexp(x[r,c]) - 1022 over this block's column range (|x| < 2^e)
+__global__ void __launch_bounds__(256)
+    row_exp_kernel(const double* __restrict__ x, int64_t ld, int rows, int64_t cols, int cpb,
+                   int* __restrict__ e) {
+  RSVD_PDL_ENTRY();
+  const int r = blockIdx.x * 256 + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t c0 = int64_t(blockIdx.y) * cpb, c1 = min(cols, c0 + cpb);
+  const double* p = x + r;
+  int mx = 0;
+  int64_t c = c0;
+  for (; c + 8 <= c1; c += 8) {
+    int h[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) h[u] = __double2hiint(__ldg(p + (c + u) * ld));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mx = max(mx, h[u] & 0x7ff00000);
+  }
+  for (; c < c1; ++c) mx = max(mx, __double2hiint(__ldg(p + c * ld)) & 0x7ff00000);
+  atomicMax(&e[r], (mx >> 20) - 1022);
+}
+// e[c] = max_r (bexp(x[r,c]) - 1022 + radd[r]) over this block's row range
+__global__ void __launch_bounds__(256)
+    col_exp_kernel(const double* __restrict__ x, int64_t ld, int rows, int rpb,
+                   const int* __restrict__ radd, int* __restrict__ e) {
+  RSVD_PDL_ENTRY();
+  const int c = blockIdx.x;
+  const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
+  const double* p = x + int64_t(c) * ld;
+  int mx = INT_MIN;
+  for (int r = r0 + threadIdx.x; r < r1; r += 256) {
+    const int b = ((__double2hiint(__ldg(p + r)) & 0x7ff00000) >> 20) - 1022;
+    mx = max(mx, b + (radd ? radd[r] : 0));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx != INT_MIN) atomicMax(&e[c], mx);
+}
+
+// -------------------------------------------------------------- slicing
+// out[s][c][r] (r contiguous, ld8 bytes per column, S x cols x ld8 in all) =
+// digit s of q = rint(x[r,c] * 2^(P - rsub[r] + radd[r] - csub[c])), P = 7S-1:
+// q = sum_s d_s 128^(S-s), d_s in [-64, 63] (top digit in [-64, 64]).
+// One thread: 4 consecutive rows of one column (one 32-bit word per slice).
+template <int S>
+__global__ void __launch_bounds__(256)
+    slice_kernel(const double* __restrict__ x, int64_t ld, int rows, int cols,
+                 const int* __restrict__ rsub, const int* __restrict__ radd,
+                 const int* __restrict__ csub, uint8_t* __restrict__ out, int64_t ld8) {
+  RSVD_PDL_ENTRY();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (blockIdx.x * 32 + lane) * 4;
+  const int c = blockIdx.y * 8 + warp;
+  if (r0 >= rows || c >= cols) return;
+  const double* p = x + int64_t(c) * ld + r0;
+  double v[4];
+  if (r0 + 3 < rows && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = r0 + u < rows ? p[u] : 0.0;
+  }
+  const int kc = 7 * S - 1 - (csub ? csub[c] : 0);
+  uint32_t w[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) w[s] = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    int k = kc;
+    if (r0 + u < rows) {
+      if (rsub) k -= rsub[r0 + u];
+      if (radd) k += radd[r0 + u];
+    }
+    long long q = __double2ll_rn(scale2(v[u], k));
+#pragma unroll
+    for (int s = S - 1; s >= 1; --s) {
+      const long long d = ((q + 64) & 127) - 64;
+      q = (q - d) >> 7;
+      w[s] |= (uint32_t(d) & 0xffu) << (8 * u);
+    }
+    w[0] |= (uint32_t(q) & 0xffu) << (8 * u);
+  }
+  const int64_t plane = int64_t(cols) * ld8;
+  uint8_t* o = out + int64_t(c) * ld8 + r0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane) = w[s];
+}
+
+// ----------------------------------------------------------------- GEMM
+struct OzParams {
+  int M, N, K;      // output M x N; contraction over K entries starting at k0
+  int k0;
+  int S;
+  int ntile, n_tiles;
+  double* C;
+  int64_t ldc;
+  const int* rexp;  // exponent per output row / column (nullptr = 0)
+  const int* cexp;
+  int accumulate;   // C += result
+  double* scratch;  // per-CTA 128 x ntile partial (S > 4)
+};
+
+// AMN = 1: A tiles are MN-major (global [k][m], the apply product of a
+// column-major A); AMN = 0: K-major (global [m][k], the adjoint product).
+template <int AMN>
+__global__ void __launch_bounds__(kThreads, 1)
+    ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, OzParams p) {
+  RSVD_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = smraw + ((1024 - (ptx::smem_u32(smraw) & 1023)) & 1023);
+  __shared__ uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full, bar_acc_empty;
+  __shared__ uint32_t tmem_base_sh;
+  const int S = p.S;
+  const int btile = p.ntile * kKS;
+  const int stage_bytes = (S * (kATile + btile) + 1023) & ~1023;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = blockIdx.x / p.n_tiles, nt = blockIdx.x % p.n_tiles;
+  const int m0 = mt * kBM, n0 = nt * p.ntile;
+  const int nk = (p.K + kKS - 1) / kKS;
+  const int ngroups = (S + 3) / 4;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&bar_full[s], 1);
+      ptx::mbar_init(&bar_empty[s], 1);
+    }
+    ptx::mbar_init(&bar_acc_full, 1);
+    ptx::mbar_init(&bar_acc_empty, 128);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     ptx::smem_u32(&tmem_base_sh)),
+                 "r"(512u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tmA);
+      ptx::prefetch_tmap(&tmB);
+      int it = 0;
+      for (int g = 0; g < ngroups; ++g) {
+        const int Sg = S - 4 * g;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          ptx::mbar_wait(&bar_empty[st], ph ^ 1);
+          ptx::mbar_expect_tx(&bar_full[st], uint32_t(Sg) * uint32_t(kATile + btile));
+          uint8_t* base = sm + st * stage_bytes;
+          const int kc = p.k0 + kb * kKS;
+          for (int s = 0; s < Sg; ++s) {
+            if (AMN) tma_load_3d(base + s * kATile, &tmA, &bar_full[st], m0, kc, s);
+            else     tma_load_3d(base + s * kATile, &tmA, &bar_full[st], kc, m0, s);
+          }
+          uint8_t* bb = base + S * kATile;
+          for (int t = 0; t < Sg; ++t) tma_load_3d(bb + t * btile, &tmB, &bar_full[st], kc, n0, t);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_i8(p.ntile, AMN);
+      int it = 0;
+      for (int g = 0; g < ngroups; ++g) {
+        const int Sg = S - 4 * g;
+        const int c_hi = Sg + 1, c_lo = max(2, c_hi - 3);
+        if (g > 0) {
+          ptx::mbar_wait(&bar_acc_empty, (g - 1) & 1);
+          tc_fence_after();
+        }
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          ptx::mbar_wait(&bar_full[st], ph);
+          tc_fence_after();
+          const uint32_t a0 = ptx::smem_u32(sm + st * stage_bytes);
+          const uint32_t b0 = a0 + S * kATile;
+          for (int c = c_hi; c >= c_lo; --c) {
+            const uint32_t acc = tb + uint32_t((c - c_lo) * p.ntile);
+            const int s_lo = max(1, c - Sg), s_hi = min(Sg, c - 1);
+            for (int s = s_lo; s <= s_hi; ++s) {
+              const int t = c - s;
+              const uint64_t ad = AMN ? smem_desc(a0 + (s - 1) * kATile, 4096, 1024, 2)
+                                      : smem_desc(a0 + (s - 1) * kATile, 0, 256, 6);
+              const uint64_t bd = smem_desc(b0 + (t - 1) * btile, 0, 256, 6);
+              umma_i8(acc, ad, bd, idesc, (kb > 0 || s > s_lo) ? 1u : 0u);
+            }
+          }
+          umma_commit(&bar_empty[st]);
+        }
+        umma_commit(&bar_acc_full);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may read
+    const int row = q * 32 + lane;
+    const int64_t grow = int64_t(m0) + row;
+    const int re = (p.rexp && grow < p.M) ? p.rexp[grow] : 0;
+    double* scr = p.scratch ? p.scratch + int64_t(blockIdx.x) * kBM * p.ntile : nullptr;
+    for (int g = 0; g < ngroups; ++g) {
+      const int Sg = S - 4 * g;
+      const int c_hi = Sg + 1, c_lo = max(2, c_hi - 3);
+      const bool last = g == ngroups - 1;
+      ptx::mbar_wait(&bar_acc_full, g & 1);
+      tc_fence_after();
+      for (int cc = 0; cc < p.ntile; cc += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0.0;
+        for (int c = c_hi; c >= c_lo; --c) {  // smallest terms first
+          uint32_t r[8];
+          tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t((c - c_lo) * p.ntile + cc), r);
+          tmem_ld_wait();
+          const double sc = exp2i(-(7 * c - 2));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = fma(double(int(r[j])), sc, v[j]);
+        }
+        if (!last) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) scr[int64_t(cc + j) * kBM + row] = v[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int col = n0 + cc + j;
+            if (grow < p.M && col < p.N) {
+              double x = v[j];
+              if (ngroups > 1) x += scr[int64_t(cc + j) * kBM + row];
+              x = scale2(x, re + (p.cexp ? p.cexp[col] : 0));
+              double* dst = p.C + int64_t(col) * p.ldc + grow;
+              *dst = p.accumulate ? *dst + x : x;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      ptx::mbar_arrive(&bar_acc_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512u)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (!fn) throw Error(RSVD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 3-D int8 map over slices stored [slice][outer][inner]: dims {inner, outer, S}
+CUtensorMap make_map_i8(const uint8_t* p, int64_t inner, int64_t outer, int64_t ld8, int S,
+                        int box_inner, int box_outer, bool swizzle128) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(outer), cuuint64_t(S)};
+  cuuint64_t strides[2] = {cuuint64_t(ld8), cuuint64_t(ld8) * cuuint64_t(outer)};
+  cuuint32_t box[3] = {cuuint32_t(box_inner), cuuint32_t(box_outer), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(p), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(RSVD_ERR_CUDA, "cuTensorMapEncodeTiled (int8) failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+// Sliced operand in device memory: S planes of `outer` columns, ld8 bytes each.
+struct Sliced {
+  uint8_t* p = nullptr;
+  int64_t inner = 0, outer = 0, ld8 = 0;
+};
+
+int64_t ld8_of(int64_t inner) { return round_up(std::max<int64_t>(inner, 16), 16); }
+
+// Buffer for an operand of up to cap_inner x outer (views of fewer rows reuse it)
+uint8_t* alloc_slices(Handle& h, int64_t cap_inner, int64_t outer, int S) {
+  uint8_t* p = static_cast<uint8_t*>(
+      h.ws.alloc_bytes(size_t(S) * size_t(outer) * size_t(ld8_of(cap_inner)) + 1024));
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+}
+Sliced view_slices(uint8_t* p, int64_t inner, int64_t outer) {
+  Sliced s;
+  s.p = p;
+  s.inner = inner;
+  s.outer = outer;
+  s.ld8 = ld8_of(inner);
+  return s;
+}
+
+void fill_exp(Handle& h, int* e, int64_t n, int init) {
+  if (n < 1) return;
+  launch_k(h, fill_int_kernel, unsigned(ceil_div(n, 256)), 256, 0, e, int(n), init);
+  RSVD_LAUNCHED(h);
+}
+
+void launch_slice(Handle& h, const DMat& X, const int* rsub, const int* radd, const int* csub,
+                  const Sliced& out, int S) {
+  if (X.rows == 0 || X.cols == 0) return;
+  dim3 grid(unsigned(ceil_div(X.rows, 128)), unsigned(ceil_div(X.cols, 8)));
+#define RSVD_SLICE_CASE(SS)                                                                       \
+  case SS:                                                                                        \
+    launch_k(h, slice_kernel<SS>, grid, 256, 0, (const double*)X.p, X.ld, int(X.rows), int(X.cols), \
+             rsub, radd, csub, out.p, out.ld8);                                                   \
+    break;
+  switch (S) {
+    RSVD_SLICE_CASE(3)
+    RSVD_SLICE_CASE(4)
+    RSVD_SLICE_CASE(5)
+    RSVD_SLICE_CASE(6)
+    RSVD_SLICE_CASE(7)
+    RSVD_SLICE_CASE(8)
+    default:
+      throw_param("ozaki: slices must be in 3..8");
+  }
+#undef RSVD_SLICE_CASE
+  RSVD_LAUNCHED(h);
+}
+
+// per-row exponents of X (rows x cols): |x_rc| < 2^e[r]
+void row_exponents(Handle& h, const DMat& X, int* e) {
+  fill_exp(h, e, X.rows, -1022);
+  if (X.rows == 0 || X.cols == 0) return;
+  // enough blocks to fill the machine: split the columns
+  const int64_t rb = ceil_div(X.rows, 256);
+  int64_t splits = std::max<int64_t>(1, std::min<int64_t>(ceil_div(X.cols, 64), ceil_div(h.sm_count * 8, rb)));
+  const int cpb = int(ceil_div(X.cols, splits));
+  splits = ceil_div(X.cols, cpb);
+  launch_k(h, row_exp_kernel, dim3(unsigned(rb), unsigned(splits)), 256, 0, (const double*)X.p, X.ld,
+           int(X.rows), X.cols, cpb, e);
+  RSVD_LAUNCHED(h);
+}
+
+// per-column exponents of diag(2^radd) X: |2^radd[r] x_rc| < 2^e[c]
+void col_exponents(Handle& h, const DMat& X, const int* radd, int* e) {
+  fill_exp(h, e, X.cols, -1022 - 1100);
+  if (X.rows == 0 || X.cols == 0) return;
+  const int rpb = 8192;
+  launch_k(h, col_exp_kernel, dim3(unsigned(X.cols), unsigned(ceil_div(X.rows, rpb))), 256, 0,
+           (const double*)X.p, X.ld, int(X.rows), rpb, radd, e);
+  RSVD_LAUNCHED(h);
+}
+
+int pick_ntile(int64_t L) {
+  const int64_t tiles = ceil_div(L, 128);
+  return int(round_up(ceil_div(L, tiles), 16));
+}
+// doubles of per-CTA partial tiles a GEMM with M x N outputs needs (S > 4)
+int64_t scratch_doubles(int64_t M, int64_t N, int S) {
+  if (S <= 4) return 0;
+  const int ntile = pick_ntile(N);
+  return ceil_div(M, kBM) * ceil_div(N, ntile) * kBM * ntile;
+}
+
+// C (M x N) (+)= sliced A  x  sliced B over K entries.
+//   amn = true : A slices are [s][k][m] (M contiguous): the apply product
+//   amn = false: A slices are [s][m][k] (K contiguous): the adjoint product
+// B slices are [s][n][k].  rexp / cexp: exponents of the output rows / columns.
+void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_t M, int64_t N,
+                 int64_t K, int S, DMat C, const int* rexp, const int* cexp, bool accumulate,
+                 double* scratch) {
+  if (M == 0 || N == 0) return;
+  if (K < 1) throw_dim("ozaki: empty contraction");
+  const int ntile = pick_ntile(N);
+  const int n_tiles = int(ceil_div(N, ntile));
+  const int64_t m_tiles = ceil_div(M, kBM);
+  const int64_t grid = m_tiles * n_tiles;
+  const int stage_bytes = int(round_up(int64_t(S) * (kATile + ntile * kKS), 1024));
+  const size_t smem = size_t(kStages) * stage_bytes + 1024;
+  const CUtensorMap ta = amn ? make_map_i8(As.p, As.inner, As.outer, As.ld8, S, kBM, kKS, true)
+                             : make_map_i8(As.p, As.inner, As.outer, As.ld8, S, kKS, kBM, false);
+  const CUtensorMap tb = make_map_i8(Bs.p, Bs.inner, Bs.outer, Bs.ld8, S, kKS, ntile, false);
+  for (int64_t k0 = 0; k0 < K; k0 += kMaxK) {
+    OzParams p;
+    p.M = int(M);
+    p.N = int(N);
+    p.K = int(std::min<int64_t>(kMaxK, K - k0));
+    p.k0 = int(k0);
+    p.S = S;
+    p.ntile = ntile;
+    p.n_tiles = n_tiles;
+    p.C = C.p;
+    p.ldc = C.ld;
+    p.rexp = rexp;
+    p.cexp = cexp;
+    p.accumulate = (accumulate || k0 > 0) ? 1 : 0;
+    p.scratch = scratch;
+    if (amn) {
+      smem_attr(ozaki_gemm_kernel<1>, smem);
+      launch_k(h, ozaki_gemm_kernel<1>, unsigned(grid), kThreads, smem, ta, tb, p);
+    } else {
+      smem_attr(ozaki_gemm_kernel<0>, smem);
+      launch_k(h, ozaki_gemm_kernel<0>, unsigned(grid), kThreads, smem, ta, tb, p);
+    }
+    RSVD_LAUNCHED(h);
+  }
+}
+
+// rows of A sliced at a time: int32 accumulation bounds the adjoint's
+// contraction length, and a sub-panel's slices stay below ~9 GB
+int64_t sub_rows(int64_t K, int S) {
+  int64_t sub = kMaxK;
+  while (sub > 1024 && double(sub) * double(K) * S > 9.0e9) sub /= 2;
+  return sub;
+}
+
+}  // namespace
+
+int ozaki_slices(const Handle& h) {
+  if (h.ozaki_slices >= 0) return h.ozaki_slices;
+  static const int env = [] {
+    const char* e = std::getenv("RSVD_OZAKI");
+    const int v = e ? std::atoi(e) : 0;
+    return (v >= 3 && v <= kMaxS) ? v : 0;
+  }();
+  return env;
+}
+
+namespace {
+void ensure_state(Handle& h, OzakiState* st, int64_t rows_total, int64_t K, int64_t L, int S,
+                  bool need_x, bool need_p) {
+  if (st->have) return;
+  st->cap = std::min<int64_t>(sub_rows(K, S), round_up(std::max<int64_t>(rows_total, 1), 128));
+  st->as = alloc_slices(h, st->cap, K, S);
+  st->e_a = static_cast<int*>(h.ws.alloc_bytes(size_t(st->cap) * 4));
+  if (need_x) {
+    st->xs = alloc_slices(h, K, L, S);
+    st->e_x = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
+  }
+  if (need_p) {
+    st->ps = alloc_slices(h, st->cap, L, S);
+    st->e_p = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
+  }
+  const int64_t sd = std::max(need_x ? scratch_doubles(st->cap, L, S) : 0,
+                              need_p ? scratch_doubles(K, L, S) : 0);
+  if (sd) st->scratch = h.ws.alloc(sd);
+  st->have = true;
+}
+}  // namespace
+
+void ozaki_dual_pass(Handle& h, const DMat& A, const DMat& Oc, const DMat& Psi, DMat Y, DMat W,
+                     int64_t row0, int64_t row_end, OzakiState* st, bool first, int S) {
+  const int64_t K = A.cols, L = Oc.cols;
+  if (Oc.rows != K || Psi.rows != A.rows || Psi.cols != L || Y.rows != A.rows || Y.cols != L ||
+      W.rows != K || W.cols != L)
+    throw_dim("ozaki_dual_pass: shape mismatch");
+  if (S < 3 || S > kMaxS) throw_param("ozaki: slices must be in 3..8");
+  const double mr = double(row_end - row0);
+  ProfScope prof(h, 3, 4.0 * mr * double(K) * double(L),
+                 8.0 * (mr * double(K) + 2.0 * double(K) * double(L) + 2.0 * mr * double(L)));
+  if (!st->have) {
+    ensure_state(h, st, A.rows, K, L, S, true, true);
+    col_exponents(h, Oc, nullptr, st->e_x);
+    launch_slice(h, Oc, nullptr, nullptr, st->e_x, view_slices(st->xs, K, L), S);
+  }
+  const Sliced xs = view_slices(st->xs, K, L);
+  for (int64_t r0 = row0; r0 < row_end; r0 += st->cap) {
+    const int64_t r1 = std::min(row_end, r0 + st->cap), rows = r1 - r0;
+    const DMat Ap(A.p + r0, rows, K, A.ld);
+    row_exponents(h, Ap, st->e_a);
+    const Sliced as = view_slices(st->as, rows, K);
+    launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, S);
+    // Y[r0:r1, :] = A_p Omega_c
+    launch_gemm(h, true, as, xs, rows, L, K, S, DMat(Y.p + r0, rows, L, Y.ld), st->e_a, st->e_x,
+                false, st->scratch);
+    // W (+)= A_p^T Psi_p, with Psi_p' = diag(2^eA) Psi_p so A's row scales cancel
+    const DMat Pp(Psi.p + r0, rows, L, Psi.ld);
+    col_exponents(h, Pp, st->e_a, st->e_p);
+    const Sliced ps = view_slices(st->ps, rows, L);
+    launch_slice(h, Pp, nullptr, st->e_a, st->e_p, ps, S);
+    launch_gemm(h, false, as, ps, K, L, rows, S, W, nullptr, st->e_p, !(first && r0 == row0),
+                st->scratch);
+  }
+  prof.end();
+}
+
+void ozaki_gemm(Handle& h, const DMat& A, const DMat& X, DMat C, bool trans, int S) {
+  if (S < 3 || S > kMaxS) throw_param("ozaki: slices must be in 3..8");
+  const int64_t L = X.cols, K = A.cols;
+  if (!trans ? (X.rows != A.cols || C.rows != A.rows || C.cols != L)
+             : (X.rows != A.rows || C.rows != A.cols || C.cols != L))
+    throw_dim("ozaki_gemm: shape mismatch");
+  OzakiState state;
+  OzakiState* st = &state;
+  ensure_state(h, st, A.rows, K, L, S, !trans, trans);
+  if (!trans) {
+    col_exponents(h, X, nullptr, st->e_x);
+    launch_slice(h, X, nullptr, nullptr, st->e_x, view_slices(st->xs, K, L), S);
+  }
+  for (int64_t r0 = 0; r0 < A.rows; r0 += st->cap) {
+    const int64_t rows = std::min<int64_t>(st->cap, A.rows - r0);
+    const DMat Ap(A.p + r0, rows, K, A.ld);
+    row_exponents(h, Ap, st->e_a);
+    const Sliced as = view_slices(st->as, rows, K);
+    launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, S);
+    if (!trans) {
+      launch_gemm(h, true, as, view_slices(st->xs, K, L), rows, L, K, S,
+                  DMat(C.p + r0, rows, L, C.ld), st->e_a, st->e_x, false, st->scratch);
+    } else {
+      const DMat Xp(X.p + r0, rows, L, X.ld);
+      col_exponents(h, Xp, st->e_a, st->e_p);
+      const Sliced ps = view_slices(st->ps, rows, L);
+      launch_slice(h, Xp, nullptr, st->e_a, st->e_p, ps, S);
+      launch_gemm(h, false, as, ps, K, L, rows, S, C, nullptr, st->e_p, r0 > 0, st->scratch);
+    }
+  }
+}
+
+}  // namespace rsvdb

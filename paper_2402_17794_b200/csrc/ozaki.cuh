@@ -1,0 +1,35 @@
+// FP64 products of the streaming passes on the INT8 tensor cores (tcgen05,
+// TMEM accumulators) by the Ozaki splitting: both operands are cut into S
+// signed 7-bit slices against a per-row / per-column power-of-two scale, the
+// S(S+1)/2 slice products that matter are exact int32 GEMMs, and the result is
+// reassembled in fp64 (ozaki.cu).  Off by default (Handle::ozaki_slices = 0).
+#pragma once
+#include "common.cuh"
+
+namespace rsvdb {
+// Slices per operand (0 = the DMMA passes): rsvd_set_ozaki_slices, else the
+// RSVD_OZAKI environment variable.  Valid: 0 or 3..8.
+int ozaki_slices(const Handle& h);
+// Work buffers of one call (device pointers into the handle's workspace),
+// reused by every sub-panel: the arena is a bump allocator and the stream
+// orders the reuse.  Lives on the caller's stack for the duration of the call.
+struct OzakiState {
+  bool have = false;
+  int64_t cap = 0;            // sub-panel rows the buffers hold
+  unsigned char* xs = nullptr;  // the K-long skinny operand's slices (Omega_c), [s][l][K]
+  int* e_x = nullptr;
+  unsigned char* as = nullptr;  // A sub-panel slices [s][K][rows]
+  int* e_a = nullptr;
+  unsigned char* ps = nullptr;  // the row-long skinny operand's slices (Psi'), [s][l][rows]
+  int* e_p = nullptr;
+  double* scratch = nullptr;
+};
+// Rows [row0, row_end) of A (M x K): Y rows of the panel = A Omega_c; W (+)=
+// A_panel^T Psi_panel.  Same contract as fused_dual_pass (fused.cuh): `first`
+// starts W, panels arrive in increasing row order on h.stream.  `state` is
+// filled by the first panel (Omega_c's slices, the panel buffers).
+void ozaki_dual_pass(Handle& h, const DMat& A, const DMat& Oc, const DMat& Psi, DMat Y, DMat W,
+                     int64_t row0, int64_t row_end, OzakiState* state, bool first, int slices);
+// C = A X (trans = 0; A m x n, X n x l) or C = A^T X (trans = 1; X m x l).
+void ozaki_gemm(Handle& h, const DMat& A, const DMat& X, DMat C, bool trans, int slices);
+}  // namespace rsvdb

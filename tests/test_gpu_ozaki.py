@@ -1,0 +1,136 @@
+"""The FP64 pass products on the INT8 tensor cores (csrc/ozaki.cu: tcgen05
+kind::i8, Ozaki splitting into S exact 7-bit slices per operand).
+
+Y = A Omega_c and W = A^T Psi of Alg 6 (reference singlepass.hpp:119-122) are
+checked against longdouble / fp64 numpy products: with S = 8 slices inside the
+bound of an fp64 product, |err_ij| <= 2 K u (|A| |X|)_ij; with fewer slices
+inside 2^-(7S-8) of the same scale.  Edge shapes (ragged tiles, K below one
+ring stage, a single row / column), graded and zero rows and columns, row
+panels, determinism, and the whole of Alg 6 against the oracle."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.asfortranarray(a)).cuda().t().contiguous().t()
+
+
+@pytest.fixture
+def oz(eng):
+    yield eng
+    eng.set_ozaki_slices(-1)
+
+
+def _bound(a, x, trans, s):
+    k = a.shape[0] if trans else a.shape[1]
+    sc = (np.abs(a).T @ np.abs(x)) if trans else (np.abs(a) @ np.abs(x))
+    rel = 2 * k * U if s == 8 else max(2 * k * U, 2.0 ** -(7 * s - 8))
+    return rel * sc + 1e-300
+
+
+@pytest.mark.parametrize("m,n,l", [(300, 200, 25), (1000, 777, 110), (257, 4099, 220), (4100, 130, 30),
+                                   (128, 32, 16), (1, 1, 1), (5, 3, 2), (129, 31, 113), (700, 1300, 550)])
+@pytest.mark.parametrize("trans", [False, True])
+def test_gemm_matches_longdouble_product(eng, m, n, l, trans):
+    rs = np.random.default_rng(m + 3 * n + l)
+    a = rs.standard_normal((m, n)) * np.exp(rs.uniform(-3, 3, (m, 1)))
+    x = rs.standard_normal((m if trans else n, l))
+    ref = (a.T.astype(np.longdouble) @ x.astype(np.longdouble)) if trans else (
+        a.astype(np.longdouble) @ x.astype(np.longdouble))
+    for s in (8, 7, 5):
+        c = eng.debug_ozaki_gemm(_t(a), _t(x), trans=trans, slices=s).cpu().numpy()
+        err = np.abs(c - ref).astype(np.float64)
+        b = _bound(a, x, trans, s)
+        assert np.all(err <= b), (s, float(np.max(err / b)))
+
+
+def test_gemm_graded_and_zero_rows_columns(eng):
+    """Row scales spanning 2^-300..2^300, zero rows of A and zero columns of X:
+    the power-of-two scaling is exact, so each output row keeps its own
+    relative accuracy."""
+    rs = np.random.default_rng(3)
+    m, n, l = 500, 300, 40
+    a = rs.standard_normal((m, n)) * (2.0 ** rs.integers(-300, 300, (m, 1)))
+    a[7] = 0.0
+    a[:, 11] = 0.0
+    x = rs.standard_normal((n, l))
+    x[:, 5] = 0.0
+    x[13] = 0.0
+    c = eng.debug_ozaki_gemm(_t(a), _t(x), slices=8).cpu().numpy()
+    ref = a.astype(np.longdouble) @ x.astype(np.longdouble)
+    b = _bound(a, x, False, 8)
+    assert np.all(np.abs(c - ref).astype(np.float64) <= b)
+    assert np.all(c[7] == 0.0) and np.all(c[:, 5] == 0.0)
+    # adjoint: the rows' scales move into the skinny operand
+    y = rs.standard_normal((m, l))
+    a2 = rs.standard_normal((m, n)) * (2.0 ** rs.integers(-30, 30, (m, 1)))
+    c2 = eng.debug_ozaki_gemm(_t(a2), _t(y), trans=True, slices=8).cpu().numpy()
+    ref2 = a2.T.astype(np.longdouble) @ y.astype(np.longdouble)
+    assert np.all(np.abs(c2 - ref2).astype(np.float64) <= _bound(a2, y, True, 8))
+
+
+def test_gemm_long_contraction_chunks(eng):
+    """K above 32768 is accumulated in chunks (int32 cannot overflow)."""
+    rs = np.random.default_rng(8)
+    m, n, l = 130, 70000, 20
+    a = rs.standard_normal((m, n))
+    x = rs.standard_normal((n, l))
+    c = eng.debug_ozaki_gemm(_t(a), _t(x), slices=8).cpu().numpy()
+    ref = a.astype(np.longdouble) @ x.astype(np.longdouble)
+    assert np.all(np.abs(c - ref).astype(np.float64) <= _bound(a, x, False, 8))
+    # extreme digits: every entry at the top of its slice range
+    a1 = np.full((m, 40000), 1.0 - 2.0 ** -52)
+    x1 = np.full((40000, 3), -(1.0 - 2.0 ** -52))
+    c1 = eng.debug_ozaki_gemm(_t(a1), _t(x1), slices=8).cpu().numpy()
+    assert np.allclose(c1, a1 @ x1, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("m,n,l,panel", [(3000, 700, 30, 256), (4096, 1024, 70, 1000), (300, 5000, 550, 0),
+                                         (2049, 4095, 57, 2048)])
+def test_dual_pass_on_int8_tensor_cores(oz, m, n, l, panel):
+    rs = np.random.default_rng(m + n + l)
+    a, oc, psi = rs.standard_normal((m, n)), rs.standard_normal((n, l)), rs.standard_normal((m, l))
+    oz.set_ozaki_slices(8)
+    y, w = oz.debug_dual_pass(_t(a), _t(oc), _t(psi), panel_rows=panel)
+    y2, w2 = oz.debug_dual_pass(_t(a), _t(oc), _t(psi), panel_rows=panel)
+    assert np.array_equal(y.cpu().numpy(), y2.cpu().numpy())  # deterministic
+    assert np.array_equal(w.cpu().numpy(), w2.cpu().numpy())
+    y, w = y.cpu().numpy(), w.cpu().numpy()
+    assert np.all(np.abs(y - a @ oc) <= 2 * _bound(a, oc, False, 8))
+    assert np.all(np.abs(w - a.T @ psi) <= 2 * _bound(a, psi, True, 8))
+
+
+@pytest.mark.parametrize("slices", [8, 7])
+def test_spsvd_on_int8_tensor_cores_matches_oracle(oz, orc, slices):
+    """Alg 6 end to end with the sliced pass: north-star tolerances vs the
+    oracle, one physical pass counted, host-streamed call included."""
+    rs = np.random.default_rng(12)
+    m, n, r = 6000, 1500, 60
+    u, _ = np.linalg.qr(rs.standard_normal((m, r)))
+    v, _ = np.linalg.qr(rs.standard_normal((n, r)))
+    a = np.asfortranarray((u * np.exp(-np.arange(r) / 10.0)) @ v.T + 1e-9 * rs.standard_normal((m, n)))
+    k, p = 30, 10
+    oz.set_ozaki_slices(slices)
+    op = oz.CountingOperator(_t(a))
+    f = oz.spsvd_general(op, k, p, oz.Rng(4))
+    assert op.apply_count() == 1 and op.adjoint_count() == 1 and op.physical_passes() == 1
+    uo, so, vo = orc.spsvd_general(a, k, p, orc.Rng(4))
+    sg = f.sigma.cpu().numpy()
+    assert np.max(np.abs(sg[:k] - so[:k]) / so[:k]) < 1e-10
+    for g, o in ((f.U.cpu().numpy(), uo), (f.V.cpu().numpy(), vo)):
+        s = np.linalg.svd(g[:, :k] - o[:, :k] @ (o[:, :k].T @ g[:, :k]), compute_uv=False)[0]
+        assert np.arcsin(min(1.0, s)) < 1e-8
+    fh = oz.spsvd_general(a, k, p, oz.Rng(4))  # pinned-host path, row panels
+    assert np.max(np.abs(np.asarray(fh.sigma)[:k] - so[:k]) / so[:k]) < 1e-10
+
+
+def test_set_ozaki_slices_rejects_bad_values(oz):
+    with pytest.raises(oz.ParameterError):
+        oz.set_ozaki_slices(2)
+    with pytest.raises(oz.ParameterError):
+        oz.set_ozaki_slices(9)
