@@ -31,8 +31,10 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "pass.cuh"
 #include "ptx.cuh"
@@ -46,6 +48,7 @@ constexpr int kKS = 32;            // contraction per ring stage = one int8 UMMA
 constexpr int kStages = 3;
 constexpr int kThreads = 192;      // producer warp, MMA warp, 4 epilogue warps
 constexpr int kATile = kBM * kKS;  // bytes of one A slice tile
+constexpr int kARegion = 8 * kATile;  // A part of a stage (8 slice tiles / 2 quad tiles)
 constexpr int kMaxS = 8;
 constexpr int kMaxK = 32768;       // (S) * K * 64 * 64 < 2^31
 
@@ -56,6 +59,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(ptx::smem_u32(dst)),
       "l"(map), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(ptx::smem_u32(dst)),
+      "l"(map), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
 // sm_100 shared-memory matrix descriptor: start address, leading / stride byte
@@ -83,6 +94,13 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           ptx::smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -164,20 +182,30 @@ __global__ void __launch_bounds__(256)
 }
 
 // -------------------------------------------------------------- slicing
-// out[s][c][r] (r contiguous, ld8 bytes per column, S x cols x ld8 in all) =
-// digit s of q = rint(x[r,c] * 2^(P - rsub[r] + radd[r] - csub[c])), P = 7S-1:
+// Digit s of q = rint(x[r,c] * 2^(P - rsub[r] + radd[r] - csub[c])), P = 7S-1:
 // q = sum_s d_s 128^(S-s), d_s in [-64, 63] (top digit in [-64, 64]).
-// One thread: 4 consecutive rows of one column (one 32-bit word per slice).
+// Two output layouts (either or both):
+//   plain      out[s][c][r]            r contiguous, ld8 bytes per column: the
+//              MN-major UMMA operand of a contraction over c (the apply);
+//   interleave outi[c][r/32][s][r%32]  ldi bytes per column, 8 slice slots of
+//              32 bytes per 32 r: a contraction over r reads it K-major, and a
+//              128-byte swizzled TMA box holds FOUR slices of one K = 32 step
+//              (the UMMA descriptor picks a slice by a 32-byte start offset),
+//              so the K-major operands get the conflict-free 128B swizzle.
+// One thread: 4 consecutive r of one column (one 32-bit word per slice).
 template <int S>
 __global__ void __launch_bounds__(256)
     slice_kernel(const double* __restrict__ x, int64_t ld, int rows, int cols,
                  const int* __restrict__ rsub, const int* __restrict__ radd,
-                 const int* __restrict__ csub, uint8_t* __restrict__ out, int64_t ld8) {
+                 const int* __restrict__ csub, uint8_t* __restrict__ out, int64_t ld8,
+                 uint8_t* __restrict__ outi, int64_t ldi) {
   RSVD_PDL_ENTRY();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = (blockIdx.x * 32 + lane) * 4;
   const int c = blockIdx.y * 8 + warp;
-  if (r0 >= rows || c >= cols) return;
+  // the interleaved layout is read in whole 32-r groups: zero-fill the last one
+  const int rows_w = outi ? ((rows + 31) & ~31) : rows;
+  if (r0 >= rows_w || c >= cols) return;
   const double* p = x + int64_t(c) * ld + r0;
   double v[4];
   if (r0 + 3 < rows && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
@@ -208,10 +236,17 @@ __global__ void __launch_bounds__(256)
     }
     w[0] |= (uint32_t(q) & 0xffu) << (8 * u);
   }
-  const int64_t plane = int64_t(cols) * ld8;
-  uint8_t* o = out + int64_t(c) * ld8 + r0;
+  if (out && r0 < rows) {
+    const int64_t plane = int64_t(cols) * ld8;
+    uint8_t* o = out + int64_t(c) * ld8 + r0;
 #pragma unroll
-  for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane) = w[s];
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(o + s * plane) = w[s];
+  }
+  if (outi) {
+    uint8_t* o = outi + int64_t(c) * ldi + int64_t(r0 >> 5) * 256 + (r0 & 31);
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(o + s * 32) = w[s];
+  }
 }
 
 // ----------------------------------------------------------------- GEMM
@@ -226,11 +261,12 @@ struct OzParams {
   const int* cexp;
   int accumulate;   // C += result
   double* scratch;  // per-CTA 128 x ntile partial (S > 4)
+  int dbg;          // RSVD_OZ_DBG: 1 = no MMAs (load path alone), 2 = loads only for the first ring fill
 };
 
 // AMN = 1: A tiles are MN-major (global [k][m], the apply product of a
 // column-major A); AMN = 0: K-major (global [m][k], the adjoint product).
-template <int AMN>
+template <int AMN, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, OzParams p) {
@@ -239,9 +275,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sm = smraw + ((1024 - (ptx::smem_u32(smraw) & 1023)) & 1023);
   __shared__ uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full, bar_acc_empty;
   __shared__ uint32_t tmem_base_sh;
-  const int S = p.S;
-  const int btile = p.ntile * kKS;
-  const int stage_bytes = (S * (kATile + btile) + 1023) & ~1023;
+  const int btile4 = p.ntile * 128;                 // four B slices of one K step
+  const int stage_bytes = kARegion + 2 * btile4;    // multiple of 1024 (ntile % 16 == 0)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = blockIdx.x / p.n_tiles, nt = blockIdx.x % p.n_tiles;
   const int m0 = mt * kBM, n0 = nt * p.ntile;
@@ -281,52 +316,82 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int st = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
           ptx::mbar_wait(&bar_empty[st], ph ^ 1);
-          ptx::mbar_expect_tx(&bar_full[st], uint32_t(Sg) * uint32_t(kATile + btile));
-          uint8_t* base = sm + st * stage_bytes;
-          const int kc = p.k0 + kb * kKS;
-          for (int s = 0; s < Sg; ++s) {
-            if (AMN) tma_load_3d(base + s * kATile, &tmA, &bar_full[st], m0, kc, s);
-            else     tma_load_3d(base + s * kATile, &tmA, &bar_full[st], kc, m0, s);
+          if ((p.dbg & 2) && it >= kStages) {
+            ptx::mbar_arrive(&bar_full[st]);
+            continue;
           }
-          uint8_t* bb = base + S * kATile;
-          for (int t = 0; t < Sg; ++t) tma_load_3d(bb + t * btile, &tmB, &bar_full[st], kc, n0, t);
+          const int nhalf = (Sg + 3) >> 2;
+          ptx::mbar_expect_tx(&bar_full[st],
+                              uint32_t(AMN ? Sg * kATile : nhalf * 4 * kATile) + uint32_t(nhalf * btile4));
+          uint8_t* base = sm + st * stage_bytes;
+          const int kc = p.k0 + kb * kKS;   // contraction index
+          const int ki = (kc >> 5) * 256;   // byte offset of its 32-group in an interleaved operand
+          if (AMN) {
+            for (int s = 0; s < Sg; ++s) tma_load_3d(base + s * kATile, &tmA, &bar_full[st], m0, kc, s);
+          } else {
+            for (int hf = 0; hf < nhalf; ++hf)
+              tma_load_2d(base + hf * 4 * kATile, &tmA, &bar_full[st], ki + hf * 128, m0);
+          }
+          uint8_t* bb = base + kARegion;
+          for (int hf = 0; hf < nhalf; ++hf)
+            tma_load_2d(bb + hf * btile4, &tmB, &bar_full[st], ki + hf * 128, n0);
         }
       }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_i8(p.ntile, AMN);
-      int it = 0;
-      for (int g = 0; g < ngroups; ++g) {
-        const int Sg = S - 4 * g;
-        const int c_hi = Sg + 1, c_lo = max(2, c_hi - 3);
-        if (g > 0) {
-          ptx::mbar_wait(&bar_acc_empty, (g - 1) & 1);
-          tc_fence_after();
-        }
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int st = it % kStages;
-          const uint32_t ph = (it / kStages) & 1;
-          ptx::mbar_wait(&bar_full[st], ph);
-          tc_fence_after();
-          const uint32_t a0 = ptx::smem_u32(sm + st * stage_bytes);
-          const uint32_t b0 = a0 + S * kATile;
+    // The whole warp runs the loop (warp-uniform control flow and operands, so
+    // descriptors stay in uniform registers) and one elected lane issues; the
+    // schedule of a K step is unrolled at compile time (S is a template
+    // parameter).  With a divergent `if (lane == 0)` around the loop the
+    // compiler wrapped every tcgen05.mma in an elect loop with four R2UR moves:
+    // 128 cycles per MMA, twice the tensor pipe's 60.
+    const uint32_t idesc = idesc_i8(p.ntile, AMN);
+    const uint64_t ad_fixed = smem_desc(0, AMN ? 4096 : 0, 1024, 2);
+    const uint64_t bd_fixed = smem_desc(0, 0, 1024, 2);
+    const uint32_t sm0 = ptx::smem_u32(sm);
+    int it = 0;
+    auto run_group = [&](auto sg_tag) {
+      constexpr int Sg = decltype(sg_tag)::value;
+      constexpr int c_hi = Sg + 1, c_lo = (c_hi - 3 > 2 ? c_hi - 3 : 2);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int st = it % kStages;
+        const uint32_t ph = (it / kStages) & 1;
+        ptx::mbar_wait(&bar_full[st], ph);
+        tc_fence_after();
+        const uint32_t a0 = (sm0 + st * stage_bytes) >> 4;
+        const uint32_t b0 = a0 + (kARegion >> 4);
+        const uint32_t kacc = kb > 0 ? 1u : 0u;
+        if (elect_one() && !(p.dbg & 1)) {
+#pragma unroll
           for (int c = c_hi; c >= c_lo; --c) {
-            const uint32_t acc = tb + uint32_t((c - c_lo) * p.ntile);
-            const int s_lo = max(1, c - Sg), s_hi = min(Sg, c - 1);
-            for (int s = s_lo; s <= s_hi; ++s) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int s_lo = (c - Sg > 1 ? c - Sg : 1), s_hi = (Sg < c - 1 ? Sg : c - 1);
+#pragma unroll
+            for (int s = 1; s <= Sg; ++s) {
+              if (s < s_lo || s > s_hi) continue;
               const int t = c - s;
-              const uint64_t ad = AMN ? smem_desc(a0 + (s - 1) * kATile, 4096, 1024, 2)
-                                      : smem_desc(a0 + (s - 1) * kATile, 0, 256, 6);
-              const uint64_t bd = smem_desc(b0 + (t - 1) * btile, 0, 256, 6);
-              umma_i8(acc, ad, bd, idesc, (kb > 0 || s > s_lo) ? 1u : 0u);
+              // K-major operands: slice j sits at byte 32 (j % 4) of the 128-byte rows
+              // of quad tile j / 4 (128B swizzle, 8-row groups 1024 bytes apart)
+              const uint32_t ao = AMN ? uint32_t((s - 1) * kATile)
+                                      : uint32_t(((s - 1) >> 2) * 4 * kATile + ((s - 1) & 3) * 32);
+              const uint32_t bo = uint32_t(((t - 1) >> 2) * btile4 + ((t - 1) & 3) * 32);
+              umma_i8(tb + uint32_t((c - c_lo) * 128), ad_fixed | uint64_t(a0 + (ao >> 4)),
+                      bd_fixed | uint64_t(b0 + (bo >> 4)), idesc, s > s_lo ? 1u : kacc);
             }
           }
-          umma_commit(&bar_empty[st]);
         }
-        umma_commit(&bar_acc_full);
+        __syncwarp();
+        if (elect_one()) umma_commit(&bar_empty[st]);
       }
+      if (elect_one()) umma_commit(&bar_acc_full);
+    };
+    run_group(std::integral_constant<int, S>{});
+    if constexpr (S > 4) {
+      ptx::mbar_wait(&bar_acc_empty, 0);
+      tc_fence_after();
+      run_group(std::integral_constant<int, (S > 4 ? S - 4 : 1)>{});
     }
   } else {
     // ---------------------------------------------------------- epilogue
@@ -347,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 8; ++j) v[j] = 0.0;
         for (int c = c_hi; c >= c_lo; --c) {  // smallest terms first
           uint32_t r[8];
-          tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t((c - c_lo) * p.ntile + cc), r);
+          tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t((c - c_lo) * 128 + cc), r);
           tmem_ld_wait();
           const double sc = exp2i(-(7 * c - 2));
 #pragma unroll
@@ -416,26 +481,53 @@ CUtensorMap make_map_i8(const uint8_t* p, int64_t inner, int64_t outer, int64_t 
   return m;
 }
 
-// Sliced operand in device memory: S planes of `outer` columns, ld8 bytes each.
+// 2-D map over an interleaved operand [outer][ldi bytes]: box {128 bytes, rows}
+CUtensorMap make_map_inter(const uint8_t* p, int64_t inner_bytes, int64_t outer, int64_t ldi,
+                           int box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cuuint64_t(inner_bytes), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(ldi)};
+  cuuint32_t box[2] = {128, cuuint32_t(box_outer)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(p), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(RSVD_ERR_CUDA, "cuTensorMapEncodeTiled (interleaved) failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+// Sliced operand in device memory (layouts: slice_kernel).  `inner` runs along
+// the source's rows (contiguous in the fp64 matrix), `outer` along its columns.
+//   plain:      S planes of `outer` columns, ld bytes each
+//   interleave: `outer` columns of ld = 256 ceil(inner / 32) bytes
 struct Sliced {
   uint8_t* p = nullptr;
-  int64_t inner = 0, outer = 0, ld8 = 0;
+  int64_t inner = 0, outer = 0, ld = 0;
 };
 
-int64_t ld8_of(int64_t inner) { return round_up(std::max<int64_t>(inner, 16), 16); }
+int64_t ld_plain(int64_t inner) { return round_up(std::max<int64_t>(inner, 16), 16); }
+int64_t ld_inter(int64_t inner) { return ceil_div(std::max<int64_t>(inner, 1), 32) * 256; }
 
-// Buffer for an operand of up to cap_inner x outer (views of fewer rows reuse it)
-uint8_t* alloc_slices(Handle& h, int64_t cap_inner, int64_t outer, int S) {
-  uint8_t* p = static_cast<uint8_t*>(
-      h.ws.alloc_bytes(size_t(S) * size_t(outer) * size_t(ld8_of(cap_inner)) + 1024));
+uint8_t* alloc_aligned(Handle& h, size_t bytes) {
+  uint8_t* p = static_cast<uint8_t*>(h.ws.alloc_bytes(bytes + 1024));
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
 }
-Sliced view_slices(uint8_t* p, int64_t inner, int64_t outer) {
+uint8_t* alloc_plain(Handle& h, int64_t cap_inner, int64_t outer, int S) {
+  return alloc_aligned(h, size_t(S) * size_t(outer) * size_t(ld_plain(cap_inner)));
+}
+uint8_t* alloc_inter(Handle& h, int64_t cap_inner, int64_t outer) {
+  return alloc_aligned(h, size_t(outer) * size_t(ld_inter(cap_inner)));
+}
+Sliced view_plain(uint8_t* p, int64_t inner, int64_t outer) {
   Sliced s;
-  s.p = p;
-  s.inner = inner;
-  s.outer = outer;
-  s.ld8 = ld8_of(inner);
+  s.p = p, s.inner = inner, s.outer = outer, s.ld = ld_plain(inner);
+  return s;
+}
+Sliced view_inter(uint8_t* p, int64_t inner, int64_t outer) {
+  Sliced s;
+  s.p = p, s.inner = inner, s.outer = outer, s.ld = ld_inter(inner);
   return s;
 }
 
@@ -445,14 +537,15 @@ void fill_exp(Handle& h, int* e, int64_t n, int init) {
   RSVD_LAUNCHED(h);
 }
 
+// plain and / or inter may be null (p == nullptr)
 void launch_slice(Handle& h, const DMat& X, const int* rsub, const int* radd, const int* csub,
-                  const Sliced& out, int S) {
+                  const Sliced& plain, const Sliced& inter, int S) {
   if (X.rows == 0 || X.cols == 0) return;
   dim3 grid(unsigned(ceil_div(X.rows, 128)), unsigned(ceil_div(X.cols, 8)));
 #define RSVD_SLICE_CASE(SS)                                                                       \
   case SS:                                                                                        \
     launch_k(h, slice_kernel<SS>, grid, 256, 0, (const double*)X.p, X.ld, int(X.rows), int(X.cols), \
-             rsub, radd, csub, out.p, out.ld8);                                                   \
+             rsub, radd, csub, plain.p, plain.ld, inter.p, inter.ld);                             \
     break;
   switch (S) {
     RSVD_SLICE_CASE(3)
@@ -504,9 +597,10 @@ int64_t scratch_doubles(int64_t M, int64_t N, int S) {
 }
 
 // C (M x N) (+)= sliced A  x  sliced B over K entries.
-//   amn = true : A slices are [s][k][m] (M contiguous): the apply product
-//   amn = false: A slices are [s][m][k] (K contiguous): the adjoint product
-// B slices are [s][n][k].  rexp / cexp: exponents of the output rows / columns.
+//   amn = true : As is plain [s][k][m] (M contiguous): the apply product
+//   amn = false: As is interleaved [m][k/32][s][k%32]: the adjoint product
+// Bs is interleaved [n][k/32][s][k%32].  rexp / cexp: exponents of the output
+// rows / columns.
 void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_t M, int64_t N,
                  int64_t K, int S, DMat C, const int* rexp, const int* cexp, bool accumulate,
                  double* scratch) {
@@ -516,11 +610,11 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
   const int n_tiles = int(ceil_div(N, ntile));
   const int64_t m_tiles = ceil_div(M, kBM);
   const int64_t grid = m_tiles * n_tiles;
-  const int stage_bytes = int(round_up(int64_t(S) * (kATile + ntile * kKS), 1024));
+  const int stage_bytes = kARegion + 2 * ntile * 128;
   const size_t smem = size_t(kStages) * stage_bytes + 1024;
-  const CUtensorMap ta = amn ? make_map_i8(As.p, As.inner, As.outer, As.ld8, S, kBM, kKS, true)
-                             : make_map_i8(As.p, As.inner, As.outer, As.ld8, S, kKS, kBM, false);
-  const CUtensorMap tb = make_map_i8(Bs.p, Bs.inner, Bs.outer, Bs.ld8, S, kKS, ntile, false);
+  const CUtensorMap ta = amn ? make_map_i8(As.p, As.inner, As.outer, As.ld, S, kBM, kKS, true)
+                             : make_map_inter(As.p, As.ld, As.outer, As.ld, kBM);
+  const CUtensorMap tb = make_map_inter(Bs.p, Bs.ld, Bs.outer, Bs.ld, ntile);
   for (int64_t k0 = 0; k0 < K; k0 += kMaxK) {
     OzParams p;
     p.M = int(M);
@@ -536,13 +630,29 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
     p.cexp = cexp;
     p.accumulate = (accumulate || k0 > 0) ? 1 : 0;
     p.scratch = scratch;
-    if (amn) {
-      smem_attr(ozaki_gemm_kernel<1>, smem);
-      launch_k(h, ozaki_gemm_kernel<1>, unsigned(grid), kThreads, smem, ta, tb, p);
-    } else {
-      smem_attr(ozaki_gemm_kernel<0>, smem);
-      launch_k(h, ozaki_gemm_kernel<0>, unsigned(grid), kThreads, smem, ta, tb, p);
+    static const int dbg = [] { const char* e = std::getenv("RSVD_OZ_DBG"); return e ? std::atoi(e) : 0; }();
+    p.dbg = dbg;
+#define RSVD_OZ_CASE(SS)                                                             \
+  case SS:                                                                           \
+    if (amn) {                                                                       \
+      smem_attr(ozaki_gemm_kernel<1, SS>, smem);                                     \
+      launch_k(h, ozaki_gemm_kernel<1, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
+    } else {                                                                         \
+      smem_attr(ozaki_gemm_kernel<0, SS>, smem);                                     \
+      launch_k(h, ozaki_gemm_kernel<0, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
+    }                                                                                \
+    break;
+    switch (S) {
+      RSVD_OZ_CASE(3)
+      RSVD_OZ_CASE(4)
+      RSVD_OZ_CASE(5)
+      RSVD_OZ_CASE(6)
+      RSVD_OZ_CASE(7)
+      RSVD_OZ_CASE(8)
+      default:
+        throw_param("ozaki: slices must be in 3..8");
     }
+#undef RSVD_OZ_CASE
     RSVD_LAUNCHED(h);
   }
 }
@@ -572,14 +682,15 @@ void ensure_state(Handle& h, OzakiState* st, int64_t rows_total, int64_t K, int6
                   bool need_x, bool need_p) {
   if (st->have) return;
   st->cap = std::min<int64_t>(sub_rows(K, S), round_up(std::max<int64_t>(rows_total, 1), 128));
-  st->as = alloc_slices(h, st->cap, K, S);
   st->e_a = static_cast<int*>(h.ws.alloc_bytes(size_t(st->cap) * 4));
   if (need_x) {
-    st->xs = alloc_slices(h, K, L, S);
+    st->as = alloc_plain(h, st->cap, K, S);
+    st->xs = alloc_inter(h, K, L);
     st->e_x = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
   }
   if (need_p) {
-    st->ps = alloc_slices(h, st->cap, L, S);
+    st->asi = alloc_inter(h, st->cap, K);
+    st->ps = alloc_inter(h, st->cap, L);
     st->e_p = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
   }
   const int64_t sd = std::max(need_x ? scratch_doubles(st->cap, L, S) : 0,
@@ -599,27 +710,29 @@ void ozaki_dual_pass(Handle& h, const DMat& A, const DMat& Oc, const DMat& Psi, 
   const double mr = double(row_end - row0);
   ProfScope prof(h, 3, 4.0 * mr * double(K) * double(L),
                  8.0 * (mr * double(K) + 2.0 * double(K) * double(L) + 2.0 * mr * double(L)));
+  const Sliced none;
   if (!st->have) {
     ensure_state(h, st, A.rows, K, L, S, true, true);
     col_exponents(h, Oc, nullptr, st->e_x);
-    launch_slice(h, Oc, nullptr, nullptr, st->e_x, view_slices(st->xs, K, L), S);
+    launch_slice(h, Oc, nullptr, nullptr, st->e_x, none, view_inter(st->xs, K, L), S);
   }
-  const Sliced xs = view_slices(st->xs, K, L);
+  const Sliced xs = view_inter(st->xs, K, L);
   for (int64_t r0 = row0; r0 < row_end; r0 += st->cap) {
     const int64_t r1 = std::min(row_end, r0 + st->cap), rows = r1 - r0;
     const DMat Ap(A.p + r0, rows, K, A.ld);
     row_exponents(h, Ap, st->e_a);
-    const Sliced as = view_slices(st->as, rows, K);
-    launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, S);
+    // one read of the panel writes both operand layouts of its slices
+    const Sliced as = view_plain(st->as, rows, K), asi = view_inter(st->asi, rows, K);
+    launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, asi, S);
     // Y[r0:r1, :] = A_p Omega_c
     launch_gemm(h, true, as, xs, rows, L, K, S, DMat(Y.p + r0, rows, L, Y.ld), st->e_a, st->e_x,
                 false, st->scratch);
     // W (+)= A_p^T Psi_p, with Psi_p' = diag(2^eA) Psi_p so A's row scales cancel
     const DMat Pp(Psi.p + r0, rows, L, Psi.ld);
     col_exponents(h, Pp, st->e_a, st->e_p);
-    const Sliced ps = view_slices(st->ps, rows, L);
-    launch_slice(h, Pp, nullptr, st->e_a, st->e_p, ps, S);
-    launch_gemm(h, false, as, ps, K, L, rows, S, W, nullptr, st->e_p, !(first && r0 == row0),
+    const Sliced ps = view_inter(st->ps, rows, L);
+    launch_slice(h, Pp, nullptr, st->e_a, st->e_p, none, ps, S);
+    launch_gemm(h, false, asi, ps, K, L, rows, S, W, nullptr, st->e_p, !(first && r0 == row0),
                 st->scratch);
   }
   prof.end();
@@ -634,25 +747,28 @@ void ozaki_gemm(Handle& h, const DMat& A, const DMat& X, DMat C, bool trans, int
   OzakiState state;
   OzakiState* st = &state;
   ensure_state(h, st, A.rows, K, L, S, !trans, trans);
+  const Sliced none;
   if (!trans) {
     col_exponents(h, X, nullptr, st->e_x);
-    launch_slice(h, X, nullptr, nullptr, st->e_x, view_slices(st->xs, K, L), S);
+    launch_slice(h, X, nullptr, nullptr, st->e_x, none, view_inter(st->xs, K, L), S);
   }
   for (int64_t r0 = 0; r0 < A.rows; r0 += st->cap) {
     const int64_t rows = std::min<int64_t>(st->cap, A.rows - r0);
     const DMat Ap(A.p + r0, rows, K, A.ld);
     row_exponents(h, Ap, st->e_a);
-    const Sliced as = view_slices(st->as, rows, K);
-    launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, S);
     if (!trans) {
-      launch_gemm(h, true, as, view_slices(st->xs, K, L), rows, L, K, S,
+      const Sliced as = view_plain(st->as, rows, K);
+      launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, none, S);
+      launch_gemm(h, true, as, view_inter(st->xs, K, L), rows, L, K, S,
                   DMat(C.p + r0, rows, L, C.ld), st->e_a, st->e_x, false, st->scratch);
     } else {
+      const Sliced asi = view_inter(st->asi, rows, K);
+      launch_slice(h, Ap, st->e_a, nullptr, nullptr, none, asi, S);
       const DMat Xp(X.p + r0, rows, L, X.ld);
       col_exponents(h, Xp, st->e_a, st->e_p);
-      const Sliced ps = view_slices(st->ps, rows, L);
-      launch_slice(h, Xp, nullptr, st->e_a, st->e_p, ps, S);
-      launch_gemm(h, false, as, ps, K, L, rows, S, C, nullptr, st->e_p, r0 > 0, st->scratch);
+      const Sliced ps = view_inter(st->ps, rows, L);
+      launch_slice(h, Xp, nullptr, st->e_a, st->e_p, none, ps, S);
+      launch_gemm(h, false, asi, ps, K, L, rows, S, C, nullptr, st->e_p, r0 > 0, st->scratch);
     }
   }
 }

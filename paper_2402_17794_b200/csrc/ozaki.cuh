@@ -16,11 +16,12 @@ int ozaki_slices(const Handle& h);
 struct OzakiState {
   bool have = false;
   int64_t cap = 0;            // sub-panel rows the buffers hold
-  unsigned char* xs = nullptr;  // the K-long skinny operand's slices (Omega_c), [s][l][K]
+  unsigned char* xs = nullptr;   // the K-long skinny operand's slices (Omega_c), interleaved
   int* e_x = nullptr;
-  unsigned char* as = nullptr;  // A sub-panel slices [s][K][rows]
+  unsigned char* as = nullptr;   // A sub-panel slices, plain [s][K][rows] (apply operand)
+  unsigned char* asi = nullptr;  // the same slices interleaved [K][rows/32][s][32] (adjoint operand)
   int* e_a = nullptr;
-  unsigned char* ps = nullptr;  // the row-long skinny operand's slices (Psi'), [s][l][rows]
+  unsigned char* ps = nullptr;   // the row-long skinny operand's slices (Psi'), interleaved
   int* e_p = nullptr;
   double* scratch = nullptr;
 };

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int N, int iters, long lon
       for (int k = 0; k < 4; ++k) {
         uint64_t ad = AMN == 0 ? smem_desc(a0 + k * 32, 0, 1024, 2) : smem_desc(a0 + k * 4096, 16384, 1024, 2);
         uint64_t bd = smem_desc(b0 + k * 32, 0, 1024, 2);
-        umma_i8(tb + (it & 1) * 256, ad, bd, idesc, 1u);
+        umma_i8(tb + (N <= 128 ? ((it * 4 + k) & 3) * 128 : (it & 1) * 256), ad, bd, idesc, 1u);
       }
     }
     umma_commit(&done);
@@ -258,12 +258,13 @@ static void run_check(int N, int K) {
   cudaFree(dA); cudaFree(dB); cudaFree(dD);
 }
 
+static int g_iters = 2048;
 template <int AMN>
 static void run_rate(int sms) {
   long long* dc; CK(cudaMalloc(&dc, 8));
   CK(cudaFuncSetAttribute(rate_kernel<AMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 49152 + 1024));
-  for (int N : {32, 48, 64, 96, 128, 192, 256}) {
-    const int iters = 2048;
+  for (int N : {32, 48, 64, 96, 112, 128, 192, 256}) {
+    const int iters = g_iters;
     rate_kernel<AMN><<<sms, 128, 4 * 49152 + 1024>>>(N, iters, dc);
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -281,7 +282,8 @@ static void run_rate(int sms) {
   cudaFree(dc);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) g_iters = atoi(argv[1]);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run_check<0>(64, 256);
   run_check<0>(256, 256);
