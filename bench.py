@@ -38,6 +38,15 @@ FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak, profiles/r01_fp64_peaks.md
 L2_FLUSH_BELOW = 256 << 20   # A below 2x L2 is L2-flushed between timed steps
 L2_FLUSH_BYTES = 512 << 20   # > 4x the 126 MB L2
 FP64_PEAK_SOURCE = "measured DMMA microbenchmark (profiles/r01_fp64_peaks.md); MEASURED_PEAKS.json has no fp64 figure"
+# INT8 tensor pipe (tcgen05.mma kind::i8), measured with tools/microbench/umma_i8.cu
+# (profiles/r02_umma_i8_rate.txt): 148 CTAs issuing M128 N128..256 K32 MMAs on
+# resident operands.  Burst (0.3-0.6 ms runs) 4.13-4.36 POP/s; sustained (30-67 ms
+# runs, under the power cap) 3.71-3.87 POP/s.  The Ozaki GEMM runs inside a long
+# step, so its roofline uses the sustained figure.
+INT8_PEAK_TOPS = 3840.0
+INT8_PEAK_BURST_TOPS = 4340.0
+INT8_PEAK_SOURCE = ("measured tcgen05 kind::i8 issue-rate microbenchmark, sustained 30-67 ms runs "
+                    "(profiles/r02_umma_i8_rate.txt; burst 4340); MEASURED_PEAKS.json has no int8 figure")
 
 
 def hbm_peak_gbs() -> float:
@@ -452,6 +461,17 @@ def main():
         per_ms = d["ms"] / d["launches"]
         fl = d["flops"] / d["launches"]
         by = d["bytes"] / d["launches"]
+        if kind == "int8":
+            # the sliced INT8 GEMM kernel (csrc/ozaki.cu): `flops` are int8
+            # multiply-adds x 2 of the S(S+1)/2 exact slice products
+            tops = fl / (per_ms * 1e-3) / 1e12
+            gbs = by / (per_ms * 1e-3) / 1e9
+            passes[kind] = {"launches_per_step": d["launches"] / args.steps, "ms_per_launch": per_ms,
+                            "bound": "tensor", "int8_tops": tops, "gbs": gbs,
+                            "frac_int8": tops / INT8_PEAK_TOPS, "frac_hbm": gbs / hbm,
+                            "frac_roofline": tops / INT8_PEAK_TOPS,
+                            "share_of_step": d["ms"] / ms_prof if ms_prof else None}
+            continue
         t_fp = fl / (FP64_PEAK_TFLOPS * 1e12)
         t_hb = by / (hbm * 1e9)
         bound = "tensor" if t_fp >= t_hb else "hbm"
@@ -462,7 +482,12 @@ def main():
                         "frac_fp64": tf / FP64_PEAK_TFLOPS, "frac_hbm": gbs / hbm,
                         "frac_roofline": max(t_fp, t_hb) / (per_ms * 1e-3),
                         "share_of_step": d["ms"] / ms_prof if ms_prof else None}
-    dom = max(passes, key=lambda k_: passes[k_]["ms_per_launch"] * passes[k_]["launches_per_step"])
+    # the INT8 GEMM launches run inside the dual pass's scope ("fused"): when
+    # present they are the dominant kernel
+    if "int8" in passes:
+        dom = "int8"
+    else:
+        dom = max(passes, key=lambda k_: passes[k_]["ms_per_launch"] * passes[k_]["launches_per_step"])
     dp = passes[dom]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -471,7 +496,18 @@ def main():
             traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
         except Exception:
             traffic = None
-    if dp["bound"] == "tensor":
+    if dom == "int8":
+        fz = passes.get("fused")
+        roof = {"bound": "tensor", "achieved": dp["int8_tops"], "peak": INT8_PEAK_TOPS,
+                "unit": "TFLOP/s", "frac": dp["int8_tops"] / INT8_PEAK_TOPS, "traffic": traffic,
+                "peak_source": INT8_PEAK_SOURCE, "peak_burst": INT8_PEAK_BURST_TOPS,
+                "op": "int8 x int8 -> int32 multiply-add, counted as 2 operations (TOP/s)",
+                "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8, TMEM int32 accumulators): the "
+                          "S(S+1)/2 exact slice products of one row panel's A Omega_c or A^T Psi",
+                "fp64_equivalent": None if not fz else {
+                    "tflops": fz["tflops"], "vs_fp64_dmma_peak": fz["tflops"] / FP64_PEAK_TFLOPS,
+                    "scope": "whole dual pass (exponent scan + slicing + both INT8 GEMMs), 4mnl flops"}}
+    elif dp["bound"] == "tensor":
         roof = {"bound": "tensor", "achieved": dp["tflops"], "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": dp["tflops"] / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": FP64_PEAK_SOURCE,
@@ -514,6 +550,10 @@ def main():
                            + " (pinned host A" + (", streamed in row panels into the pass)"
                                                   if cfg["alg"] >= 5 else ")")},
             "roofline": roof,
+            "pass_arithmetic": ("fp64 products of the pass on the INT8 tensor cores: Ozaki splitting into "
+                                + (os.environ.get("RSVD_OZAKI") or "8") + " exact 7-bit slices per operand, "
+                                "int32 partial products in TMEM, fp64 reassembly (csrc/ozaki.cu)")
+                               if "int8" in passes else "fp64 DMMA (mma.sync m8n8k4.f64)",
             "passes": passes,
             "profiled_run_ms_per_step": ms_prof / args.steps,
             "cpu_baseline": cpu,

@@ -317,7 +317,7 @@ class Engine:
 
     def profile_read(self) -> dict:
         out = {}
-        for kind, name in ((0, "apply"), (1, "adjoint"), (2, "other"), (3, "fused")):
+        for kind, name in ((0, "apply"), (1, "adjoint"), (2, "other"), (3, "fused"), (4, "int8")):
             n, ms, fl, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
             _check(_load().rsvd_profile_read(self._h, kind, ctypes.byref(n), ctypes.byref(ms),
                                              ctypes.byref(fl), ctypes.byref(by)))

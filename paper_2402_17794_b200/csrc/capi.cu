@@ -583,7 +583,7 @@ rsvd_status rsvd_profile_enable(rsvd_handle* hd, int on) {
   if (!hd) return RSVD_ERR_PARAMETER;
   rsvdb::Handle& h = hd->h;
   h.prof = on != 0;
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 5; ++k) {
     h.prof_ms[k] = h.prof_flops[k] = h.prof_bytes[k] = 0;
     h.prof_count[k] = 0;
   }
@@ -592,7 +592,7 @@ rsvd_status rsvd_profile_enable(rsvd_handle* hd, int on) {
 
 rsvd_status rsvd_profile_read(rsvd_handle* hd, int kind, int64_t* launches, double* ms,
                               double* flops, double* bytes) {
-  if (!hd || kind < 0 || kind > 3) return RSVD_ERR_PARAMETER;
+  if (!hd || kind < 0 || kind > 4) return RSVD_ERR_PARAMETER;
   rsvdb::Handle& h = hd->h;
   if (launches) *launches = h.prof_count[kind];
   if (ms) *ms = h.prof_ms[kind];

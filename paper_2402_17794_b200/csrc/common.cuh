@@ -88,6 +88,12 @@ class Arena {
     return DMat(alloc(ld * c), r, c, ld);
   }
   size_t high_water() const { return high_; }
+  // largest request the held chunks can serve without a new cudaMalloc
+  size_t remaining() const {
+    size_t r = 0;
+    for (const auto& c : chunks_) r = c.cap - c.off > r ? c.cap - c.off : r;
+    return r;
+  }
   // bumped whenever chunk addresses change (captured CUDA graphs hold them)
   uint64_t generation() const { return gen_; }
 
@@ -164,14 +170,14 @@ struct Handle {
   bool prof = false;
   struct ProfRec {
     cudaEvent_t a, b;
-    int kind;  // 0 = NN (Y = A X), 1 = TN (Z = A^T Y), 2 = other, 3 = fused Alg-6 pass
+    int kind;  // 0 = NN (Y = A X), 1 = TN (Z = A^T Y), 2 = other, 3 = Alg-6 dual pass, 4 = INT8 slice GEMM
     double flops, bytes;
     bool graph = false;  // events owned by a captured graph (not pooled)
   };
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> prof_pool;
-  double prof_ms[4] = {0, 0, 0, 0}, prof_flops[4] = {0, 0, 0, 0}, prof_bytes[4] = {0, 0, 0, 0};
-  int64_t prof_count[4] = {0, 0, 0, 0};
+  double prof_ms[5] = {0, 0, 0, 0, 0}, prof_flops[5] = {0, 0, 0, 0, 0}, prof_bytes[5] = {0, 0, 0, 0, 0};
+  int64_t prof_count[5] = {0, 0, 0, 0, 0};
   // Launch-site trace (rsvd_trace_enable): an event after every launch; the
   // time between consecutive events (kernel + any idle gap before it) is
   // charged to the launch site at the call's final synchronization.

@@ -68,9 +68,23 @@ void Arena::reset() {
 
 void* Arena::alloc_bytes(size_t bytes) {
   bytes = size_t(round_up(int64_t(std::max<size_t>(bytes, 1)), 256));
-  if (chunks_.empty() || chunks_.back().off + bytes > chunks_.back().cap) {
+  // first fit over the chunks already held (an earlier chunk's tail is not
+  // lost when a large request opened a new chunk behind it)
+  for (auto& c : chunks_) {
+    if (c.off + bytes <= c.cap) {
+      void* p = c.p + c.off;
+      c.off += bytes;
+      used_total_ += bytes;
+      high_ = std::max(high_, used_total_);
+      return p;
+    }
+  }
+  {
     size_t want = std::max<size_t>(bytes, arena_tiny() ? (size_t(256) << 10) : (size_t(64) << 20));
-    if (!chunks_.empty() && !arena_tiny()) want = std::max(want, 2 * chunks_.back().cap);
+    // geometric growth, bounded: after a matrix-sized chunk the next request
+    // must not ask for twice that again
+    if (!chunks_.empty() && !arena_tiny())
+      want = std::max(want, std::min<size_t>(2 * chunks_.back().cap, size_t(4) << 30));
     Chunk c{nullptr, want, 0};
     cudaError_t e = cudaMalloc(&c.p, c.cap);
     if (e != cudaSuccess) {
@@ -460,7 +474,7 @@ void op_dual(Handle& h, const Problem& P, const DMat& Oc, const DMat& Psi, DMat 
   }
   // RSVD_OZAKI / rsvd_set_ozaki_slices: the same dual product on the INT8
   // tensor cores from exact integer slices of each row panel (ozaki.cu)
-  const int oz = ozaki_slices(h);
+  const int oz = ozaki_slices_auto(h, P.m_global, A.cols, Oc.cols);
   OzakiState ost;
   int* sem = oz ? nullptr
                 : reinterpret_cast<int*>(h.ws.alloc_bytes(size_t(fused_semaphores(A.rows, A.cols, Oc.cols)) * 4));

@@ -632,6 +632,10 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
     p.scratch = scratch;
     static const int dbg = [] { const char* e = std::getenv("RSVD_OZ_DBG"); return e ? std::atoi(e) : 0; }();
     p.dbg = dbg;
+    // the kernel's algorithmic work: S(S+1)/2 exact int8 products of M x N x K,
+    // every slice byte of both operands read once, the fp64 tile written
+    ProfScope prof(h, 4, double(S * (S + 1) / 2) * 2.0 * double(M) * double(N) * double(p.K),
+                   double(S) * double(p.K) * double(M + N) + 8.0 * double(M) * double(N));
 #define RSVD_OZ_CASE(SS)                                                             \
   case SS:                                                                           \
     if (amn) {                                                                       \
@@ -654,14 +658,19 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
     }
 #undef RSVD_OZ_CASE
     RSVD_LAUNCHED(h);
+    prof.end();
   }
 }
 
-// rows of A sliced at a time: int32 accumulation bounds the adjoint's
-// contraction length, and a sub-panel's slices stay below ~9 GB
-int64_t sub_rows(int64_t K, int S) {
+// Rows of A sliced at a time: int32 accumulation bounds the adjoint's
+// contraction length (kMaxK); `copies` layouts of the sub-panel's slices
+// (S K bytes per row each) must fit in ~9 GB and in what the device has left.
+int64_t sub_rows(Handle& h, int64_t K, int S, int copies) {
+  size_t free_b = 0, total_b = 0;
+  RSVD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double budget = std::min(18.0e9, 0.8 * (double(free_b) + double(h.ws.remaining())));
   int64_t sub = kMaxK;
-  while (sub > 1024 && double(sub) * double(K) * S > 9.0e9) sub /= 2;
+  while (sub > 1024 && double(sub) * double(K) * S * copies > budget) sub /= 2;
   return sub;
 }
 
@@ -671,17 +680,30 @@ int ozaki_slices(const Handle& h) {
   if (h.ozaki_slices >= 0) return h.ozaki_slices;
   static const int env = [] {
     const char* e = std::getenv("RSVD_OZAKI");
-    const int v = e ? std::atoi(e) : 0;
+    if (!e) return -1;
+    const int v = std::atoi(e);
     return (v >= 3 && v <= kMaxS) ? v : 0;
   }();
   return env;
+}
+
+// Default policy of the Alg-6 dual pass (engine.cu op_dual): the sliced INT8
+// product with 8 slices (inside the error bound of an fp64 product, see the
+// header) when the sketch is wide enough for the tensor pipe to pay for the
+// slicing passes (l >= 128: at l = 110 it breaks even with the DMMA pass,
+// below that the pass is HBM-bound anyway) and A is large (>= 2^26 entries).
+int ozaki_slices_auto(const Handle& h, int64_t rows, int64_t K, int64_t L) {
+  const int s = ozaki_slices(h);
+  if (s >= 0) return s;
+  return (L >= 128 && double(rows) * double(K) >= double(int64_t(1) << 26)) ? 8 : 0;
 }
 
 namespace {
 void ensure_state(Handle& h, OzakiState* st, int64_t rows_total, int64_t K, int64_t L, int S,
                   bool need_x, bool need_p) {
   if (st->have) return;
-  st->cap = std::min<int64_t>(sub_rows(K, S), round_up(std::max<int64_t>(rows_total, 1), 128));
+  st->cap = std::min<int64_t>(sub_rows(h, K, S, (need_x ? 1 : 0) + (need_p ? 1 : 0)),
+                              round_up(std::max<int64_t>(rows_total, 1), 128));
   st->e_a = static_cast<int*>(h.ws.alloc_bytes(size_t(st->cap) * 4));
   if (need_x) {
     st->as = alloc_plain(h, st->cap, K, S);

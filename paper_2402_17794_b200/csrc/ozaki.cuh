@@ -2,14 +2,17 @@
 // TMEM accumulators) by the Ozaki splitting: both operands are cut into S
 // signed 7-bit slices against a per-row / per-column power-of-two scale, the
 // S(S+1)/2 slice products that matter are exact int32 GEMMs, and the result is
-// reassembled in fp64 (ozaki.cu).  Off by default (Handle::ozaki_slices = 0).
+// reassembled in fp64 (ozaki.cu).  Default for wide sketches of large matrices (ozaki_slices_auto).
 #pragma once
 #include "common.cuh"
 
 namespace rsvdb {
-// Slices per operand (0 = the DMMA passes): rsvd_set_ozaki_slices, else the
-// RSVD_OZAKI environment variable.  Valid: 0 or 3..8.
+// Slices per operand: rsvd_set_ozaki_slices, else the RSVD_OZAKI environment
+// variable (0 = the DMMA passes, 3..8 = slices), else -1 = automatic.
 int ozaki_slices(const Handle& h);
+// The dual pass's choice for an A of rows x K and l = L sketch columns: the
+// explicit setting, else 8 slices for wide sketches of large matrices, else 0.
+int ozaki_slices_auto(const Handle& h, int64_t rows, int64_t K, int64_t L);
 // Work buffers of one call (device pointers into the handle's workspace),
 // reused by every sub-panel: the arena is a bump allocator and the stream
 // orders the reuse.  Lives on the caller's stack for the duration of the call.

@@ -27,6 +27,17 @@ def _run(config):
     import bench
     import oracle
     import paper_2402_17794_b200 as eng
+    # "C5-dmma": C5 with the FP64 DMMA fused pass forced (the default for C5's
+    # wide sketch is the sliced INT8 tensor-core pass, csrc/ozaki.cu)
+    config, _, variant = config.partition("-")
+    eng.set_ozaki_slices(0 if variant == "dmma" else -1)
+    try:
+        return _run_cfg(config, torch, bench, oracle, eng)
+    finally:
+        eng.set_ozaki_slices(-1)
+
+
+def _run_cfg(config, torch, bench, oracle, eng):
     cfg = bench.CONFIGS[config]
     torch.cuda.set_device(0)
     a = bench.make_input(cfg, torch.device("cuda", 0))
@@ -58,10 +69,12 @@ def _run(config):
     return cfg, out, ref
 
 
-@pytest.mark.parametrize("config", ["C1", "C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("config", ["C1", "C2", "C3", "C4", "C5", "C5-dmma"])
 def test_config_parity(config):
     cfg, (u, s, v), (uo, so, vo) = _run(config)
     k = cfg["k"]
+    print(f"{config}: sigma rel {np.max(np.abs(s[:k] - so[:k]) / np.abs(so[:k])):.3e}, "
+          f"U angle {sin_max(u[:, :k], uo[:, :k]):.3e}")
     rel = np.max(np.abs(s[:k] - so[:k]) / np.abs(so[:k]))
     assert rel < SIG_TOL, f"{config}: top-k relative error {rel:.3e}"
     ang = sin_max(u[:, :k], uo[:, :k])
