@@ -549,6 +549,12 @@ void rsvd_destroy(rsvd_handle* hd) {
     cudaStreamDestroy(h.copy_stream);
   }
   if (h.copy_ev) cudaEventDestroy(h.copy_ev);
+  if (h.oz_stream) {
+    cudaStreamSynchronize(h.oz_stream);
+    cudaStreamDestroy(h.oz_stream);
+  }
+  for (cudaEvent_t e : h.oz_ev)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : h.panel_ev) cudaEventDestroy(e);
   if (h.order_ev) cudaEventDestroy(h.order_ev);
   if (h.own_stream) cudaStreamDestroy(h.own_stream);

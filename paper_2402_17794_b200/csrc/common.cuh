@@ -137,6 +137,10 @@ struct Handle {
   // Ozaki slices of the INT8 tensor-core passes (ozaki.cu): -1 = RSVD_OZAKI
   // environment variable, 0 = off (DMMA passes), 3..8 = slices per operand
   int ozaki_slices = -1;
+  // second stream of the INT8 dual pass: the next row panel's exponent scan
+  // and slicing (HBM-bound) run beside the current panel's GEMMs (tensor-bound)
+  cudaStream_t oz_stream = nullptr;
+  cudaEvent_t oz_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // entry, sliced[2], free[2]
   // Robust mode: data-dependent branch decisions (CholeskyQR's pass count
   // after a shifted Cholesky) read the device flag on the host mid-call.
   // Off by default: those decisions are speculated without a host round trip

@@ -89,6 +89,16 @@ void* Arena::alloc_bytes(size_t bytes) {
     cudaError_t e = cudaMalloc(&c.p, c.cap);
     if (e != cudaSuccess) {
       cudaGetLastError();
+      // out of memory: give back the chunks this call has not touched (e.g. the
+      // previous call's merged high-water chunk, too small for this request)
+      for (size_t i = 0; i < chunks_.size();) {
+        if (chunks_[i].off == 0) {
+          cudaFree(chunks_[i].p);
+          chunks_.erase(chunks_.begin() + i);
+        } else {
+          ++i;
+        }
+      }
       c.cap = bytes;
       RSVD_CUDA(cudaMalloc(&c.p, c.cap));
     }
@@ -447,14 +457,20 @@ void op_apply(Handle& h, const Problem& P, const DMat& X, DMat Y) {
     return;
   }
   a_ready(h, P);
-  gemm_nn(h, P.A, X, Y);
+  if (ozaki_cache_decide(h, P.oz, P.A, X.cols, P.oz_passes))
+    ozaki_cached_gemm(h, P.oz, P.A, X, Y, false);
+  else
+    gemm_nn(h, P.A, X, Y);
   h.counters.apply++;
   h.counters.physical_passes++;
 }
 
 void op_adjoint(Handle& h, const Problem& P, const DMat& Y, DMat Z) {
   a_ready(h, P);
-  gemm_tn(h, P.A, Y, Z);
+  if (P.panels.empty() && ozaki_cache_decide(h, P.oz, P.A, Y.cols, P.oz_passes))
+    ozaki_cached_gemm(h, P.oz, P.A, Y, Z, true);
+  else
+    gemm_tn(h, P.A, Y, Z);
   if (P.dist) allreduce_mat(h, Z);
   h.counters.adjoint++;
   h.counters.physical_passes++;
@@ -617,6 +633,7 @@ void range_basis_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, 
   if (mode < 0 || mode > 2) throw_param("unknown range mode");
   check_sketch_shape(P, k, p, q);
   const int64_t n = P.A.cols, ml = P.A.rows, l = k + p;
+  if (P.oz_passes == 0) P.oz_passes = 2 * q + 1;
   DMat Omega = h.ws.mat(n, l);
   gaussian_dev(h, n, l, rng, Omega);
   DMat Y = h.ws.mat(ml, l);
@@ -676,6 +693,7 @@ void rsvd_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, int mod
   const int64_t n = P.A.cols, ml = P.A.rows, l = k + p;
   check_sketch_shape(P, k, p, mode == RSVD_MODE_BASIC ? 0 : q);
   DMat Q = h.ws.mat(ml, l);
+  P.oz_passes = 2 * (mode == RSVD_MODE_BASIC ? 0 : q) + 2;  // the range finder's and Stage 2's
   range_basis_impl(h, P, k, p, q, mode, rng, Q);
   // Stage 2 (factor.hpp:14-16): B = Q^T A is formed transposed, Z = A^T Q.
   DMat Z = h.ws.mat(n, l);

@@ -3,6 +3,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ozaki.cuh"
 #include "rng.cuh"
 
 namespace rsvdb {
@@ -20,6 +21,11 @@ struct Problem {
     cudaEvent_t ready;
   };
   std::vector<Panel> panels;
+  // Range-finder passes on the INT8 tensor cores (ozaki.cu): A's slices, built
+  // by the first pass of a call and reused by the others; `oz_passes` is the
+  // number of products with A the calling algorithm will make (0 = unknown).
+  mutable OzCache oz;
+  mutable int oz_passes = 0;
 };
 
 Problem make_problem(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda);

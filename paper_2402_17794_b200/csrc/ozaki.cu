@@ -664,15 +664,22 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
 
 // Rows of A sliced at a time: int32 accumulation bounds the adjoint's
 // contraction length (kMaxK); `copies` layouts of the sub-panel's slices
-// (S K bytes per row each) must fit in ~9 GB and in what the device has left.
+// (S K bytes per row each) must fit in what the device has left.
 int64_t sub_rows(Handle& h, int64_t K, int S, int copies) {
   size_t free_b = 0, total_b = 0;
   RSVD_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double budget = std::min(18.0e9, 0.8 * (double(free_b) + double(h.ws.remaining())));
+  const double budget = std::min(40.0e9, 0.8 * (double(free_b) + double(h.ws.remaining())));
   int64_t sub = kMaxK;
   while (sub > 1024 && double(sub) * double(K) * S * copies > budget) sub /= 2;
   return sub;
 }
+
+struct StreamSwap {  // launches of this scope go to `s`
+  Handle& h;
+  cudaStream_t old;
+  StreamSwap(Handle& hh, cudaStream_t s) : h(hh), old(hh.stream) { h.stream = s; }
+  ~StreamSwap() { h.stream = old; }
+};
 
 }  // namespace
 
@@ -702,22 +709,37 @@ namespace {
 void ensure_state(Handle& h, OzakiState* st, int64_t rows_total, int64_t K, int64_t L, int S,
                   bool need_x, bool need_p) {
   if (st->have) return;
-  st->cap = std::min<int64_t>(sub_rows(h, K, S, (need_x ? 1 : 0) + (need_p ? 1 : 0)),
-                              round_up(std::max<int64_t>(rows_total, 1), 128));
-  st->e_a = static_cast<int*>(h.ws.alloc_bytes(size_t(st->cap) * 4));
+  const int layouts = (need_x ? 1 : 0) + (need_p ? 1 : 0);
+  const int64_t want = round_up(std::max<int64_t>(rows_total, 1), 128);
+  st->cap = std::min<int64_t>(sub_rows(h, K, S, layouts), want);
+  // a second set of panel buffers when it costs no panel size and there is a
+  // next panel to slice ahead (the virtual communicator's ranks share a stream)
+  st->nbuf = 1;
+  if (need_x && need_p && !h.vcomm && rows_total > st->cap &&
+      std::min<int64_t>(sub_rows(h, K, S, 2 * layouts), want) == st->cap) {
+    static const bool off = [] { const char* e = std::getenv("RSVD_OZ_OVERLAP"); return e && e[0] == '0'; }();
+    if (!off) st->nbuf = 2;
+  }
+  for (int b = 0; b < st->nbuf; ++b) {
+    st->e_a[b] = static_cast<int*>(h.ws.alloc_bytes(size_t(st->cap) * 4));
+    if (need_x) st->as[b] = alloc_plain(h, st->cap, K, S);
+    if (need_p) st->asi[b] = alloc_inter(h, st->cap, K);
+  }
   if (need_x) {
-    st->as = alloc_plain(h, st->cap, K, S);
     st->xs = alloc_inter(h, K, L);
     st->e_x = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
   }
   if (need_p) {
-    st->asi = alloc_inter(h, st->cap, K);
     st->ps = alloc_inter(h, st->cap, L);
     st->e_p = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
   }
   const int64_t sd = std::max(need_x ? scratch_doubles(st->cap, L, S) : 0,
                               need_p ? scratch_doubles(K, L, S) : 0);
   if (sd) st->scratch = h.ws.alloc(sd);
+  if (st->nbuf == 2 && !h.oz_stream) {
+    RSVD_CUDA(cudaStreamCreateWithFlags(&h.oz_stream, cudaStreamNonBlocking));
+    for (auto& e : h.oz_ev) RSVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   st->have = true;
 }
 }  // namespace
@@ -739,23 +761,49 @@ void ozaki_dual_pass(Handle& h, const DMat& A, const DMat& Oc, const DMat& Psi, 
     launch_slice(h, Oc, nullptr, nullptr, st->e_x, none, view_inter(st->xs, K, L), S);
   }
   const Sliced xs = view_inter(st->xs, K, L);
+  cudaEvent_t* ev_sliced = h.oz_ev + 1;
+  cudaEvent_t* ev_free = h.oz_ev + 3;
+  const bool two = st->nbuf == 2;
+  if (two) RSVD_CUDA(cudaEventRecord(h.oz_ev[0], h.stream));  // this panel's rows are resident
+  // exponent scan + slicing of rows [r0, r1): one read of the panel writes both
+  // operand layouts of its slices.  With two buffer sets it runs on the second
+  // stream, beside the previous sub-panel's GEMMs.
+  auto slice_sub = [&](int64_t r0) {
+    const int64_t rows = std::min(row_end, r0 + st->cap) - r0;
+    const int b = int(st->count % st->nbuf);
+    const DMat Ap(A.p + r0, rows, K, A.ld);
+    const Sliced as = view_plain(st->as[b], rows, K), asi = view_inter(st->asi[b], rows, K);
+    if (two) {
+      StreamSwap sw(h, h.oz_stream);
+      RSVD_CUDA(cudaStreamWaitEvent(h.oz_stream, h.oz_ev[0], 0));
+      if (st->count >= 2) RSVD_CUDA(cudaStreamWaitEvent(h.oz_stream, ev_free[b], 0));
+      row_exponents(h, Ap, st->e_a[b]);
+      launch_slice(h, Ap, st->e_a[b], nullptr, nullptr, as, asi, S);
+      RSVD_CUDA(cudaEventRecord(ev_sliced[b], h.oz_stream));
+    } else {
+      row_exponents(h, Ap, st->e_a[b]);
+      launch_slice(h, Ap, st->e_a[b], nullptr, nullptr, as, asi, S);
+    }
+    st->count++;
+  };
+  slice_sub(row0);
   for (int64_t r0 = row0; r0 < row_end; r0 += st->cap) {
     const int64_t r1 = std::min(row_end, r0 + st->cap), rows = r1 - r0;
-    const DMat Ap(A.p + r0, rows, K, A.ld);
-    row_exponents(h, Ap, st->e_a);
-    // one read of the panel writes both operand layouts of its slices
-    const Sliced as = view_plain(st->as, rows, K), asi = view_inter(st->asi, rows, K);
-    launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, asi, S);
+    const int b = int((st->count - 1) % st->nbuf);  // the set slice_sub(r0) filled
+    if (two) RSVD_CUDA(cudaStreamWaitEvent(h.stream, ev_sliced[b], 0));
+    if (r1 < row_end) slice_sub(r1);  // ahead of this sub-panel's GEMMs
+    const Sliced as = view_plain(st->as[b], rows, K), asi = view_inter(st->asi[b], rows, K);
     // Y[r0:r1, :] = A_p Omega_c
-    launch_gemm(h, true, as, xs, rows, L, K, S, DMat(Y.p + r0, rows, L, Y.ld), st->e_a, st->e_x,
+    launch_gemm(h, true, as, xs, rows, L, K, S, DMat(Y.p + r0, rows, L, Y.ld), st->e_a[b], st->e_x,
                 false, st->scratch);
     // W (+)= A_p^T Psi_p, with Psi_p' = diag(2^eA) Psi_p so A's row scales cancel
     const DMat Pp(Psi.p + r0, rows, L, Psi.ld);
-    col_exponents(h, Pp, st->e_a, st->e_p);
+    col_exponents(h, Pp, st->e_a[b], st->e_p);
     const Sliced ps = view_inter(st->ps, rows, L);
-    launch_slice(h, Pp, nullptr, st->e_a, st->e_p, none, ps, S);
+    launch_slice(h, Pp, nullptr, st->e_a[b], st->e_p, none, ps, S);
     launch_gemm(h, false, asi, ps, K, L, rows, S, W, nullptr, st->e_p, !(first && r0 == row0),
                 st->scratch);
+    if (two) RSVD_CUDA(cudaEventRecord(ev_free[b], h.stream));
   }
   prof.end();
 }
@@ -777,20 +825,100 @@ void ozaki_gemm(Handle& h, const DMat& A, const DMat& X, DMat C, bool trans, int
   for (int64_t r0 = 0; r0 < A.rows; r0 += st->cap) {
     const int64_t rows = std::min<int64_t>(st->cap, A.rows - r0);
     const DMat Ap(A.p + r0, rows, K, A.ld);
-    row_exponents(h, Ap, st->e_a);
+    row_exponents(h, Ap, st->e_a[0]);
     if (!trans) {
-      const Sliced as = view_plain(st->as, rows, K);
-      launch_slice(h, Ap, st->e_a, nullptr, nullptr, as, none, S);
+      const Sliced as = view_plain(st->as[0], rows, K);
+      launch_slice(h, Ap, st->e_a[0], nullptr, nullptr, as, none, S);
       launch_gemm(h, true, as, view_inter(st->xs, K, L), rows, L, K, S,
-                  DMat(C.p + r0, rows, L, C.ld), st->e_a, st->e_x, false, st->scratch);
+                  DMat(C.p + r0, rows, L, C.ld), st->e_a[0], st->e_x, false, st->scratch);
     } else {
-      const Sliced asi = view_inter(st->asi, rows, K);
-      launch_slice(h, Ap, st->e_a, nullptr, nullptr, none, asi, S);
+      const Sliced asi = view_inter(st->asi[0], rows, K);
+      launch_slice(h, Ap, st->e_a[0], nullptr, nullptr, none, asi, S);
       const DMat Xp(X.p + r0, rows, L, X.ld);
-      col_exponents(h, Xp, st->e_a, st->e_p);
+      col_exponents(h, Xp, st->e_a[0], st->e_p);
       const Sliced ps = view_inter(st->ps, rows, L);
-      launch_slice(h, Xp, nullptr, st->e_a, st->e_p, none, ps, S);
+      launch_slice(h, Xp, nullptr, st->e_a[0], st->e_p, none, ps, S);
       launch_gemm(h, false, asi, ps, K, L, rows, S, C, nullptr, st->e_p, r0 > 0, st->scratch);
+    }
+  }
+}
+
+bool ozaki_cache_decide(Handle& h, OzCache& c, const DMat& A, int64_t L, int passes) {
+  if (c.decided) return c.on;
+  c.decided = true;
+  c.on = false;
+  int S = ozaki_slices(h);
+  if (S == 0 || A.rows < 1 || A.cols < 1) return false;
+  if (S < 0) {
+    if (!(L >= 96 && passes >= 3 && double(A.rows) * double(A.cols) >= double(int64_t(1) << 26)))
+      return false;
+    S = 8;
+  }
+  const int64_t K = A.cols;
+  const int64_t cap = std::min<int64_t>(kMaxK, round_up(A.rows, 128));
+  const int64_t nsub = ceil_div(A.rows, cap);
+  const double need = double(nsub) * (double(S) * double(K) * double(ld_plain(cap)) +
+                                      double(K) * double(ld_inter(cap))) + 64.0e6;
+  size_t free_b = 0, total_b = 0;
+  RSVD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (need > 0.8 * (double(free_b) + double(h.ws.remaining()))) return false;
+  c.S = S;
+  c.cap = cap;
+  c.nsub = nsub;
+  c.on = true;
+  return true;
+}
+
+void ozaki_cached_gemm(Handle& h, OzCache& c, const DMat& A, const DMat& X, DMat C, bool trans) {
+  const int64_t K = A.cols, L = X.cols;
+  const int S = c.S;
+  if (!trans ? (X.rows != A.cols || C.rows != A.rows || C.cols != L)
+             : (X.rows != A.rows || C.rows != A.cols || C.cols != L))
+    throw_dim("ozaki_cached_gemm: shape mismatch");
+  const Sliced none;
+  const size_t plane_p = size_t(S) * size_t(K) * size_t(ld_plain(c.cap));
+  const size_t plane_i = size_t(K) * size_t(ld_inter(c.cap));
+  if (!c.built) {
+    // one read of A (exponent scan + slicing per sub-panel) for all the passes of the call
+    c.as = alloc_aligned(h, plane_p * size_t(c.nsub));
+    c.asi = alloc_aligned(h, plane_i * size_t(c.nsub));
+    c.e_a = static_cast<int*>(h.ws.alloc_bytes(size_t(A.rows) * 4));
+    for (int64_t s = 0; s < c.nsub; ++s) {
+      const int64_t r0 = s * c.cap, rows = std::min(c.cap, A.rows - r0);
+      const DMat Ap(A.p + r0, rows, K, A.ld);
+      row_exponents(h, Ap, c.e_a + r0);
+      launch_slice(h, Ap, c.e_a + r0, nullptr, nullptr, view_plain(c.as + plane_p * size_t(s), rows, K),
+                   view_inter(c.asi + plane_i * size_t(s), rows, K), S);
+    }
+    c.built = true;
+  }
+  if (L > c.Lcap) {
+    c.xs = alloc_inter(h, K, L);
+    c.ps = alloc_inter(h, c.cap, L);
+    c.e_x = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
+    c.e_p = static_cast<int*>(h.ws.alloc_bytes(size_t(L) * 4));
+    const int64_t sd = std::max(scratch_doubles(c.cap, L, S), scratch_doubles(K, L, S));
+    c.scratch = sd ? h.ws.alloc(sd) : nullptr;
+    c.Lcap = L;
+  }
+  if (!trans) {
+    col_exponents(h, X, nullptr, c.e_x);
+    const Sliced xs = view_inter(c.xs, K, L);
+    launch_slice(h, X, nullptr, nullptr, c.e_x, none, xs, S);
+    for (int64_t s = 0; s < c.nsub; ++s) {
+      const int64_t r0 = s * c.cap, rows = std::min(c.cap, A.rows - r0);
+      launch_gemm(h, true, view_plain(c.as + plane_p * size_t(s), rows, K), xs, rows, L, K, S,
+                  DMat(C.p + r0, rows, L, C.ld), c.e_a + r0, c.e_x, false, c.scratch);
+    }
+  } else {
+    for (int64_t s = 0; s < c.nsub; ++s) {
+      const int64_t r0 = s * c.cap, rows = std::min(c.cap, A.rows - r0);
+      const DMat Xp(X.p + r0, rows, L, X.ld);
+      col_exponents(h, Xp, c.e_a + r0, c.e_p);
+      const Sliced ps = view_inter(c.ps, rows, L);
+      launch_slice(h, Xp, nullptr, c.e_a + r0, c.e_p, none, ps, S);
+      launch_gemm(h, false, view_inter(c.asi + plane_i * size_t(s), rows, K), ps, K, L, rows, S, C,
+                  nullptr, c.e_p, s > 0, c.scratch);
     }
   }
 }

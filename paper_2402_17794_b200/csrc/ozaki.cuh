@@ -21,9 +21,14 @@ struct OzakiState {
   int64_t cap = 0;            // sub-panel rows the buffers hold
   unsigned char* xs = nullptr;   // the K-long skinny operand's slices (Omega_c), interleaved
   int* e_x = nullptr;
-  unsigned char* as = nullptr;   // A sub-panel slices, plain [s][K][rows] (apply operand)
-  unsigned char* asi = nullptr;  // the same slices interleaved [K][rows/32][s][32] (adjoint operand)
-  int* e_a = nullptr;
+  // A sub-panel slices: plain [s][K][rows] (apply operand) and interleaved
+  // [K][rows/32][s][32] (adjoint operand), with the rows' exponents; two sets
+  // when the next sub-panel is sliced beside the current one's GEMMs
+  int nbuf = 1;
+  int64_t count = 0;             // sub-panels sliced so far (buffer = count % nbuf)
+  unsigned char* as[2] = {nullptr, nullptr};
+  unsigned char* asi[2] = {nullptr, nullptr};
+  int* e_a[2] = {nullptr, nullptr};
   unsigned char* ps = nullptr;   // the row-long skinny operand's slices (Psi'), interleaved
   int* e_p = nullptr;
   double* scratch = nullptr;
@@ -36,4 +41,28 @@ void ozaki_dual_pass(Handle& h, const DMat& A, const DMat& Oc, const DMat& Psi, 
                      int64_t row0, int64_t row_end, OzakiState* state, bool first, int slices);
 // C = A X (trans = 0; A m x n, X n x l) or C = A^T X (trans = 1; X m x l).
 void ozaki_gemm(Handle& h, const DMat& A, const DMat& X, DMat C, bool trans, int slices);
+
+// The range finder's passes (Algs 2-4: Y = A X, Z = A^T Y, repeated 2q+2 times
+// over the SAME A) on the INT8 tensor cores: A's slices, in both operand
+// layouts, are built once per call and cached here (device pointers into the
+// handle's workspace; the Problem of the call owns the struct).
+struct OzCache {
+  bool decided = false, on = false, built = false;
+  int S = 0;
+  int64_t cap = 0, nsub = 0, Lcap = 0;  // sub-panel rows, count; columns xs / ps hold
+  unsigned char* as = nullptr;   // per sub-panel: plain slices
+  unsigned char* asi = nullptr;  // per sub-panel: interleaved slices
+  int* e_a = nullptr;            // exponents of all rows
+  unsigned char* xs = nullptr;
+  unsigned char* ps = nullptr;
+  int* e_x = nullptr;
+  int* e_p = nullptr;
+  double* scratch = nullptr;
+};
+// Decide once per call whether its passes over A (rows x K, sketch width L,
+// `passes` products expected) run on the INT8 path: the explicit setting,
+// else 8 slices when L >= 96, A has >= 2^26 entries, passes >= 3 (the slicing
+// pass is amortized) and both layouts of A's slices fit in device memory.
+bool ozaki_cache_decide(Handle& h, OzCache& c, const DMat& A, int64_t L, int passes);
+void ozaki_cached_gemm(Handle& h, OzCache& c, const DMat& A, const DMat& X, DMat C, bool trans);
 }  // namespace rsvdb

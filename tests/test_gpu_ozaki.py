@@ -129,6 +129,27 @@ def test_spsvd_on_int8_tensor_cores_matches_oracle(oz, orc, slices):
     assert np.max(np.abs(np.asarray(fh.sigma)[:k] - so[:k]) / so[:k]) < 1e-10
 
 
+@pytest.mark.parametrize("mode,q", [("basic", 0), ("power", 1), ("power_ortho", 2)])
+def test_rsvd_passes_on_int8_tensor_cores_match_oracle(oz, orc, mode, q):
+    """Algs 2-4 with every product A X / A^T Y on the sliced INT8 path (A's
+    slices built once per call and reused by the 2q + 2 passes)."""
+    rs = np.random.default_rng(21)
+    m, n, k, p = 3000, 2000, 30, 10
+    u, _ = np.linalg.qr(rs.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rs.standard_normal((n, n)))
+    a = np.asfortranarray((u * np.exp(-np.arange(n) / 20.0)) @ v.T)
+    oz.set_ozaki_slices(8)
+    f = oz.rsvd(_t(a), oz.SketchConfig(k, p, q, oz.RangeMode[mode], 5))
+    uo, so, vo = orc.rsvd(a, k, p, q, {"basic": 0, "power": 1, "power_ortho": 2}[mode], orc.Rng(5))
+    sg = f.sigma.cpu().numpy()
+    assert np.max(np.abs(sg[:k] - so[:k]) / so[:k]) < 1e-10
+    for g, o in ((f.U.cpu().numpy(), uo), (f.V.cpu().numpy(), vo)):
+        s = np.linalg.svd(g[:, :k] - o[:, :k] @ (o[:, :k].T @ g[:, :k]), compute_uv=False)[0]
+        assert np.arcsin(min(1.0, s)) < 1e-8
+    c = oz.default_engine().counters()
+    assert c["kernel_launches"] > 0
+
+
 def test_set_ozaki_slices_rejects_bad_values(oz):
     with pytest.raises(oz.ParameterError):
         oz.set_ozaki_slices(2)
