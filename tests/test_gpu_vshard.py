@@ -97,6 +97,43 @@ def test_sharded_spsvd_matches_oracle(eng, orc, vcomms, nranks):
     assert sin_max(v[:, :k], vo[:, :k]) < ANG_TOL
 
 
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_int8_passes_match_oracle(eng, orc, vcomms, nranks):
+    """The INT8 tensor-core passes (csrc/ozaki.cu) on row shards: every rank
+    slices its own rows (row exponents are local, Psi's local rows carry
+    them), the partial W / Z are allreduced as on the DMMA path.  Alg 6 and
+    Alg 4 against the oracle, replicated outputs bitwise equal on all ranks."""
+    a = haar_matrix(1500, 700, np.exp(-np.arange(200) / 30.0), 8)
+    k, p = 30, 10
+    shards = _shards(a, nranks)
+
+    def run6(r, e):
+        eng.set_ozaki_slices(8, e)
+        try:
+            f = eng.spsvd_general(shards[r], k, p, eng.Rng(5))
+        finally:
+            eng.set_ozaki_slices(-1, e)
+        return f.U.cpu().numpy(), f.sigma.cpu().numpy(), f.V.cpu().numpy()
+    u, s, v = _assemble(vcomms(nranks).run(run6))
+    uo, so, vo = orc.spsvd_general(a, k, p, orc.Rng(5))
+    assert np.max(np.abs(s[:k] - so[:k]) / so[:k]) < SIG_TOL
+    assert sin_max(u[:, :k], uo[:, :k]) < ANG_TOL
+    assert sin_max(v[:, :k], vo[:, :k]) < ANG_TOL
+
+    def run4(r, e):
+        eng.set_ozaki_slices(8, e)
+        try:
+            f = eng.rsvd(shards[r], eng.SketchConfig(k, p, 2, eng.RangeMode(2), 1))
+        finally:
+            eng.set_ozaki_slices(-1, e)
+        return f.U.cpu().numpy(), f.sigma.cpu().numpy(), f.V.cpu().numpy()
+    u, s, v = _assemble(vcomms(nranks).run(run4))
+    uo, so, vo = orc.rsvd(a, k, p, 2, 2, orc.Rng(1))
+    assert np.max(np.abs(s[:k] - so[:k]) / so[:k]) < SIG_TOL
+    assert sin_max(u[:, :k], uo[:, :k]) < ANG_TOL
+    assert sin_max(v[:, :k], vo[:, :k]) < ANG_TOL
+
+
 def _sym(n, seed):
     rs = np.random.default_rng(seed)
     uq, _ = np.linalg.qr(rs.standard_normal((n, n)))
