@@ -448,6 +448,242 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------- CTA-pair variant
+// Two CTAs of a cluster (one TPC) run the MMAs as one `cta_group::2`
+// instruction of M = 256: each CTA holds its own 128 rows of A and HALF of the
+// B tile (64 of the pair's 128 output columns), so a CTA reads 6 KB of
+// operands per MMA instead of 7.5 KB for 112 columns -- the single-CTA kernel
+// above is bound by shared-memory bandwidth (78 cycles per MMA against the
+// tensor pipe's 60).  The leader CTA (cluster rank 0) issues the MMAs and owns
+// the full / accumulator-empty barriers; both CTAs' TMA loads signal the
+// leader's full barrier, the leader's commits are multicast to both CTAs'
+// empty / accumulator-full barriers; each CTA's epilogue drains its own TMEM.
+constexpr int kStages2 = 4;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;     // shared::cluster address of the same offset in CTA 0
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma2_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(ptx::smem_u32(dst)),
+      "l"(map), "r"(ptx::smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(ptx::smem_u32(dst)),
+      "l"(map), "r"(ptx::smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive (once all earlier MMAs are done) on the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(ptx::smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                   ptx::smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+
+template <int AMN, int S>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    ozaki_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmB, OzParams p) {
+  RSVD_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = smraw + ((1024 - (ptx::smem_u32(smraw) & 1023)) & 1023);
+  __shared__ uint64_t bar_full[kStages2], bar_empty[kStages2], bar_acc_full, bar_acc_empty;
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = int(cluster_ctarank());
+  const int pair = blockIdx.x >> 1;
+  const int nt = pair % p.n_tiles, mt = 2 * (pair / p.n_tiles) + rank;
+  const int NT = p.ntile;                 // output columns per pair: 64, 96 or 128
+  const int bhalf4 = (NT / 2) * 128;      // this CTA's half of four B slices of one K step
+  const int stage_bytes = kARegion + 2 * bhalf4;
+  const int m0 = mt * kBM, n0 = nt * NT;
+  const int nk = (p.K + kKS - 1) / kKS;
+  constexpr int ngroups = (S + 3) / 4;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages2; ++s) {
+      ptx::mbar_init(&bar_full[s], 1);
+      ptx::mbar_init(&bar_empty[s], 1);
+    }
+    ptx::mbar_init(&bar_acc_full, 1);
+    ptx::mbar_init(&bar_acc_empty, 256);  // both CTAs' epilogue threads (leader's copy is used)
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     ptx::smem_u32(&tmem_base_sh)),
+                 "r"(512u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tb = tmem_base_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------- TMA producer (both CTAs)
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tmA);
+      ptx::prefetch_tmap(&tmB);
+      int it = 0;
+      for (int g = 0; g < ngroups; ++g) {
+        const int Sg = S - 4 * g;
+        const int nhalf = (Sg + 3) >> 2;
+        const uint32_t bytes = uint32_t(AMN ? Sg * kATile : nhalf * 4 * kATile) + uint32_t(nhalf * bhalf4);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % kStages2;
+          const uint32_t ph = (it / kStages2) & 1;
+          ptx::mbar_wait(&bar_empty[st], ph ^ 1);
+          if (rank == 0) ptx::mbar_expect_tx(&bar_full[st], 2 * bytes);  // both CTAs' loads land here
+          uint8_t* base = sm + st * stage_bytes;
+          const int kc = p.k0 + kb * kKS;
+          const int ki = (kc >> 5) * 256;
+          if (AMN) {
+            for (int s = 0; s < Sg; ++s) tma2_load_3d(base + s * kATile, &tmA, &bar_full[st], m0, kc, s);
+          } else {
+            for (int hf = 0; hf < nhalf; ++hf)
+              tma2_load_2d(base + hf * 4 * kATile, &tmA, &bar_full[st], ki + hf * 128, m0);
+          }
+          uint8_t* bb = base + kARegion;
+          for (int hf = 0; hf < nhalf; ++hf)
+            tma2_load_2d(bb + hf * bhalf4, &tmB, &bar_full[st], ki + hf * 128, n0 + rank * (NT / 2));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------- MMA issuer (leader CTA)
+    if (rank == 0) {
+      // M = 256 (the pair), N = NT
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(AMN) << 15) |
+                             (uint32_t(NT >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+      const uint64_t ad_fixed = smem_desc(0, AMN ? 4096 : 0, 1024, 2);
+      const uint64_t bd_fixed = smem_desc(0, 0, 1024, 2);
+      const uint32_t sm0 = ptx::smem_u32(sm);
+      int it = 0;
+      auto run_group = [&](auto sg_tag) {
+        constexpr int Sg = decltype(sg_tag)::value;
+        constexpr int c_hi = Sg + 1, c_lo = (c_hi - 3 > 2 ? c_hi - 3 : 2);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % kStages2;
+          const uint32_t ph = (it / kStages2) & 1;
+          ptx::mbar_wait(&bar_full[st], ph);
+          tc_fence_after();
+          const uint32_t a0 = (sm0 + st * stage_bytes) >> 4;
+          const uint32_t b0 = a0 + (kARegion >> 4);
+          const uint32_t kacc = kb > 0 ? 1u : 0u;
+          if (elect_one()) {
+#pragma unroll
+            for (int c = c_hi; c >= c_lo; --c) {
+              const int s_lo = (c - Sg > 1 ? c - Sg : 1), s_hi = (Sg < c - 1 ? Sg : c - 1);
+#pragma unroll
+              for (int s = 1; s <= Sg; ++s) {
+                if (s < s_lo || s > s_hi) continue;
+                const int t = c - s;
+                const uint32_t ao = AMN ? uint32_t((s - 1) * kATile)
+                                        : uint32_t(((s - 1) >> 2) * 4 * kATile + ((s - 1) & 3) * 32);
+                const uint32_t bo = uint32_t(((t - 1) >> 2) * bhalf4 + ((t - 1) & 3) * 32);
+                umma2_i8(tb + uint32_t((c - c_lo) * 128), ad_fixed | uint64_t(a0 + (ao >> 4)),
+                         bd_fixed | uint64_t(b0 + (bo >> 4)), idesc, s > s_lo ? 1u : kacc);
+              }
+            }
+          }
+          __syncwarp();
+          if (elect_one()) umma2_commit_both(&bar_empty[st]);
+        }
+        if (elect_one()) umma2_commit_both(&bar_acc_full);
+      };
+      run_group(std::integral_constant<int, S>{});
+      if constexpr (S > 4) {
+        ptx::mbar_wait(&bar_acc_empty, 0);
+        tc_fence_after();
+        run_group(std::integral_constant<int, (S > 4 ? S - 4 : 1)>{});
+      }
+    }
+  } else {
+    // ------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int64_t grow = int64_t(m0) + row;
+    const int re = (p.rexp && grow < p.M) ? p.rexp[grow] : 0;
+    double* scr = p.scratch ? p.scratch + int64_t(blockIdx.x) * kBM * NT : nullptr;
+    for (int g = 0; g < ngroups; ++g) {
+      const int Sg = S - 4 * g;
+      const int c_hi = Sg + 1, c_lo = max(2, c_hi - 3);
+      const bool last = g == ngroups - 1;
+      ptx::mbar_wait(&bar_acc_full, g & 1);
+      tc_fence_after();
+      for (int cc = 0; cc < NT; cc += 8) {
+        if (n0 + cc >= p.N) break;
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0.0;
+        for (int c = c_hi; c >= c_lo; --c) {  // smallest terms first
+          uint32_t r[8];
+          tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t((c - c_lo) * 128 + cc), r);
+          tmem_ld_wait();
+          const double sc = exp2i(-(7 * c - 2));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = fma(double(int(r[j])), sc, v[j]);
+        }
+        if (!last) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) scr[int64_t(cc + j) * kBM + row] = v[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int col = n0 + cc + j;
+            if (grow < p.M && col < p.N) {
+              double x = v[j];
+              if (ngroups > 1) x += scr[int64_t(cc + j) * kBM + row];
+              x = scale2(x, re + (p.cexp ? p.cexp[col] : 0));
+              double* dst = p.C + int64_t(col) * p.ldc + grow;
+              *dst = p.accumulate ? *dst + x : x;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_leader(&bar_acc_empty);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512u)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -585,7 +821,24 @@ void col_exponents(Handle& h, const DMat& X, const int* radd, int* e) {
   RSVD_LAUNCHED(h);
 }
 
+// CTA-pair kernel (cta_group::2, 128 output columns per pair) unless RSVD_OZ_CG2=0
+bool use_pair_kernel() {
+  static const bool on = [] {
+    const char* e = std::getenv("RSVD_OZ_CG2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 int pick_ntile(int64_t L) {
+  if (use_pair_kernel()) {
+    // cta_group::2 takes N in multiples of 32: the width that pads L least
+    static const int forced = [] { const char* e = std::getenv("RSVD_OZ_NT"); return e ? std::atoi(e) : 0; }();
+    if (forced == 64 || forced == 96 || forced == 128) return forced;
+    int best = 128;
+    for (int w : {96, 64})
+      if (round_up(L, w) < round_up(L, best)) best = w;
+    return best;
+  }
   const int64_t tiles = ceil_div(L, 128);
   return int(round_up(ceil_div(L, tiles), 16));
 }
@@ -593,7 +846,7 @@ int pick_ntile(int64_t L) {
 int64_t scratch_doubles(int64_t M, int64_t N, int S) {
   if (S <= 4) return 0;
   const int ntile = pick_ntile(N);
-  return ceil_div(M, kBM) * ceil_div(N, ntile) * kBM * ntile;
+  return round_up(ceil_div(M, kBM), 2) * ceil_div(N, ntile) * kBM * ntile;
 }
 
 // C (M x N) (+)= sliced A  x  sliced B over K entries.
@@ -608,13 +861,14 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
   if (K < 1) throw_dim("ozaki: empty contraction");
   const int ntile = pick_ntile(N);
   const int n_tiles = int(ceil_div(N, ntile));
-  const int64_t m_tiles = ceil_div(M, kBM);
+  const bool pair = use_pair_kernel();
+  const int64_t m_tiles = pair ? round_up(ceil_div(M, kBM), 2) : ceil_div(M, kBM);
   const int64_t grid = m_tiles * n_tiles;
-  const int stage_bytes = kARegion + 2 * ntile * 128;
-  const size_t smem = size_t(kStages) * stage_bytes + 1024;
+  const int stage_bytes = pair ? kARegion + ntile * 128 : kARegion + 2 * ntile * 128;
+  const size_t smem = size_t(pair ? kStages2 : kStages) * stage_bytes + 1024;
   const CUtensorMap ta = amn ? make_map_i8(As.p, As.inner, As.outer, As.ld, S, kBM, kKS, true)
                              : make_map_inter(As.p, As.ld, As.outer, As.ld, kBM);
-  const CUtensorMap tb = make_map_inter(Bs.p, Bs.ld, Bs.outer, Bs.ld, ntile);
+  const CUtensorMap tb = make_map_inter(Bs.p, Bs.ld, Bs.outer, Bs.ld, pair ? ntile / 2 : ntile);
   for (int64_t k0 = 0; k0 < K; k0 += kMaxK) {
     OzParams p;
     p.M = int(M);
@@ -638,7 +892,13 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
                    double(S) * double(p.K) * double(M + N) + 8.0 * double(M) * double(N));
 #define RSVD_OZ_CASE(SS)                                                             \
   case SS:                                                                           \
-    if (amn) {                                                                       \
+    if (pair && amn) {                                                               \
+      smem_attr(ozaki_gemm2_kernel<1, SS>, smem);                                    \
+      launch_k(h, ozaki_gemm2_kernel<1, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
+    } else if (pair) {                                                               \
+      smem_attr(ozaki_gemm2_kernel<0, SS>, smem);                                    \
+      launch_k(h, ozaki_gemm2_kernel<0, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
+    } else if (amn) {                                                                \
       smem_attr(ozaki_gemm_kernel<1, SS>, smem);                                     \
       launch_k(h, ozaki_gemm_kernel<1, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
     } else {                                                                         \
