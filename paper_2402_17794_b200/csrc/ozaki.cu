@@ -1110,8 +1110,10 @@ bool ozaki_cache_decide(Handle& h, OzCache& c, const DMat& A, int64_t L, int pas
   int S = ozaki_slices(h);
   if (S == 0 || A.rows < 1 || A.cols < 1) return false;
   if (S < 0) {
-    if (!(L >= 96 && passes >= 3 && double(A.rows) * double(A.cols) >= double(int64_t(1) << 26)))
-      return false;
+    // >= 3 products share one slicing pass from l = 96 up; a single product
+    // (Alg 5) pays for its own slicing from l ~ 160 up (break-even at l = 110)
+    const bool wide = passes >= 3 ? L >= 96 : (passes >= 1 && L >= 160);
+    if (!(wide && double(A.rows) * double(A.cols) >= double(int64_t(1) << 26))) return false;
     S = 8;
   }
   const int64_t K = A.cols;

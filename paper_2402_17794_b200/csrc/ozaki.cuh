@@ -61,8 +61,9 @@ struct OzCache {
 };
 // Decide once per call whether its passes over A (rows x K, sketch width L,
 // `passes` products expected) run on the INT8 path: the explicit setting,
-// else 8 slices when L >= 96, A has >= 2^26 entries, passes >= 3 (the slicing
-// pass is amortized) and both layouts of A's slices fit in device memory.
+// else 8 slices when A has >= 2^26 entries, both layouts of its slices fit in
+// device memory and the sketch is wide enough to amortize the slicing pass
+// (L >= 96 for passes >= 3, L >= 160 for a single product).
 bool ozaki_cache_decide(Handle& h, OzCache& c, const DMat& A, int64_t L, int passes);
 void ozaki_cached_gemm(Handle& h, OzCache& c, const DMat& A, const DMat& X, DMat C, bool trans);
 }  // namespace rsvdb
