@@ -38,6 +38,7 @@
 
 #include "pass.cuh"
 #include "ptx.cuh"
+#include "small.cuh"
 
 namespace rsvdb {
 
@@ -145,7 +146,7 @@ __global__ void fill_int_kernel(int* p, int n, int v) {
 // e[r] = max_c bexp(x[r,c]) - 1022 over this block's column range (|x| < 2^e)
 __global__ void __launch_bounds__(256)
     row_exp_kernel(const double* __restrict__ x, int64_t ld, int rows, int64_t cols, int cpb,
-                   int* __restrict__ e) {
+                   int* __restrict__ e, int* __restrict__ flags) {
   RSVD_PDL_ENTRY();
   const int r = blockIdx.x * 256 + threadIdx.x;
   if (r >= rows) return;
@@ -161,12 +162,15 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < 8; ++u) mx = max(mx, h[u] & 0x7ff00000);
   }
   for (; c < c1; ++c) mx = max(mx, __double2hiint(__ldg(p + c * ld)) & 0x7ff00000);
+  // Inf / NaN cannot be sliced: the call ends in NumericError, as when a
+  // non-finite entry reaches the FP64 pass's outputs
+  if (mx == 0x7ff00000) atomicOr(flags, kFlagNonFinite);
   atomicMax(&e[r], (mx >> 20) - 1022);
 }
 // e[c] = max_r (bexp(x[r,c]) - 1022 + radd[r]) over this block's row range
 __global__ void __launch_bounds__(256)
     col_exp_kernel(const double* __restrict__ x, int64_t ld, int rows, int rpb,
-                   const int* __restrict__ radd, int* __restrict__ e) {
+                   const int* __restrict__ radd, int* __restrict__ e, int* __restrict__ flags) {
   RSVD_PDL_ENTRY();
   const int c = blockIdx.x;
   const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
@@ -174,6 +178,7 @@ __global__ void __launch_bounds__(256)
   int mx = INT_MIN;
   for (int r = r0 + threadIdx.x; r < r1; r += 256) {
     const int b = ((__double2hiint(__ldg(p + r)) & 0x7ff00000) >> 20) - 1022;
+    if (b == 2047 - 1022) atomicOr(flags, kFlagNonFinite);
     mx = max(mx, b + (radd ? radd[r] : 0));
   }
 #pragma unroll
@@ -807,7 +812,7 @@ void row_exponents(Handle& h, const DMat& X, int* e) {
   const int cpb = int(ceil_div(X.cols, splits));
   splits = ceil_div(X.cols, cpb);
   launch_k(h, row_exp_kernel, dim3(unsigned(rb), unsigned(splits)), 256, 0, (const double*)X.p, X.ld,
-           int(X.rows), X.cols, cpb, e);
+           int(X.rows), X.cols, cpb, e, h.d_flags);
   RSVD_LAUNCHED(h);
 }
 
@@ -817,7 +822,7 @@ void col_exponents(Handle& h, const DMat& X, const int* radd, int* e) {
   if (X.rows == 0 || X.cols == 0) return;
   const int rpb = 8192;
   launch_k(h, col_exp_kernel, dim3(unsigned(X.cols), unsigned(ceil_div(X.rows, rpb))), 256, 0,
-           (const double*)X.p, X.ld, int(X.rows), rpb, radd, e);
+           (const double*)X.p, X.ld, int(X.rows), rpb, radd, e, h.d_flags);
   RSVD_LAUNCHED(h);
 }
 

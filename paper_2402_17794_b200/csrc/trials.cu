@@ -89,6 +89,9 @@ void range_basis_trials_impl(Handle& h, const Problem& P, int64_t k, int64_t p, 
   if (mode == RSVD_MODE_BASIC) q = 0;  // SketchConfig::normalized (rangefinder.hpp:37-41)
   check_trials(P, k, p, q, mode, T);
   const int64_t n = P.A.cols, ml = P.A.rows, l = k + p, L = T * l;
+  // the shared passes are T l columns wide: from ~100 columns up they run on
+  // the INT8 tensor cores with A's slices cached for the call (ozaki.cu)
+  if (P.oz_passes == 0) P.oz_passes = 2 * q + 1;
   DMat Om = h.ws.mat(n, L);
   gaussian_trials(h, n, l, seed_base, T, Om);
   DMat Y = h.ws.mat(ml, L);
@@ -123,6 +126,7 @@ void rsvd_trials_impl(Handle& h, const Problem& P, int64_t k, int64_t p, int q, 
                       uint64_t seed_base, int64_t T, DMat U, double* sigma, DMat V) {
   const int64_t n = P.A.cols, ml = P.A.rows, l = k + p, L = T * l;
   DMat Q = h.ws.mat(ml, L);
+  P.oz_passes = 2 * (mode == RSVD_MODE_BASIC ? 0 : q) + 2;
   range_basis_trials_impl(h, P, k, p, q, mode, seed_base, T, Q);
   DMat Z = h.ws.mat(n, L);
   op_adjoint(h, P, Q, Z);  // B_t^T = A^T Q_t for every trial: one pass

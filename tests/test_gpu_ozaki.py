@@ -150,6 +150,23 @@ def test_rsvd_passes_on_int8_tensor_cores_match_oracle(oz, orc, mode, q):
     assert c["kernel_launches"] > 0
 
 
+def test_non_finite_inputs_raise_numeric_error_on_int8_path(oz):
+    """Inf / NaN cannot be sliced; the exponent scans flag them and the call
+    ends in NumericError like the FP64 passes (core.hpp:36-39)."""
+    rs = np.random.default_rng(0)
+    a = rs.standard_normal((400, 300))
+    oz.set_ozaki_slices(8)
+    for bad in (np.nan, np.inf, -np.inf):
+        b = a.copy()
+        b[17, 23] = bad
+        with pytest.raises(oz.NumericError):
+            oz.rsvd(_t(b), oz.SketchConfig(5, 2, 1, oz.RangeMode.power, 1))
+        with pytest.raises(oz.NumericError):
+            oz.spsvd_general(_t(b), 5, 2, oz.Rng(1))
+    f = oz.spsvd_general(_t(a), 5, 2, oz.Rng(1))  # the engine stays usable
+    assert np.isfinite(f.sigma.cpu().numpy()).all()
+
+
 def test_set_ozaki_slices_rejects_bad_values(oz):
     with pytest.raises(oz.ParameterError):
         oz.set_ozaki_slices(2)
