@@ -268,6 +268,9 @@ rsvd_status rsvd_debug_dual_pass_dev(rsvd_handle* h, int64_t m, int64_t n, int64
  * FP64 DMMA pass), 3..8 = slices.  8 slices are below fp64's own rounding of
  * the product; 7 are 2^-49 of the row/column maxima. */
 rsvd_status rsvd_set_ozaki_slices(rsvd_handle* h, int slices);
+/* Which INT8 GEMM kernel runs (process-wide; unit tests): 1 = CTA pair
+ * (tcgen05 cta_group::2, the default), 0 = single CTA, -1 = default. */
+rsvd_status rsvd_debug_ozaki_kernel(int pair);
 /* C = A X (trans = 0: A m x n, X n x l, C m x l) or C = A^T X (trans = 1: X
  * m x l, C n x l) by the sliced INT8 product alone: for unit parity tests. */
 rsvd_status rsvd_debug_ozaki_gemm_dev(rsvd_handle* h, int trans, int64_t m, int64_t n,

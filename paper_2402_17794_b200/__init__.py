@@ -183,6 +183,8 @@ def _load():
         L.rsvd_debug_dual_pass_dev.restype = ctypes.c_int
         L.rsvd_set_ozaki_slices.argtypes = [P, I]
         L.rsvd_set_ozaki_slices.restype = ctypes.c_int
+        L.rsvd_debug_ozaki_kernel.argtypes = [I]
+        L.rsvd_debug_ozaki_kernel.restype = ctypes.c_int
         L.rsvd_debug_ozaki_gemm_dev.argtypes = [P, I, I64, I64, P, I64, I64, P, I64, P, I64, I]
         L.rsvd_debug_ozaki_gemm_dev.restype = ctypes.c_int
         L.rsvd_debug_log_window.argtypes = [ctypes.c_void_p, I64, ctypes.c_void_p, ctypes.c_void_p]
@@ -899,6 +901,12 @@ def set_ozaki_slices(slices: int, engine=None) -> None:
     slices, -1 = follow the RSVD_OZAKI environment variable."""
     e = engine or default_engine()
     _check(_load().rsvd_set_ozaki_slices(e.handle, int(slices)))
+
+
+def debug_ozaki_kernel(pair: int) -> None:
+    """Select the INT8 GEMM kernel process-wide: 1 = CTA pair (cta_group::2,
+    default), 0 = single CTA, -1 = default.  For unit tests."""
+    _check(_load().rsvd_debug_ozaki_kernel(int(pair)))
 
 
 def debug_ozaki_gemm(a, x, trans: bool = False, slices: int = 8):

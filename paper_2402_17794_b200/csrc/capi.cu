@@ -877,6 +877,11 @@ rsvd_status rsvd_set_ozaki_slices(rsvd_handle* hd, int slices) {
   });
 }
 
+rsvd_status rsvd_debug_ozaki_kernel(int pair) {
+  rsvdb::ozaki_force_pair_kernel(pair);
+  return RSVD_OK;
+}
+
 rsvd_status rsvd_debug_ozaki_gemm_dev(rsvd_handle* hd, int trans, int64_t m, int64_t n,
                                       const double* a, int64_t lda, int64_t l, const double* x,
                                       int64_t ldx, double* c, int64_t ldc, int slices) {

@@ -14,22 +14,28 @@
 // maxima: S = 8 is below fp64's own rounding of the product, S = 7 is 2^-49.
 //
 // Pipeline per row panel of A (<= 32768 rows, so int32 cannot overflow):
-//   row_exp -> slice (A read twice from HBM as fp64, slices written once)
-//   -> apply GEMM (Y rows of the panel) -> Psi' = 2^eA Psi sliced per column
-//   -> adjoint GEMM (W += A_panel^T Psi_panel) from the SAME slices of A
-// (MN-major UMMA operand for the apply, K-major for the adjoint).
+//   row_exp -> slice (A read twice from HBM as fp64, slices written once per
+//   operand layout) -> apply GEMM (Y rows of the panel) -> Psi' = 2^eA Psi
+//   sliced per column -> adjoint GEMM (W += A_panel^T Psi_panel) from the SAME
+//   slices of A (MN-major UMMA operand for the apply, K-major for the adjoint).
+// The range finder's 2q+2 products of one call share one slicing of A
+// (OzCache).
 //
-// GEMM kernel: one CTA per 128 x ntile output tile; warp 0 = TMA producer
-// (3-D maps over [slice][col][row] int8), warp 1 = MMA issuer + TMEM owner,
-// warps 2-5 = epilogue (TMEM -> fp64).  A 3-stage ring of K = 32 steps; each
+// GEMM kernels: warp 0 = TMA producer, warp 1 = MMA issuer + TMEM owner,
+// warps 2-5 = epilogue (TMEM -> fp64).  An mbarrier ring of K = 32 steps; each
 // step holds every needed slice tile of both operands; the diagonals c are
-// accumulated four at a time (4 x ntile TMEM columns), high c first.
+// accumulated four at a time (4 x 128 TMEM columns), high c first.
+//   ozaki_gemm2_kernel: a CTA pair per 256 x {64,96,128} output tile, one
+//                       tcgen05.mma.cta_group::2 per slice product (default)
+//   ozaki_gemm_kernel : one CTA per 128 x ntile tile (RSVD_OZ_CG2=0)
+// DESIGN.md section 3c has the measurements behind each choice.
 #include "ozaki.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdio>
 #include <cstring>
@@ -827,7 +833,10 @@ void col_exponents(Handle& h, const DMat& X, const int* radd, int* e) {
 }
 
 // CTA-pair kernel (cta_group::2, 128 output columns per pair) unless RSVD_OZ_CG2=0
+std::atomic<int> g_pair_kernel{-1};  // -1 = RSVD_OZ_CG2 (default on), 0 / 1 = forced (tests)
 bool use_pair_kernel() {
+  const int f = g_pair_kernel.load(std::memory_order_relaxed);
+  if (f >= 0) return f != 0;
   static const bool on = [] {
     const char* e = std::getenv("RSVD_OZ_CG2");
     return !(e && e[0] == '0');
@@ -947,6 +956,8 @@ struct StreamSwap {  // launches of this scope go to `s`
 };
 
 }  // namespace
+
+void ozaki_force_pair_kernel(int pair) { g_pair_kernel.store(pair < 0 ? -1 : (pair ? 1 : 0)); }
 
 int ozaki_slices(const Handle& h) {
   if (h.ozaki_slices >= 0) return h.ozaki_slices;

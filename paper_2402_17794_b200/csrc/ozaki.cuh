@@ -10,6 +10,9 @@ namespace rsvdb {
 // Slices per operand: rsvd_set_ozaki_slices, else the RSVD_OZAKI environment
 // variable (0 = the DMMA passes, 3..8 = slices), else -1 = automatic.
 int ozaki_slices(const Handle& h);
+// Which GEMM kernel runs: 1 = the CTA-pair kernel (cta_group::2), 0 = the
+// single-CTA kernel, -1 = RSVD_OZ_CG2 / default (pair).  Process-wide; tests.
+void ozaki_force_pair_kernel(int pair);
 // The dual pass's choice for an A of rows x K and l = L sketch columns: the
 // explicit setting, else 8 slices for wide sketches of large matrices, else 0.
 int ozaki_slices_auto(const Handle& h, int64_t rows, int64_t K, int64_t L);

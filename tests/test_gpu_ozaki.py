@@ -33,10 +33,18 @@ def _bound(a, x, trans, s):
     return rel * sc + 1e-300
 
 
+@pytest.fixture(params=[1, 0], ids=["pair", "single"])
+def kernel(eng, request):
+    """Both GEMM kernels: the CTA pair (cta_group::2, default) and the single CTA."""
+    eng.debug_ozaki_kernel(request.param)
+    yield request.param
+    eng.debug_ozaki_kernel(-1)
+
+
 @pytest.mark.parametrize("m,n,l", [(300, 200, 25), (1000, 777, 110), (257, 4099, 220), (4100, 130, 30),
                                    (128, 32, 16), (1, 1, 1), (5, 3, 2), (129, 31, 113), (700, 1300, 550)])
 @pytest.mark.parametrize("trans", [False, True])
-def test_gemm_matches_longdouble_product(eng, m, n, l, trans):
+def test_gemm_matches_longdouble_product(eng, kernel, m, n, l, trans):
     rs = np.random.default_rng(m + 3 * n + l)
     a = rs.standard_normal((m, n)) * np.exp(rs.uniform(-3, 3, (m, 1)))
     x = rs.standard_normal((m if trans else n, l))
