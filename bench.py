@@ -204,7 +204,7 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference arm
-def cpu_reference(cfg, steps, warmup, threads, a_host=None):
+def cpu_reference(cfg, steps, warmup, threads, a_host=None, budget_s=None):
     """The reference's algorithm on the host CPU: oracle/rsvd_oracle.cpp, a
     C++ restatement of the reference (which cannot be compiled here: Eigen is
     absent) over libstdc++'s mt19937_64 + scipy's OpenBLAS LAPACK."""
@@ -223,10 +223,18 @@ def cpu_reference(cfg, steps, warmup, threads, a_host=None):
         return oracle.rsvd(a_host, cfg["k"], cfg["p"], cfg["q"], mode, oracle.Rng(SEED_OMEGA))
     for _ in range(warmup):
         run()
+    # bounded sample: at most `steps` factorizations and (after the first) at
+    # most `budget_s` seconds, so the multi-GB configurations (C5: ~28 s per
+    # factorization on 16 cores) end within a few minutes
     t0 = time.perf_counter()
-    for _ in range(steps):
+    done = 0
+    while done < max(steps, 1):
         run()
-    dt = (time.perf_counter() - t0) / max(steps, 1)
+        done += 1
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    dt = (time.perf_counter() - t0) / done
+    cpu_reference.last_count = done
     return dt
 
 
@@ -277,7 +285,10 @@ def run_reference_arm(args, cfg):
         return 0
     threads = os.cpu_count() or 1
     steps = args.steps
-    dt = cpu_reference(cfg, steps, min(args.warmup, 1), threads)
+    big = cfg["m"] * cfg["n"] * 8 > (8 << 30)
+    budget = float(os.environ.get("RSVD_REF_BUDGET_S", "150"))
+    dt = cpu_reference(cfg, steps, 0 if big else min(args.warmup, 1), threads, budget_s=budget)
+    timed = cpu_reference.last_count
     value = 1.0 / dt
     line = {
         "impl": "reference", "metric": f"rsvd factorizations/s ({cfg['name']})", "value": value,
@@ -287,8 +298,10 @@ def run_reference_arm(args, cfg):
         "config": workload_config(args.config, cfg, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": {"value": value, "unit": "factorizations/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{steps} full {args.config} factorizations, oracle/rsvd_oracle.cpp "
-                                   f"with {threads} OpenBLAS threads",
+                         "sample": f"{timed} full {args.config} factorization(s) (of --steps {steps}; "
+                                   f"{budget:.0f} s budget), oracle/rsvd_oracle.cpp with {threads} "
+                                   f"OpenBLAS threads",
+                         "timed_factorizations": timed,
                          "host": host_info()},
         "e2e": {"value": value, "unit": "factorizations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
