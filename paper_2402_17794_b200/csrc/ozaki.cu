@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(256)
                  uint8_t* __restrict__ outi, int64_t ldi) {
   RSVD_PDL_ENTRY();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = (blockIdx.x * 32 + lane) * 4;
-  const int c = blockIdx.y * 8 + warp;
+  const int r0 = (blockIdx.y * 32 + lane) * 4;  // rows on grid.y (<= 8.3 M), columns on grid.x
+  const int c = blockIdx.x * 8 + warp;
   // the interleaved layout is read in whole 32-r groups: zero-fill the last one
   const int rows_w = outi ? ((rows + 31) & ~31) : rows;
   if (r0 >= rows_w || c >= cols) return;
@@ -788,7 +788,8 @@ void fill_exp(Handle& h, int* e, int64_t n, int init) {
 void launch_slice(Handle& h, const DMat& X, const int* rsub, const int* radd, const int* csub,
                   const Sliced& plain, const Sliced& inter, int S) {
   if (X.rows == 0 || X.cols == 0) return;
-  dim3 grid(unsigned(ceil_div(X.rows, 128)), unsigned(ceil_div(X.cols, 8)));
+  if (ceil_div(X.rows, 128) > 65535) throw_dim("ozaki: operand with more than 8388480 rows per slicing launch");
+  dim3 grid(unsigned(ceil_div(X.cols, 8)), unsigned(ceil_div(X.rows, 128)));
 #define RSVD_SLICE_CASE(SS)                                                                       \
   case SS:                                                                                        \
     launch_k(h, slice_kernel<SS>, grid, 256, 0, (const double*)X.p, X.ld, int(X.rows), int(X.cols), \

@@ -82,6 +82,19 @@ def test_gemm_graded_and_zero_rows_columns(eng):
     assert np.all(np.abs(c2 - ref2).astype(np.float64) <= _bound(a2, y, True, 8))
 
 
+def test_gemm_very_wide_matrix(eng):
+    """More than 65535 * 8 columns of A: the slicing grid puts columns on grid.x."""
+    rs = np.random.default_rng(2)
+    m, n, l = 40, 600000, 3
+    a = rs.standard_normal((m, n))
+    x = rs.standard_normal((n, l))
+    c = eng.debug_ozaki_gemm(_t(a), _t(x), slices=8).cpu().numpy()
+    assert np.all(np.abs(c - a @ x) <= 2 * _bound(a, x, False, 8))
+    y = rs.standard_normal((m, l))
+    c2 = eng.debug_ozaki_gemm(_t(a), _t(y), trans=True, slices=8).cpu().numpy()
+    assert np.all(np.abs(c2 - a.T @ y) <= 2 * _bound(a, y, True, 8))
+
+
 def test_gemm_long_contraction_chunks(eng):
     """K above 32768 is accumulated in chunks (int32 cannot overflow)."""
     rs = np.random.default_rng(8)
