@@ -188,6 +188,38 @@ def test_non_finite_inputs_raise_numeric_error_on_int8_path(oz):
     assert np.isfinite(f.sigma.cpu().numpy()).all()
 
 
+@pytest.mark.slow
+def test_c5_size_pass_int8_agrees_with_dmma(oz):
+    """BASELINE C5's full-size dual pass (A 262144 x 32768, l = 550) on both
+    arithmetic paths: the INT8 tensor-core products and the FP64 DMMA fused
+    pass agree entrywise within the sum of their fp64 error bounds, with
+    (|A||X|)_ij bounded by ||a_i||_2 ||x_j||_2 (no second 68.7 GB matrix)."""
+    import torch
+    import bench
+    cfg = bench.CONFIGS["C5"]
+    dev = torch.device("cuda", 0)
+    a = bench.make_input(cfg, dev)
+    m, n = a.shape
+    l = cfg["k"] + cfg["p"]
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    oc = torch.randn((l, n), dtype=torch.float64, device=dev, generator=g).t()
+    psi = torch.randn((l, m), dtype=torch.float64, device=dev, generator=g).t()
+    oz.set_ozaki_slices(8)
+    y8, w8 = oz.debug_dual_pass(a, oc, psi)
+    oz.set_ozaki_slices(0)
+    yd, wd = oz.debug_dual_pass(a, oc, psi)
+    rown = torch.linalg.vector_norm(a, dim=1)
+    coln = torch.linalg.vector_norm(a, dim=0)
+    by = 4 * n * U * rown[:, None] * torch.linalg.vector_norm(oc, dim=0)[None, :]
+    bw = 4 * m * U * coln[:, None] * torch.linalg.vector_norm(psi, dim=0)[None, :]
+    ry = float(((y8 - yd).abs() / by).max())
+    rw = float(((w8 - wd).abs() / bw).max())
+    print(f"C5-size pass: max |Y8 - Yd| / bound {ry:.3e}, max |W8 - Wd| / bound {rw:.3e}; "
+          f"relative to max|Y| {float((y8 - yd).abs().max() / yd.abs().max()):.3e}")
+    assert ry <= 1.0 and rw <= 1.0
+
+
 def test_set_ozaki_slices_rejects_bad_values(oz):
     with pytest.raises(oz.ParameterError):
         oz.set_ozaki_slices(2)
