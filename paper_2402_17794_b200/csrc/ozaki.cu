@@ -228,6 +228,16 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < 4; ++u) v[u] = r0 + u < rows ? p[u] : 0.0;
   }
   const int kc = 7 * S - 1 - (csub ? csub[c] : 0);
+  // Balanced digits without carries: with B = sum_{j < S-1} 64 * 128^j added,
+  // the base-128 digits of q + B are d_j + 64 in [0, 127] (plain 7-bit fields,
+  // the top one d_top in [-64, 64] unbiased), so each digit is one shift and
+  // mask, the four rows' digits of a slice are packed into a word, and the
+  // bias comes off all four bytes with one __vsub4.
+  constexpr long long kBias = [] {
+    long long b = 0;
+    for (int j = 0; j < S - 1; ++j) b += 64LL << (7 * j);
+    return b;
+  }();
   uint32_t w[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) w[s] = 0;
@@ -238,15 +248,24 @@ __global__ void __launch_bounds__(256)
       if (rsub) k -= rsub[r0 + u];
       if (radd) k += radd[r0 + u];
     }
-    long long q = __double2ll_rn(scale2(v[u], k));
+    const long long qb = __double2ll_rn(scale2(v[u], k)) + kBias;
+    const uint32_t lo = uint32_t(qb), hi = uint32_t(uint64_t(qb) >> 32);
 #pragma unroll
-    for (int s = S - 1; s >= 1; --s) {
-      const long long d = ((q + 64) & 127) - 64;
-      q = (q - d) >> 7;
-      w[s] |= (uint32_t(d) & 0xffu) << (8 * u);
+    for (int j = 0; j < S - 1; ++j) {  // digit j (weight 128^j) belongs to slice S - j
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int sh = 7 * j;
+      uint32_t f;
+      if (sh + 7 <= 32) f = lo >> sh;
+      else if (sh >= 32) f = hi >> (sh - 32);
+      else f = __funnelshift_r(lo, hi, sh);
+      w[S - 1 - j] |= (f & 127u) << (8 * u);
     }
-    w[0] |= (uint32_t(q) & 0xffu) << (8 * u);
+    const int top = int(qb >> (7 * (S - 1)));  // arithmetic shift: in [-64, 64]
+    w[0] |= (uint32_t(top) & 0xffu) << (8 * u);
   }
+#pragma unroll
+  for (int s = 1; s < S; ++s) w[s] = __vsub4(w[s], 0x40404040u);
   if (out && r0 < rows) {
     const int64_t plane = int64_t(cols) * ld8;
     uint8_t* o = out + int64_t(c) * ld8 + r0;
