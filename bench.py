@@ -564,7 +564,7 @@ def main():
                                                   if cfg["alg"] >= 5 else ")")},
             "roofline": roof,
             "pass_arithmetic": ("fp64 products of the pass on the INT8 tensor cores: Ozaki splitting into "
-                                + (os.environ.get("RSVD_OZAKI") or "8") + " exact 7-bit slices per operand, "
+                                + (os.environ.get("RSVD_OZAKI") or "7") + " exact 8-bit slices per operand, "
                                 "int32 partial products in TMEM, fp64 reassembly (csrc/ozaki.cu)")
                                if "int8" in passes else "fp64 DMMA (mma.sync m8n8k4.f64)",
             "passes": passes,

@@ -5,15 +5,19 @@
 // top out at the 37 TFLOP/s FP64 pipe.  The products of the range finder are
 // C = A X with A huge and X skinny (reference rangefinder.hpp:70-79,
 // singlepass.hpp:119-122); here each operand is written as
-//     a_ik = 2^eA[i] * sum_{s=1..S} d_s(i,k) 2^-(7s-1),   |d_s| <= 64
-// (d_s: balanced base-128 digits of the value rounded ONCE to 7S-1 fractional
-// bits below its row's largest power of two; X likewise per column), so
-//     C_ij = 2^(eA[i]+eX[j]) * sum_{c=2..S+1} 2^-(7c-2) * P_c(i,j),
+//     a_ik = 2^eA[i] * sum_{s=1..S} d_s(i,k) 2^(2-8s),   |d_s| <= 128
+// (d_s: balanced base-256 digits -- int8 -- of the value rounded ONCE to 8S-2
+// fractional bits below its row's largest power of two, the leading digit in
+// [-64, 64]; X likewise per column), so
+//     C_ij = 2^(eA[i]+eX[j]) * sum_{c=2..S+1} 2^(4-8c) * P_c(i,j),
 //     P_c  = sum_{s+t=c} D^A_s D^X_t          (exact int32 GEMMs)
-// The dropped terms (s+t > S+1) are below 2^-7S relative to the row/column
-// maxima: S = 8 is below fp64's own rounding of the product, S = 7 is 2^-49.
+// The dropped terms (s+t > S+1) are below 2^(-8S+6) relative to the row /
+// column maxima: S = 7 (54 fractional bits, 28 slice products) is at fp64's
+// own rounding of the product, S = 6 is 2^-46.  int32 holds a diagonal's sum
+// of up to 7 products of |d| <= 128 over 16384 contraction steps (max_k);
+// longer contractions are accumulated in chunks.
 //
-// Pipeline per row panel of A (<= 32768 rows, so int32 cannot overflow):
+// Pipeline per row panel of A (<= 32768 rows):
 //   row_exp -> slice (A read twice from HBM as fp64, slices written once per
 //   operand layout) -> apply GEMM (Y rows of the panel) -> Psi' = 2^eA Psi
 //   sliced per column -> adjoint GEMM (W += A_panel^T Psi_panel) from the SAME
@@ -57,7 +61,19 @@ constexpr int kThreads = 192;      // producer warp, MMA warp, 4 epilogue warps
 constexpr int kATile = kBM * kKS;  // bytes of one A slice tile
 constexpr int kARegion = 8 * kATile;  // A part of a stage (8 slice tiles / 2 quad tiles)
 constexpr int kMaxS = 8;
-constexpr int kMaxK = 32768;       // (S) * K * 64 * 64 < 2^31
+constexpr int kAutoSlices = 7;     // 54 fractional bits: at fp64's own rounding of the product
+constexpr int kMaxRows = 32768;    // rows of A sliced at a time (workspace)
+// contraction steps one int32 accumulation may cover: (S - 1 or S) products of
+// |d| <= 128 per diagonal and step, (S) * K * 2^14 < 2^31
+__host__ __device__ constexpr int max_k(int S) { return S >= 8 ? 8192 : 16384; }
+// Diagonal groups (four int32 accumulators fit in TMEM beside each other):
+// S <= 4: one sweep over c = 2..S+1.  S > 4: sweep 0 takes the high diagonals
+// c = 6..S+1 (every slice), sweep 1 the low ones c = 2..5 (slices 1..4 only:
+// one quad tile per operand) -- 18 + 10 MMAs per K step for S = 7, both sweeps
+// bound by the tensor pipe rather than by their loads.
+__host__ __device__ constexpr int grp_c_lo(int S, int g) { return (S > 4 && g == 0) ? 6 : 2; }
+__host__ __device__ constexpr int grp_c_hi(int S, int g) { return (S > 4 && g == 1) ? 5 : S + 1; }
+__host__ __device__ constexpr int grp_slices(int S, int g) { return (S > 4 && g == 1) ? 4 : S; }
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
@@ -193,8 +209,8 @@ __global__ void __launch_bounds__(256)
 }
 
 // -------------------------------------------------------------- slicing
-// Digit s of q = rint(x[r,c] * 2^(P - rsub[r] + radd[r] - csub[c])), P = 7S-1:
-// q = sum_s d_s 128^(S-s), d_s in [-64, 63] (top digit in [-64, 64]).
+// Digit s of q = rint(x[r,c] * 2^(P - rsub[r] + radd[r] - csub[c])), P = 8S-2:
+// q = sum_s d_s 256^(S-s), d_s in [-128, 127] (top digit in [-64, 64]).
 // Two output layouts (either or both):
 //   plain      out[s][c][r]            r contiguous, ld8 bytes per column: the
 //              MN-major UMMA operand of a contraction over c (the apply);
@@ -227,15 +243,15 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = r0 + u < rows ? p[u] : 0.0;
   }
-  const int kc = 7 * S - 1 - (csub ? csub[c] : 0);
-  // Balanced digits without carries: with B = sum_{j < S-1} 64 * 128^j added,
-  // the base-128 digits of q + B are d_j + 64 in [0, 127] (plain 7-bit fields,
-  // the top one d_top in [-64, 64] unbiased), so each digit is one shift and
-  // mask, the four rows' digits of a slice are packed into a word, and the
-  // bias comes off all four bytes with one __vsub4.
+  const int kc = 8 * S - 2 - (csub ? csub[c] : 0);
+  // Balanced digits without carries: with B = sum_{j < S-1} 128 * 256^j added,
+  // the base-256 digits of q + B are d_j + 128 in [0, 255] -- the BYTES of
+  // q + B -- and the top one d_top in [-64, 64] is unbiased.  The four rows'
+  // bytes of a slice are packed into a word and the bias comes off all four
+  // with one XOR (b - 128 = b ^ 0x80 mod 256).
   constexpr long long kBias = [] {
     long long b = 0;
-    for (int j = 0; j < S - 1; ++j) b += 64LL << (7 * j);
+    for (int j = 0; j < S - 1; ++j) b += 128LL << (8 * j);
     return b;
   }();
   uint32_t w[S];
@@ -251,21 +267,15 @@ __global__ void __launch_bounds__(256)
     const long long qb = __double2ll_rn(scale2(v[u], k)) + kBias;
     const uint32_t lo = uint32_t(qb), hi = uint32_t(uint64_t(qb) >> 32);
 #pragma unroll
-    for (int j = 0; j < S - 1; ++j) {  // digit j (weight 128^j) belongs to slice S - j
-      constexpr int dummy = 0;
-      (void)dummy;
-      const int sh = 7 * j;
-      uint32_t f;
-      if (sh + 7 <= 32) f = lo >> sh;
-      else if (sh >= 32) f = hi >> (sh - 32);
-      else f = __funnelshift_r(lo, hi, sh);
-      w[S - 1 - j] |= (f & 127u) << (8 * u);
+    for (int j = 0; j < S - 1; ++j) {  // byte j (weight 256^j) belongs to slice S - j
+      const uint32_t f = j < 4 ? (lo >> (8 * j)) : (hi >> (8 * (j - 4)));
+      w[S - 1 - j] |= (f & 255u) << (8 * u);
     }
-    const int top = int(qb >> (7 * (S - 1)));  // arithmetic shift: in [-64, 64]
+    const int top = int(qb >> (8 * (S - 1)));  // arithmetic shift: in [-64, 64]
     w[0] |= (uint32_t(top) & 0xffu) << (8 * u);
   }
 #pragma unroll
-  for (int s = 1; s < S; ++s) w[s] = __vsub4(w[s], 0x40404040u);
+  for (int s = 1; s < S; ++s) w[s] ^= 0x80808080u;
   if (out && r0 < rows) {
     const int64_t plane = int64_t(cols) * ld8;
     uint8_t* o = out + int64_t(c) * ld8 + r0;
@@ -312,6 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int m0 = mt * kBM, n0 = nt * p.ntile;
   const int nk = (p.K + kKS - 1) / kKS;
   const int ngroups = (S + 3) / 4;
+  constexpr int kchunk = max_k(S) / kKS;  // K steps one int32 accumulation may cover
+  const int nchunks = (nk + kchunk - 1) / kchunk;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -341,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::prefetch_tmap(&tmB);
       int it = 0;
       for (int g = 0; g < ngroups; ++g) {
-        const int Sg = S - 4 * g;
+        const int Sg = grp_slices(S, g);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int st = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
@@ -380,18 +392,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t ad_fixed = smem_desc(0, AMN ? 4096 : 0, 1024, 2);
     const uint64_t bd_fixed = smem_desc(0, 0, 1024, 2);
     const uint32_t sm0 = ptx::smem_u32(sm);
-    int it = 0;
+    int it = 0, drains = 0;
     auto run_group = [&](auto sg_tag) {
-      constexpr int Sg = decltype(sg_tag)::value;
-      constexpr int c_hi = Sg + 1, c_lo = (c_hi - 3 > 2 ? c_hi - 3 : 2);
+      constexpr int G = decltype(sg_tag)::value;
+      constexpr int Sg = grp_slices(S, G), c_hi = grp_c_hi(S, G), c_lo = grp_c_lo(S, G);
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int st = it % kStages;
         const uint32_t ph = (it / kStages) & 1;
+        const bool chunk_start = kb % kchunk == 0;
+        if (chunk_start && drains > 0) {  // the epilogue has drained the previous accumulation
+          ptx::mbar_wait(&bar_acc_empty, uint32_t(drains - 1) & 1);
+          tc_fence_after();
+        }
         ptx::mbar_wait(&bar_full[st], ph);
         tc_fence_after();
         const uint32_t a0 = (sm0 + st * stage_bytes) >> 4;
         const uint32_t b0 = a0 + (kARegion >> 4);
-        const uint32_t kacc = kb > 0 ? 1u : 0u;
+        const uint32_t kacc = chunk_start ? 0u : 1u;
         if (elect_one() && !(p.dbg & 1)) {
 #pragma unroll
           for (int c = c_hi; c >= c_lo; --c) {
@@ -414,15 +431,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (elect_one()) umma_commit(&bar_empty[st]);
+        if (kb % kchunk == kchunk - 1 || kb == nk - 1) {  // int32 headroom: drain per K chunk
+          if (elect_one()) umma_commit(&bar_acc_full);
+          ++drains;
+        }
       }
-      if (elect_one()) umma_commit(&bar_acc_full);
     };
-    run_group(std::integral_constant<int, S>{});
-    if constexpr (S > 4) {
-      ptx::mbar_wait(&bar_acc_empty, 0);
-      tc_fence_after();
-      run_group(std::integral_constant<int, (S > 4 ? S - 4 : 1)>{});
-    }
+    run_group(std::integral_constant<int, 0>{});
+    if constexpr (S > 4) run_group(std::integral_constant<int, 1>{});
   } else {
     // ---------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may read
@@ -430,23 +446,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t grow = int64_t(m0) + row;
     const int re = (p.rexp && grow < p.M) ? p.rexp[grow] : 0;
     double* scr = p.scratch ? p.scratch + int64_t(blockIdx.x) * kBM * p.ntile : nullptr;
-    for (int g = 0; g < ngroups; ++g) {
-      const int Sg = S - 4 * g;
-      const int c_hi = Sg + 1, c_lo = max(2, c_hi - 3);
-      const bool last = g == ngroups - 1;
-      ptx::mbar_wait(&bar_acc_full, g & 1);
+    for (int d = 0; d < ngroups * nchunks; ++d) {  // one drain per (diagonal group, K chunk)
+      const int g = d / nchunks;
+      const int c_hi = grp_c_hi(S, g), c_lo = grp_c_lo(S, g);
+      const bool first_d = d == 0, last = d == ngroups * nchunks - 1;
+      ptx::mbar_wait(&bar_acc_full, uint32_t(d) & 1);
       tc_fence_after();
       for (int cc = 0; cc < p.ntile; cc += 8) {
         double v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = 0.0;
-        for (int c = c_hi; c >= c_lo; --c) {  // smallest terms first
-          uint32_t r[8];
-          tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t((c - c_lo) * 128 + cc), r);
-          tmem_ld_wait();
-          const double sc = exp2i(-(7 * c - 2));
+        // all four accumulators' loads in flight before one wait
+        uint32_t r[4][8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = fma(double(int(r[j])), sc, v[j]);
+        for (int i = 0; i < 4; ++i)
+          if (c_lo + i <= c_hi) tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t(i * 128 + cc), r[i]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {  // smallest terms (highest c) first
+          if (c_lo + i > c_hi) continue;
+          const double sc = exp2i(-(8 * (c_lo + i) - 4));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = fma(double(int(r[i][j])), sc, v[j]);
+        }
+        if (!first_d) {  // running sum of the earlier drains (this thread's own writes)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] += scr[int64_t(cc + j) * kBM + row];
         }
         if (!last) {
 #pragma unroll
@@ -457,7 +482,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col = n0 + cc + j;
             if (grow < p.M && col < p.N) {
               double x = v[j];
-              if (ngroups > 1) x += scr[int64_t(cc + j) * kBM + row];
               x = scale2(x, re + (p.cexp ? p.cexp[col] : 0));
               double* dst = p.C + int64_t(col) * p.ldc + grow;
               *dst = p.accumulate ? *dst + x : x;
@@ -557,6 +581,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int m0 = mt * kBM, n0 = nt * NT;
   const int nk = (p.K + kKS - 1) / kKS;
   constexpr int ngroups = (S + 3) / 4;
+  constexpr int kchunk = max_k(S) / kKS;  // K steps one int32 accumulation may cover
+  const int nchunks = (nk + kchunk - 1) / kchunk;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages2; ++s) {
@@ -586,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::prefetch_tmap(&tmB);
       int it = 0;
       for (int g = 0; g < ngroups; ++g) {
-        const int Sg = S - 4 * g;
+        const int Sg = grp_slices(S, g);
         const int nhalf = (Sg + 3) >> 2;
         const uint32_t bytes = uint32_t(AMN ? Sg * kATile : nhalf * 4 * kATile) + uint32_t(nhalf * bhalf4);
         for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -618,18 +644,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t ad_fixed = smem_desc(0, AMN ? 4096 : 0, 1024, 2);
       const uint64_t bd_fixed = smem_desc(0, 0, 1024, 2);
       const uint32_t sm0 = ptx::smem_u32(sm);
-      int it = 0;
+      int it = 0, drains = 0;
       auto run_group = [&](auto sg_tag) {
-        constexpr int Sg = decltype(sg_tag)::value;
-        constexpr int c_hi = Sg + 1, c_lo = (c_hi - 3 > 2 ? c_hi - 3 : 2);
+        constexpr int G = decltype(sg_tag)::value;
+        constexpr int Sg = grp_slices(S, G), c_hi = grp_c_hi(S, G), c_lo = grp_c_lo(S, G);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int st = it % kStages2;
           const uint32_t ph = (it / kStages2) & 1;
+          const bool chunk_start = kb % kchunk == 0;
+          if (chunk_start && drains > 0) {  // both CTAs' epilogues drained the previous accumulation
+            ptx::mbar_wait(&bar_acc_empty, uint32_t(drains - 1) & 1);
+            tc_fence_after();
+          }
           ptx::mbar_wait(&bar_full[st], ph);
           tc_fence_after();
           const uint32_t a0 = (sm0 + st * stage_bytes) >> 4;
           const uint32_t b0 = a0 + (kARegion >> 4);
-          const uint32_t kacc = kb > 0 ? 1u : 0u;
+          const uint32_t kacc = chunk_start ? 0u : 1u;
           if (elect_one()) {
 #pragma unroll
             for (int c = c_hi; c >= c_lo; --c) {
@@ -648,15 +679,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
           if (elect_one()) umma2_commit_both(&bar_empty[st]);
+          if (kb % kchunk == kchunk - 1 || kb == nk - 1) {  // int32 headroom: drain per K chunk
+            if (elect_one()) umma2_commit_both(&bar_acc_full);
+            ++drains;
+          }
         }
-        if (elect_one()) umma2_commit_both(&bar_acc_full);
       };
-      run_group(std::integral_constant<int, S>{});
-      if constexpr (S > 4) {
-        ptx::mbar_wait(&bar_acc_empty, 0);
-        tc_fence_after();
-        run_group(std::integral_constant<int, (S > 4 ? S - 4 : 1)>{});
-      }
+      run_group(std::integral_constant<int, 0>{});
+      if constexpr (S > 4) run_group(std::integral_constant<int, 1>{});
     }
   } else {
     // ------------------------------------------- epilogue (both CTAs)
@@ -665,24 +695,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int64_t grow = int64_t(m0) + row;
     const int re = (p.rexp && grow < p.M) ? p.rexp[grow] : 0;
     double* scr = p.scratch ? p.scratch + int64_t(blockIdx.x) * kBM * NT : nullptr;
-    for (int g = 0; g < ngroups; ++g) {
-      const int Sg = S - 4 * g;
-      const int c_hi = Sg + 1, c_lo = max(2, c_hi - 3);
-      const bool last = g == ngroups - 1;
-      ptx::mbar_wait(&bar_acc_full, g & 1);
+    for (int d = 0; d < ngroups * nchunks; ++d) {  // one drain per (diagonal group, K chunk)
+      const int g = d / nchunks;
+      const int c_hi = grp_c_hi(S, g), c_lo = grp_c_lo(S, g);
+      const bool first_d = d == 0, last = d == ngroups * nchunks - 1;
+      ptx::mbar_wait(&bar_acc_full, uint32_t(d) & 1);
       tc_fence_after();
       for (int cc = 0; cc < NT; cc += 8) {
         if (n0 + cc >= p.N) break;
         double v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = 0.0;
-        for (int c = c_hi; c >= c_lo; --c) {  // smallest terms first
-          uint32_t r[8];
-          tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t((c - c_lo) * 128 + cc), r);
-          tmem_ld_wait();
-          const double sc = exp2i(-(7 * c - 2));
+        // all four accumulators' loads in flight before one wait
+        uint32_t r[4][8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = fma(double(int(r[j])), sc, v[j]);
+        for (int i = 0; i < 4; ++i)
+          if (c_lo + i <= c_hi) tmem_ld8(tb + (uint32_t(q * 32) << 16) + uint32_t(i * 128 + cc), r[i]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {  // smallest terms (highest c) first
+          if (c_lo + i > c_hi) continue;
+          const double sc = exp2i(-(8 * (c_lo + i) - 4));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = fma(double(int(r[i][j])), sc, v[j]);
+        }
+        if (!first_d) {  // running sum of the earlier drains (this thread's own writes)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] += scr[int64_t(cc + j) * kBM + row];
         }
         if (!last) {
 #pragma unroll
@@ -693,7 +732,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int col = n0 + cc + j;
             if (grow < p.M && col < p.N) {
               double x = v[j];
-              if (ngroups > 1) x += scr[int64_t(cc + j) * kBM + row];
               x = scale2(x, re + (p.cexp ? p.cexp[col] : 0));
               double* dst = p.C + int64_t(col) * p.ldc + grow;
               *dst = p.accumulate ? *dst + x : x;
@@ -878,7 +916,7 @@ int pick_ntile(int64_t L) {
 }
 // doubles of per-CTA partial tiles a GEMM with M x N outputs needs (S > 4)
 int64_t scratch_doubles(int64_t M, int64_t N, int S) {
-  if (S <= 4) return 0;
+  (void)S;  // every launch may drain more than once (diagonal groups, K chunks)
   const int ntile = pick_ntile(N);
   return round_up(ceil_div(M, kBM), 2) * ceil_div(N, ntile) * kBM * ntile;
 }
@@ -903,11 +941,14 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
   const CUtensorMap ta = amn ? make_map_i8(As.p, As.inner, As.outer, As.ld, S, kBM, kKS, true)
                              : make_map_inter(As.p, As.ld, As.outer, As.ld, kBM);
   const CUtensorMap tb = make_map_inter(Bs.p, Bs.ld, Bs.outer, Bs.ld, pair ? ntile / 2 : ntile);
-  for (int64_t k0 = 0; k0 < K; k0 += kMaxK) {
+  // the kernel drains its int32 accumulators every max_k(S) contraction steps;
+  // a launch covers up to 2^24 of them (indices stay far inside int)
+  const int64_t kmax = int64_t(1) << 24;
+  for (int64_t k0 = 0; k0 < K; k0 += kmax) {
     OzParams p;
     p.M = int(M);
     p.N = int(N);
-    p.K = int(std::min<int64_t>(kMaxK, K - k0));
+    p.K = int(std::min<int64_t>(kmax, K - k0));
     p.k0 = int(k0);
     p.S = S;
     p.ntile = ntile;
@@ -957,13 +998,13 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
 }
 
 // Rows of A sliced at a time: int32 accumulation bounds the adjoint's
-// contraction length (kMaxK); `copies` layouts of the sub-panel's slices
+// contraction length per launch, not the panel; `copies` layouts of the sub-panel's slices
 // (S K bytes per row each) must fit in what the device has left.
 int64_t sub_rows(Handle& h, int64_t K, int S, int copies) {
   size_t free_b = 0, total_b = 0;
   RSVD_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double budget = std::min(40.0e9, 0.8 * (double(free_b) + double(h.ws.remaining())));
-  int64_t sub = kMaxK;
+  int64_t sub = kMaxRows;
   while (sub > 1024 && double(sub) * double(K) * S * copies > budget) sub /= 2;
   return sub;
 }
@@ -991,14 +1032,14 @@ int ozaki_slices(const Handle& h) {
 }
 
 // Default policy of the Alg-6 dual pass (engine.cu op_dual): the sliced INT8
-// product with 8 slices (inside the error bound of an fp64 product, see the
+// product with 7 slices (inside the error bound of an fp64 product, see the
 // header) when the sketch is wide enough for the tensor pipe to pay for the
 // slicing passes (l >= 128: at l = 110 it breaks even with the DMMA pass,
 // below that the pass is HBM-bound anyway) and A is large (>= 2^26 entries).
 int ozaki_slices_auto(const Handle& h, int64_t rows, int64_t K, int64_t L) {
   const int s = ozaki_slices(h);
   if (s >= 0) return s;
-  return (L >= 128 && double(rows) * double(K) >= double(int64_t(1) << 26)) ? 8 : 0;
+  return (L >= 128 && double(rows) * double(K) >= double(int64_t(1) << 26)) ? kAutoSlices : 0;
 }
 
 namespace {
@@ -1150,10 +1191,10 @@ bool ozaki_cache_decide(Handle& h, OzCache& c, const DMat& A, int64_t L, int pas
     // (Alg 5) pays for its own slicing from l ~ 160 up (break-even at l = 110)
     const bool wide = passes >= 3 ? L >= 96 : (passes >= 1 && L >= 160);
     if (!(wide && double(A.rows) * double(A.cols) >= double(int64_t(1) << 26))) return false;
-    S = 8;
+    S = kAutoSlices;
   }
   const int64_t K = A.cols;
-  const int64_t cap = std::min<int64_t>(kMaxK, round_up(A.rows, 128));
+  const int64_t cap = std::min<int64_t>(kMaxRows, round_up(A.rows, 128));
   const int64_t nsub = ceil_div(A.rows, cap);
   const double need = double(nsub) * (double(S) * double(K) * double(ld_plain(cap)) +
                                       double(K) * double(ld_inter(cap))) + 64.0e6;

@@ -1,6 +1,6 @@
 // FP64 products of the streaming passes on the INT8 tensor cores (tcgen05,
 // TMEM accumulators) by the Ozaki splitting: both operands are cut into S
-// signed 7-bit slices against a per-row / per-column power-of-two scale, the
+// signed 8-bit slices (balanced base-256 digits) against a per-row / per-column power-of-two scale, the
 // S(S+1)/2 slice products that matter are exact int32 GEMMs, and the result is
 // reassembled in fp64 (ozaki.cu).  Default for wide sketches of large matrices (ozaki_slices_auto).
 #pragma once
@@ -14,7 +14,7 @@ int ozaki_slices(const Handle& h);
 // single-CTA kernel, -1 = RSVD_OZ_CG2 / default (pair).  Process-wide; tests.
 void ozaki_force_pair_kernel(int pair);
 // The dual pass's choice for an A of rows x K and l = L sketch columns: the
-// explicit setting, else 8 slices for wide sketches of large matrices, else 0.
+// explicit setting, else 7 slices for wide sketches of large matrices, else 0.
 int ozaki_slices_auto(const Handle& h, int64_t rows, int64_t K, int64_t L);
 // Work buffers of one call (device pointers into the handle's workspace),
 // reused by every sub-panel: the arena is a bump allocator and the stream
@@ -64,7 +64,7 @@ struct OzCache {
 };
 // Decide once per call whether its passes over A (rows x K, sketch width L,
 // `passes` products expected) run on the INT8 path: the explicit setting,
-// else 8 slices when A has >= 2^26 entries, both layouts of its slices fit in
+// else 7 slices when A has >= 2^26 entries, both layouts of its slices fit in
 // device memory and the sketch is wide enough to amortize the slicing pass
 // (L >= 96 for passes >= 3, L >= 160 for a single product).
 bool ozaki_cache_decide(Handle& h, OzCache& c, const DMat& A, int64_t L, int passes);

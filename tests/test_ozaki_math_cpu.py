@@ -1,14 +1,14 @@
 """The arithmetic of the INT8 tensor-core passes (csrc/ozaki.cu), restated in
-numpy and checked on the CPU: the slicing (one rounding to 7S-1 fractional
-bits below a power-of-two row / column scale, balanced base-128 digits by the
+numpy and checked on the CPU: the slicing (one rounding to 8S-2 fractional
+bits below a power-of-two row / column scale, balanced base-256 digits by the
 bias trick of slice_kernel), the exact integer slice products grouped by
 diagonal c = s + t <= S + 1, and the fp64 reassembly.
 
-Pins the properties the CUDA kernels rely on: digits fit int8 ([-64, 63], top
-digit [-64, 64]); the digits reproduce the rounded value exactly; every
-diagonal's accumulation stays below 2^31 for contractions up to 32768; with
-S = 8 the product is inside the fp64 bound 2 K u (|A||X|), with S = 7 / 6 inside
-2^-(7S-8) of it; the adjoint's row scales move into the skinny operand
+Pins the properties the CUDA kernels rely on: digits fit int8 ([-128, 127],
+top digit [-64, 64]); the digits reproduce the rounded value exactly; every
+diagonal's accumulation stays below 2^31 for contractions up to 16384 (8192
+with 8 slices); with S >= 7 the product is inside the fp64 bound
+2 K u (|A||X|), with S = 6 / 5 inside 2^-(8S-12) of it; the adjoint's row scales move into the skinny operand
 exactly.  (The GPU tests compare the kernels with the same bounds.)"""
 import numpy as np
 import pytest
@@ -25,20 +25,20 @@ def exponents(x, axis):
 
 
 def digits(x, shift, s_count):
-    """slice_kernel: q = rint(x 2^shift), balanced base-128 digits most significant first."""
+    """slice_kernel: q = rint(x 2^shift), balanced base-256 digits most significant first."""
     q = np.rint(np.ldexp(x, shift)).astype(np.int64)
-    bias = sum(64 << (7 * j) for j in range(s_count - 1))
+    bias = sum(128 << (8 * j) for j in range(s_count - 1))
     qb = q + bias
     out = []
     for j in range(s_count - 1):
-        out.append(((qb >> (7 * j)) & 127) - 64)
-    out.append(qb >> (7 * (s_count - 1)))
+        out.append(((qb >> (8 * j)) & 255) - 128)
+    out.append(qb >> (8 * (s_count - 1)))
     return q, out[::-1]
 
 
 def ozaki_product(a, x, s_count, trans=False):
     """C = A X (or A^T X) as the kernels compute it."""
-    p = 7 * s_count - 1
+    p = 8 * s_count - 2
     ea = exponents(a, axis=1)
     qa, da = digits(a, (p - ea)[:, None], s_count)
     if not trans:
@@ -59,7 +59,7 @@ def ozaki_product(a, x, s_count, trans=False):
         for s in range(max(1, c - s_count), min(s_count, c - 1) + 1):
             pc += left[s - 1] @ dx[c - s - 1].astype(np.int64)
         worst = max(worst, int(np.abs(pc).max()))
-        acc += pc.astype(np.float64) * 2.0 ** -(7 * c - 2)
+        acc += pc.astype(np.float64) * 2.0 ** -(8 * c - 4)
     out = np.ldexp(acc, (scale_rows[:, None] + scale_cols[None, :]))
     return out, da, dx, qa, worst
 
@@ -70,7 +70,7 @@ def test_digits_fit_int8_and_reproduce_the_rounded_value(s_count):
     a = rs.standard_normal((60, 90)) * np.exp(rs.uniform(-4, 4, (60, 1)))
     a[5] = 0.0
     a[7, 3] = np.abs(a[7]).max() * (2.0 - 2.0 ** -52)  # just below the next power of two
-    p = 7 * s_count - 1
+    p = 8 * s_count - 2
     ea = exponents(a, axis=1)
     assert np.all(np.abs(a) < np.ldexp(1.0, ea)[:, None])
     q, d = digits(a, (p - ea)[:, None], s_count)
@@ -79,15 +79,15 @@ def test_digits_fit_int8_and_reproduce_the_rounded_value(s_count):
         if j == 0:
             assert dj.min() >= -64 and dj.max() <= 64
         else:
-            assert dj.min() >= -64 and dj.max() <= 63
-    back = sum(dj.astype(np.int64) << (7 * (s_count - 1 - j)) for j, dj in enumerate(d))
+            assert dj.min() >= -128 and dj.max() <= 127
+    back = sum(dj.astype(np.int64) << (8 * (s_count - 1 - j)) for j, dj in enumerate(d))
     assert np.array_equal(back, q)
     # the rounded value is within half a unit of the last kept bit of the row's scale
     assert np.all(np.abs(np.ldexp(q.astype(np.float64), (ea - p)[:, None]) - a) <= np.ldexp(0.5, ea - p)[:, None])
 
 
 @pytest.mark.parametrize("trans", [False, True])
-@pytest.mark.parametrize("s_count,rel", [(8, None), (7, 2.0 ** -41), (6, 2.0 ** -34)])
+@pytest.mark.parametrize("s_count,rel", [(8, None), (7, None), (6, 2.0 ** -36), (5, 2.0 ** -28)])
 def test_product_error_bounds(s_count, rel, trans):
     rs = np.random.default_rng(11 + s_count)
     m, n, l = 70, 300, 9
@@ -103,15 +103,18 @@ def test_product_error_bounds(s_count, rel, trans):
 
 
 def test_int32_accumulators_cannot_overflow():
-    """Worst case: every digit at +-64 over a contraction of 32768 (kMaxK): a
-    diagonal sums at most 8 slice products, 8 * 32768 * 64 * 64 = 2^30."""
-    k = 32768
-    a = np.full((2, k), 1.0 - 2.0 ** -52)
-    x = np.full((k, 1), -(1.0 - 2.0 ** -52))
-    _, da, dx, _, worst = ozaki_product(a, x, 8)
-    assert da[0].max() == 64 and dx[0].min() == -64
+    """Worst case per contraction chunk (max_k in ozaki.cu: 16384 steps for
+    S <= 7, 8192 for S = 8): a diagonal sums at most S products of |d| <= 128."""
+    assert 7 * 16384 * 128 * 128 < 2 ** 31
+    assert 8 * 8192 * 128 * 128 < 2 ** 31
+    # every lower digit at -128: a value just above -2^-7 of its scale
+    k = 16384
+    a = np.full((2, k), -(2.0 ** -7) * (1 - 2.0 ** -40))
+    a[:, 0] = 1.0 - 2.0 ** -52
+    x = a.T.copy()
+    _, da, dx, _, worst = ozaki_product(a, x[:, :1], 7)
+    assert min(d.min() for d in da[1:]) == -128
     assert worst < 2 ** 31
-    assert 8 * k * 64 * 64 <= 2 ** 30
 
 
 def test_graded_rows_keep_their_own_relative_accuracy():

@@ -1,7 +1,7 @@
 """One Alg-6 dual pass on the INT8 tensor cores (csrc/ozaki.cu) at a C5 row
 panel's shape, for ncu captures:
 
-  python tools/ncu_ozaki.py [m n l slices]      (default 32768 32768 550 8)
+  python tools/ncu_ozaki.py [m n l slices]      (default 32768 32768 550 7)
 """
 import os
 import sys
@@ -14,7 +14,7 @@ import paper_2402_17794_b200 as eng  # noqa: E402
 
 def main():
     d = [int(v) for v in sys.argv[1:5]]
-    m, n, l, s = (d + [32768, 32768, 550, 8][len(d):])
+    m, n, l, s = (d + [32768, 32768, 550, 7][len(d):])
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev)
     g.manual_seed(1)
