@@ -262,11 +262,13 @@ rsvd_status rsvd_debug_dual_pass_dev(rsvd_handle* h, int64_t m, int64_t n, int64
                                      const double* psi, int64_t ldp, double* y, int64_t ldy,
                                      double* w, int64_t ldw, int64_t panel_rows, int macroblock);
 
-/* Alg 6's dual product on the INT8 tensor cores (tcgen05 kind::i8, Ozaki
- * splitting into `slices` exact 7-bit slices per operand; csrc/ozaki.cu):
- * -1 = follow the RSVD_OZAKI environment variable (default), 0 = off (the
- * FP64 DMMA pass), 3..8 = slices.  8 slices are below fp64's own rounding of
- * the product; 7 are 2^-49 of the row/column maxima. */
+/* The products with A of wide sketches on the INT8 tensor cores (tcgen05
+ * kind::i8, Ozaki splitting into `slices` exact 8-bit slices per operand,
+ * 8*slices - 2 fractional bits; csrc/ozaki.cu): -1 = the automatic policy,
+ * which also follows the RSVD_OZAKI environment variable (default), 0 = off
+ * (the FP64 DMMA passes), 3..8 = slices.  7 slices (the automatic choice)
+ * are at fp64's own rounding of the product, 8 are below it, 6 are 2^-46 of
+ * the row / column maxima. */
 rsvd_status rsvd_set_ozaki_slices(rsvd_handle* h, int slices);
 /* Which INT8 GEMM kernel runs (process-wide; unit tests): 1 = CTA pair
  * (tcgen05 cta_group::2, the default), 0 = single CTA, -1 = default. */

@@ -896,9 +896,10 @@ def debug_dual_pass(a, oc, psi, panel_rows: int = 0, macroblock: int = 0):
 
 
 def set_ozaki_slices(slices: int, engine=None) -> None:
-    """Run Alg 6's dual product on the INT8 tensor cores with `slices` exact
-    7-bit slices per operand (csrc/ozaki.cu): 0 = off (FP64 DMMA pass), 3..8 =
-    slices, -1 = follow the RSVD_OZAKI environment variable."""
+    """Run the wide-sketch products with A on the INT8 tensor cores with
+    `slices` exact 8-bit slices per operand (csrc/ozaki.cu): 0 = off (FP64
+    DMMA passes), 3..8 = slices (7 = fp64-equivalent, the automatic choice),
+    -1 = the automatic policy / the RSVD_OZAKI environment variable."""
     e = engine or default_engine()
     _check(_load().rsvd_set_ozaki_slices(e.handle, int(slices)))
 

@@ -1,8 +1,10 @@
 // FP64 products of the streaming passes on the INT8 tensor cores (tcgen05,
 // TMEM accumulators) by the Ozaki splitting: both operands are cut into S
-// signed 8-bit slices (balanced base-256 digits) against a per-row / per-column power-of-two scale, the
-// S(S+1)/2 slice products that matter are exact int32 GEMMs, and the result is
-// reassembled in fp64 (ozaki.cu).  Default for wide sketches of large matrices (ozaki_slices_auto).
+// signed 8-bit slices (balanced base-256 digits) against a per-row /
+// per-column power-of-two scale, the S(S+1)/2 slice products that matter are
+// exact int32 GEMMs, and the result is reassembled in fp64 (ozaki.cu).
+// Default (S = 7) for wide sketches of large matrices (ozaki_slices_auto,
+// ozaki_cache_decide).
 #pragma once
 #include "common.cuh"
 
