@@ -99,15 +99,21 @@ def test_gemm_very_wide_matrix(eng):
     assert np.all(np.abs(c2 - a.T @ y) <= 2 * _bound(a, y, True, 8))
 
 
-def test_gemm_long_contraction_chunks(eng):
-    """K above 32768 is accumulated in chunks (int32 cannot overflow)."""
+def test_gemm_long_contraction_chunks(eng, kernel):
+    """Contractions longer than 16384 steps: the kernels drain their int32
+    accumulators to fp64 every 16384 steps (8192 with 8 slices)."""
     rs = np.random.default_rng(8)
     m, n, l = 130, 70000, 20
     a = rs.standard_normal((m, n))
     x = rs.standard_normal((n, l))
-    c = eng.debug_ozaki_gemm(_t(a), _t(x), slices=8).cpu().numpy()
     ref = a.astype(np.longdouble) @ x.astype(np.longdouble)
-    assert np.all(np.abs(c - ref).astype(np.float64) <= _bound(a, x, False, 8))
+    for s in (8, 7):
+        c = eng.debug_ozaki_gemm(_t(a), _t(x), slices=s).cpu().numpy()
+        assert np.all(np.abs(c - ref).astype(np.float64) <= _bound(a, x, False, s))
+    y = rs.standard_normal((n, 7))  # adjoint: contraction over 70000 rows (sub-panels and chunks)
+    c = eng.debug_ozaki_gemm(_t(a.T.copy()), _t(y), trans=True, slices=7).cpu().numpy()
+    refa = a.astype(np.longdouble) @ y.astype(np.longdouble)
+    assert np.all(np.abs(c - refa).astype(np.float64) <= _bound(a.T, y, True, 7))
     # extreme digits: every entry at the top of its slice range
     a1 = np.full((m, 40000), 1.0 - 2.0 ** -52)
     x1 = np.full((40000, 3), -(1.0 - 2.0 ** -52))
