@@ -549,11 +549,11 @@ __device__ __forceinline__ void umma2_i8(uint32_t d_tmem, uint64_t adesc, uint64
       : "memory");
 }
 // arrive (once all earlier MMAs are done) on the barrier at this offset in both CTAs
-__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar, uint16_t pair_mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(ptx::smem_u32(bar)),
-      "h"(uint16_t(3))
+      "h"(pair_mask)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
@@ -563,7 +563,7 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
 }
 
 template <int AMN, int S>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     ozaki_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, OzParams p) {
   RSVD_PDL_ENTRY();
@@ -572,7 +572,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_full[kStages2], bar_empty[kStages2], bar_acc_full, bar_acc_empty;
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = int(cluster_ctarank());
+  // launched as clusters of 2 c CTAs (c CTA pairs with consecutive column tiles
+  // of one row-tile pair: they start together and share A's tiles through L2)
+  const int crank = int(cluster_ctarank());
+  const int rank = crank & 1;  // within the pair
   const int pair = blockIdx.x >> 1;
   const int nt = pair % p.n_tiles, mt = 2 * (pair / p.n_tiles) + rank;
   const int NT = p.ntile;                 // output columns per pair: 64, 96 or 128
@@ -644,6 +647,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t ad_fixed = smem_desc(0, AMN ? 4096 : 0, 1024, 2);
       const uint64_t bd_fixed = smem_desc(0, 0, 1024, 2);
       const uint32_t sm0 = ptx::smem_u32(sm);
+      const uint16_t pair_mask = uint16_t(3u << (crank & ~1));  // this pair's two CTAs in the cluster
       int it = 0, drains = 0;
       auto run_group = [&](auto sg_tag) {
         constexpr int G = decltype(sg_tag)::value;
@@ -678,9 +682,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
           __syncwarp();
-          if (elect_one()) umma2_commit_both(&bar_empty[st]);
+          if (elect_one()) umma2_commit_both(&bar_empty[st], pair_mask);
           if (kb % kchunk == kchunk - 1 || kb == nk - 1) {  // int32 headroom: drain per K chunk
-            if (elect_one()) umma2_commit_both(&bar_acc_full);
+            if (elect_one()) umma2_commit_both(&bar_acc_full, pair_mask);
             ++drains;
           }
         }
@@ -766,6 +770,27 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   });
   if (!fn) throw Error(RSVD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   return fn;
+}
+
+// Launch with a runtime cluster size (and as a programmatic dependent, like launch_k)
+template <typename... KArgs, typename... Args>
+void launch_cluster(Handle& h, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                    int csize, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h.stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(csize);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  RSVD_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 // 3-D int8 map over slices stored [slice][outer][inner]: dims {inner, outer, S}
@@ -941,6 +966,16 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
   const CUtensorMap ta = amn ? make_map_i8(As.p, As.inner, As.outer, As.ld, S, kBM, kKS, true)
                              : make_map_inter(As.p, As.ld, As.outer, As.ld, kBM);
   const CUtensorMap tb = make_map_inter(Bs.p, Bs.ld, Bs.outer, Bs.ld, pair ? ntile / 2 : ntile);
+  // CTA-pair kernel: clusters of 3 pairs (consecutive column tiles of one
+  // row-tile pair) when the column tiles allow it, so the pairs sharing A's
+  // tiles start together (RSVD_OZ_CLUSTER=2 keeps plain pairs)
+  int csize = 2;
+  if (pair) {
+    static const int forced = [] { const char* e = std::getenv("RSVD_OZ_CLUSTER"); return e ? std::atoi(e) : 0; }();
+    if (n_tiles % 3 == 0) csize = 6;
+    else if (n_tiles % 2 == 0) csize = 4;
+    if (forced == 2 || forced == 4 || forced == 6) csize = (n_tiles * 2) % forced == 0 ? forced : 2;
+  }
   // the kernel drains its int32 accumulators every max_k(S) contraction steps;
   // a launch covers up to 2^24 of them (indices stay far inside int)
   const int64_t kmax = int64_t(1) << 24;
@@ -969,10 +1004,10 @@ void launch_gemm(Handle& h, bool amn, const Sliced& As, const Sliced& Bs, int64_
   case SS:                                                                           \
     if (pair && amn) {                                                               \
       smem_attr(ozaki_gemm2_kernel<1, SS>, smem);                                    \
-      launch_k(h, ozaki_gemm2_kernel<1, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
+      launch_cluster(h, ozaki_gemm2_kernel<1, SS>, unsigned(grid), kThreads, smem, csize, ta, tb, p); \
     } else if (pair) {                                                               \
       smem_attr(ozaki_gemm2_kernel<0, SS>, smem);                                    \
-      launch_k(h, ozaki_gemm2_kernel<0, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
+      launch_cluster(h, ozaki_gemm2_kernel<0, SS>, unsigned(grid), kThreads, smem, csize, ta, tb, p); \
     } else if (amn) {                                                                \
       smem_attr(ozaki_gemm_kernel<1, SS>, smem);                                     \
       launch_k(h, ozaki_gemm_kernel<1, SS>, unsigned(grid), kThreads, smem, ta, tb, p); \
